@@ -1,0 +1,373 @@
+"""Benchmark of the DraftAttention sparse-attention call on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config hv720|wan720|tiny]
+                    [--sparsity S] [--impl ours|reference]
+
+One step = one attention call over all heads of the configuration (pool ->
+draft scores -> global top-fraction selection -> block-sparse attention, output
+in original token order). N = 1: inputs resident in HBM (value); the same call
+through the public API with pinned-host inputs and a host copy of the output
+(e2e). N > 1: inputs arrive sequence-sharded, NCCL all-to-all reshards to
+head-sharded, each rank runs its heads, all-to-all back (strong scaling: the
+call's total work is fixed). Inputs (2.2 GB for HV720) are larger than L2, so
+no L2 flush is needed between steps.
+
+--impl reference times the CPU oracle port of the reference algorithm
+(oracle/, the reference itself is numpy) on the host cores, on a bounded
+sample of the same call (one head's selection stages in full plus a fixed
+subset of its query regions), extrapolated to ms per call.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: frames, height, width, patch_h, patch_w, heads, head_dim, sparsity
+    "hv720": (33, 45, 80, 8, 8, 24, 128, 0.9),
+    "wan720": (21, 45, 80, 8, 8, 40, 128, 0.75),
+    "tiny": (4, 16, 16, 4, 4, 2, 64, 0.5),
+}
+METRIC = "ms/attn call at HunyuanVideo 720p, 90% sparse; effective TFLOP/s per B200"
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def _profile_traffic(config_name):
+    """DRAM bytes per K4 launch from the committed ncu --set full summary, if any."""
+    p = ROOT / "profiles" / "ncu_k4_summary.json"
+    try:
+        data = json.loads(p.read_text())
+        return data.get(config_name, {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.result = None
+        if self.proc is None:
+            return False
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+            out = ""
+        sms, maxes, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxes.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if sms:
+            self.result = {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(maxes),
+                           "reasons": sorted(reasons), "samples": len(sms)}
+        return False
+
+
+# --------------------------------------------------------------------------
+# CPU reference arm / baseline (oracle port of the reference algorithm)
+# --------------------------------------------------------------------------
+
+def cpu_reference_sample(cfg, seed=0, n_rows=48):
+    """Time the reference algorithm (oracle port) on one head: selection stages
+    in full, the executor on ``n_rows`` evenly spaced query regions.
+    Returns (ms_per_call_extrapolated, sample description, threads)."""
+    import numpy as np
+    from oracle import draftattn_oracle as O
+
+    f, h, w, ph, pw, heads, d, sp = cfg
+    grid = O.Grid(f, h, w, ph, pw)
+    q, k, v = O.gen_real_inputs(grid, d, seed, heads, head_ids=[0])
+    q, k, v = (x[0].astype(np.float64) for x in (q, k, v))
+    t0 = time.perf_counter()
+    mask, _ = O.draft_mask(q, k, grid, sp)
+    t1 = time.perf_counter()
+    rows = np.linspace(0, grid.num_regions - 1, min(n_rows, grid.num_regions)).astype(np.int64)
+    qr, kr, vr = O.permute_in(q, grid), O.permute_in(k, grid), O.permute_in(v, grid)
+    kv = None if grid.divisible else O.valid_reordered(grid)
+    t2 = time.perf_counter()
+    O.block_sparse_attention(qr, kr, vr, mask.kept, O.head_dim_scale(d), key_valid=kv, rows=rows)
+    t3 = time.perf_counter()
+    exec_full = (t3 - t2) * grid.num_regions / len(rows)
+    per_head = (t1 - t0) + (t2 - t1) + exec_full
+    threads = os.cpu_count() or 1
+    sample = (f"1 of {heads} heads: pool+draft+select in full ({t1 - t0:.2f}s), executor on "
+              f"{len(rows)}/{grid.num_regions} query regions ({t3 - t2:.2f}s); x{grid.num_regions // len(rows)} "
+              f"regions, x{heads} heads extrapolated; float64 numpy, BLAS threads={threads}")
+    return per_head * heads * 1e3, sample, threads
+
+
+def run_reference(args, cfg, name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals, sample, threads = [], "", 1
+    for _ in range(args.warmup_ref):
+        cpu_reference_sample(cfg, n_rows=8)
+    for _ in range(args.steps):
+        ms, sample, threads = cpu_reference_sample(cfg)
+        vals.append(ms)
+    ms = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(name, cfg, args.gpus),
+        "cpu_baseline": {"value": ms, "unit": "ms/call", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": ms, "unit": "ms/call", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(name, cfg, n):
+    f, h, w, ph, pw, heads, d, sp = cfg
+    return {"workload": f"{name}: {f}x{h}x{w} tokens ({f * h * w}), {heads} heads, d={d}, "
+                        f"{ph}x{pw} pool, {int(sp * 100)}% sparsity",
+            "frames": f, "height": h, "width": w, "patch": [ph, pw], "heads": heads, "head_dim": d,
+            "sparsity": sp, "parallelism": f"head-parallel x{n}" if n > 1 else "single GPU",
+            "l2": "inputs (3 x heads x n x d bf16) exceed the 126 MB L2; no flush needed"}
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+
+def run_ours(args, cfg, name):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_14708_b200 as da
+    from paper_2505_14708_b200 import _lib
+    from paper_2505_14708_b200.build import build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.init_process_group("nccl")
+        dist.barrier()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    f, h, w, ph, pw, heads, d, sp = cfg
+    plan = da.pad_plan(f, h, w, ph, pw)
+    n = plan.num_valid
+    g = plan.layout.num_regions
+    p = plan.layout.region_size
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+
+    if world == 1:
+        q, k, v = (torch.randn(heads, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+                   for _ in range(3))
+
+        def step(events=None):
+            return da.api._pipeline(q, k, v, plan, sp, da.head_dim_scale(d), "average", "logits", True, False,
+                                    "hnd", attn_events=events)
+    else:
+        from paper_2505_14708_b200.headpar import HeadParallelAttention
+
+        assert n % world == 0 and heads % world == 0, "tokens and heads must divide the world size"
+        nl = n // world
+        q, k, v = (torch.randn(nl, heads, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+                   for _ in range(3))
+        hp = HeadParallelAttention(plan, sp, world, rank)
+
+        def step(events=None):
+            return hp(q, k, v, attn_events=events)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kept_total = None
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record()
+        for s in range(args.steps):
+            res = step(ev[s])
+        end.record()
+        torch.cuda.synchronize()
+    elapsed = start.elapsed_time(end)
+    k4_ms = statistics.mean(b.elapsed_time(e) for b, e in ev)
+    mask = res[1]
+    kept_total = int(mask.kept_counts.sum().item())
+    if world > 1:
+        t = torch.tensor([elapsed, k4_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed, k4_ms = float(t[0]), float(t[1])
+        kt = torch.tensor([kept_total], device=dev, dtype=torch.int64)
+        dist.all_reduce(kt)
+        kept_total = int(kt.item())
+    ms = elapsed / args.steps
+
+    # effective work: 4 p^2 d per kept block pair (sparse.py:74-84 on the padded layout)
+    eff_flops = 4.0 * p * p * d * kept_total
+    peaks = _peaks()
+    peak_tf = peaks.get("bf16_tflops_sustained") or 1419.7
+    k4_tflops = eff_flops / (k4_ms * 1e-3) / 1e12 / world
+    e2e = None
+    cpu_base = None
+    dense_ms = None
+    if world == 1:
+        e2e = _e2e(da, plan, cfg, dev, args)
+        dense_ms = _dense_sdpa_ms(heads, n, d, dev) if args.dense else None
+        if not args.no_cpu:
+            cms, sample, threads = cpu_reference_sample(cfg)
+            cpu_base = {"value": cms, "unit": "ms/call", "cores": threads, "kind": "port", "sample": sample}
+    if rank == 0:
+        launches = _lib.lib().da_pipeline_launches(0, 0) * args.steps
+        line = {
+            "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn gaussian, seeded)",
+            "config": _config_dict(name, cfg, world),
+            "effective_tflops_per_gpu": eff_flops / (ms * 1e-3) / 1e12 / world,
+            "kept_blocks": kept_total,
+            "roofline": {"bound": "tensor", "kernel": "sparse_attn_tc_kernel (K4)", "achieved": k4_tflops,
+                         "peak": peak_tf, "unit": "TFLOP/s", "frac": k4_tflops / peak_tf,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
+                         "k4_ms": k4_ms, "k4_share_of_step": k4_ms / ms,
+                         "algorithmic_flops_per_launch": eff_flops / world,
+                         "traffic": _profile_traffic(name)},
+            "gpu_launches": launches,
+            "clocks": clocks.result,
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if dense_ms is not None:
+            line["dense_sdpa_ms"] = dense_ms
+            line["speedup_vs_dense_sdpa"] = dense_ms / ms
+        if cpu_base is not None:
+            line["cpu_baseline"] = cpu_base
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _e2e(da, plan, cfg, dev, args):
+    """Public API with pinned host inputs and a host copy of the output."""
+    import torch
+
+    f, h, w, ph, pw, heads, d, sp = cfg
+    n = plan.num_valid
+    host = [torch.randn(heads, n, d, dtype=torch.float32).to(torch.bfloat16).pin_memory() for _ in range(3)]
+    out_host = torch.empty(heads, n, d, dtype=torch.bfloat16).pin_memory()
+
+    def once():
+        qd, kd, vd = (x.to(dev, non_blocking=True) for x in host)
+        o = da.multi_head_sparse_attention(qd, kd, vd, plan, sp)
+        out_host.copy_(o, non_blocking=True)
+        return o
+
+    for _ in range(2):
+        once()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(2, min(args.steps, 5))
+    s.record()
+    for _ in range(steps):
+        once()
+    e.record()
+    torch.cuda.synchronize()
+    nb = heads * n * d * 2
+    return {"value": s.elapsed_time(e) / steps, "unit": "ms/call", "h2d_bytes_per_step": 3 * nb,
+            "d2h_bytes_per_step": nb}
+
+
+def _dense_sdpa_ms(heads, n, d, dev):
+    import torch
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    q, k, v = (torch.randn(1, heads, n, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
+    try:
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION]):
+            F.scaled_dot_product_attention(q, k, v)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(3):
+                F.scaled_dot_product_attention(q, k, v)
+            e.record()
+            torch.cuda.synchronize()
+        return s.elapsed_time(e) / 3
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="hv720", choices=sorted(CONFIGS))
+    ap.add_argument("--sparsity", type=float, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--dense", action="store_true", help="also time dense cuDNN SDPA at the same shape")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.sparsity is not None:
+        cfg = cfg[:7] + (args.sparsity,)
+    if args.impl == "reference":
+        args.warmup_ref = 1 if args.warmup > 0 else 0
+        args.steps = max(1, min(args.steps, 3))
+        run_reference(args, cfg, args.config)
+    else:
+        run_ours(args, cfg, args.config)
+
+
+if __name__ == "__main__":
+    main()

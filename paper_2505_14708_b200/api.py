@@ -1,0 +1,664 @@
+"""Drop-in GPU API for the DraftAttention sparse-attention path.
+
+Mirrors the reference package's operator surface (names, positional order,
+defaults and ValueError messages of /root/reference/pkg/src/draftattn):
+
+    padded_sparse_attention   padding.py:95-165
+    draft_sparse_attention    sparse.py:193-246
+    multi_head_sparse_attention  sparse.py:249-302
+    block_sparse_attention    sparse.py:88-166   (reordered seam)
+    select_top_fraction       masking.py:59-91
+    draft_logits / pool_regions / top_fraction_count / head_dim_scale / flops_count
+
+Tensors are torch CUDA tensors (bf16 compute; other float dtypes are cast to
+bf16 on entry and the output is cast back, matching the reference's
+``result_type(q, k, v)`` output dtype). Token matrices are ``(n, d)`` or
+``(heads, n, d)``; ``qkv_layout="nhd"`` accepts the DiT ``(n, heads, d)``
+layout without a copy. All work runs in hand-written sm_100a kernels behind the
+C ABI (include/draftattn_b200.h); there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import DaAttnArgs, DaPipelineArgs, check, lib, make_grid
+
+_CEIL_EPS = 1e-9
+POOL_MODES = ("average", "max")
+SELECT_MODES = ("logits", "softmax")
+
+
+# --------------------------------------------------------------------------
+# host-side geometry (layout.py:10-60, padding.py:21-56)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class LatentLayout:
+    """Token grid partitioned into pooling patches (layout.py:10-60)."""
+
+    frames: int
+    height: int
+    width: int
+    patch_h: int
+    patch_w: int
+
+    def __post_init__(self) -> None:
+        for name in ("frames", "height", "width", "patch_h", "patch_w"):
+            value = getattr(self, name)
+            if not isinstance(value, int) or isinstance(value, bool) or value < 1:
+                raise ValueError(f"{name} must be a positive integer, got {value!r}")
+        if self.height % self.patch_h != 0:
+            raise ValueError(f"patch_h={self.patch_h} does not divide height={self.height}; "
+                             "pad the grid first (see draftattn.padding)")
+        if self.width % self.patch_w != 0:
+            raise ValueError(f"patch_w={self.patch_w} does not divide width={self.width}; "
+                             "pad the grid first (see draftattn.padding)")
+
+    @property
+    def num_tokens(self) -> int:
+        return self.frames * self.height * self.width
+
+    @property
+    def region_size(self) -> int:
+        return self.patch_h * self.patch_w
+
+    @property
+    def patches_h(self) -> int:
+        return self.height // self.patch_h
+
+    @property
+    def patches_w(self) -> int:
+        return self.width // self.patch_w
+
+    @property
+    def num_regions(self) -> int:
+        return self.frames * self.patches_h * self.patches_w
+
+
+@dataclass(frozen=True)
+class PadPlan:
+    """Padded geometry of a real grid (padding.py:21-42); validity is closed form."""
+
+    frames: int
+    height: int
+    width: int
+    layout: LatentLayout
+
+    @property
+    def num_valid(self) -> int:
+        return self.frames * self.height * self.width
+
+    @property
+    def is_identity(self) -> bool:
+        return self.layout.height == self.height and self.layout.width == self.width
+
+
+def pad_plan(frames: int, height: int, width: int, patch_h: int, patch_w: int) -> PadPlan:
+    """Smallest patch-divisible grid containing (height, width) (padding.py:45-56)."""
+    if min(frames, height, width, patch_h, patch_w) < 1:
+        raise ValueError("all grid dimensions must be positive")
+    ph = -(-height // patch_h) * patch_h
+    pw = -(-width // patch_w) * patch_w
+    return PadPlan(frames, height, width, LatentLayout(frames, ph, pw, patch_h, patch_w))
+
+
+def head_dim_scale(head_dim: int) -> float:
+    """1/sqrt(d) (core.py:13-17)."""
+    if head_dim < 1:
+        raise ValueError(f"head_dim must be positive, got {head_dim}")
+    return 1.0 / math.sqrt(head_dim)
+
+
+def top_fraction_count(num_entries: int, keep_ratio: float) -> int:
+    """ceil(r*N - 1e-9) clamped to [1, N] (masking.py:49-56)."""
+    if not 0.0 < keep_ratio <= 1.0:
+        raise ValueError(f"keep_ratio must be in (0, 1], got {keep_ratio}")
+    if num_entries < 1:
+        raise ValueError(f"num_entries must be positive, got {num_entries}")
+    m = math.ceil(keep_ratio * num_entries - _CEIL_EPS)
+    return min(max(m, 1), num_entries)
+
+
+# --------------------------------------------------------------------------
+# result types (masking.py:16-46, sparse.py:15-43, 183-190)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True, eq=False)
+class RegionMask:
+    """Block mask of one or more heads, resident on the GPU.
+
+    ``bitmap`` is the reference's packed row-major MSB-first layout
+    (masking.py:168-170), one row of ``ceil(g*g/8)`` bytes per head;
+    ``row_ptr``/``col_idx`` are the executor feed (ascending kept columns).
+    ``threshold``, ``forced_row_keeps`` and ``kept_count`` are per head
+    (Python scalars for a single-head mask).
+    """
+
+    g: int
+    keep_ratio: float
+    bitmap: torch.Tensor          # (heads, ceil(g*g/8)) uint8
+    row_ptr: torch.Tensor         # (heads, g+1) int32
+    col_idx: torch.Tensor         # (heads, cap) int32
+    thresholds: torch.Tensor      # (heads,) float64
+    forced: torch.Tensor          # (heads,) int64
+    kept_counts: torch.Tensor     # (heads,) int64
+    single: bool = True
+    _host: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def heads(self) -> int:
+        return int(self.row_ptr.shape[0])
+
+    def _scalars(self):
+        if "s" not in self._host:
+            self._host["s"] = (self.thresholds.cpu().tolist(), self.forced.cpu().tolist(),
+                               self.kept_counts.cpu().tolist())
+        return self._host["s"]
+
+    @property
+    def threshold(self):
+        t = self._scalars()[0]
+        return t[0] if self.single else t
+
+    @property
+    def forced_row_keeps(self):
+        f = self._scalars()[1]
+        return f[0] if self.single else f
+
+    @property
+    def kept_count(self):
+        k = self._scalars()[2]
+        return k[0] if self.single else k
+
+    @property
+    def kept(self) -> torch.Tensor:
+        """Unpacked boolean (g, g) (or (heads, g, g)) matrix, on the GPU."""
+        bits = torch.tensor([128, 64, 32, 16, 8, 4, 2, 1], dtype=torch.uint8, device=self.bitmap.device)
+        kept = ((self.bitmap.unsqueeze(-1) & bits) != 0).reshape(self.heads, -1)[:, : self.g * self.g]
+        kept = kept.reshape(self.heads, self.g, self.g)
+        return kept[0] if self.single else kept
+
+    @property
+    def row_kept_counts(self) -> torch.Tensor:
+        c = (self.row_ptr[:, 1:] - self.row_ptr[:, :-1]).to(torch.int64)
+        return c[0] if self.single else c
+
+    def bitmap_bytes(self, head: int = 0) -> bytes:
+        """mask_to_bitmap (masking.py:168-170) of one head."""
+        return self.bitmap[head].cpu().numpy().tobytes()
+
+    def head(self, h: int) -> "RegionMask":
+        return RegionMask(self.g, self.keep_ratio, self.bitmap[h:h + 1], self.row_ptr[h:h + 1],
+                          self.col_idx[h:h + 1], self.thresholds[h:h + 1], self.forced[h:h + 1],
+                          self.kept_counts[h:h + 1], single=True)
+
+
+def mask_density_stats(mask: RegionMask, head: int = 0) -> dict:
+    """Occupancy summary of one head (masking.py:128-141)."""
+    m = mask.head(head) if not mask.single else mask
+    rows = m.row_kept_counts.double()
+    kept = int(m.kept_count)
+    return {
+        "g": m.g,
+        "keep_ratio": m.keep_ratio,
+        "threshold": m.threshold,
+        "kept_count": kept,
+        "kept_fraction": kept / (m.g * m.g),
+        "row_kept_min": int(rows.min().item()),
+        "row_kept_mean": float(rows.mean().item()),
+        "row_kept_max": int(rows.max().item()),
+        "forced_row_keeps": m.forced_row_keeps,
+    }
+
+
+@dataclass(frozen=True)
+class FlopsReport:
+    """Matmul FLOP accounting for one head (sparse.py:15-43)."""
+
+    full_logits_flops: int
+    full_av_flops: int
+    draft_flops: int
+    sparse_logits_flops: int
+    sparse_av_flops: int
+    overhead_ratio: float
+    total_ratio: float
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+def flops_count(layout: LatentLayout, head_dim: int, sparsity: float | None = None,
+                kept_count: int | None = None, force_row_keep_extras: int = 0) -> FlopsReport:
+    """FLOP model (sparse.py:45-85)."""
+    if head_dim < 1:
+        raise ValueError(f"head_dim must be positive, got {head_dim}")
+    n, g, p = layout.num_tokens, layout.num_regions, layout.region_size
+    if kept_count is None:
+        if sparsity is None:
+            raise ValueError("pass sparsity or kept_count")
+        if not 0.0 <= sparsity < 1.0:
+            raise ValueError(f"sparsity must be in [0, 1), got {sparsity}")
+        kept_count = min(top_fraction_count(g * g, 1.0 - sparsity) + force_row_keep_extras, g * g)
+    elif not 0 <= kept_count <= g * g:
+        raise ValueError(f"kept_count {kept_count} outside [0, {g * g}]")
+    full = 2 * n * n * head_dim
+    draft = 2 * g * g * head_dim
+    sparse = 2 * kept_count * p * p * head_dim
+    return FlopsReport(full, full, draft, sparse, sparse, draft / full, (draft + sparse) / full)
+
+
+@dataclass(frozen=True, eq=False)
+class PipelineResult:
+    """Output plus the artifacts that produced it (sparse.py:183-190)."""
+
+    output: torch.Tensor
+    mask: RegionMask
+    flops: FlopsReport | list
+    mask_stats: dict | list
+
+
+# --------------------------------------------------------------------------
+# tensor plumbing
+# --------------------------------------------------------------------------
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _as_heads(x: torch.Tensor, qkv_layout: str, name: str):
+    """Return (tensor_3d, head_stride, row_stride, squeeze) for (n,d)/(h,n,d)/(n,h,d)."""
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor on a CUDA device")
+    if x.ndim == 2:
+        x3 = x.unsqueeze(0)
+        squeeze = True
+    elif x.ndim == 3:
+        x3 = x if qkv_layout == "hnd" else x.transpose(0, 1)
+        squeeze = False
+    else:
+        raise ValueError(f"{name} must be 2-d (n, d) or 3-d, got shape {tuple(x.shape)}")
+    return x3, squeeze
+
+
+def _prep(x3: torch.Tensor) -> torch.Tensor:
+    """bf16, CUDA, unit stride on features, 16-byte aligned rows (copy only if needed)."""
+    if not x3.is_cuda:
+        raise ValueError("inputs must be CUDA tensors (the B200 path has no CPU fallback)")
+    if x3.dtype != torch.bfloat16:
+        x3 = x3.to(torch.bfloat16)
+    ok = (x3.stride(2) == 1 and x3.stride(0) % 8 == 0 and x3.stride(1) % 8 == 0
+          and x3.data_ptr() % 16 == 0 and x3.shape[2] % 8 == 0)
+    return x3 if ok else x3.contiguous()
+
+
+def _out_dtype(q, k, v):
+    return torch.promote_types(torch.promote_types(q.dtype, k.dtype), v.dtype)
+
+
+def _alloc_like_layout(heads, n, dv, qkv_layout, device):
+    if qkv_layout == "nhd":
+        base = torch.empty((n, heads, dv), dtype=torch.bfloat16, device=device)
+        return base, base.transpose(0, 1)
+    base = torch.empty((heads, n, dv), dtype=torch.bfloat16, device=device)
+    return base, base
+
+
+def _attn_struct(q3, k3, v3, o3, d, dv, layout_code, scale) -> DaAttnArgs:
+    a = DaAttnArgs()
+    a.q, a.k, a.v, a.out = q3.data_ptr(), k3.data_ptr(), v3.data_ptr(), o3.data_ptr()
+    a.q_head_stride, a.q_row_stride = q3.stride(0), q3.stride(1)
+    a.k_head_stride, a.k_row_stride = k3.stride(0), k3.stride(1)
+    a.v_head_stride, a.v_row_stride = v3.stride(0), v3.stride(1)
+    a.o_head_stride, a.o_row_stride = o3.stride(0), o3.stride(1)
+    a.heads = q3.shape[0]
+    a.d, a.dv, a.layout = d, dv, layout_code
+    a.scale = float(scale)
+    return a
+
+
+def _validate_pipeline_args(sparsity, select_on, pool_mode):
+    if not 0.0 <= sparsity < 1.0:
+        raise ValueError(f"sparsity must be in [0, 1), got {sparsity}")
+    if select_on not in SELECT_MODES:
+        raise ValueError(f"select_on must be 'logits' or 'softmax', got {select_on!r}")
+    if pool_mode not in POOL_MODES:
+        raise ValueError(f"mode must be one of {POOL_MODES}, got {pool_mode!r}")
+
+
+def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
+              shared_head_mask, qkv_layout, force_portable=False, attn_events=None):
+    """Run the fused C-ABI pipeline; returns (output, mask, squeeze)."""
+    q3, squeeze = _as_heads(q, qkv_layout, "q")
+    k3, _ = _as_heads(k, qkv_layout, "k")
+    v3, _ = _as_heads(v, qkv_layout, "v")
+    heads, n, d = q3.shape
+    if k3.shape != q3.shape:
+        raise ValueError(f"k shape {tuple(k3.shape)} does not match q shape {tuple(q3.shape)}")
+    if v3.shape[:2] != q3.shape[:2]:
+        raise ValueError(f"v rows {v3.shape[1]} != key rows {n}")
+    out_dtype = _out_dtype(q, k, v)
+    q3, k3, v3 = _prep(q3), _prep(k3), _prep(v3)
+    dv = v3.shape[2]
+    layout = plan.layout
+    g, dev = layout.num_regions, q3.device
+    grid = make_grid(plan.frames, plan.height, plan.width, layout.patch_h, layout.patch_w)
+    m = top_fraction_count(g * g, 1.0 - sparsity)
+    mheads = 1 if shared_head_mask else heads
+    cap = m + g
+    row_ptr = torch.empty((mheads, g + 1), dtype=torch.int32, device=dev)
+    col_idx = torch.empty((mheads, cap), dtype=torch.int32, device=dev)
+    bitmap = torch.empty((mheads, (g * g + 7) // 8), dtype=torch.uint8, device=dev)
+    thr = torch.empty(mheads, dtype=torch.float64, device=dev)
+    forced = torch.empty(mheads, dtype=torch.int64, device=dev)
+    kept = torch.empty(mheads, dtype=torch.int64, device=dev)
+    ws_bytes = lib().da_pipeline_workspace_size(ctypes.byref(grid), heads, d)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    o_base, o3 = _alloc_like_layout(heads, n, dv, qkv_layout if not squeeze else "hnd", dev)
+    pa = DaPipelineArgs()
+    pa.attn = _attn_struct(q3, k3, v3, o3, d, dv, _lib.LAYOUT_ORIGINAL, scale)
+    pa.attn.force_portable = 1 if force_portable else 0
+    pa.m = m
+    pa.force_row_keep = 1 if force_row_keep else 0
+    pa.pool_mode = POOL_MODES.index(pool_mode)
+    pa.select_softmax = 1 if select_on == "softmax" else 0
+    pa.shared_head_mask = 1 if shared_head_mask else 0
+    pa.row_ptr, pa.col_idx, pa.bitmap = row_ptr.data_ptr(), col_idx.data_ptr(), bitmap.data_ptr()
+    pa.threshold, pa.forced, pa.kept = thr.data_ptr(), forced.data_ptr(), kept.data_ptr()
+    pa.workspace = ws.data_ptr()
+    if attn_events is not None:  # (begin, end) torch.cuda.Event pair around the K4 launch
+        pa.ev_attn_begin = attn_events[0].cuda_event
+        pa.ev_attn_end = attn_events[1].cuda_event
+    with torch.cuda.device(dev):
+        check(lib().da_sparse_attention(ctypes.byref(pa), ctypes.byref(grid), _stream_ptr(dev)),
+              "sparse_attention")
+    out = o3[0] if squeeze else (o_base if qkv_layout == "nhd" else o3)
+    if out_dtype != torch.bfloat16:
+        out = out.to(out_dtype)
+    mask = RegionMask(g, float(1.0 - sparsity), bitmap, row_ptr, col_idx, thr, forced, kept,
+                      single=(squeeze or shared_head_mask))
+    return out, mask, squeeze
+
+
+def _details(out, mask: RegionMask, layout: LatentLayout, d: int):
+    if mask.single:
+        return PipelineResult(out, mask, flops_count(layout, d, kept_count=int(mask.kept_count)),
+                              mask_density_stats(mask))
+    flops = [flops_count(layout, d, kept_count=int(c)) for c in mask.kept_count]
+    stats = [mask_density_stats(mask, h) for h in range(mask.heads)]
+    return PipelineResult(out, mask, flops, stats)
+
+
+# --------------------------------------------------------------------------
+# public operators
+# --------------------------------------------------------------------------
+
+def padded_sparse_attention(q, k, v, frames, height, width, patch_h, patch_w, sparsity,
+                            scale=None, pool_mode="average", select_on="logits",
+                            force_row_keep=True, two_pass=False, return_details=False,
+                            *, qkv_layout="hnd"):
+    """Draft-guided block-sparse attention on any grid (padding.py:95-165).
+
+    Ragged grids are padded inside the kernels: pooling averages over real
+    tokens only, padded keys are masked, padded rows never reach the output.
+    ``two_pass`` (the reference's debug executor) computes the same function
+    and is accepted for signature compatibility.
+    """
+    del two_pass
+    plan = pad_plan(frames, height, width, patch_h, patch_w)
+    _validate_pipeline_args(sparsity, select_on, pool_mode)
+    if not plan.is_identity and pool_mode != "average":
+        raise ValueError("padded grids support average pooling only")
+    q3, _ = _as_heads(q, qkv_layout, "q")
+    if q3.shape[1] != plan.num_valid:
+        raise ValueError(f"expected ({plan.num_valid}, d) real-token rows, got {tuple(q.shape)}")
+    d = q3.shape[2]
+    if scale is None:
+        scale = head_dim_scale(d)
+    out, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                             False, qkv_layout)
+    if not return_details:
+        return out
+    return _details(out, mask, plan.layout, d)
+
+
+def draft_sparse_attention(q, k, v, layout: LatentLayout, sparsity, scale=None, pool_mode="average",
+                           select_on="logits", force_row_keep=True, two_pass=False,
+                           return_details=False, *, qkv_layout="hnd"):
+    """Full pipeline on a divisible grid (sparse.py:193-246)."""
+    del two_pass
+    _validate_pipeline_args(sparsity, select_on, pool_mode)
+    q3, _ = _as_heads(q, qkv_layout, "q")
+    if q3.shape[1] != layout.num_tokens:
+        raise ValueError(f"q rows {q3.shape[1]} != layout token count {layout.num_tokens}")
+    d = q3.shape[2]
+    if scale is None:
+        scale = head_dim_scale(d)
+    plan = PadPlan(layout.frames, layout.height, layout.width, layout)
+    out, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                             False, qkv_layout)
+    if not return_details:
+        return out
+    return _details(out, mask, layout, d)
+
+
+def multi_head_sparse_attention(q, k, v, layout: LatentLayout, sparsity, shared_head_mask=False,
+                                scale=None, pool_mode="average", select_on="logits",
+                                force_row_keep=True, *, qkv_layout="hnd", return_details=False):
+    """Stacked (heads, n, d) inputs (sparse.py:249-302); all heads in one launch per stage.
+
+    ``layout`` may also be a PadPlan for ragged grids (the reference has no
+    padded multi-head entry; this is the batched form of its per-head loop).
+    """
+    if q.ndim != 3:
+        raise ValueError(f"expected (heads, n, d) inputs, got shape {tuple(q.shape)}")
+    _validate_pipeline_args(sparsity, select_on, pool_mode)
+    plan = layout if isinstance(layout, PadPlan) else PadPlan(layout.frames, layout.height,
+                                                                layout.width, layout)
+    if not plan.is_identity and pool_mode != "average":
+        raise ValueError("padded grids support average pooling only")
+    q3, _ = _as_heads(q, qkv_layout, "q")
+    if q3.shape[1] != plan.num_valid:
+        raise ValueError(f"q rows {q3.shape[1]} != layout token count {plan.num_valid}")
+    d = q3.shape[2]
+    if scale is None:
+        scale = head_dim_scale(d)
+    out, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                             shared_head_mask, qkv_layout)
+    if not return_details:
+        return out
+    return _details(out, mask, plan.layout, d)
+
+
+# --------------------------------------------------------------------------
+# lower seams
+# --------------------------------------------------------------------------
+
+def reorder_tokens(x, plan: PadPlan, *, qkv_layout="hnd") -> torch.Tensor:
+    """permute_rows(embed_rows(x, plan), perm) (padding.py:140-142): K1, bit-exact.
+
+    Returns dense (heads, n_pad, d) (or (n_pad, d) for 2-d input) in patch-contiguous order.
+    """
+    x3, squeeze = _as_heads(x, qkv_layout, "x")
+    x3 = _prep(x3)
+    heads, n, d = x3.shape
+    if n != plan.num_valid:
+        raise ValueError(f"expected ({plan.num_valid}, d) real-token rows, got {tuple(x.shape)}")
+    lay = plan.layout
+    out = torch.empty((heads, lay.num_tokens, d), dtype=torch.bfloat16, device=x3.device)
+    grid = make_grid(plan.frames, plan.height, plan.width, lay.patch_h, lay.patch_w)
+    with torch.cuda.device(x3.device):
+        check(lib().da_permute_in(x3.data_ptr(), x3.stride(0), x3.stride(1), out.data_ptr(), heads, d,
+                                  ctypes.byref(grid), _stream_ptr(x3.device)), "permute_in")
+    return out[0] if squeeze else out
+
+
+def restore_tokens(x_r, plan: PadPlan) -> torch.Tensor:
+    """extract_rows(permute_rows(x_r, perm.inverse), plan) (padding.py:157): K5, bit-exact."""
+    x3, squeeze = _as_heads(x_r, "hnd", "x_r")
+    x3 = _prep(x3).contiguous()
+    heads, n_pad, d = x3.shape
+    lay = plan.layout
+    if n_pad != lay.num_tokens:
+        raise ValueError(f"expected {lay.num_tokens} padded rows, got {n_pad}")
+    out = torch.empty((heads, plan.num_valid, d), dtype=torch.bfloat16, device=x3.device)
+    grid = make_grid(plan.frames, plan.height, plan.width, lay.patch_h, lay.patch_w)
+    with torch.cuda.device(x3.device):
+        check(lib().da_permute_out(x3.data_ptr(), out.data_ptr(), out.stride(0), out.stride(1), heads, d,
+                                   ctypes.byref(grid), _stream_ptr(x3.device)), "permute_out")
+    return out[0] if squeeze else out
+
+
+def pool_tokens(x, plan: PadPlan, mode="average", *, qkv_layout="hnd") -> torch.Tensor:
+    """Region pooling straight from original token order, float64 result (K2).
+
+    Equals pool_regions_valid(permute_rows(embed_rows(x)), valid_r, p)
+    (padding.py:78-92) on ragged grids and pool_regions (pooling.py:12-32) on
+    divisible ones.
+    """
+    if mode not in POOL_MODES:
+        raise ValueError(f"mode must be one of {POOL_MODES}, got {mode!r}")
+    if mode != "average" and not plan.is_identity:
+        raise ValueError("padded grids support average pooling only")
+    x3, squeeze = _as_heads(x, qkv_layout, "x")
+    x3 = _prep(x3)
+    heads, n, d = x3.shape
+    lay = plan.layout
+    out = torch.empty((heads, lay.num_regions, d), dtype=torch.float64, device=x3.device)
+    grid = make_grid(plan.frames, plan.height, plan.width, lay.patch_h, lay.patch_w)
+    with torch.cuda.device(x3.device):
+        check(lib().da_pool(x3.data_ptr(), x3.stride(0), x3.stride(1), out.data_ptr(), heads, d, ctypes.byref(grid),
+                            POOL_MODES.index(mode), _stream_ptr(x3.device)), "pool")
+    return out[0] if squeeze else out
+
+
+def pool_regions(x_r, region_size: int, mode="average") -> torch.Tensor:
+    """Contiguous region mean/max of reordered rows (pooling.py:12-32), float64 result."""
+    if mode not in POOL_MODES:
+        raise ValueError(f"mode must be one of {POOL_MODES}, got {mode!r}")
+    x3, squeeze = _as_heads(x_r, "hnd", "x")
+    n = x3.shape[1]
+    if region_size < 1:
+        raise ValueError(f"region_size must be positive, got {region_size}")
+    if n % region_size != 0:
+        raise ValueError(f"row count {n} is not a multiple of region_size {region_size}")
+    # contiguous regions == a grid of n/p frames of one 1 x p patch each
+    plan = pad_plan(n // region_size, 1, region_size, 1, region_size)
+    out = pool_tokens(x3, plan, mode)
+    return out[0] if squeeze else out
+
+
+def draft_logits(q_pooled, k_pooled, scale=None, head_dim=None, *, softmax=False) -> torch.Tensor:
+    """scale * q_pooled @ k_pooled^T in float64 (pooling.py:35-56, core.py:20-35): K3a."""
+    if scale is not None and head_dim is not None:
+        raise ValueError("pass at most one of scale and head_dim")
+    qp3, squeeze = _as_heads(q_pooled, "hnd", "q_pooled")
+    kp3, _ = _as_heads(k_pooled, "hnd", "k_pooled")
+    if qp3.shape[2] != kp3.shape[2]:
+        raise ValueError(f"head_dim mismatch: q has {qp3.shape[2]}, k has {kp3.shape[2]}")
+    if qp3.shape[1] != kp3.shape[1]:
+        raise ValueError("draft scores need the same number of query and key regions")
+    if head_dim is not None:
+        scale = head_dim_scale(head_dim)
+    if scale is None:
+        scale = head_dim_scale(qp3.shape[2])
+    qp3 = qp3.to(torch.float64).contiguous()
+    kp3 = kp3.to(torch.float64).contiguous()
+    heads, g, d = qp3.shape
+    out = torch.empty((heads, g, g), dtype=torch.float64, device=qp3.device)
+    with torch.cuda.device(qp3.device):
+        check(lib().da_draft_scores(qp3.data_ptr(), kp3.data_ptr(), out.data_ptr(), heads, g, d, float(scale),
+                                    1 if softmax else 0, _stream_ptr(qp3.device)), "draft_scores")
+    return out[0] if squeeze else out
+
+
+def select_top_fraction(scores, keep_ratio: float, force_row_keep: bool = False,
+                        dead_columns=None) -> RegionMask:
+    """Global top-ceil(r*g^2) with flat-index ties (+ row argmax keep) (masking.py:59-91): K3b.
+
+    ``scores`` is (g, g) or (heads, g, g) on the GPU (computed in float64).
+    ``dead_columns`` (optional) are dropped afterwards (masking.py:94-105).
+    """
+    s3, squeeze = _as_heads(scores, "hnd", "scores")
+    if s3.shape[1] != s3.shape[2]:
+        raise ValueError(f"expected a square score matrix, got shape {tuple(scores.shape)}")
+    heads, g, _ = s3.shape
+    m = top_fraction_count(g * g, keep_ratio)
+    s3 = s3.to(torch.float64).contiguous()
+    dev = s3.device
+    cap = m + g
+    row_ptr = torch.empty((heads, g + 1), dtype=torch.int32, device=dev)
+    col_idx = torch.empty((heads, cap), dtype=torch.int32, device=dev)
+    bitmap = torch.empty((heads, (g * g + 7) // 8), dtype=torch.uint8, device=dev)
+    thr = torch.empty(heads, dtype=torch.float64, device=dev)
+    forced = torch.empty(heads, dtype=torch.int64, device=dev)
+    kept = torch.empty(heads, dtype=torch.int64, device=dev)
+    ws = torch.empty(lib().da_select_workspace_size(heads, g), dtype=torch.uint8, device=dev)
+    dead_ptr = None
+    if dead_columns is not None:
+        dead = torch.zeros(g, dtype=torch.uint8, device=dev)
+        idx = torch.as_tensor(dead_columns, dtype=torch.int64, device=dev)
+        if idx.numel():
+            dead[idx] = 1
+        dead_ptr = dead.data_ptr()
+    with torch.cuda.device(dev):
+        check(lib().da_select(s3.data_ptr(), heads, g, m, 1 if force_row_keep else 0, dead_ptr, ws.data_ptr(),
+                              row_ptr.data_ptr(), col_idx.data_ptr(), bitmap.data_ptr(), thr.data_ptr(),
+                              forced.data_ptr(), kept.data_ptr(), _stream_ptr(dev)), "select")
+    return RegionMask(g, float(keep_ratio), bitmap, row_ptr, col_idx, thr, forced, kept, single=squeeze)
+
+
+def block_sparse_attention(q_r, k_r, v_r, mask: RegionMask, scale=None, key_valid=None, two_pass=False,
+                           *, force_portable=False) -> torch.Tensor:
+    """Executor over reordered inputs, kept key blocks only (sparse.py:88-166): K4.
+
+    q_r/k_r/v_r: (n, d) or (heads, n, d) in patch-contiguous order; ``mask``
+    from select_top_fraction (one head, or one per input head). ``key_valid``:
+    optional bool (n,) of keys allowed to receive attention. Output stays in
+    reordered order.
+    """
+    del two_pass
+    q3, squeeze = _as_heads(q_r, "hnd", "q")
+    k3, _ = _as_heads(k_r, "hnd", "k")
+    v3, _ = _as_heads(v_r, "hnd", "v")
+    heads, n, d = q3.shape
+    if k3.shape != q3.shape:
+        raise ValueError(f"k shape {tuple(k3.shape)} does not match q shape {tuple(q3.shape)}")
+    if v3.shape[1] != n:
+        raise ValueError(f"v rows {v3.shape[1]} != key rows {n}")
+    g = mask.g
+    if n % g != 0:
+        raise ValueError(f"token count {n} is not a multiple of region count {g}")
+    p = n // g
+    if scale is None:
+        scale = head_dim_scale(d)
+    out_dtype = _out_dtype(q_r, k_r, v_r)
+    q3, k3, v3 = _prep(q3).contiguous(), _prep(k3).contiguous(), _prep(v3).contiguous()
+    dv = v3.shape[2]
+    kv_ptr = None
+    if key_valid is not None:
+        kv = torch.as_tensor(key_valid, device=q3.device).to(torch.bool)
+        if tuple(kv.shape) != (n,):
+            raise ValueError(f"key_valid shape {tuple(kv.shape)} != ({n},)")
+        kv = kv.to(torch.uint8).contiguous()
+        kv_ptr = kv.data_ptr()
+    if mask.heads not in (1, heads):
+        raise ValueError(f"mask has {mask.heads} heads for {heads} input heads")
+    out = torch.empty((heads, n, dv), dtype=torch.bfloat16, device=q3.device)
+    # a reordered (g*p)-row tensor is the grid of g frames of one 1 x p patch
+    grid = make_grid(g, 1, p, 1, p)
+    a = _attn_struct(q3, k3, v3, out, d, dv, _lib.LAYOUT_REORDERED, scale)
+    a.row_ptr, a.col_idx, a.mask_cap = mask.row_ptr.data_ptr(), mask.col_idx.data_ptr(), mask.col_idx.shape[1]
+    a.key_valid = kv_ptr
+    a.shared_mask = 1 if mask.heads == 1 else 0
+    a.force_portable = 1 if force_portable else 0
+    with torch.cuda.device(q3.device):
+        check(lib().da_block_sparse_fwd(ctypes.byref(a), ctypes.byref(grid), _stream_ptr(q3.device)),
+              "block_sparse_fwd")
+    out = out[0] if squeeze else out
+    return out.to(out_dtype) if out_dtype != torch.bfloat16 else out

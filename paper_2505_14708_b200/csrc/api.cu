@@ -1,0 +1,247 @@
+// C-ABI entry points (include/draftattn_b200.h): argument validation, error
+// reporting, workspace carving and the whole-pipeline driver. Validation
+// mirrors the reference's ValueError conditions where they apply to raw
+// buffers; the Python host layer raises the reference's own messages first.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return DA_OK;
+  return fail(DA_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool grid_ok(const da_grid* g) {
+  return g && g->frames > 0 && g->height > 0 && g->width > 0 && g->patch_h > 0 && g->patch_w > 0;
+}
+
+size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
+
+}  // namespace
+
+extern "C" {
+
+int32_t da_version(void) { return 100; }
+
+const char* da_last_error(void) { return g_err.c_str(); }
+
+int32_t da_num_regions(const da_grid* grid) {
+  if (!grid_ok(grid)) return -1;
+  return da::make_geo(*grid).g;
+}
+
+int32_t da_region_size(const da_grid* grid) {
+  if (!grid_ok(grid)) return -1;
+  return grid->patch_h * grid->patch_w;
+}
+
+int64_t da_padded_tokens(const da_grid* grid) {
+  if (!grid_ok(grid)) return -1;
+  return da::make_geo(*grid).n_pad;
+}
+
+int64_t da_mask_capacity(int32_t g, int64_t m) { return m + g; }
+
+int da_permute_in(const void* x, int64_t head_stride, int64_t row_stride, void* x_r, int32_t heads, int32_t d,
+                  const da_grid* grid, void* stream) {
+  if (!grid_ok(grid)) return fail(DA_EINVAL, "all grid dimensions must be positive");
+  if (!x || !x_r || heads < 1 || d < 8 || d % 8) return fail(DA_EINVAL, "permute_in: need d %% 8 == 0, heads >= 1");
+  if (head_stride % 8 || row_stride % 8 || (reinterpret_cast<uintptr_t>(x) & 15) ||
+      (reinterpret_cast<uintptr_t>(x_r) & 15))
+    return fail(DA_EINVAL, "permute_in: 16-byte aligned rows required");
+  da::Geo g = da::make_geo(*grid);
+  return cuda_status(da::launch_permute_in(x, head_stride, row_stride, x_r, heads, d, g, (cudaStream_t)stream),
+                     "permute_in");
+}
+
+int da_permute_out(const void* o_r, void* out, int64_t head_stride, int64_t row_stride, int32_t heads, int32_t d,
+                   const da_grid* grid, void* stream) {
+  if (!grid_ok(grid)) return fail(DA_EINVAL, "all grid dimensions must be positive");
+  if (!o_r || !out || heads < 1 || d < 8 || d % 8) return fail(DA_EINVAL, "permute_out: need d %% 8 == 0");
+  if (head_stride % 8 || row_stride % 8 || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      (reinterpret_cast<uintptr_t>(o_r) & 15))
+    return fail(DA_EINVAL, "permute_out: 16-byte aligned rows required");
+  da::Geo g = da::make_geo(*grid);
+  return cuda_status(da::launch_permute_out(o_r, out, head_stride, row_stride, heads, d, g, (cudaStream_t)stream),
+                     "permute_out");
+}
+
+int da_pool(const void* x, int64_t head_stride, int64_t row_stride, double* pooled, int32_t heads, int32_t d,
+            const da_grid* grid, int32_t mode, void* stream) {
+  if (!grid_ok(grid)) return fail(DA_EINVAL, "all grid dimensions must be positive");
+  if (!x || !pooled || heads < 1 || d < 8 || d % 8 || d > 2048) return fail(DA_EINVAL, "pool: need d %% 8 == 0");
+  if (mode != 0 && mode != 1) return fail(DA_EINVAL, "pool mode must be 0 (average) or 1 (max)");
+  if (mode == 1 && (grid->height % grid->patch_h || grid->width % grid->patch_w))
+    return fail(DA_EINVAL, "padded grids support average pooling only");
+  if (head_stride % 8 || row_stride % 8 || (reinterpret_cast<uintptr_t>(x) & 15))
+    return fail(DA_EINVAL, "pool: 16-byte aligned rows required");
+  da::Geo g = da::make_geo(*grid);
+  return cuda_status(da::launch_pool(x, head_stride, row_stride, pooled, heads, d, mode, g, (cudaStream_t)stream),
+                     "pool");
+}
+
+int da_draft_scores(const double* qp, const double* kp, double* scores, int32_t heads, int32_t g, int32_t d,
+                    double scale, int32_t softmax, void* stream) {
+  if (!qp || !kp || !scores || heads < 1 || g < 1 || d < 1) return fail(DA_EINVAL, "draft_scores: bad arguments");
+  return cuda_status(da::launch_draft_scores(qp, kp, scores, heads, g, d, scale, softmax, (cudaStream_t)stream),
+                     "draft_scores");
+}
+
+size_t da_select_workspace_size(int32_t heads, int32_t g) {
+  if (heads < 1 || g < 1) return 0;
+  return da::select_workspace_size(heads, g);
+}
+
+int da_select(const double* scores, int32_t heads, int32_t g, int64_t m, int32_t force_row_keep,
+              const uint8_t* dead_cols, void* workspace, int32_t* row_ptr, int32_t* col_idx, uint8_t* bitmap,
+              double* threshold, int64_t* forced, int64_t* kept, void* stream) {
+  if (!scores || !workspace || !row_ptr || !col_idx || !threshold || !forced || !kept)
+    return fail(DA_EINVAL, "select: null buffer");
+  if (heads < 1 || g < 1 || (int64_t)g * g > 0x7fffffffLL) return fail(DA_EINVAL, "select: bad g");
+  if (m < 1 || m > (int64_t)g * g) return fail(DA_EINVAL, "select: m must be in [1, g*g]");
+  return cuda_status(da::launch_select(scores, heads, g, m, force_row_keep, dead_cols, workspace, row_ptr, col_idx,
+                                       bitmap, threshold, forced, kept, da_mask_capacity(g, m),
+                                       (cudaStream_t)stream),
+                     "select");
+}
+
+static int check_attn(const da_attn_args* a, const da_grid* grid) {
+  if (!a || !grid_ok(grid)) return fail(DA_EINVAL, "block_sparse_fwd: bad arguments");
+  if (!a->q || !a->k || !a->v || !a->out || !a->row_ptr || !a->col_idx)
+    return fail(DA_EINVAL, "block_sparse_fwd: null buffer");
+  if (a->heads < 1 || a->d < 1 || a->dv < 1) return fail(DA_EINVAL, "block_sparse_fwd: bad sizes");
+  if (a->layout != DA_LAYOUT_REORDERED && a->layout != DA_LAYOUT_ORIGINAL)
+    return fail(DA_EINVAL, "block_sparse_fwd: unknown layout");
+  if (a->layout == DA_LAYOUT_ORIGINAL && a->key_valid)
+    return fail(DA_EINVAL, "block_sparse_fwd: key_valid requires the reordered layout");
+  return DA_OK;
+}
+
+int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* stream) {
+  int rc = check_attn(args, grid);
+  if (rc) return rc;
+  da::Geo g = da::make_geo(*grid);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!args->force_portable && da::tc_supported(*args, g)) {
+    const char* why = "";
+    cudaError_t e = da::launch_tc_attn(*args, g, st, &why);
+    if (e == cudaErrorInvalidValue && why[0]) return fail(DA_ECUDA, "block_sparse_fwd (tcgen05): %s", why);
+    return cuda_status(e, "block_sparse_fwd (tcgen05)");
+  }
+  if (da::portable_smem_bytes(g.p, args->d, args->dv) > 227 * 1024)
+    return fail(DA_EINVAL, "block_sparse_fwd: region size %d with d=%d, dv=%d exceeds the portable kernel's "
+                           "shared-memory tile", g.p, args->d, args->dv);
+  return cuda_status(da::launch_portable_attn(*args, g, st), "block_sparse_fwd (portable)");
+}
+
+// ---------------------------------------------------------------------------
+// whole pipeline
+// ---------------------------------------------------------------------------
+struct PipeWs {
+  double* qp;
+  double* kp;
+  double* scores;
+  void* sel;
+  size_t total;
+};
+
+static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
+  PipeWs w;
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = p ? p + off : nullptr; off += align256(bytes); return r; };
+  w.qp = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * d));
+  w.kp = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * d));
+  w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * g.g));
+  w.sel = take(da::select_workspace_size(heads, g.g));
+  w.total = off;
+  return w;
+}
+
+__global__ void head_mean_kernel(const double* __restrict__ scores, double* __restrict__ out, int heads,
+                                 long long n) {
+  // basis_sum = basis_0 + basis_1 + ... (left fold), then / heads (sparse.py:296-297)
+  long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = scores[e];
+  for (int h = 1; h < heads; ++h) s = s + scores[(long long)h * n + e];
+  out[e] = s / (double)heads;
+}
+
+size_t da_pipeline_workspace_size(const da_grid* grid, int32_t heads, int32_t d) {
+  if (!grid_ok(grid) || heads < 1 || d < 1) return 0;
+  da::Geo g = da::make_geo(*grid);
+  // + one extra g x g buffer for the shared-head mean
+  return carve(nullptr, g, heads, d).total + align256(sizeof(double) * (size_t)g.g * g.g);
+}
+
+int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
+  // pool x2, draft GEMM (+ row softmax), [head mean], selection (init, 6 x
+  // (histogram + scan), tie counts, tie scan, mark, row scan, collect, finish),
+  // attention
+  return 2 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + (1 + 12 + 1 + 1 + 1 + 1 + 1 + 1) + 1;
+}
+
+int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
+  if (!pa || !grid_ok(grid)) return fail(DA_EINVAL, "sparse_attention: bad arguments");
+  const da_attn_args& a = pa->attn;
+  if (a.layout != DA_LAYOUT_ORIGINAL) return fail(DA_EINVAL, "sparse_attention: inputs must be in original order");
+  if (!pa->workspace || !pa->row_ptr || !pa->col_idx || !pa->threshold || !pa->forced || !pa->kept)
+    return fail(DA_EINVAL, "sparse_attention: null buffer");
+  const bool divisible = grid->height % grid->patch_h == 0 && grid->width % grid->patch_w == 0;
+  if (pa->pool_mode == 1 && !divisible) return fail(DA_EINVAL, "padded grids support average pooling only");
+  da::Geo g = da::make_geo(*grid);
+  if (pa->m < 1 || pa->m > (int64_t)g.g * g.g) return fail(DA_EINVAL, "sparse_attention: m out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  PipeWs w = carve(pa->workspace, g, a.heads, a.d);
+  int rc;
+  if ((rc = da_pool(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.heads, a.d, grid, pa->pool_mode, stream))) return rc;
+  if ((rc = da_pool(a.k, a.k_head_stride, a.k_row_stride, w.kp, a.heads, a.d, grid, pa->pool_mode, stream))) return rc;
+  if ((rc = da_draft_scores(w.qp, w.kp, w.scores, a.heads, g.g, a.d, a.scale, pa->select_softmax, stream))) return rc;
+  const double* sel_scores = w.scores;
+  int sel_heads = a.heads;
+  if (pa->shared_head_mask) {
+    double* mean = reinterpret_cast<double*>(static_cast<char*>(pa->workspace) + w.total);
+    long long n = (long long)g.g * g.g;
+    head_mean_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.scores, mean, a.heads, n);
+    if ((rc = cuda_status(cudaGetLastError(), "head_mean"))) return rc;
+    sel_scores = mean;
+    sel_heads = 1;
+  }
+  // a padded grid never has an all-padding region (the last patch of each axis
+  // starts inside the real extent), so no dead columns (padding.py:151-153)
+  if ((rc = da_select(sel_scores, sel_heads, g.g, pa->m, pa->force_row_keep, nullptr, w.sel, pa->row_ptr,
+                      pa->col_idx, pa->bitmap, pa->threshold, pa->forced, pa->kept, stream)))
+    return rc;
+  da_attn_args aa = a;
+  aa.row_ptr = pa->row_ptr;
+  aa.col_idx = pa->col_idx;
+  aa.mask_cap = da_mask_capacity(g.g, pa->m);
+  aa.key_valid = nullptr;
+  aa.shared_mask = pa->shared_head_mask ? 1 : 0;
+  if (pa->ev_attn_begin) cudaEventRecord((cudaEvent_t)pa->ev_attn_begin, st);
+  rc = da_block_sparse_fwd(&aa, grid, stream);
+  if (pa->ev_attn_end) cudaEventRecord((cudaEvent_t)pa->ev_attn_end, st);
+  return rc;
+}
+
+}  // extern "C"

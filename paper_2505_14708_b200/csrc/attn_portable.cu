@@ -1,0 +1,172 @@
+// Portable block-sparse attention forward (CUDA cores, fp32 math) for region
+// sizes / head dims the tcgen05 kernel does not cover (e.g. the tiny config:
+// 4x4 pool, d=64). Same semantics as the reference executor
+// (sparse.py:88-166): per query region, kept key regions in ascending order,
+// streaming softmax over valid keys, fully dropped rows -> 0.
+//
+// grid: (g, heads); block 256. Shared memory: Q, K, V tiles (fp32), the p x p
+// score tile, the fp32 output accumulator and per-row m / l.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace da {
+
+struct PortableArgs {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  __nv_bfloat16* out;
+  long long qh, qr, kh, kr, vh, vr, oh, orow;
+  int d, dv, layout;
+  float scale;
+  const int* row_ptr;
+  const int* col_idx;
+  long long cap;
+  const uint8_t* key_valid;
+  int mask_h;  // 1 = per-head masks, 0 = head 0's mask for all heads
+  Geo geo;
+};
+
+// row of token (region, offset) in the caller's tensor; -1 = not stored
+DA_DEV long long token_row(const PortableArgs& a, int region, int r) {
+  if (a.layout == DA_LAYOUT_REORDERED) return (long long)region * a.geo.p + r;
+  return real_row(a.geo, region, r);
+}
+
+DA_DEV bool key_ok(const PortableArgs& a, int region, int r) {
+  if (a.key_valid != nullptr) return a.key_valid[(long long)region * a.geo.p + r] != 0;
+  return key_is_valid(a.geo, region, r);
+}
+
+__global__ void __launch_bounds__(256) portable_attn_kernel(PortableArgs a) {
+  extern __shared__ float sm[];
+  const int p = a.geo.p, d = a.d, dv = a.dv;
+  float* Qs = sm;                 // p*d
+  float* Ks = Qs + p * d;         // p*d
+  float* Vs = Ks + p * d;         // p*dv
+  float* S = Vs + p * dv;         // p*p
+  float* O = S + p * p;           // p*dv
+  float* M = O + p * dv;          // p
+  float* L = M + p;               // p
+  float* alpha = L + p;           // p
+  int* kval = reinterpret_cast<int*>(alpha + p);  // p
+
+  const int i = blockIdx.x, h = blockIdx.y;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int g = a.geo.g;
+  const int* rp = a.row_ptr + (long long)(h * a.mask_h) * (g + 1);
+  const int beg = rp[i], end = rp[i + 1];
+  const int* cols = a.col_idx + (long long)(h * a.mask_h) * a.cap;
+
+  for (int e = tid; e < p * d; e += nt) {
+    int r = e / d, c = e - r * d;
+    long long row = token_row(a, i, r);
+    Qs[e] = row >= 0 ? __bfloat162float(a.q[h * a.qh + row * a.qr + c]) : 0.f;
+  }
+  for (int e = tid; e < p * dv; e += nt) O[e] = 0.f;
+  for (int r = tid; r < p; r += nt) { M[r] = -INFINITY; L[r] = 0.f; }
+  __syncthreads();
+
+  for (int t = beg; t < end; ++t) {
+    const int j = cols[t];
+    for (int e = tid; e < p * d; e += nt) {
+      int r = e / d, c = e - r * d;
+      long long row = token_row(a, j, r);
+      Ks[e] = row >= 0 ? __bfloat162float(a.k[h * a.kh + row * a.kr + c]) : 0.f;
+    }
+    for (int e = tid; e < p * dv; e += nt) {
+      int r = e / dv, c = e - r * dv;
+      long long row = token_row(a, j, r);
+      Vs[e] = row >= 0 ? __bfloat162float(a.v[h * a.vh + row * a.vr + c]) : 0.f;
+    }
+    for (int r = tid; r < p; r += nt) kval[r] = key_ok(a, j, r);
+    __syncthreads();
+    for (int e = tid; e < p * p; e += nt) {
+      int r = e / p, c = e - r * p;
+      float s = -INFINITY;
+      if (kval[c]) {
+        float acc = 0.f;
+        for (int kk = 0; kk < d; ++kk) acc = fmaf(Qs[r * d + kk], Ks[c * d + kk], acc);
+        s = acc * a.scale;
+      }
+      S[e] = s;
+    }
+    __syncthreads();
+    // per-row online softmax update, one warp per row
+    const int lane = tid % 32, w = tid / 32, nw = nt / 32;
+    for (int r = w; r < p; r += nw) {
+      float mx = -INFINITY;
+      for (int c = lane; c < p; c += 32) mx = fmaxf(mx, S[r * p + c]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float mold = M[r];
+      float mnew = fmaxf(mold, mx);
+      float sum = 0.f;
+      if (mnew == -INFINITY) {  // block entirely invalid for this row: skip
+        for (int c = lane; c < p; c += 32) S[r * p + c] = 0.f;
+      } else {
+        for (int c = lane; c < p; c += 32) {
+          float s = S[r * p + c];
+          float pr = s == -INFINITY ? 0.f : expf(s - mnew);
+          S[r * p + c] = pr;
+          sum += pr;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        float al = (mold == -INFINITY) ? 0.f : expf(mold - mnew);
+        if (mnew == -INFINITY) al = 1.f;
+        alpha[r] = al;
+        L[r] = L[r] * al + sum;
+        M[r] = mnew;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < p * dv; e += nt) {
+      int r = e / dv, c = e - r * dv;
+      float acc = O[e] * alpha[r];
+      for (int kk = 0; kk < p; ++kk) acc = fmaf(S[r * p + kk], Vs[kk * dv + c], acc);
+      O[e] = acc;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < p * dv; e += nt) {
+    int r = e / dv, c = e - r * dv;
+    long long row = token_row(a, i, r);
+    if (row < 0) continue;
+    float l = L[r];
+    float o = l > 0.f ? O[e] / l : 0.f;
+    a.out[h * a.oh + row * a.orow + c] = __float2bfloat16_rn(o);
+  }
+}
+
+size_t portable_smem_bytes(int p, int d, int dv) {
+  return sizeof(float) * ((size_t)p * d * 2 + (size_t)p * dv * 2 + (size_t)p * p + 3 * (size_t)p) + sizeof(int) * p;
+}
+
+cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st) {
+  PortableArgs a;
+  a.q = static_cast<const __nv_bfloat16*>(args.q);
+  a.k = static_cast<const __nv_bfloat16*>(args.k);
+  a.v = static_cast<const __nv_bfloat16*>(args.v);
+  a.out = static_cast<__nv_bfloat16*>(args.out);
+  a.qh = args.q_head_stride; a.qr = args.q_row_stride;
+  a.kh = args.k_head_stride; a.kr = args.k_row_stride;
+  a.vh = args.v_head_stride; a.vr = args.v_row_stride;
+  a.oh = args.o_head_stride; a.orow = args.o_row_stride;
+  a.d = args.d; a.dv = args.dv; a.layout = args.layout;
+  a.scale = (float)args.scale;
+  a.row_ptr = args.row_ptr; a.col_idx = args.col_idx; a.cap = args.mask_cap;
+  a.key_valid = args.key_valid;
+  a.mask_h = args.shared_mask ? 0 : 1;
+  a.geo = geo;
+  size_t smem = portable_smem_bytes(geo.p, args.d, args.dv);
+  cudaError_t e = cudaFuncSetAttribute(portable_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(geo.g, args.heads);
+  portable_attn_kernel<<<grid, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace da

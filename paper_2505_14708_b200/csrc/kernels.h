@@ -1,0 +1,34 @@
+// Internal launcher declarations (host side) shared by the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/draftattn_b200.h"
+
+namespace da {
+
+struct Geo;
+
+cudaError_t launch_permute_in(const void* x, long long hs, long long rs, void* x_r, int heads, int d, const Geo& g,
+                              cudaStream_t st);
+cudaError_t launch_permute_out(const void* o_r, void* out, long long hs, long long rs, int heads, int d,
+                               const Geo& g, cudaStream_t st);
+cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
+                        const Geo& g, cudaStream_t st);
+cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
+                                double scale, int softmax, cudaStream_t st);
+
+size_t select_workspace_size(int heads, int g);
+long long bitmap_bytes_per_head(int g);
+cudaError_t launch_select(const double* scores, int heads, int g, long long m, int force, const uint8_t* dead,
+                          void* ws, int* row_ptr, int* col_idx, uint8_t* bitmap, double* threshold,
+                          int64_t* forced, int64_t* kept, long long cap, cudaStream_t st);
+
+size_t portable_smem_bytes(int p, int d, int dv);
+cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st);
+
+bool tc_supported(const da_attn_args& a, const Geo& g);
+cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why);
+
+}  // namespace da

@@ -1,0 +1,377 @@
+"""GPU parity: every stage of the CUDA path against the CPU oracle and the
+reference's golden fixtures, through the C ABI.
+
+Bars (north_star): permutation and pooling bit-exact; selected block set,
+forced count and kept count identical (threshold equal to fp64 roundoff);
+attention output within bf16 tolerance  max-abs <= 1e-2  and  cosine >= 0.9999
+against the float64 oracle on the same bf16 inputs.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import draftattn_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = Path(__file__).resolve().parent / "golden"
+MAX_ABS = 1e-2
+MIN_COS = 0.9999
+
+da = None
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _module():
+    global da
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2505_14708_b200.build import build
+
+    build()
+    import paper_2505_14708_b200 as mod
+
+    da = mod
+
+
+def _npz(name):
+    return np.load(GOLD / f"{name}.npz")
+
+
+def _inputs(dims, head_ids=None):
+    f, h, w, ph, pw, d, heads, seed = (int(x) for x in dims)
+    grid = O.Grid(f, h, w, ph, pw)
+    q, k, v = O.gen_real_inputs(grid, d, seed, heads, head_ids=head_ids)
+    tq, tk, tv = (torch.from_numpy(x).to("cuda").to(torch.bfloat16) for x in (q, k, v))
+    f64 = lambda t: t.double().cpu().numpy()  # noqa: E731
+    return grid, (tq, tk, tv), (f64(tq), f64(tk), f64(tv))
+
+
+def _close(out, ref, max_abs=MAX_ABS, min_cos=MIN_COS):
+    out = np.asarray(out, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    err = np.abs(out - ref).max() if out.size else 0.0
+    cos = float((out * ref).sum() / (np.linalg.norm(out) * np.linalg.norm(ref) + 1e-300))
+    assert err <= max_abs, f"max-abs {err:.3e} > {max_abs}"
+    assert cos >= min_cos, f"cosine {cos:.8f} < {min_cos}"
+    return err, cos
+
+
+# ---------------------------------------------------------------- K1 / K5
+
+@pytest.mark.parametrize("dims", [(4, 16, 16, 4, 4, 64), (2, 13, 10, 4, 4, 32), (1, 8, 11, 4, 4, 16),
+                                  (3, 45, 80, 8, 8, 128), (2, 7, 3, 2, 2, 8)])
+def test_permutation_bit_exact(dims):
+    f, h, w, ph, pw, d = dims
+    grid = O.Grid(f, h, w, ph, pw)
+    plan = da.pad_plan(f, h, w, ph, pw)
+    x = torch.randn(3, grid.n_real, d, device="cuda").to(torch.bfloat16)
+    xr = da.reorder_tokens(x, plan)
+    xs = x.view(torch.int16).cpu().numpy()
+    ref = np.stack([O.permute_in(xs[hh], grid) for hh in range(3)])
+    assert np.array_equal(xr.view(torch.int16).cpu().numpy(), ref)
+    back = da.restore_tokens(xr, plan)
+    assert torch.equal(back.view(torch.int16), x.view(torch.int16))
+
+
+def test_permutation_bit_exact_hv720_full():
+    grid = O.Grid(33, 45, 80, 8, 8)
+    plan = da.pad_plan(33, 45, 80, 8, 8)
+    x = torch.randn(24, grid.n_real, 128, device="cuda").to(torch.bfloat16)
+    xr = da.reorder_tokens(x, plan)
+    xs = x.view(torch.int16)
+    src = torch.from_numpy(O.real_source_index(grid)).cuda()
+    live = src >= 0
+    ref = torch.zeros(24, grid.n_pad, 128, dtype=torch.int16, device="cuda")
+    ref[:, live] = xs[:, src[live]]
+    assert torch.equal(xr.view(torch.int16), ref)
+    assert torch.equal(da.restore_tokens(xr, plan).view(torch.int16), xs)
+
+
+def test_permutation_nhd_layout():
+    grid = O.Grid(2, 45, 80, 8, 8)
+    plan = da.pad_plan(2, 45, 80, 8, 8)
+    x = torch.randn(grid.n_real, 4, 128, device="cuda").to(torch.bfloat16)  # (n, heads, d)
+    xr = da.reorder_tokens(x, plan, qkv_layout="nhd")
+    ref = da.reorder_tokens(x.transpose(0, 1).contiguous(), plan)
+    assert torch.equal(xr, ref)
+
+
+# ---------------------------------------------------------------- K2
+
+@pytest.mark.parametrize("dims,mode", [((4, 16, 16, 4, 4, 64), "average"), ((4, 16, 16, 4, 4, 64), "max"),
+                                       ((2, 13, 10, 4, 4, 32), "average"), ((3, 45, 80, 8, 8, 128), "average"),
+                                       ((2, 8, 16, 8, 16, 64), "average")])
+def test_pooling_bit_exact(dims, mode):
+    f, h, w, ph, pw, d = dims
+    grid = O.Grid(f, h, w, ph, pw)
+    plan = da.pad_plan(f, h, w, ph, pw)
+    x = torch.randn(2, grid.n_real, d, device="cuda").to(torch.bfloat16)
+    got = da.pool_tokens(x, plan, mode).cpu().numpy()
+    x64 = x.double().cpu().numpy()
+    for hh in range(2):
+        xr = O.permute_in(x64[hh], grid)
+        if grid.divisible:
+            ref = O.pool_regions(xr, grid.region_size, mode)
+        else:
+            ref = O.pool_valid(xr, O.valid_reordered(grid), grid.region_size)
+        assert np.array_equal(got[hh], ref)
+
+
+def test_pool_regions_seam_matches_reference_fixture():
+    z = _npz("pooling")
+    x = torch.from_numpy(z["x"]).to(torch.bfloat16).cuda()
+    assert np.array_equal(da.pool_regions(x, 16, "average").cpu().numpy(), z["pool_avg"])
+    assert np.array_equal(da.pool_regions(x, 16, "max").cpu().numpy(), z["pool_max"])
+
+
+# ---------------------------------------------------------------- K3
+
+def test_draft_logits_float64():
+    rng = np.random.default_rng(0)
+    qp = rng.standard_normal((3, 100, 128))
+    kp = rng.standard_normal((3, 100, 128))
+    got = da.draft_logits(torch.from_numpy(qp).cuda(), torch.from_numpy(kp).cuda()).cpu().numpy()
+    for hh in range(3):
+        ref = O.draft_logits(qp[hh], kp[hh], O.head_dim_scale(128))
+        np.testing.assert_allclose(got[hh], ref, rtol=1e-13, atol=1e-14)
+    sm = da.draft_logits(torch.from_numpy(qp).cuda(), torch.from_numpy(kp).cuda(), softmax=True).cpu().numpy()
+    np.testing.assert_allclose(sm[0], O.softmax_rows(O.draft_logits(qp[0], kp[0], O.head_dim_scale(128))),
+                               rtol=1e-12, atol=1e-15)
+
+
+def test_selection_matches_reference_fixtures_bit_exact():
+    z = _npz("selection")
+    for c in range(int(z["count"])):
+        r, force, thr, forced, kept = z[f"c{c}_meta"]
+        scores = torch.from_numpy(z[f"c{c}_scores"]).cuda()
+        m = da.select_top_fraction(scores, float(r), bool(force))
+        assert m.bitmap_bytes() == z[f"c{c}_bitmap"].tobytes(), f"case {c}"
+        assert m.threshold == thr and m.forced_row_keeps == forced and m.kept_count == kept
+        rows = m.row_kept_counts.cpu().numpy()
+        kept_np = m.kept.cpu().numpy()
+        assert np.array_equal(rows, kept_np.sum(axis=1))
+        cols = m.col_idx[0].cpu().numpy()
+        rp = m.row_ptr[0].cpu().numpy()
+        for i in range(m.g):
+            assert np.array_equal(cols[rp[i]:rp[i + 1]], np.flatnonzero(kept_np[i]))
+
+
+def test_selection_edge_cases():
+    # hand cases (test_masking.py:59-64, :77-81, :95-103) + negative zero + large ties
+    m = da.select_top_fraction(torch.tensor([[9.0, 1.0], [5.0, 7.0]], device="cuda"), 0.5)
+    assert m.kept.cpu().tolist() == [[True, False], [False, True]] and m.threshold == 7.0
+    m = da.select_top_fraction(torch.zeros(3, 3, device="cuda", dtype=torch.float64), 4 / 9)
+    assert m.kept.reshape(-1).cpu().tolist() == [True] * 4 + [False] * 5
+    s = torch.full((4, 4), -10.0, dtype=torch.float64)
+    s[0] = torch.tensor([4.0, 3.0, 2.0, 1.0])
+    m = da.select_top_fraction(s.cuda(), 0.25, force_row_keep=True)
+    assert m.forced_row_keeps == 3
+    z = np.zeros((5, 5))
+    z[1, 2] = -0.0
+    z[0, 0] = -0.0
+    ref = O.select_top_fraction(z, 0.3, True)
+    m = da.select_top_fraction(torch.from_numpy(z).cuda(), 0.3, True)
+    assert m.bitmap_bytes() == O.mask_bitmap(ref.kept)
+    big = np.round(np.random.default_rng(5).standard_normal((300, 300)))  # heavy ties, g^2 = 90000
+    for r in (0.1, 0.37, 0.9):
+        for force in (False, True):
+            ref = O.select_top_fraction(big, r, force)
+            m = da.select_top_fraction(torch.from_numpy(big).cuda(), r, force)
+            assert m.bitmap_bytes() == O.mask_bitmap(ref.kept)
+            assert m.threshold == ref.threshold and m.forced_row_keeps == ref.forced_row_keeps
+
+
+def test_selection_dead_columns():
+    s = np.random.default_rng(3).standard_normal((20, 20))
+    ref = O.drop_key_regions(O.select_top_fraction(s, 0.3, True), [3, 7])
+    m = da.select_top_fraction(torch.from_numpy(s).cuda(), 0.3, True, dead_columns=[3, 7])
+    assert m.bitmap_bytes() == O.mask_bitmap(ref.kept)
+    assert m.kept_count == ref.kept_count and m.forced_row_keeps == ref.forced_row_keeps
+
+
+# ---------------------------------------------------------------- pipelines vs reference fixtures
+
+def _check_mask(mask, h, z, key):
+    got = mask.head(h) if not mask.single else mask
+    assert got.bitmap_bytes() == z[f"{key}_bitmap"].tobytes()
+    thr, forced, kept = z[f"{key}_meta"]
+    assert got.forced_row_keeps == forced and got.kept_count == kept
+    assert abs(got.threshold - thr) <= 1e-12 * max(1.0, abs(thr))
+
+
+@pytest.mark.parametrize("name", ["tiny", "ragged_small", "ragged_w"])
+def test_pipeline_full_output_vs_reference(name):
+    z = _npz(name)
+    grid, (q, k, v), _ = _inputs(z["dims"])
+    heads = q.shape[0]
+    res = da.multi_head_sparse_attention(q, k, v, da.pad_plan(grid.frames, grid.height, grid.width,
+                                                              grid.patch_h, grid.patch_w),
+                                         float(z["sparsity"]), return_details=True)
+    out = res.output.float().cpu().numpy()
+    for h in range(heads):
+        _check_mask(res.mask, h, z, f"h{h}")
+        _close(out[h], z[f"h{h}_out"])
+    # the single-head reference-signature entry gives the same result
+    one = da.padded_sparse_attention(q[0], k[0], v[0], grid.frames, grid.height, grid.width,
+                                     grid.patch_h, grid.patch_w, float(z["sparsity"]))
+    assert torch.equal(one, res.output[0])
+
+
+@pytest.mark.parametrize("name,head_ids", [("hv720_f2", None), ("hv720", [0, 1])])
+def test_pipeline_720p_masks_and_sampled_rows(name, head_ids):
+    z = _npz(name)
+    grid, (q, k, v), _ = _inputs(z["dims"], head_ids)
+    plan = da.pad_plan(grid.frames, grid.height, grid.width, grid.patch_h, grid.patch_w)
+    res = da.multi_head_sparse_attention(q, k, v, plan, float(z["sparsity"]), return_details=True)
+    ids = head_ids or list(range(q.shape[0]))
+    src = O.real_source_index(grid)
+    out = res.output.float().cpu().numpy()
+    for slot, h in enumerate(ids):
+        _check_mask(res.mask, slot, z, f"h{h}")
+        rows = z[f"h{h}_rows"]
+        pos = (rows[:, None] * grid.region_size + np.arange(grid.region_size)[None, :]).reshape(-1)
+        live = src[pos] >= 0
+        _close(out[slot][src[pos][live]], z[f"h{h}_out_rows"][live])
+
+
+def test_hv720_all_heads_masks_vs_oracle():
+    grid, (q, k, v), (q64, k64, v64) = _inputs((33, 45, 80, 8, 8, 128, 24, 0), head_ids=[2, 3, 11, 23])
+    plan = da.pad_plan(33, 45, 80, 8, 8)
+    res = da.multi_head_sparse_attention(q, k, v, plan, 0.9, return_details=True)
+    for slot in range(4):
+        ref, _ = O.draft_mask(q64[slot], k64[slot], grid, 0.9)
+        got = res.mask.head(slot)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.kept)
+        assert got.kept_count == ref.kept_count and got.forced_row_keeps == ref.forced_row_keeps
+    # sampled output rows of one head against the float64 oracle
+    rows = np.array([3, 500, 1979])
+    ref, _ = O.draft_mask(q64[0], k64[0], grid, 0.9)
+    out_r = O.block_sparse_attention(O.permute_in(q64[0], grid), O.permute_in(k64[0], grid),
+                                     O.permute_in(v64[0], grid), ref.kept, O.head_dim_scale(128),
+                                     key_valid=O.valid_reordered(grid), rows=rows)
+    pos = (rows[:, None] * 64 + np.arange(64)[None, :]).reshape(-1)
+    src = O.real_source_index(grid)[pos]
+    live = src >= 0
+    _close(res.output[0].float().cpu().numpy()[src[live]], out_r[pos][live])
+
+
+@pytest.mark.parametrize("sparsity", [0.5, 0.75, 0.95])
+def test_hv720_sparsity_sweep_masks(sparsity):
+    grid, (q, k, v), (q64, k64, _) = _inputs((33, 45, 80, 8, 8, 128, 24, 0), head_ids=[0])
+    res = da.padded_sparse_attention(q[0], k[0], v[0], 33, 45, 80, 8, 8, sparsity, return_details=True)
+    ref, _ = O.draft_mask(q64[0], k64[0], grid, sparsity)
+    assert res.mask.bitmap_bytes() == O.mask_bitmap(ref.kept)
+    assert res.mask.kept_count == ref.kept_count
+    assert res.flops.sparse_logits_flops == 2 * ref.kept_count * 64 * 64 * 128
+
+
+# ---------------------------------------------------------------- executor seams and edge cases
+
+def _seam_case(g, p, d, heads, density, seed, key_valid=False):
+    rng = np.random.default_rng(seed)
+    n = g * p
+    q = torch.from_numpy(rng.standard_normal((heads, n, d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    k = torch.from_numpy(rng.standard_normal((heads, n, d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    v = torch.from_numpy(rng.standard_normal((heads, n, d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    scores = rng.standard_normal((heads, g, g))
+    kv = None
+    if key_valid:
+        kv = rng.random(n) < 0.7
+        kv[p:2 * p] = False  # one key block fully invalid
+    return q, k, v, scores, kv
+
+
+@pytest.mark.parametrize("g,p,d,force_portable", [(40, 64, 128, False), (40, 64, 128, True), (30, 16, 64, False),
+                                                   (20, 128, 64, False), (25, 64, 128, False)])
+def test_block_sparse_seam_vs_oracle(g, p, d, force_portable):
+    q, k, v, scores, _ = _seam_case(g, p, d, 2, 0.3, g + p + d)
+    mask = da.select_top_fraction(torch.from_numpy(scores).cuda(), 0.3, True)
+    out = da.block_sparse_attention(q, k, v, mask, force_portable=force_portable).float().cpu().numpy()
+    q64, k64, v64 = (t.double().cpu().numpy() for t in (q, k, v))
+    kept = mask.kept.cpu().numpy()
+    for h in range(2):
+        ref = O.block_sparse_attention(q64[h], k64[h], v64[h], kept[h], O.head_dim_scale(d))
+        _close(out[h], ref)
+
+
+def test_block_sparse_key_valid_and_dropped_rows():
+    g, p, d = 24, 64, 128
+    q, k, v, scores, kv = _seam_case(g, p, d, 1, 0.3, 9, key_valid=True)
+    scores[0, 5, :] = -1e9  # row 5 never selected ...
+    mask = da.select_top_fraction(torch.from_numpy(scores).cuda(), 0.3, False)  # ... and not forced
+    out = da.block_sparse_attention(q, k, v, mask, key_valid=torch.from_numpy(kv)).float().cpu().numpy()
+    q64, k64, v64 = (t.double().cpu().numpy() for t in (q, k, v))
+    ref = O.block_sparse_attention(q64[0], k64[0], v64[0], mask.kept.cpu().numpy()[0], O.head_dim_scale(d),
+                                   key_valid=kv)
+    assert np.all(out[0][5 * p:6 * p] == 0.0)
+    _close(out[0], ref)
+
+
+def test_tcgen05_matches_portable_kernel():
+    q, k, v, scores, _ = _seam_case(48, 64, 128, 3, 0.2, 17)
+    mask = da.select_top_fraction(torch.from_numpy(scores).cuda(), 0.2, True)
+    a = da.block_sparse_attention(q, k, v, mask).float()
+    b = da.block_sparse_attention(q, k, v, mask, force_portable=True).float()
+    assert (a - b).abs().max().item() <= 4e-3
+
+
+def test_extreme_logits_stay_finite():
+    # test_sparse.py:204-211: huge logits must not overflow (rescale path)
+    q, k, v, scores, _ = _seam_case(16, 64, 128, 1, 0.5, 21)
+    q = (q.float() * 40).to(torch.bfloat16)
+    mask = da.select_top_fraction(torch.from_numpy(scores).cuda(), 0.5, True)
+    out = da.block_sparse_attention(q, k, v, mask).float()
+    assert torch.isfinite(out).all()
+    q64, k64, v64 = (t.double().cpu().numpy() for t in (q, k, v))
+    ref = O.block_sparse_attention(q64[0], k64[0], v64[0], mask.kept.cpu().numpy()[0], O.head_dim_scale(128))
+    _close(out.cpu().numpy()[0], ref, max_abs=3e-2, min_cos=0.999)
+
+
+def test_zero_sparsity_equals_dense():
+    # test_sparse.py:241-247 / test_padding.py:138-145 on a ragged grid
+    grid = O.Grid(2, 13, 16, 8, 8)
+    plan = da.pad_plan(2, 13, 16, 8, 8)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q, k, v = (torch.randn(2, grid.n_real, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    out = da.multi_head_sparse_attention(q, k, v, plan, 0.0).float()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float())
+    _close(out.cpu().numpy(), ref.cpu().numpy())
+
+
+def test_shared_head_mask_and_softmax_selection():
+    z = (4, 16, 16, 4, 4, 64, 3, 7)
+    grid, (q, k, v), (q64, k64, v64) = _inputs(z)
+    lay = da.LatentLayout(4, 16, 16, 4, 4)
+    out = da.multi_head_sparse_attention(q, k, v, lay, 0.6, shared_head_mask=True).float().cpu().numpy()
+    ref = O.multi_head_sparse_attention(q64, k64, v64, 4, 16, 16, 4, 4, 0.6, shared_head_mask=True)
+    _close(out, ref)
+    out = da.multi_head_sparse_attention(q, k, v, lay, 0.6, select_on="softmax").float().cpu().numpy()
+    ref = O.multi_head_sparse_attention(q64, k64, v64, 4, 16, 16, 4, 4, 0.6, select_on="softmax")
+    _close(out, ref)
+    out = da.multi_head_sparse_attention(q, k, v, lay, 0.6, pool_mode="max").float().cpu().numpy()
+    ref = O.multi_head_sparse_attention(q64, k64, v64, 4, 16, 16, 4, 4, 0.6, pool_mode="max")
+    _close(out, ref)
+
+
+def test_nhd_layout_and_dtype_roundtrip():
+    grid, (q, k, v), _ = _inputs((2, 45, 80, 8, 8, 128, 3, 4))
+    plan = da.pad_plan(2, 45, 80, 8, 8)
+    ref = da.multi_head_sparse_attention(q, k, v, plan, 0.8)
+    nhd = da.multi_head_sparse_attention(q.transpose(0, 1), k.transpose(0, 1), v.transpose(0, 1), plan, 0.8,
+                                         qkv_layout="nhd")
+    assert nhd.shape == (grid.n_real, 3, 128)
+    assert torch.equal(nhd.transpose(0, 1), ref)
+    f32 = da.multi_head_sparse_attention(q.float(), k.float(), v.float(), plan, 0.8)
+    assert f32.dtype == torch.float32 and torch.equal(f32.to(torch.bfloat16), ref)
+
+
+def test_deterministic():
+    grid, (q, k, v), _ = _inputs((3, 45, 80, 8, 8, 128, 2, 5))
+    plan = da.pad_plan(3, 45, 80, 8, 8)
+    a = da.multi_head_sparse_attention(q, k, v, plan, 0.9)
+    b = da.multi_head_sparse_attention(q, k, v, plan, 0.9)
+    assert torch.equal(a, b)

@@ -1,0 +1,88 @@
+"""Host-side logic of the drop-in API (CPU only): geometry, counts, FLOP model
+and the reference's ValueError contract, raised before any device work."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2505_14708_b200 as da
+from oracle import draftattn_oracle as O
+
+
+def test_layout_validation_matches_reference():
+    # layout.py:25-39
+    with pytest.raises(ValueError, match="positive integer"):
+        da.LatentLayout(0, 4, 4, 2, 2)
+    with pytest.raises(ValueError, match="patch_h=3 does not divide height=4"):
+        da.LatentLayout(1, 4, 4, 3, 2)
+    lay = da.LatentLayout(4, 16, 16, 4, 4)
+    assert (lay.num_tokens, lay.region_size, lay.num_regions) == (1024, 16, 64)
+
+
+def test_pad_plan_geometry():
+    plan = da.pad_plan(33, 45, 80, 8, 8)
+    assert (plan.layout.height, plan.layout.width) == (48, 80)
+    assert plan.num_valid == 118800 and plan.layout.num_tokens == 126720
+    assert not plan.is_identity
+    assert da.pad_plan(2, 4, 8, 2, 4).is_identity
+    with pytest.raises(ValueError, match="positive"):
+        da.pad_plan(0, 4, 4, 2, 2)
+
+
+@pytest.mark.parametrize("n,r", [(100, 0.1), (3920400, 0.1), (3920400, 0.5), (3920400, 0.25),
+                                 (3920400, 0.05), (5715360, 0.25), (4096, 0.5), (9, 0.5), (16, 0.001)])
+def test_top_fraction_count_equals_oracle(n, r):
+    assert da.top_fraction_count(n, r) == O.top_fraction_count(n, r)
+
+
+def test_hv720_keep_counts():
+    # SURVEY 8(a) a8
+    g2 = 1980 ** 2
+    assert [da.top_fraction_count(g2, 1.0 - s) for s in (0.5, 0.75, 0.9, 0.95)] == \
+        [1960200, 980100, 392040, 196020]
+
+
+def test_flops_model_matches_oracle():
+    lay = da.LatentLayout(33, 48, 80, 8, 8)
+    f = da.flops_count(lay, 128, kept_count=392040)
+    ref = O.flops_count(126720, 1980, 64, 128, 392040)
+    assert f.as_dict() == ref
+    assert da.flops_count(lay, 128, sparsity=0.9).sparse_logits_flops == ref["sparse_logits_flops"]
+    with pytest.raises(ValueError, match="sparsity must be in"):
+        da.flops_count(lay, 128, sparsity=1.0)
+
+
+def _cpu_qkv(n=30, d=8):
+    x = torch.zeros(n, d, dtype=torch.bfloat16)
+    return x, x, x
+
+
+def test_pipeline_argument_errors_raise_reference_messages():
+    q, k, v = _cpu_qkv()
+    with pytest.raises(ValueError, match=r"sparsity must be in \[0, 1\)"):
+        da.padded_sparse_attention(q, k, v, 2, 3, 5, 2, 4, 1.0)
+    with pytest.raises(ValueError, match="select_on must be 'logits' or 'softmax'"):
+        da.padded_sparse_attention(q, k, v, 2, 3, 5, 2, 4, 0.5, select_on="bogus")
+    with pytest.raises(ValueError, match="padded grids support average pooling only"):
+        da.padded_sparse_attention(q, k, v, 2, 3, 5, 2, 4, 0.5, pool_mode="max")
+    with pytest.raises(ValueError, match="real-token rows"):
+        da.padded_sparse_attention(q[:29], k[:29], v[:29], 2, 3, 5, 2, 4, 0.5)
+    lay = da.LatentLayout(1, 4, 8, 2, 4)
+    with pytest.raises(ValueError, match="q rows 30 != layout token count 32"):
+        da.draft_sparse_attention(q, k, v, lay, 0.5)
+    with pytest.raises(ValueError, match=r"expected \(heads, n, d\)"):
+        da.multi_head_sparse_attention(q, k, v, lay, 0.5)
+
+
+def test_cpu_tensors_are_rejected_not_computed():
+    # the B200 path has no CPU fallback: valid arguments on CPU tensors raise
+    q = torch.zeros(32, 8, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="CUDA"):
+        da.draft_sparse_attention(q, q, q, da.LatentLayout(1, 4, 8, 2, 4), 0.5)
+
+
+def test_selection_argument_errors():
+    with pytest.raises(ValueError, match="keep_ratio must be in"):
+        da.top_fraction_count(10, 0.0)
+    with pytest.raises(ValueError, match="square"):
+        da.select_top_fraction(torch.zeros(2, 3), 0.5)
