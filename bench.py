@@ -228,6 +228,9 @@ def run_ours(args, cfg, name):
         dist.barrier()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for pair in ev:  # torch creates the CUDA event lazily on first record; the C library records them
+        for e_ in pair:
+            e_.record()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kept_total = None
     with ClockSampler(local) as clocks:
