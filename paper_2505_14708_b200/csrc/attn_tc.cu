@@ -8,48 +8,53 @@
 // of ONE query region and puts the 128 keys on M:
 //     GEMM1  S^T[128 keys x 64 q]  = K_pair[128 x 128d] . Q^T          (K-major A and B)
 //     GEMM2  O^T[128 d  x 64 q]   += V_pair^T[128d x 128 keys] . P^T    (MN-major A and B)
-// S^T and O^T live in TMEM (lane = key / feature, column = query). The
-// softmax warpgroup owns one TMEM lane per thread, i.e. one KEY per thread:
-// masking invalid (padded) keys is a per-thread predicate and P^T rows are
-// written to shared memory as 128-byte swizzled rows. Softmax statistics are
-// per query column: the running max m[q] is kept in shared memory and only
-// recomputed (a cross-lane column reduction, plus an O^T/l rescale) when some
-// score exceeds it by more than TAU (log2 units) — a barrier.red.or vote per
-// step; row sums l[q] are per-thread partials reduced once per region.
+// S^T and O^T live in TMEM (lane = key / feature, column = query). A softmax
+// thread owns one TMEM lane, i.e. one KEY: masking padded keys is a per-thread
+// predicate and P^T rows go to shared memory as 128-byte swizzled rows.
+// Softmax statistics are per query column: the running max m[q] lives in
+// shared memory and is only recomputed (a cross-lane column reduction plus an
+// O^T / l rescale of the affected columns) when a score exceeds it by more
+// than TAU (log2 units) — one barrier.red.or vote per half step; row sums l[q]
+// are per-thread partials reduced once per region.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+ TMEM
-// owner), warps 4..7 = softmax / epilogue warpgroup. Persistent CTAs walk the
-// (head, query region) items round-robin. Key/value blocks are fetched with
-// TMA either from the reordered (heads, n_pad, 128) tensors (2-D maps) or
-// straight from the ORIGINAL (f, y, x)-ordered tensors with 5-D maps whose box
-// is one 8x8 region (out-of-bounds rows of ragged edge regions are zero-filled
-// by TMA), so the patch permutation of padding.py:139-143 costs no extra pass.
-// The epilogue writes rows back in original order (padding.py:157 fused).
+// Roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+ TMEM
+// owner), warps 4-7 and 8-11 = two softmax/epilogue warpgroups. Each CTA walks
+// its (head, query region) items; even items go to warpgroup 0, odd ones to
+// warpgroup 1, and the producer / MMA interleave the two warpgroups step by
+// step so one warpgroup's exponentials overlap the other's matrix products.
+// K/V blocks are fetched by TMA either from reordered (heads, n_pad, 128)
+// tensors (2-D maps) or straight from the ORIGINAL (f, y, x)-ordered tensors
+// with 5-D maps whose box is one 8x8 region (out-of-bounds rows of ragged edge
+// regions are zero-filled), so the patch permutation of padding.py:139-143
+// costs no extra pass; the epilogue writes rows back in original order
+// (padding.py:157 fused).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace da {
 namespace tc {
 
-constexpr int P = 64;           // region size
-constexpr int D = 128;          // head dim
-constexpr int KST = 3;          // K ring stages (one pair of key regions each)
-constexpr int VST = 2;          // V ring stages
-constexpr int BOX = 64 * 128;   // one TMA box: 64 rows x 64 bf16 = 8 KB
+constexpr int P = 64;            // region size
+constexpr int D = 128;           // head dim
+constexpr int NWG = 2;           // softmax warpgroups
+constexpr int KST = 2;           // K ring stages (one pair of key regions each)
+constexpr int VST = 2;           // V ring stages
+constexpr int BOX = 64 * 128;    // one TMA box: 64 rows x 64 bf16 = 8 KB
 constexpr int Q_BYTES = 2 * BOX;
-constexpr int KV_BYTES = 4 * BOX;  // two regions x two feature halves
-constexpr int P_BYTES = 128 * 128; // 128 keys x 64 queries bf16
+constexpr int KV_BYTES = 4 * BOX;   // two regions x two feature halves
+constexpr int P_BYTES = 128 * 128;  // 128 keys x 64 queries bf16
 constexpr float TAU = 8.0f;
 
 constexpr int SMEM_Q = 0;
-constexpr int SMEM_K = SMEM_Q + Q_BYTES;
+constexpr int SMEM_K = SMEM_Q + NWG * Q_BYTES;
 constexpr int SMEM_V = SMEM_K + KST * KV_BYTES;
 constexpr int SMEM_P = SMEM_V + VST * KV_BYTES;
-constexpr int SMEM_END = SMEM_P + 2 * P_BYTES;
+constexpr int SMEM_END = SMEM_P + NWG * P_BYTES;
 constexpr int SMEM_ALLOC = SMEM_END + 1024;  // + alignment slack
 
-constexpr uint32_t TMEM_COLS = 256;
-constexpr uint32_t COL_S0 = 0, COL_S1 = 64, COL_O = 128;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t WG_COLS = 192;  // per warpgroup: S0 [0,64), S1 [64,128), O [128,192)
+constexpr uint32_t COL_O = 128;
 
 struct Params {
   __nv_bfloat16* out;
@@ -63,47 +68,93 @@ struct Params {
   const uint8_t* key_valid;
   int mask_h;  // 1 = per-head masks, 0 = shared
   Geo geo;
+  RegionDecoder dec;
+  FastDiv per_head;  // g
   long long n_pad;
 };
 
-struct __align__(8) Bars {
+struct WgBars {
   uint64_t q_full, q_empty;
-  uint64_t k_full[KST], k_empty[KST];
-  uint64_t v_full[VST], v_empty[VST];
   uint64_t s_full[2], s_free[2];
-  uint64_t p_full[2], p_free[2];
+  uint64_t p_full, p_free;
   uint64_t o_full, o_empty;
 };
-
+struct __align__(8) Bars {
+  uint64_t k_full[KST], k_empty[KST];
+  uint64_t v_full[VST], v_empty[VST];
+  WgBars wg[NWG];
+};
+struct WgAux {
+  float neg_m[P];  // -(running column max), log2 units
+  float alpha[P];
+  float red[4][P];
+};
 struct SmemAux {
   Bars bars;
   uint32_t tmem_base;
-  float m[P];          // running column max (log2 units)
-  float alpha[P];
-  float red[4][P];     // per-warp column partials
+  WgAux wg[NWG];
 };
+
+struct Item {
+  int h, i, n;
+  const int* cols;
+};
+
+DA_DEV bool fetch_item(const Params& p, long long it, long long items, Item& out) {
+  if (it >= items) return false;
+  const int g = p.geo.g;
+  const int h = (int)fdiv((uint32_t)it, p.per_head);
+  const int i = (int)(it - (long long)h * g);
+  const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
+  const int beg = rp[i];
+  out.h = h;
+  out.i = i;
+  out.n = rp[i + 1] - beg;
+  out.cols = p.col_idx + (long long)(h * p.mask_h) * p.cap + beg;
+  return true;
+}
+
+// Cursor over one warpgroup's NONEMPTY items (producer and MMA views).
+struct Cursor {
+  long long k;  // CTA-local item index (item = blockIdx.x + k * gridDim.x)
+  Item item;
+  int steps, t;
+  bool active;
+};
+
+DA_DEV void cursor_seek(Cursor& c, const Params& p, long long items) {
+  while (true) {
+    const long long it = blockIdx.x + c.k * (long long)gridDim.x;
+    if (!fetch_item(p, it, items, c.item)) {
+      c.active = false;
+      return;
+    }
+    if (c.item.n > 0) {
+      c.steps = (c.item.n + 1) / 2;
+      c.t = 0;
+      c.active = true;
+      return;
+    }
+    c.k += NWG;
+  }
+}
 
 DA_DEV void load_region(const CUtensorMap* map, void* dst, uint64_t* bar, const Params& p, int h, int region,
                         int half) {
   if (p.layout == DA_LAYOUT_REORDERED) {
     tma_load_2d(dst, map, bar, half * 64, (int)(h * p.n_pad + (long long)region * P));
   } else {
-    const Geo& g = p.geo;
-    int f = region / (g.Ph * g.Pw);
-    int rest = region - f * g.Ph * g.Pw;
-    int a = rest / g.Pw, b = rest - a * g.Pw;
-    tma_load_5d(dst, map, bar, half * 64, b * g.pw, a * g.ph, f, h);
+    const RegionXY rc = p.dec(region);
+    tma_load_5d(dst, map, bar, half * 64, rc.x0, rc.y0, rc.f, h);
   }
 }
 
-DA_DEV bool key_valid_at(const Params& p, int region, int r) {
-  if (p.key_valid != nullptr) return p.key_valid[(long long)region * P + r] != 0;
-  return key_is_valid(p.geo, region, r);
-}
-
-DA_DEV long long out_row(const Params& p, int region, int r) {
+DA_DEV long long out_row(const Params& p, const RegionXY& rc, int region, int r) {
   if (p.layout == DA_LAYOUT_REORDERED) return (long long)region * P + r;
-  return real_row(p.geo, region, r);
+  const int u = r / p.geo.pw, v = r - u * p.geo.pw;
+  const int y = rc.y0 + u, x = rc.x0 + v;
+  if (y >= p.geo.H || x >= p.geo.W) return -1;
+  return ((long long)rc.f * p.geo.H + y) * p.geo.W + x;
 }
 
 // Column reduction of 32 values held one row per thread across the 32 lanes
@@ -127,7 +178,7 @@ DA_DEV float warp_col_reduce32(float (&v)[32], int lane) {
   return v[0];
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     sparse_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -136,23 +187,21 @@ __global__ void __launch_bounds__(256, 1)
   Bars& B = aux.bars;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const Geo& geo = p.geo;
-  const int g = geo.g;
-  const long long items = (long long)p.heads * g;
+  const long long items = (long long)p.heads * p.geo.g;
 
   if (threadIdx.x == 0) {
-    mbar_init(&B.q_full, 1);
-    mbar_init(&B.q_empty, 1);
     for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&B.s_full[s], 1);
-      mbar_init(&B.s_free[s], 128);
-      mbar_init(&B.p_full[s], 128);
-      mbar_init(&B.p_free[s], 1);
+    for (int w = 0; w < NWG; ++w) {
+      WgBars& wb = B.wg[w];
+      mbar_init(&wb.q_full, 1);
+      mbar_init(&wb.q_empty, 1);
+      for (int s = 0; s < 2; ++s) { mbar_init(&wb.s_full[s], 1); mbar_init(&wb.s_free[s], 128); }
+      mbar_init(&wb.p_full, 128);
+      mbar_init(&wb.p_free, 1);
+      mbar_init(&wb.o_full, 1);
+      mbar_init(&wb.o_empty, 128);
     }
-    mbar_init(&B.o_full, 1);
-    mbar_init(&B.o_empty, 128);
     fence_barrier_init();
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_k);
@@ -169,44 +218,59 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sV = smem + SMEM_V;
   uint8_t* sP = smem + SMEM_P;
 
+  // registers: the producer / MMA warpgroup hands its budget to the softmax warpgroups
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
   if (warp == 0) {
     // ============================ TMA producer ============================
     if (lane == 0) {
-      int kq = 0, vq = 0, qi = 0;
-      for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-        const int h = (int)(it / g), i = (int)(it % g);
-        const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
-        const int beg = rp[i], n = rp[i + 1] - beg;
-        if (n == 0) continue;
-        const int* cols = p.col_idx + (long long)(h * p.mask_h) * p.cap + beg;
-        const int steps = (n + 1) / 2;
-        if (qi > 0) mbar_wait(&B.q_empty, (qi - 1) & 1);
-        mbar_expect_tx(&B.q_full, Q_BYTES);
-        load_region(&tm_q, sQ, &B.q_full, p, h, i, 0);
-        load_region(&tm_q, sQ + BOX, &B.q_full, p, h, i, 1);
-        for (int t = 0; t < steps; ++t) {
-          const int j0 = cols[2 * t];
-          const int j1 = (2 * t + 1 < n) ? cols[2 * t + 1] : j0;
+      Cursor c[NWG];
+      int qi[NWG];
+      for (int w = 0; w < NWG; ++w) {
+        c[w].k = w;
+        qi[w] = 0;
+        cursor_seek(c[w], p, items);
+      }
+      int kq = 0, vq = 0;
+      while (c[0].active || c[1].active) {
+#pragma unroll
+        for (int w = 0; w < NWG; ++w) {
+          if (!c[w].active) continue;
+          Cursor& cu = c[w];
+          WgBars& wb = B.wg[w];
+          if (cu.t == 0) {
+            if (qi[w] > 0) mbar_wait(&wb.q_empty, (qi[w] - 1) & 1);
+            mbar_expect_tx(&wb.q_full, Q_BYTES);
+            uint8_t* q = sQ + w * Q_BYTES;
+            load_region(&tm_q, q, &wb.q_full, p, cu.item.h, cu.item.i, 0);
+            load_region(&tm_q, q + BOX, &wb.q_full, p, cu.item.h, cu.item.i, 1);
+          }
+          const int j0 = cu.item.cols[2 * cu.t];
+          const int j1 = (2 * cu.t + 1 < cu.item.n) ? cu.item.cols[2 * cu.t + 1] : j0;
           const int ks = kq % KST;
           if (kq >= KST) mbar_wait(&B.k_empty[ks], ((kq / KST) - 1) & 1);
           uint8_t* kb = sK + ks * KV_BYTES;  // [half][slot][64 x 128B]
           mbar_expect_tx(&B.k_full[ks], KV_BYTES);
-          load_region(&tm_k, kb, &B.k_full[ks], p, h, j0, 0);
-          load_region(&tm_k, kb + BOX, &B.k_full[ks], p, h, j1, 0);
-          load_region(&tm_k, kb + 2 * BOX, &B.k_full[ks], p, h, j0, 1);
-          load_region(&tm_k, kb + 3 * BOX, &B.k_full[ks], p, h, j1, 1);
+          load_region(&tm_k, kb, &B.k_full[ks], p, cu.item.h, j0, 0);
+          load_region(&tm_k, kb + BOX, &B.k_full[ks], p, cu.item.h, j1, 0);
+          load_region(&tm_k, kb + 2 * BOX, &B.k_full[ks], p, cu.item.h, j0, 1);
+          load_region(&tm_k, kb + 3 * BOX, &B.k_full[ks], p, cu.item.h, j1, 1);
           ++kq;
           const int vs = vq % VST;
           if (vq >= VST) mbar_wait(&B.v_empty[vs], ((vq / VST) - 1) & 1);
           uint8_t* vb = sV + vs * KV_BYTES;  // [slot][half][64 x 128B]
           mbar_expect_tx(&B.v_full[vs], KV_BYTES);
-          load_region(&tm_v, vb, &B.v_full[vs], p, h, j0, 0);
-          load_region(&tm_v, vb + BOX, &B.v_full[vs], p, h, j0, 1);
-          load_region(&tm_v, vb + 2 * BOX, &B.v_full[vs], p, h, j1, 0);
-          load_region(&tm_v, vb + 3 * BOX, &B.v_full[vs], p, h, j1, 1);
+          load_region(&tm_v, vb, &B.v_full[vs], p, cu.item.h, j0, 0);
+          load_region(&tm_v, vb + BOX, &B.v_full[vs], p, cu.item.h, j0, 1);
+          load_region(&tm_v, vb + 2 * BOX, &B.v_full[vs], p, cu.item.h, j1, 0);
+          load_region(&tm_v, vb + 3 * BOX, &B.v_full[vs], p, cu.item.h, j1, 1);
           ++vq;
+          if (++cu.t == cu.steps) {
+            ++qi[w];
+            cu.k += NWG;
+            cursor_seek(cu, p, items);
+          }
         }
-        ++qi;
       }
     }
   } else if (warp == 1) {
@@ -214,174 +278,231 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       constexpr uint32_t IDESC1 = umma_idesc_bf16(128, 64, 0, 0);  // K-major A, K-major B
       constexpr uint32_t IDESC2 = umma_idesc_bf16(128, 64, 1, 1);  // MN-major A, MN-major B
-      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
-      int kq = 0, vq = 0, qi = 0;
-      long long G = 0;
-      auto gemm2 = [&](long long Gp, bool first) {
+      // descriptor templates; start addresses (>> 4) are added to the low word
+      const uint64_t dK = umma_desc_sw128(0, 16, 1024);
+      const uint64_t dV = umma_desc_sw128(0, BOX, 1024);
+      const uint32_t aQ = smem_u32(sQ) >> 4, aK = smem_u32(sK) >> 4, aV = smem_u32(sV) >> 4;
+      const uint32_t aP = smem_u32(sP) >> 4;
+      Cursor c[NWG];
+      int qi[NWG];
+      long long G[NWG];
+      for (int w = 0; w < NWG; ++w) {
+        c[w].k = w;
+        qi[w] = 0;
+        G[w] = 0;
+        cursor_seek(c[w], p, items);
+      }
+      int kq = 0, vq = 0;
+      struct Pend {
+        int w, qi;
+        long long G;
+        bool first, last, valid;
+      } pend;
+      pend.valid = false;
+      auto gemm2 = [&](const Pend& s) {
+        WgBars& wb = B.wg[s.w];
         const int vs = vq % VST;
         mbar_wait(&B.v_full[vs], (vq / VST) & 1);
-        const int pb = (int)(Gp & 1);
-        mbar_wait(&B.p_full[pb], (uint32_t)((Gp >> 1) & 1));
-        if (first && qi > 0) mbar_wait(&B.o_empty, (qi - 1) & 1);
+        mbar_wait(&wb.p_full, (uint32_t)(s.G & 1));
+        if (s.first && s.qi > 0) mbar_wait(&wb.o_empty, (s.qi - 1) & 1);
         tc_fence_after();
-        const uint32_t vbase = aV + vs * KV_BYTES;
-        const uint32_t pbase = aP + pb * P_BYTES;
+        const uint32_t vbase = aV + vs * (KV_BYTES >> 4);
+        const uint32_t pbase = aP + s.w * (P_BYTES >> 4);
+        const uint32_t dO = tmem + s.w * WG_COLS + COL_O;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t slot = kk >> 2;
-          uint64_t a = umma_desc_sw128(vbase + slot * 2 * BOX + (kk & 3) * 2048, 2 * BOX / 2, 1024);
-          uint64_t b = umma_desc_sw128(pbase + kk * 2048, BOX, 1024);
-          umma_bf16(tmem + COL_O, a, b, IDESC2, (first && kk == 0) ? 0u : 1u);
+          const uint64_t a = dV + (uint64_t)(vbase + (kk >> 2) * (2 * BOX >> 4) + (kk & 3) * (2048 >> 4));
+          const uint64_t b = dV + (uint64_t)(pbase + kk * (2048 >> 4));
+          umma_bf16(dO, a, b, IDESC2, (s.first && kk == 0) ? 0u : 1u);
         }
         umma_commit(&B.v_empty[vs]);
-        umma_commit(&B.p_free[pb]);
+        umma_commit(&wb.p_free);
+        if (s.last) umma_commit(&wb.o_full);
         ++vq;
       };
-      for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-        const int h = (int)(it / g), i = (int)(it % g);
-        const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
-        const int n = rp[i + 1] - rp[i];
-        if (n == 0) continue;
-        const int steps = (n + 1) / 2;
-        mbar_wait(&B.q_full, qi & 1);
-        for (int t = 0; t < steps; ++t) {
+      while (c[0].active || c[1].active) {
+#pragma unroll
+        for (int w = 0; w < NWG; ++w) {
+          if (!c[w].active) continue;
+          Cursor& cu = c[w];
+          WgBars& wb = B.wg[w];
+          if (cu.t == 0) mbar_wait(&wb.q_full, qi[w] & 1);
           const int ks = kq % KST;
           mbar_wait(&B.k_full[ks], (kq / KST) & 1);
-          const int b = (int)(G & 1);
-          if (G >= 2) mbar_wait(&B.s_free[b], (uint32_t)(((G >> 1) - 1) & 1));
+          const int b = (int)(G[w] & 1);
+          if (G[w] >= 2) mbar_wait(&wb.s_free[b], (uint32_t)(((G[w] >> 1) - 1) & 1));
           tc_fence_after();
-          const uint32_t kbase = aK + ks * KV_BYTES;
+          const uint32_t kbase = aK + ks * (KV_BYTES >> 4);
+          const uint32_t qbase = aQ + w * (Q_BYTES >> 4);
+          const uint32_t dS = tmem + w * WG_COLS + b * 64;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            uint64_t a = umma_desc_sw128(kbase + (kk >> 2) * 2 * BOX + (kk & 3) * 32, 16, 1024);
-            uint64_t bq = umma_desc_sw128(aQ + (kk >> 2) * BOX + (kk & 3) * 32, 16, 1024);
-            umma_bf16(tmem + (b ? COL_S1 : COL_S0), a, bq, IDESC1, kk > 0 ? 1u : 0u);
+            const uint64_t a = dK + (uint64_t)(kbase + (kk >> 2) * (2 * BOX >> 4) + (kk & 3) * 2);
+            const uint64_t bq = dK + (uint64_t)(qbase + (kk >> 2) * (BOX >> 4) + (kk & 3) * 2);
+            umma_bf16(dS, a, bq, IDESC1, kk > 0 ? 1u : 0u);
           }
           umma_commit(&B.k_empty[ks]);
-          umma_commit(&B.s_full[b]);
-          if (t == steps - 1) umma_commit(&B.q_empty);
+          umma_commit(&wb.s_full[b]);
+          if (cu.t == cu.steps - 1) umma_commit(&wb.q_empty);
           ++kq;
-          if (t >= 1) gemm2(G - 1, t == 1);
-          ++G;
+          if (pend.valid) gemm2(pend);
+          pend.w = w;
+          pend.qi = qi[w];
+          pend.G = G[w];
+          pend.first = cu.t == 0;
+          pend.last = cu.t == cu.steps - 1;
+          pend.valid = true;
+          ++G[w];
+          if (++cu.t == cu.steps) {
+            ++qi[w];
+            cu.k += NWG;
+            cursor_seek(cu, p, items);
+          }
         }
-        gemm2(G - 1, steps == 1);
-        umma_commit(&B.o_full);
-        ++qi;
       }
+      if (pend.valid) gemm2(pend);
     }
-  } else if (warp >= 4) {
-    // ======================= softmax / epilogue warpgroup ====================
-    const int tid = threadIdx.x - 128;  // key / feature lane 0..127
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    // ===================== softmax / epilogue warpgroups ====================
+    const int wg = (warp - 4) >> 2;
+    const int tid = threadIdx.x - 128 - wg * 128;  // key / feature lane 0..127
     const int q4 = tid >> 5;
+    const int bar_id = 1 + wg;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tbase = tmem + wg * WG_COLS + lane_off;
+    WgBars& wb = B.wg[wg];
+    WgAux& X = aux.wg[wg];
+    uint8_t* myP = sP + wg * P_BYTES;
     const int slot = tid >> 6, r = tid & 63;
+    const int ru = r / p.geo.pw, rv = r - ru * p.geo.pw;  // in-patch row / column of my key
+    const float sl2 = p.scale_log2;
     long long G = 0;
     int qi = 0;
-    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-      const int h = (int)(it / g), i = (int)(it % g);
-      const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
-      const int beg = rp[i], n = rp[i + 1] - beg;
-      __nv_bfloat16* outh = p.out + h * p.oh;
+    for (long long k = wg;; k += NWG) {
+      Item itm;
+      if (!fetch_item(p, blockIdx.x + k * (long long)gridDim.x, items, itm)) break;
+      const int i = itm.i, n = itm.n;
+      __nv_bfloat16* outh = p.out + itm.h * p.oh;
+      const RegionXY qrc = p.layout == DA_LAYOUT_REORDERED ? RegionXY{0, 0, 0} : p.dec(i);
       if (n == 0) {
         // no kept key region: zero rows (sparse.py:137-138)
         for (int c = tid; c < P * (D / 8); c += 128) {
-          int q = c >> 4, part = c & 15;
-          long long row = out_row(p, i, q);
-          if (row >= 0) reinterpret_cast<uint4*>(outh + row * p.orow)[part] = make_uint4(0, 0, 0, 0);
+          const long long row = out_row(p, qrc, i, c >> 4);
+          if (row >= 0) reinterpret_cast<uint4*>(outh + row * p.orow)[c & 15] = make_uint4(0, 0, 0, 0);
         }
         continue;
       }
-      const int* cols = p.col_idx + (long long)(h * p.mask_h) * p.cap + beg;
       const int steps = (n + 1) / 2;
-      float l[P];
+      float2 l2[P / 2];
 #pragma unroll
-      for (int c = 0; c < P; ++c) l[c] = 0.f;
+      for (int c = 0; c < P / 2; ++c) l2[c] = make_float2(0.f, 0.f);
       bool mvalid = false;
       for (int t = 0; t < steps; ++t) {
         const int b = (int)(G & 1);
         const int js = 2 * t + slot;
-        const bool valid = js < n && key_valid_at(p, cols[js], r);
-        mbar_wait(&B.s_full[b], (uint32_t)((G >> 1) & 1));
-        tc_fence_after();
-        const uint32_t sa = tmem + lane_off + (b ? COL_S1 : COL_S0);
-        float x[P];
-        tmem_ld32_at<0>(sa, x);
-        tmem_ld32_at<32>(sa + 32, x);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < P; ++c) x[c] = valid ? x[c] * p.scale_log2 : -INFINITY;
-        bool exceed = !mvalid;
-        if (mvalid) {
-#pragma unroll
-          for (int c = 0; c < P; ++c) exceed |= (x[c] - aux.m[c]) > TAU;
+        bool valid = false;
+        if (js < n) {
+          const int j = itm.cols[js];
+          if (p.key_valid != nullptr) {
+            valid = p.key_valid[(long long)j * P + r] != 0;
+          } else {
+            const RegionXY kc = p.dec(j);
+            valid = (kc.y0 + ru < p.geo.H) && (kc.x0 + rv < p.geo.W);
+          }
         }
-        const bool need = bar_red_or(1, 128, exceed);
-        if (need) {
-          // column max over the 128 keys of this step (two 32-column halves)
+        const float vf = valid ? 1.f : 0.f;
+        const uint32_t vmask = valid ? 0xffffffffu : 0u;
+        mbar_wait(&wb.s_full[b], (uint32_t)((G >> 1) & 1));
+        // P^T rows go to a buffer that is free once the previous step's GEMM2 consumed it
+        if (G >= 1) mbar_wait(&wb.p_free, (uint32_t)((G - 1) & 1));
+        tc_fence_after();
+        const uint32_t sa = tbase + b * 64;
+        uint8_t* prow = myP + tid * 128;
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            float tmp[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) tmp[c] = x[hf * 32 + c];
-            aux.red[q4][hf * 32 + lane] = warp_col_reduce32<true>(tmp, lane);
-          }
-          bar_sync(1, 128);
-          if (tid < P) {
-            float ms = fmaxf(fmaxf(aux.red[0][tid], aux.red[1][tid]), fmaxf(aux.red[2][tid], aux.red[3][tid]));
-            float mold = mvalid ? aux.m[tid] : -INFINITY;
-            float mnew = fmaxf(mold, ms);
-            aux.alpha[tid] = (mold == -INFINITY || mnew == -INFINITY) ? 0.f : exp2f(mold - mnew);
-            aux.m[tid] = mnew;
-          }
-          bar_sync(1, 128);
-          const bool now_valid = aux.m[0] != -INFINITY;
+        for (int hf = 0; hf < 2; ++hf) {
+          float x[32];
+          tmem_ld32(sa + hf * 32, x);
+          tmem_ld_wait();
+          bool exceed = !mvalid;
           if (mvalid) {
+            float emax = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < P; ++c) l[c] *= aux.alpha[c];
-            if (t > 0) {
-              // O^T holds GEMM2 results up to step t-1: wait for it, rescale columns
-              const long long Gp = G - 1;
-              mbar_wait(&B.p_free[Gp & 1], (uint32_t)((Gp >> 1) & 1));
-              tc_fence_after();
+            for (int c = 0; c < 32; c += 2) {
+              const float2 nm = *reinterpret_cast<const float2*>(&X.neg_m[hf * 32 + c]);
+              const float2 e = ffma2(make_float2(x[c], x[c + 1]), make_float2(sl2, sl2), nm);
+              x[c] = e.x;
+              x[c + 1] = e.y;
+              emax = fmaxf(emax, fmaxf(e.x, e.y));
+            }
+            exceed = valid && emax > TAU;
+          }
+          if (bar_red_or(bar_id, 128, exceed)) {
+            // (re)establish the running max of these 32 columns over this step's keys
+            tmem_ld32(sa + hf * 32, x);
+            tmem_ld_wait();
 #pragma unroll
-              for (int hf = 0; hf < 2; ++hf) {
+            for (int c = 0; c < 32; ++c) x[c] = valid ? x[c] * sl2 : -INFINITY;
+            {
+              float tmp[32];
+#pragma unroll
+              for (int c = 0; c < 32; ++c) tmp[c] = x[c];
+              X.red[q4][hf * 32 + lane] = warp_col_reduce32<true>(tmp, lane);
+            }
+            bar_sync(bar_id, 128);
+            if (tid < 32) {
+              const int c = hf * 32 + tid;
+              const float ms = fmaxf(fmaxf(X.red[0][c], X.red[1][c]), fmaxf(X.red[2][c], X.red[3][c]));
+              const float mold = mvalid ? -X.neg_m[c] : -INFINITY;
+              const float mnew = fmaxf(mold, ms);
+              X.alpha[c] = (mold == -INFINITY || mnew == -INFINITY) ? 0.f : exp2f(mold - mnew);
+              X.neg_m[c] = -mnew;
+            }
+            bar_sync(bar_id, 128);
+            if (mvalid) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                l2[hf * 16 + c].x *= X.alpha[hf * 32 + 2 * c];
+                l2[hf * 16 + c].y *= X.alpha[hf * 32 + 2 * c + 1];
+              }
+              if (t > 0) {
+                // O^T holds GEMM2 results up to the previous step (p_free waited above)
                 float o[32];
-                const uint32_t oa = tmem + lane_off + COL_O + hf * 32;
+                const uint32_t oa = tbase + COL_O + hf * 32;
                 tmem_ld32(oa, o);
                 tmem_ld_wait();
 #pragma unroll
-                for (int c = 0; c < 32; ++c) o[c] *= aux.alpha[hf * 32 + c];
+                for (int c = 0; c < 32; ++c) o[c] *= X.alpha[hf * 32 + c];
                 tmem_st32(oa, o);
+                tmem_st_wait();
               }
-              tmem_st_wait();
             }
+            const bool any = X.neg_m[hf * 32] != INFINITY;  // m finite <=> some valid key seen
+#pragma unroll
+            for (int c = 0; c < 32; ++c) x[c] = any ? x[c] + X.neg_m[hf * 32 + c] : -INFINITY;
           }
-          mvalid = now_valid;
-        }
-        // P^T row for this key -> shared memory (128B-swizzled, MN-major)
-        if (G >= 2) mbar_wait(&B.p_free[b], (uint32_t)(((G >> 1) - 1) & 1));
-        uint8_t* prow = sP + b * P_BYTES + tid * 128;
+          // probabilities of my key for these 32 queries -> P^T row (128B-swizzled, MN-major)
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          uint32_t w[4];
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t w4[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = cc * 8 + 2 * e;
-            float p0 = 0.f, p1 = 0.f;
-            if (mvalid) {  // invalid keys carry x = -inf -> exp2 = +0
-              p0 = fast_exp2(x[c] - aux.m[c]);
-              p1 = fast_exp2(x[c + 1] - aux.m[c + 1]);
+            for (int e = 0; e < 4; ++e) {
+              const int c = cc * 8 + 2 * e;
+              const float p0 = fast_exp2(x[c]);
+              const float p1 = fast_exp2(x[c + 1]);
+              l2[hf * 16 + c / 2] = ffma2(make_float2(p0, p1), make_float2(vf, vf), l2[hf * 16 + c / 2]);
+              w4[e] = pack_bf16(p0, p1) & vmask;
             }
-            l[c] += p0;
-            l[c + 1] += p1;
-            w[e] = pack_bf16(p0, p1);
+            const int chunk = hf * 4 + cc;
+            *reinterpret_cast<uint4*>(prow + ((chunk ^ (tid & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
           }
-          *reinterpret_cast<uint4*>(prow + ((cc ^ (tid & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
+        if (!mvalid) mvalid = X.neg_m[0] != INFINITY;
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(&B.p_full[b]);
-        mbar_arrive(&B.s_free[b]);  // S[b] no longer needed (re-read above on the rare rescale path)
+        mbar_arrive(&wb.p_full);
+        mbar_arrive(&wb.s_free[b]);
         ++G;
       }
       // ------------------------------ epilogue ------------------------------
@@ -389,38 +510,40 @@ __global__ void __launch_bounds__(256, 1)
       for (int hf = 0; hf < 2; ++hf) {
         float tmp[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) tmp[c] = l[hf * 32 + c];
-        aux.red[q4][hf * 32 + lane] = warp_col_reduce32<false>(tmp, lane);
+        for (int c = 0; c < 16; ++c) {
+          tmp[2 * c] = l2[hf * 16 + c].x;
+          tmp[2 * c + 1] = l2[hf * 16 + c].y;
+        }
+        X.red[q4][hf * 32 + lane] = warp_col_reduce32<false>(tmp, lane);
       }
-      mbar_wait(&B.o_full, qi & 1);
+      mbar_wait(&wb.o_full, qi & 1);
       tc_fence_after();
-      bar_sync(1, 128);
-      if (tid < P) aux.alpha[tid] = aux.red[0][tid] + aux.red[1][tid] + aux.red[2][tid] + aux.red[3][tid];
-      bar_sync(1, 128);
+      bar_sync(bar_id, 128);
+      if (tid < P) X.alpha[tid] = X.red[0][tid] + X.red[1][tid] + X.red[2][tid] + X.red[3][tid];
+      bar_sync(bar_id, 128);
       // O^T row d = tid -> normalised bf16 into the staging tile [64 q][128 d]
-      __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(sP);
+      __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(myP);
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      for (int hf = 0; hf < 2; ++hf) {
         float o[32];
-        tmem_ld32(tmem + lane_off + COL_O + half * 32, o);
+        tmem_ld32(tbase + COL_O + hf * 32, o);
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          const float lq = aux.alpha[half * 32 + c];
-          const float v = lq > 0.f ? o[c] / lq : 0.f;
-          stage[(half * 32 + c) * D + tid] = __float2bfloat16_rn(v);
+          const float lq = X.alpha[hf * 32 + c];
+          stage[(hf * 32 + c) * D + tid] = __float2bfloat16_rn(lq > 0.f ? o[c] / lq : 0.f);
         }
       }
       tc_fence_before();
-      mbar_arrive(&B.o_empty);
-      bar_sync(1, 128);
+      mbar_arrive(&wb.o_empty);
+      bar_sync(bar_id, 128);
       for (int c = tid; c < P * (D / 8); c += 128) {
-        const int q = c >> 4, part = c & 15;
-        const long long row = out_row(p, i, q);
+        const int q = c >> 4;
+        const long long row = out_row(p, qrc, i, q);
         if (row >= 0)
-          reinterpret_cast<uint4*>(outh + row * p.orow)[part] = reinterpret_cast<const uint4*>(stage + q * D)[part];
+          reinterpret_cast<uint4*>(outh + row * p.orow)[c & 15] = reinterpret_cast<const uint4*>(stage + q * D)[c & 15];
       }
-      bar_sync(1, 128);
+      bar_sync(bar_id, 128);
       ++qi;
     }
   }
@@ -496,7 +619,7 @@ bool tc_supported(const da_attn_args& a, const Geo& g) {
     if (a.q_head_stride % 8 || a.k_head_stride % 8 || a.v_head_stride % 8) return false;
   }
   if (a.o_row_stride % 8 || a.o_head_stride % 8) return false;
-  return true;
+  return (long long)a.heads * g.g < (1ll << 31);
 }
 
 cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why) {
@@ -527,6 +650,8 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   p.key_valid = a.key_valid;
   p.mask_h = a.shared_mask ? 0 : 1;
   p.geo = g;
+  p.dec = make_decoder(g);
+  p.per_head = make_fastdiv((uint32_t)g.g);
   p.n_pad = g.n_pad;
   static int num_sms = 0;
   if (num_sms == 0) {
@@ -539,7 +664,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   if (e != cudaSuccess) return e;
   long long items = (long long)a.heads * g.g;
   int grid = (int)(items < num_sms ? items : num_sms);
-  tc::sparse_attn_tc_kernel<<<grid, 256, tc::SMEM_ALLOC, st>>>(mq, mk, mv, p);
+  tc::sparse_attn_tc_kernel<<<grid, 384, tc::SMEM_ALLOC, st>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
 

@@ -38,6 +38,46 @@ inline Geo make_geo(const da_grid& gr) {
   return g;
 }
 
+// Division by a runtime constant with a precomputed multiplier
+// (q = (umulhi(n, mul) + n) >> shift; exact for n < 2^31).
+struct FastDiv {
+  uint32_t d, mul, shift;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.shift = 0;
+  while ((1ull << f.shift) < d) ++f.shift;
+  f.mul = (uint32_t)(((1ull << 32) * ((1ull << f.shift) - d)) / d + 1);
+  return f;
+}
+DA_DEV uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
+
+// Region coordinates: frame, first padded row and column of region i.
+struct RegionXY {
+  int f, y0, x0;
+};
+struct RegionDecoder {
+  FastDiv per_frame;  // Ph*Pw
+  FastDiv per_row;    // Pw
+  int ph, pw;
+  DA_DEV RegionXY operator()(int i) const {
+    int f = (int)fdiv((uint32_t)i, per_frame);
+    int rest = i - f * (int)per_frame.d;
+    int a = (int)fdiv((uint32_t)rest, per_row);
+    int b = rest - a * (int)per_row.d;
+    return {f, a * ph, b * pw};
+  }
+};
+inline RegionDecoder make_decoder(const Geo& g) {
+  RegionDecoder d;
+  d.per_frame = make_fastdiv((uint32_t)(g.Ph * g.Pw));
+  d.per_row = make_fastdiv((uint32_t)g.Pw);
+  d.ph = g.ph;
+  d.pw = g.pw;
+  return d;
+}
+
 // Real-token row of reordered position (region i, offset r), or -1 for padding.
 DA_DEV long long real_row(const Geo& g, int i, int r) {
   int f = i / (g.Ph * g.Pw);
@@ -237,6 +277,16 @@ DA_DEV float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// Packed fp32x2 FMA (Blackwell FFMA2): d = a * b + c, lane-wise.
+DA_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
 }
 
 }  // namespace da
