@@ -84,8 +84,8 @@ struct __align__(8) Bars {
   uint64_t v_full[VST], v_empty[VST];
   WgBars wg[NWG];
 };
-struct WgAux {
-  float neg_m[P];  // -(running column max), log2 units
+struct __align__(16) WgAux {
+  float neg_m[P];  // -(running column max), log2 units (read as float2)
   float alpha[P];
   float red[4][P];
 };

@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
   __syncthreads();
   // valid count of the region (closed form, same for every column)
   if (tid < d) {
-    int cnt = 0;
-    for (int r = 0; r < g.p; ++r) cnt += region_real_row(g, rc, r) >= 0;
+    const int vy = min(g.ph, g.H - rc.y0), vx = min(g.pw, g.W - rc.x0);
+    const int cnt = vy * vx;
     double s = red[tid];
     for (int q = 1; q < RG; ++q) s = mode == 0 ? s + red[q * d + tid] : fmax(s, red[q * d + tid]);
     double outv;
