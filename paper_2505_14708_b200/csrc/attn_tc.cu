@@ -53,7 +53,10 @@ constexpr int SMEM_END = SMEM_P + NWG * P_BYTES;
 constexpr int SMEM_ALLOC = SMEM_END + 1024;  // + alignment slack
 
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t WG_COLS = 192;  // per warpgroup: S0 [0,64), S1 [64,128), O [128,192)
+// per warpgroup: S0 [0,64), S1 [64,128), O0 [128,192), O1 [192,256); the O
+// accumulator alternates between items so the next item's GEMM2 does not wait
+// for this item's epilogue
+constexpr uint32_t WG_COLS = 256;
 constexpr uint32_t COL_O = 128;
 
 struct Params {
@@ -77,7 +80,7 @@ struct WgBars {
   uint64_t q_full, q_empty;
   uint64_t s_full[2], s_free[2];
   uint64_t p_full, p_free;
-  uint64_t o_full, o_empty;
+  uint64_t o_full[2], o_empty[2];
 };
 struct __align__(8) Bars {
   uint64_t k_full[KST], k_empty[KST];
@@ -139,13 +142,15 @@ DA_DEV void cursor_seek(Cursor& c, const Params& p, long long items) {
   }
 }
 
+// Q blocks are read once (evict first); K/V blocks are re-read by ~10% of the
+// head's query regions while the head is in flight (normal priority).
 DA_DEV void load_region(const CUtensorMap* map, void* dst, uint64_t* bar, const Params& p, int h, int region,
-                        int half) {
+                        int half, uint64_t policy = L2_EVICT_NORMAL) {
   if (p.layout == DA_LAYOUT_REORDERED) {
-    tma_load_2d(dst, map, bar, half * 64, (int)(h * p.n_pad + (long long)region * P));
+    tma_load_2d(dst, map, bar, half * 64, (int)(h * p.n_pad + (long long)region * P), policy);
   } else {
     const RegionXY rc = p.dec(region);
-    tma_load_5d(dst, map, bar, half * 64, rc.x0, rc.y0, rc.f, h);
+    tma_load_5d(dst, map, bar, half * 64, rc.x0, rc.y0, rc.f, h, policy);
   }
 }
 
@@ -199,8 +204,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int s = 0; s < 2; ++s) { mbar_init(&wb.s_full[s], 1); mbar_init(&wb.s_free[s], 128); }
       mbar_init(&wb.p_full, 128);
       mbar_init(&wb.p_free, 1);
-      mbar_init(&wb.o_full, 1);
-      mbar_init(&wb.o_empty, 128);
+      for (int s = 0; s < 2; ++s) { mbar_init(&wb.o_full[s], 1); mbar_init(&wb.o_empty[s], 128); }
     }
     fence_barrier_init();
     tma_prefetch(&tm_q);
@@ -242,8 +246,8 @@ __global__ void __launch_bounds__(384, 1)
             if (qi[w] > 0) mbar_wait(&wb.q_empty, (qi[w] - 1) & 1);
             mbar_expect_tx(&wb.q_full, Q_BYTES);
             uint8_t* q = sQ + w * Q_BYTES;
-            load_region(&tm_q, q, &wb.q_full, p, cu.item.h, cu.item.i, 0);
-            load_region(&tm_q, q + BOX, &wb.q_full, p, cu.item.h, cu.item.i, 1);
+            load_region(&tm_q, q, &wb.q_full, p, cu.item.h, cu.item.i, 0, L2_EVICT_FIRST);
+            load_region(&tm_q, q + BOX, &wb.q_full, p, cu.item.h, cu.item.i, 1, L2_EVICT_FIRST);
           }
           const int j0 = cu.item.cols[2 * cu.t];
           const int j1 = (2 * cu.t + 1 < cu.item.n) ? cu.item.cols[2 * cu.t + 1] : j0;
@@ -304,11 +308,12 @@ __global__ void __launch_bounds__(384, 1)
         const int vs = vq % VST;
         mbar_wait(&B.v_full[vs], (vq / VST) & 1);
         mbar_wait(&wb.p_full, (uint32_t)(s.G & 1));
-        if (s.first && s.qi > 0) mbar_wait(&wb.o_empty, (s.qi - 1) & 1);
+        const int ob = s.qi & 1;  // O buffer of this item
+        if (s.first && s.qi >= 2) mbar_wait(&wb.o_empty[ob], ((s.qi >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t vbase = aV + vs * (KV_BYTES >> 4);
         const uint32_t pbase = aP + s.w * (P_BYTES >> 4);
-        const uint32_t dO = tmem + s.w * WG_COLS + COL_O;
+        const uint32_t dO = tmem + s.w * WG_COLS + COL_O + ob * 64;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t a = dV + (uint64_t)(vbase + (kk >> 2) * (2 * BOX >> 4) + (kk & 3) * (2048 >> 4));
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         umma_commit(&B.v_empty[vs]);
         umma_commit(&wb.p_free);
-        if (s.last) umma_commit(&wb.o_full);
+        if (s.last) umma_commit(&wb.o_full[ob]);
         ++vq;
       };
       while (c[0].active || c[1].active) {
@@ -395,6 +400,8 @@ __global__ void __launch_bounds__(384, 1)
         continue;
       }
       const int steps = (n + 1) / 2;
+      const int ob = qi & 1;
+      const uint32_t tO = tbase + COL_O + ob * 64;  // this item's O^T accumulator
       float2 l2[P / 2];
 #pragma unroll
       for (int c = 0; c < P / 2; ++c) l2[c] = make_float2(0.f, 0.f);
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(384, 1)
         if (G >= 1) mbar_wait(&wb.p_free, (uint32_t)((G - 1) & 1));
         tc_fence_after();
         const uint32_t sa = tbase + b * 64;
-        uint8_t* prow = myP + tid * 128;
+        const uint32_t prow = smem_u32(myP) + tid * 128;
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           float x[32];
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(384, 1)
               if (t > 0) {
                 // O^T holds GEMM2 results up to the previous step (p_free waited above)
                 float o[32];
-                const uint32_t oa = tbase + COL_O + hf * 32;
+                const uint32_t oa = tO + hf * 32;
                 tmem_ld32(oa, o);
                 tmem_ld_wait();
 #pragma unroll
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(384, 1)
               w4[e] = pack_bf16(p0, p1) & vmask;
             }
             const int chunk = hf * 4 + cc;
-            *reinterpret_cast<uint4*>(prow + ((chunk ^ (tid & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            sts128(prow + ((chunk ^ (tid & 7)) << 4), w4[0], w4[1], w4[2], w4[3]);
           }
         }
         if (!mvalid) mvalid = X.neg_m[0] != INFINITY;
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         X.red[q4][hf * 32 + lane] = warp_col_reduce32<false>(tmp, lane);
       }
-      mbar_wait(&wb.o_full, qi & 1);
+      mbar_wait(&wb.o_full[ob], (uint32_t)((qi >> 1) & 1));
       tc_fence_after();
       bar_sync(bar_id, 128);
       if (tid < P) X.alpha[tid] = X.red[0][tid] + X.red[1][tid] + X.red[2][tid] + X.red[3][tid];
@@ -526,7 +533,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         float o[32];
-        tmem_ld32(tbase + COL_O + hf * 32, o);
+        tmem_ld32(tO + hf * 32, o);
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&wb.o_empty);
+      mbar_arrive(&wb.o_empty[ob]);
       bar_sync(bar_id, 128);
       for (int c = tid; c < P * (D / 8); c += 128) {
         const int q = c >> 4;
