@@ -195,10 +195,12 @@ size_t da_pipeline_workspace_size(const da_grid* grid, int32_t heads, int32_t d)
 }
 
 int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
-  // pool x2, draft GEMM (+ row softmax), [head mean], selection (init, 6 x
-  // (histogram + scan), tie counts, tie scan, mark, row scan, collect, finish),
-  // attention
-  return 2 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + (1 + 12 + 1 + 1 + 1 + 1 + 1 + 1) + 1;
+  // pool (Q and K), draft GEMM (+ row softmax) [+ head mean], selection: init,
+  // digit histograms (digit 0 fused into the GEMM on the per-head logits path)
+  // and scans, candidate compaction + finish, tie counts + scan, mark, row
+  // scan, collect, threshold, kept totals, packbits (bitmap requested); attention
+  const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
+  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 1;
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
@@ -214,9 +216,22 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   cudaStream_t st = (cudaStream_t)stream;
   PipeWs w = carve(pa->workspace, g, a.heads, a.d);
   int rc;
-  if ((rc = da_pool(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.heads, a.d, grid, pa->pool_mode, stream))) return rc;
-  if ((rc = da_pool(a.k, a.k_head_stride, a.k_row_stride, w.kp, a.heads, a.d, grid, pa->pool_mode, stream))) return rc;
-  if ((rc = da_draft_scores(w.qp, w.kp, w.scores, a.heads, g.g, a.d, a.scale, pa->select_softmax, stream))) return rc;
+  if (a.d % 8 || a.d > 2048 || a.q_head_stride % 8 || a.q_row_stride % 8 || a.k_head_stride % 8 ||
+      a.k_row_stride % 8 || (reinterpret_cast<uintptr_t>(a.q) & 15) || (reinterpret_cast<uintptr_t>(a.k) & 15))
+    return fail(DA_EINVAL, "sparse_attention: q/k need d %% 8 == 0 and 16-byte aligned rows");
+  // K2: pool Q and K in one launch
+  if ((rc = cuda_status(da::launch_pool2(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.k, a.k_head_stride,
+                                         a.k_row_stride, w.kp, a.heads, a.d, pa->pool_mode, g, st),
+                        "pool")))
+    return rc;
+  // K3a: draft scores; when the selection runs per head on raw logits, the
+  // GEMM epilogue also histograms digit 0 of the selection keys
+  const bool fuse_digit0 = !pa->select_softmax && !pa->shared_head_mask;
+  if (fuse_digit0) da::select_init(w.sel, a.heads, g.g, pa->m, st);
+  if ((rc = cuda_status(da::launch_draft_scores(w.qp, w.kp, w.scores, a.heads, g.g, a.d, a.scale, pa->select_softmax,
+                                                st, fuse_digit0 ? da::select_hist_buffer(w.sel, a.heads, g.g) : nullptr),
+                        "draft_scores")))
+    return rc;
   const double* sel_scores = w.scores;
   int sel_heads = a.heads;
   if (pa->shared_head_mask) {
@@ -229,8 +244,10 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   }
   // a padded grid never has an all-padding region (the last patch of each axis
   // starts inside the real extent), so no dead columns (padding.py:151-153)
-  if ((rc = da_select(sel_scores, sel_heads, g.g, pa->m, pa->force_row_keep, nullptr, w.sel, pa->row_ptr,
-                      pa->col_idx, pa->bitmap, pa->threshold, pa->forced, pa->kept, stream)))
+  if ((rc = cuda_status(da::launch_select(sel_scores, sel_heads, g.g, pa->m, pa->force_row_keep, nullptr, w.sel,
+                                          pa->row_ptr, pa->col_idx, pa->bitmap, pa->threshold, pa->forced, pa->kept,
+                                          da_mask_capacity(g.g, pa->m), st, fuse_digit0),
+                        "select")))
     return rc;
   da_attn_args aa = a;
   aa.row_ptr = pa->row_ptr;

@@ -78,6 +78,16 @@ inline RegionDecoder make_decoder(const Geo& g) {
   return d;
 }
 
+// Order-preserving 64-bit key of a float64 selection score: larger score <=>
+// larger key; -0.0 folded onto +0.0 (they tie, as numpy compares them); NaN
+// below everything (a stable descending argsort puts NaN last).
+DA_DEV unsigned long long score_key(double s) {
+  if (s != s) return 0ull;
+  if (s == 0.0) s = 0.0;
+  unsigned long long b = (unsigned long long)__double_as_longlong(s);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 // Real-token row of reordered position (region i, offset r), or -1 for padding.
 DA_DEV long long real_row(const Geo& g, int i, int r) {
   int f = i / (g.Ph * g.Pw);

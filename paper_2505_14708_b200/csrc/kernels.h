@@ -16,14 +16,20 @@ cudaError_t launch_permute_out(const void* o_r, void* out, long long hs, long lo
                                const Geo& g, cudaStream_t st);
 cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
                         const Geo& g, cudaStream_t st);
+// pools two tensors (Q and K) in one launch
+cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
+                         long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st);
+// hist0 (optional): per-head 2048-bin histogram of the top 11 key bits, filled in the epilogue
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
-                                double scale, int softmax, cudaStream_t st);
+                                double scale, int softmax, cudaStream_t st, unsigned int* hist0 = nullptr);
 
 size_t select_workspace_size(int heads, int g);
 long long bitmap_bytes_per_head(int g);
+unsigned int* select_hist_buffer(void* ws, int heads, int g);
+void select_init(void* ws, int heads, int g, long long m, cudaStream_t st);
 cudaError_t launch_select(const double* scores, int heads, int g, long long m, int force, const uint8_t* dead,
                           void* ws, int* row_ptr, int* col_idx, uint8_t* bitmap, double* threshold,
-                          int64_t* forced, int64_t* kept, long long cap, cudaStream_t st);
+                          int64_t* forced, int64_t* kept, long long cap, cudaStream_t st, bool digit0_done = false);
 
 size_t portable_smem_bytes(int p, int d, int dv);
 cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st);

@@ -2,8 +2,9 @@
 //
 // K1/K5 and K2 are HBM-bound: one CTA per (head, region) moves the region's p
 // rows with 16-byte vector accesses; the region's coordinates are decoded once
-// per CTA so the per-chunk index math is a shift and an add. K3a is a small
-// float64 GEMM (g x d x g per head) tiled through shared memory.
+// per CTA. K3a is a float64 GEMM (g x d x g per head): 128 x 128 output tiles,
+// 8 x 8 register blocking, k-chunks staged through shared memory; its epilogue
+// can also histogram the top 11 bits of the selection keys (digit 0 of K3b).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -13,22 +14,24 @@ namespace da {
 // K1 / K5
 // ---------------------------------------------------------------------------
 struct RegionCoord {
-  int f, y0, x0;
+  int f, y0, x0, vy, vx;  // frame, first row / column, valid rows / columns
 };
 
 DA_DEV RegionCoord region_coord(const Geo& g, int i) {
   int f = i / (g.Ph * g.Pw);
   int rest = i - f * g.Ph * g.Pw;
   int a = rest / g.Pw, b = rest - a * g.Pw;
-  return {f, a * g.ph, b * g.pw};
+  RegionCoord rc{f, a * g.ph, b * g.pw, 0, 0};
+  rc.vy = min(g.ph, g.H - rc.y0);
+  rc.vx = min(g.pw, g.W - rc.x0);
+  return rc;
 }
 
 // Real row of offset r inside the region, or -1.
 DA_DEV long long region_real_row(const Geo& g, const RegionCoord& rc, int r) {
   int u = r / g.pw, v = r - u * g.pw;
-  int y = rc.y0 + u, x = rc.x0 + v;
-  if (y >= g.H || x >= g.W) return -1;
-  return ((long long)rc.f * g.H + y) * g.W + x;
+  if (u >= rc.vy || v >= rc.vx) return -1;
+  return ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
 }
 
 // grid: (g regions, heads); block 256. d8 = d / 8 sixteen-byte chunks per row.
@@ -67,113 +70,139 @@ __global__ void __launch_bounds__(256) permute_out_kernel(const uint4* __restric
 // ---------------------------------------------------------------------------
 // K2 pooling: float64 sums of bf16 values (exact), one division by the valid
 // count (padding.py:91-92), or a coordinatewise max (pooling.py:31-32).
-// grid: (g, heads); block 256 = RG row groups x d8 column chunks.
+// grid: (g, heads, tensors); block = RG row groups x d8 column chunks. Up to
+// two tensors (Q and K) per launch.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restrict__ x, long long head_stride,
-                                                   long long row_stride, double* __restrict__ pooled, int d,
-                                                   int mode, Geo g) {
+struct PoolSrc {
+  const __nv_bfloat16* x[2];
+  long long hs[2], rs[2];
+  double* out[2];
+};
+
+__global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode, Geo g) {
   extern __shared__ double red[];  // [RG][d]
-  const int i = blockIdx.x, h = blockIdx.y;
+  const int i = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
   const int d8 = d / 8;
-  const int RG = blockDim.x / d8;  // row groups
+  const int RG = blockDim.x / d8;
   const int tid = threadIdx.x;
   const int k = tid % d8, rg = tid / d8;
   const RegionCoord rc = region_coord(g, i);
-  const __nv_bfloat16* src = x + h * head_stride;
+  const __nv_bfloat16* base = src.x[z] + h * src.hs[z];
+  const long long rs = src.rs[z];
   double acc[8];
   const double init = mode == 0 ? 0.0 : -INFINITY;
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = init;
-  int count = 0;
-  if (rg < RG) {
-    for (int r = rg; r < g.p; r += RG) {
-      long long row = region_real_row(g, rc, r);
-      if (row < 0) continue;
-      ++count;
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(src + row * row_stride) + k);
-      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+  // rows of the region: (u, v) with u < vy, v < vx, visited as r = u*pw + v
+  for (int r = rg; r < g.p; r += RG) {
+    const int u = r / g.pw, v = r - u * g.pw;
+    if (u >= rc.vy || v >= rc.vx) continue;
+    const long long row = ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
+    uint4 q = __ldg(reinterpret_cast<const uint4*>(base + row * rs) + k);
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&q);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        double xv = (double)__bfloat162float(b[e]);
-        acc[e] = mode == 0 ? acc[e] + xv : fmax(acc[e], xv);
-      }
+    for (int e = 0; e < 8; ++e) {
+      const double xv = (double)__bfloat162float(b[e]);
+      acc[e] = mode == 0 ? acc[e] + xv : fmax(acc[e], xv);
     }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) red[rg * d + k * 8 + e] = acc[e];
   }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[rg * d + k * 8 + e] = acc[e];
   __syncthreads();
-  // valid count of the region (closed form, same for every column)
-  if (tid < d) {
-    const int vy = min(g.ph, g.H - rc.y0), vx = min(g.pw, g.W - rc.x0);
-    const int cnt = vy * vx;
-    double s = red[tid];
-    for (int q = 1; q < RG; ++q) s = mode == 0 ? s + red[q * d + tid] : fmax(s, red[q * d + tid]);
+  for (int c = tid; c < d; c += blockDim.x) {
+    const int cnt = rc.vy * rc.vx;
+    double s = red[c];
+    for (int q = 1; q < RG; ++q) s = mode == 0 ? s + red[q * d + c] : fmax(s, red[q * d + c]);
     double outv;
-    if (mode == 0) {
-      outv = s / (double)(cnt > 1 ? cnt : 1);
-    } else {
-      outv = cnt > 0 ? s : 0.0;
-    }
-    pooled[((long long)h * g.g + i) * d + tid] = outv;
+    if (mode == 0) outv = s / (double)(cnt > 1 ? cnt : 1);
+    else outv = cnt > 0 ? s : 0.0;
+    src.out[z][((long long)h * g.g + i) * d + c] = outv;
   }
-  (void)count;
 }
 
 // ---------------------------------------------------------------------------
 // K3a: scores[h] = (qp[h] kp[h]^T) * scale in float64.
-// 64x64 output tile per CTA, 256 threads, 4x4 outputs per thread, k-chunks of
-// 16 staged in shared memory (transposed so the inner loop reads broadcast-
-// free float64 pairs).
+// 128x128 output tile per CTA, 256 threads (16 x 16), 8 x 8 outputs per thread
+// at stride 16 (broadcast / conflict-free shared reads), k-chunks of 8 with a
+// register prefetch of the next chunk.
 // ---------------------------------------------------------------------------
-constexpr int DT = 64, DK = 16;
+constexpr int DT = 128, DK = 8;
+
 __global__ void __launch_bounds__(256) draft_gemm_kernel(const double* __restrict__ qp, const double* __restrict__ kp,
-                                                         double* __restrict__ scores, int g, int d, double scale) {
-  __shared__ double sq[DK][DT + 1];
-  __shared__ double sk[DK][DT + 1];
+                                                         double* __restrict__ scores, int g, int d, double scale,
+                                                         unsigned int* __restrict__ hist0) {
+  __shared__ double sq[DK][DT];
+  __shared__ double sk[DK][DT];
+  __shared__ unsigned int sh[2048];
   const int h = blockIdx.z;
   const int i0 = blockIdx.y * DT, j0 = blockIdx.x * DT;
   const double* Q = qp + (long long)h * g * d;
   const double* K = kp + (long long)h * g * d;
   const int tid = threadIdx.x;
-  const int ty = tid / 16, tx = tid % 16;  // 16 x 16 threads, 4 x 4 outputs each
-  double acc[4][4];
+  const int ty = tid >> 4, tx = tid & 15;
+  if (hist0)
+    for (int b = tid; b < 2048; b += 256) sh[b] = 0;
+  // loader mapping: 1024 doubles per operand chunk -> 4 per thread
+  // element e = tid + 256*t: row = e / DK, col = e % DK
+  double pq[4], pk[4];
+  auto load = [&](int k0) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int t = 0; t < 4; ++t) {
+      const int e = tid + 256 * t;
+      const int r = e / DK, c = e % DK;
+      const int kk = k0 + c;
+      pq[t] = (i0 + r < g && kk < d) ? __ldg(Q + (long long)(i0 + r) * d + kk) : 0.0;
+      pk[t] = (j0 + r < g && kk < d) ? __ldg(K + (long long)(j0 + r) * d + kk) : 0.0;
+    }
+  };
+  double acc[8][8];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+  load(0);
   for (int k0 = 0; k0 < d; k0 += DK) {
-    for (int e = tid; e < DT * DK; e += 256) {
-      int r = e / DK, c = e % DK;
-      int gi = i0 + r, gj = j0 + r, kk = k0 + c;
-      sq[c][r] = (gi < g && kk < d) ? Q[(long long)gi * d + kk] : 0.0;
-      sk[c][r] = (gj < g && kk < d) ? K[(long long)gj * d + kk] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = tid + 256 * t;
+      sq[e % DK][e / DK] = pq[t];
+      sk[e % DK][e / DK] = pk[t];
     }
     __syncthreads();
+    if (k0 + DK < d) load(k0 + DK);
 #pragma unroll
     for (int c = 0; c < DK; ++c) {
-      double a[4], b[4];
+      double a[8], b[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = sq[c][ty + 16 * u];
-        b[u] = sk[c][tx + 16 * u];
-      }
+      for (int u = 0; u < 8; ++u) a[u] = sq[c][ty + 16 * u];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int v = 0; v < 8; ++v) b[v] = sk[c][tx + 16 * v];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
     }
-    __syncthreads();
   }
   double* S = scores + (long long)h * g * g;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    int gi = i0 + ty + 16 * u;
+  for (int u = 0; u < 8; ++u) {
+    const int gi = i0 + ty + 16 * u;
     if (gi >= g) continue;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      int gj = j0 + tx + 16 * v;
-      if (gj < g) S[(long long)gi * g + gj] = acc[u][v] * scale;
+    for (int v = 0; v < 8; ++v) {
+      const int gj = j0 + tx + 16 * v;
+      if (gj < g) {
+        const double s = acc[u][v] * scale;
+        S[(long long)gi * g + gj] = s;
+        if (hist0) atomicAdd(&sh[(unsigned)(score_key(s) >> 53)], 1u);
+      }
     }
+  }
+  if (hist0) {
+    __syncthreads();
+    for (int b = tid; b < 2048; b += 256)
+      if (sh[b]) atomicAdd(&hist0[(long long)h * 2048 + b], sh[b]);
   }
 }
 
@@ -215,25 +244,36 @@ cudaError_t launch_permute_out(const void* o_r, void* out, long long hs, long lo
   return cudaGetLastError();
 }
 
-cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
-                        const Geo& g, cudaStream_t st) {
-  int d8 = d / 8;
+cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
+                         long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st) {
+  PoolSrc src;
+  src.x[0] = static_cast<const __nv_bfloat16*>(x0);
+  src.hs[0] = hs0; src.rs[0] = rs0; src.out[0] = out0;
+  src.x[1] = static_cast<const __nv_bfloat16*>(x1 ? x1 : x0);
+  src.hs[1] = x1 ? hs1 : hs0; src.rs[1] = x1 ? rs1 : rs0; src.out[1] = x1 ? out1 : out0;
+  const int d8 = d / 8;
   int rg = 256 / d8;
   if (rg < 1) rg = 1;
-  int threads = rg * d8;
-  size_t smem = sizeof(double) * rg * d;
+  const int threads = rg * d8;
+  const size_t smem = sizeof(double) * rg * d;
   if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
   }
-  dim3 grid(g.g, heads);
-  pool_kernel<<<grid, threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), hs, rs, pooled, d, mode, g);
+  dim3 grid(g.g, heads, x1 ? 2 : 1);
+  pool_kernel<<<grid, threads, smem, st>>>(src, d, mode, g);
   return cudaGetLastError();
 }
 
+cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
+                        const Geo& g, cudaStream_t st) {
+  return launch_pool2(x, hs, rs, pooled, nullptr, 0, 0, nullptr, heads, d, mode, g, st);
+}
+
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
-                                double scale, int softmax, cudaStream_t st) {
+                                double scale, int softmax, cudaStream_t st, unsigned int* hist0) {
   dim3 grid((g + DT - 1) / DT, (g + DT - 1) / DT, heads);
-  draft_gemm_kernel<<<grid, 256, 0, st>>>(qp, kp, scores, g, d, scale);
+  draft_gemm_kernel<<<grid, 256, 0, st>>>(qp, kp, scores, g, d, scale, softmax ? nullptr : hist0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !softmax) return e;
   long long rows = (long long)heads * g;
