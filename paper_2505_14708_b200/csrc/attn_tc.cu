@@ -225,9 +225,12 @@ __global__ void __launch_bounds__(384, 1)
   // registers: the producer / MMA warpgroup hands its budget to the softmax warpgroups
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-  if (warp == 0) {
-    // ============================ TMA producer ============================
+  if (warp == 0 || warp == 2) {
+    // ================= TMA producers: warp 0 = Q and K, warp 2 = V =================
+    // Separate threads so the K ring (freed right after GEMM1) is never held
+    // back by the V ring (freed only after the softmax and GEMM2).
     if (lane == 0) {
+      const bool is_k = warp == 0;
       Cursor c[NWG];
       int qi[NWG];
       for (int w = 0; w < NWG; ++w) {
@@ -235,40 +238,42 @@ __global__ void __launch_bounds__(384, 1)
         qi[w] = 0;
         cursor_seek(c[w], p, items);
       }
-      int kq = 0, vq = 0;
+      int kq = 0;
       while (c[0].active || c[1].active) {
 #pragma unroll
         for (int w = 0; w < NWG; ++w) {
           if (!c[w].active) continue;
           Cursor& cu = c[w];
           WgBars& wb = B.wg[w];
-          if (cu.t == 0) {
-            if (qi[w] > 0) mbar_wait(&wb.q_empty, (qi[w] - 1) & 1);
-            mbar_expect_tx(&wb.q_full, Q_BYTES);
-            uint8_t* q = sQ + w * Q_BYTES;
-            load_region(&tm_q, q, &wb.q_full, p, cu.item.h, cu.item.i, 0, L2_EVICT_FIRST);
-            load_region(&tm_q, q + BOX, &wb.q_full, p, cu.item.h, cu.item.i, 1, L2_EVICT_FIRST);
-          }
           const int j0 = cu.item.cols[2 * cu.t];
           const int j1 = (2 * cu.t + 1 < cu.item.n) ? cu.item.cols[2 * cu.t + 1] : j0;
-          const int ks = kq % KST;
-          if (kq >= KST) mbar_wait(&B.k_empty[ks], ((kq / KST) - 1) & 1);
-          uint8_t* kb = sK + ks * KV_BYTES;  // [half][slot][64 x 128B]
-          mbar_expect_tx(&B.k_full[ks], KV_BYTES);
-          load_region(&tm_k, kb, &B.k_full[ks], p, cu.item.h, j0, 0);
-          load_region(&tm_k, kb + BOX, &B.k_full[ks], p, cu.item.h, j1, 0);
-          load_region(&tm_k, kb + 2 * BOX, &B.k_full[ks], p, cu.item.h, j0, 1);
-          load_region(&tm_k, kb + 3 * BOX, &B.k_full[ks], p, cu.item.h, j1, 1);
+          if (is_k) {
+            if (cu.t == 0) {
+              if (qi[w] > 0) mbar_wait(&wb.q_empty, (qi[w] - 1) & 1);
+              mbar_expect_tx(&wb.q_full, Q_BYTES);
+              uint8_t* q = sQ + w * Q_BYTES;
+              load_region(&tm_q, q, &wb.q_full, p, cu.item.h, cu.item.i, 0, L2_EVICT_FIRST);
+              load_region(&tm_q, q + BOX, &wb.q_full, p, cu.item.h, cu.item.i, 1, L2_EVICT_FIRST);
+            }
+            const int ks = kq % KST;
+            if (kq >= KST) mbar_wait(&B.k_empty[ks], ((kq / KST) - 1) & 1);
+            uint8_t* kb = sK + ks * KV_BYTES;  // [half][slot][64 x 128B]
+            mbar_expect_tx(&B.k_full[ks], KV_BYTES);
+            load_region(&tm_k, kb, &B.k_full[ks], p, cu.item.h, j0, 0);
+            load_region(&tm_k, kb + BOX, &B.k_full[ks], p, cu.item.h, j1, 0);
+            load_region(&tm_k, kb + 2 * BOX, &B.k_full[ks], p, cu.item.h, j0, 1);
+            load_region(&tm_k, kb + 3 * BOX, &B.k_full[ks], p, cu.item.h, j1, 1);
+          } else {
+            const int vs = kq % VST;
+            if (kq >= VST) mbar_wait(&B.v_empty[vs], ((kq / VST) - 1) & 1);
+            uint8_t* vb = sV + vs * KV_BYTES;  // [slot][half][64 x 128B]
+            mbar_expect_tx(&B.v_full[vs], KV_BYTES);
+            load_region(&tm_v, vb, &B.v_full[vs], p, cu.item.h, j0, 0);
+            load_region(&tm_v, vb + BOX, &B.v_full[vs], p, cu.item.h, j0, 1);
+            load_region(&tm_v, vb + 2 * BOX, &B.v_full[vs], p, cu.item.h, j1, 0);
+            load_region(&tm_v, vb + 3 * BOX, &B.v_full[vs], p, cu.item.h, j1, 1);
+          }
           ++kq;
-          const int vs = vq % VST;
-          if (vq >= VST) mbar_wait(&B.v_empty[vs], ((vq / VST) - 1) & 1);
-          uint8_t* vb = sV + vs * KV_BYTES;  // [slot][half][64 x 128B]
-          mbar_expect_tx(&B.v_full[vs], KV_BYTES);
-          load_region(&tm_v, vb, &B.v_full[vs], p, cu.item.h, j0, 0);
-          load_region(&tm_v, vb + BOX, &B.v_full[vs], p, cu.item.h, j0, 1);
-          load_region(&tm_v, vb + 2 * BOX, &B.v_full[vs], p, cu.item.h, j1, 0);
-          load_region(&tm_v, vb + 3 * BOX, &B.v_full[vs], p, cu.item.h, j1, 1);
-          ++vq;
           if (++cu.t == cu.steps) {
             ++qi[w];
             cu.k += NWG;
