@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(384, 1)
 
   // registers: the producer / MMA warpgroup hands its budget to the softmax warpgroups
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
   if (warp == 0 || warp == 2) {
     // ================= TMA producers: warp 0 = Q and K, warp 2 = V =================
     // Separate threads so the K ring (freed right after GEMM1) is never held
@@ -302,12 +302,15 @@ __global__ void __launch_bounds__(384, 1)
         cursor_seek(c[w], p, items);
       }
       int kq = 0, vq = 0;
+      // GEMM2 of a warpgroup's step is issued after the GEMM1 of its NEXT step,
+      // so S(t+1) is computed while the softmax of step t runs (per-warpgroup
+      // lookahead); issue order stays the global step order, as the V ring needs
       struct Pend {
         int w, qi;
         long long G;
         bool first, last, valid;
-      } pend;
-      pend.valid = false;
+      } pend[NWG];
+      for (int w = 0; w < NWG; ++w) pend[w].valid = false;
       auto gemm2 = [&](const Pend& s) {
         WgBars& wb = B.wg[s.w];
         const int vs = vq % VST;
@@ -333,7 +336,13 @@ __global__ void __launch_bounds__(384, 1)
       while (c[0].active || c[1].active) {
 #pragma unroll
         for (int w = 0; w < NWG; ++w) {
-          if (!c[w].active) continue;
+          if (!c[w].active) {
+            if (pend[w].valid) {  // this warpgroup has no more steps: retire its last GEMM2 in order
+              gemm2(pend[w]);
+              pend[w].valid = false;
+            }
+            continue;
+          }
           Cursor& cu = c[w];
           WgBars& wb = B.wg[w];
           if (cu.t == 0) mbar_wait(&wb.q_full, qi[w] & 1);
@@ -355,13 +364,13 @@ __global__ void __launch_bounds__(384, 1)
           umma_commit(&wb.s_full[b]);
           if (cu.t == cu.steps - 1) umma_commit(&wb.q_empty);
           ++kq;
-          if (pend.valid) gemm2(pend);
-          pend.w = w;
-          pend.qi = qi[w];
-          pend.G = G[w];
-          pend.first = cu.t == 0;
-          pend.last = cu.t == cu.steps - 1;
-          pend.valid = true;
+          if (pend[w].valid) gemm2(pend[w]);
+          pend[w].w = w;
+          pend[w].qi = qi[w];
+          pend[w].G = G[w];
+          pend[w].first = cu.t == 0;
+          pend[w].last = cu.t == cu.steps - 1;
+          pend[w].valid = true;
           ++G[w];
           if (++cu.t == cu.steps) {
             ++qi[w];
@@ -370,11 +379,12 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
       }
-      if (pend.valid) gemm2(pend);
+      for (int w = 0; w < NWG; ++w)
+        if (pend[w].valid) gemm2(pend[w]);
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ===================== softmax / epilogue warpgroups ====================
     const int wg = (warp - 4) >> 2;
     const int tid = threadIdx.x - 128 - wg * 128;  // key / feature lane 0..127
@@ -427,8 +437,6 @@ __global__ void __launch_bounds__(384, 1)
         const float vf = valid ? 1.f : 0.f;
         const uint32_t vmask = valid ? 0xffffffffu : 0u;
         mbar_wait(&wb.s_full[b], (uint32_t)((G >> 1) & 1));
-        // P^T rows go to a buffer that is free once the previous step's GEMM2 consumed it
-        if (G >= 1) mbar_wait(&wb.p_free, (uint32_t)((G - 1) & 1));
         tc_fence_after();
         const uint32_t sa = tbase + b * 64;
         const uint32_t prow = smem_u32(myP) + tid * 128;
@@ -479,7 +487,9 @@ __global__ void __launch_bounds__(384, 1)
                 l2[hf * 16 + c].y *= X.alpha[hf * 32 + 2 * c + 1];
               }
               if (t > 0) {
-                // O^T holds GEMM2 results up to the previous step (p_free waited above)
+                // O^T holds GEMM2 results up to the previous step: wait, rescale these columns
+                mbar_wait(&wb.p_free, (uint32_t)((G - 1) & 1));
+                tc_fence_after();
                 float o[32];
                 const uint32_t oa = tO + hf * 32;
                 tmem_ld32(oa, o);
@@ -495,20 +505,20 @@ __global__ void __launch_bounds__(384, 1)
             for (int c = 0; c < 32; ++c) x[c] = any ? x[c] + X.neg_m[hf * 32 + c] : -INFINITY;
           }
           // probabilities of my key for these 32 queries -> P^T row (128B-swizzled, MN-major)
+          uint32_t w16[16];
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            uint32_t w4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c = cc * 8 + 2 * e;
-              const float p0 = fast_exp2(x[c]);
-              const float p1 = fast_exp2(x[c + 1]);
-              l2[hf * 16 + c / 2] = ffma2(make_float2(p0, p1), make_float2(vf, vf), l2[hf * 16 + c / 2]);
-              w4[e] = pack_bf16(p0, p1) & vmask;
-            }
-            const int chunk = hf * 4 + cc;
-            sts128(prow + ((chunk ^ (tid & 7)) << 4), w4[0], w4[1], w4[2], w4[3]);
+          for (int c = 0; c < 32; c += 2) {
+            const float p0 = fast_exp2(x[c]);
+            const float p1 = fast_exp2(x[c + 1]);
+            l2[hf * 16 + c / 2] = ffma2(make_float2(p0, p1), make_float2(vf, vf), l2[hf * 16 + c / 2]);
+            w16[c / 2] = pack_bf16(p0, p1) & vmask;
           }
+          // the P^T buffer is free once the previous step's GEMM2 has consumed it
+          if (hf == 0 && G >= 1) mbar_wait(&wb.p_free, (uint32_t)((G - 1) & 1));
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            sts128(prow + (((hf * 4 + cc) ^ (tid & 7)) << 4), w16[4 * cc], w16[4 * cc + 1], w16[4 * cc + 2],
+                   w16[4 * cc + 3]);
         }
         if (!mvalid) mvalid = X.neg_m[0] != INFINITY;
         fence_proxy_async_smem();
