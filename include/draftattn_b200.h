@@ -175,6 +175,12 @@ size_t da_pipeline_workspace_size(const da_grid* grid, int32_t heads, int32_t d)
 int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask);
 int da_sparse_attention(const da_pipeline_args* args, const da_grid* grid, void* stream);
 
+/* ---- Diagnostics -------------------------------------------------------------
+ * While set, the tcgen05 kernel of CTA 0 records clock64() stamps of its
+ * pipeline events (16 event rows x 1024 steps, int64) into this device buffer.
+ * NULL disables. Not thread-safe; for profiling only. */
+int da_debug_trace(void* device_buffer);
+
 #ifdef __cplusplus
 }
 #endif

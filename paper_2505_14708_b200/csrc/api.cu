@@ -42,6 +42,11 @@ extern "C" {
 
 int32_t da_version(void) { return 100; }
 
+int da_debug_trace(void* device_buffer) {
+  da::set_tc_trace(device_buffer);
+  return DA_OK;
+}
+
 const char* da_last_error(void) { return g_err.c_str(); }
 
 int32_t da_num_regions(const da_grid* grid) {

@@ -74,7 +74,15 @@ struct Params {
   RegionDecoder dec;
   FastDiv per_head;  // g
   long long n_pad;
+  long long* trace;  // diagnostics: per-step clock64 stamps of CTA 0 (nullptr = off)
 };
+
+constexpr int TRACE_N = 1024;
+#define DA_TRACE(ev, idx)                                                     \
+  do {                                                                        \
+    if (p.trace != nullptr && blockIdx.x == 0 && (idx) < TRACE_N)             \
+      p.trace[(ev) * TRACE_N + (idx)] = (long long)clock64();                 \
+  } while (0)
 
 struct WgBars {
   uint64_t q_full, q_empty;
@@ -257,6 +265,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             const int ks = kq % KST;
             if (kq >= KST) mbar_wait(&B.k_empty[ks], ((kq / KST) - 1) & 1);
+            DA_TRACE(0, kq);
             uint8_t* kb = sK + ks * KV_BYTES;  // [half][slot][64 x 128B]
             mbar_expect_tx(&B.k_full[ks], KV_BYTES);
             load_region(&tm_k, kb, &B.k_full[ks], p, cu.item.h, j0, 0);
@@ -266,6 +275,7 @@ __global__ void __launch_bounds__(384, 1)
           } else {
             const int vs = kq % VST;
             if (kq >= VST) mbar_wait(&B.v_empty[vs], ((kq / VST) - 1) & 1);
+            DA_TRACE(1, kq);
             uint8_t* vb = sV + vs * KV_BYTES;  // [slot][half][64 x 128B]
             mbar_expect_tx(&B.v_full[vs], KV_BYTES);
             load_region(&tm_v, vb, &B.v_full[vs], p, cu.item.h, j0, 0);
@@ -315,7 +325,9 @@ __global__ void __launch_bounds__(384, 1)
         WgBars& wb = B.wg[s.w];
         const int vs = vq % VST;
         mbar_wait(&B.v_full[vs], (vq / VST) & 1);
+        DA_TRACE(3, vq);
         mbar_wait(&wb.p_full, (uint32_t)(s.G & 1));
+        DA_TRACE(4, vq);
         const int ob = s.qi & 1;  // O buffer of this item
         if (s.first && s.qi >= 2) mbar_wait(&wb.o_empty[ob], ((s.qi >> 1) - 1) & 1);
         tc_fence_after();
@@ -347,7 +359,9 @@ __global__ void __launch_bounds__(384, 1)
           WgBars& wb = B.wg[w];
           if (cu.t == 0) mbar_wait(&wb.q_full, qi[w] & 1);
           const int ks = kq % KST;
+          DA_TRACE(15, kq);
           mbar_wait(&B.k_full[ks], (kq / KST) & 1);
+          DA_TRACE(2, kq);
           const int b = (int)(G[w] & 1);
           if (G[w] >= 2) mbar_wait(&wb.s_free[b], (uint32_t)(((G[w] >> 1) - 1) & 1));
           tc_fence_after();
@@ -436,7 +450,9 @@ __global__ void __launch_bounds__(384, 1)
         }
         const float vf = valid ? 1.f : 0.f;
         const uint32_t vmask = valid ? 0xffffffffu : 0u;
+        if (tid == 0) DA_TRACE(11 + 3 * wg, G);
         mbar_wait(&wb.s_full[b], (uint32_t)((G >> 1) & 1));
+        if (tid == 0) DA_TRACE(5 + 3 * wg, G);
         tc_fence_after();
         const uint32_t sa = tbase + b * 64;
         const uint32_t prow = smem_u32(myP) + tid * 128;
@@ -514,6 +530,7 @@ __global__ void __launch_bounds__(384, 1)
             w16[c / 2] = pack_bf16(p0, p1) & vmask;
           }
           // the P^T buffer is free once the previous step's GEMM2 has consumed it
+          if (hf == 0 && tid == 0) DA_TRACE(6 + 3 * wg, G);
           if (hf == 0 && G >= 1) mbar_wait(&wb.p_free, (uint32_t)((G - 1) & 1));
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc)
@@ -524,6 +541,7 @@ __global__ void __launch_bounds__(384, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&wb.p_full);
+        if (tid == 0) DA_TRACE(7 + 3 * wg, G);
         mbar_arrive(&wb.s_free[b]);
         ++G;
       }
@@ -582,6 +600,9 @@ __global__ void __launch_bounds__(384, 1)
 // ---------------------------------------------------------------------------
 // host side: tensor maps + launch
 // ---------------------------------------------------------------------------
+static long long* g_trace = nullptr;  // diagnostics (da_debug_trace)
+void set_tc_trace(void* buf) { g_trace = static_cast<long long*>(buf); }
+
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -675,6 +696,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   p.dec = make_decoder(g);
   p.per_head = make_fastdiv((uint32_t)g.g);
   p.n_pad = g.n_pad;
+  p.trace = g_trace;
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;

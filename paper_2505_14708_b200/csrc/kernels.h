@@ -34,6 +34,7 @@ cudaError_t launch_select(const double* scores, int heads, int g, long long m, i
 size_t portable_smem_bytes(int p, int d, int dv);
 cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st);
 
+void set_tc_trace(void* buf);
 bool tc_supported(const da_attn_args& a, const Geo& g);
 cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why);
 
