@@ -38,7 +38,7 @@ constexpr int P = 64;            // region size
 constexpr int D = 128;           // head dim
 constexpr int NWG = 2;           // softmax warpgroups
 constexpr int KST = 2;           // K ring stages (one pair of key regions each)
-constexpr int VST = 2;           // V ring stages
+constexpr int VST = 3;           // V ring stages (V is recycled only after the softmax + GEMM2)
 constexpr int BOX = 64 * 128;    // one TMA box: 64 rows x 64 bf16 = 8 KB
 constexpr int Q_BYTES = 2 * BOX;
 constexpr int KV_BYTES = 4 * BOX;   // two regions x two feature halves
@@ -50,7 +50,8 @@ constexpr int SMEM_K = SMEM_Q + NWG * Q_BYTES;
 constexpr int SMEM_V = SMEM_K + KST * KV_BYTES;
 constexpr int SMEM_P = SMEM_V + VST * KV_BYTES;
 constexpr int SMEM_END = SMEM_P + NWG * P_BYTES;
-constexpr int SMEM_ALLOC = SMEM_END + 1024;  // + alignment slack
+// barriers and softmax state follow the tiles in dynamic shared memory (no
+// static shared memory, so the dynamic window starts 1024-byte aligned)
 
 constexpr uint32_t TMEM_COLS = 512;
 // per warpgroup: S0 [0,64), S1 [64,128), O0 [128,192), O1 [192,256); the O
@@ -98,13 +99,15 @@ struct __align__(8) Bars {
 struct __align__(16) WgAux {
   float neg_m[P];  // -(running column max), log2 units (read as float2)
   float alpha[P];
-  float red[4][P];
+  float red[4][P / 2];  // per-warp column partials of one 32-column half
 };
 struct SmemAux {
   Bars bars;
   uint32_t tmem_base;
   WgAux wg[NWG];
 };
+constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
+static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
 
 struct Item {
   int h, i, n;
@@ -194,9 +197,9 @@ DA_DEV float warp_col_reduce32(float (&v)[32], int lane) {
 __global__ void __launch_bounds__(384, 1)
     sparse_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ SmemAux aux;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();  // SWIZZLE_128B tiles need 1024-byte alignment
+  SmemAux& aux = *reinterpret_cast<SmemAux*>(smem + SMEM_END);
   Bars& B = aux.bars;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -484,12 +487,13 @@ __global__ void __launch_bounds__(384, 1)
               float tmp[32];
 #pragma unroll
               for (int c = 0; c < 32; ++c) tmp[c] = x[c];
-              X.red[q4][hf * 32 + lane] = warp_col_reduce32<true>(tmp, lane);
+              X.red[q4][lane] = warp_col_reduce32<true>(tmp, lane);
             }
             bar_sync(bar_id, 128);
             if (tid < 32) {
               const int c = hf * 32 + tid;
-              const float ms = fmaxf(fmaxf(X.red[0][c], X.red[1][c]), fmaxf(X.red[2][c], X.red[3][c]));
+              const float ms =
+                  fmaxf(fmaxf(X.red[0][tid], X.red[1][tid]), fmaxf(X.red[2][tid], X.red[3][tid]));
               const float mold = mvalid ? -X.neg_m[c] : -INFINITY;
               const float mnew = fmaxf(mold, ms);
               X.alpha[c] = (mold == -INFINITY || mnew == -INFINITY) ? 0.f : exp2f(mold - mnew);
@@ -554,12 +558,14 @@ __global__ void __launch_bounds__(384, 1)
           tmp[2 * c] = l2[hf * 16 + c].x;
           tmp[2 * c + 1] = l2[hf * 16 + c].y;
         }
-        X.red[q4][hf * 32 + lane] = warp_col_reduce32<false>(tmp, lane);
+        const float part = warp_col_reduce32<false>(tmp, lane);
+        bar_sync(bar_id, 128);  // previous readers of red are done
+        X.red[q4][lane] = part;
+        bar_sync(bar_id, 128);
+        if (tid < 32) X.alpha[hf * 32 + tid] = X.red[0][tid] + X.red[1][tid] + X.red[2][tid] + X.red[3][tid];
       }
       mbar_wait(&wb.o_full[ob], (uint32_t)((qi >> 1) & 1));
       tc_fence_after();
-      bar_sync(bar_id, 128);
-      if (tid < P) X.alpha[tid] = X.red[0][tid] + X.red[1][tid] + X.red[2][tid] + X.red[3][tid];
       bar_sync(bar_id, 128);
       // O^T row d = tid -> normalised bf16 into the staging tile [64 q][128 d]
       __nv_bfloat16* stage = reinterpret_cast<__nv_bfloat16*>(myP);
