@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(384, 1)
       auto gemm2 = [&](const Pend& s) {
         WgBars& wb = B.wg[s.w];
         const int vs = vq % VST;
+        DA_TRACE(13, vq);
         mbar_wait(&B.v_full[vs], (vq / VST) & 1);
         DA_TRACE(3, vq);
         mbar_wait(&wb.p_full, (uint32_t)(s.G & 1));
@@ -367,6 +368,7 @@ __global__ void __launch_bounds__(384, 1)
           DA_TRACE(2, kq);
           const int b = (int)(G[w] & 1);
           if (G[w] >= 2) mbar_wait(&wb.s_free[b], (uint32_t)(((G[w] >> 1) - 1) & 1));
+          DA_TRACE(12, kq);
           tc_fence_after();
           const uint32_t kbase = aK + ks * (KV_BYTES >> 4);
           const uint32_t qbase = aQ + w * (Q_BYTES >> 4);

@@ -31,10 +31,10 @@ _lib.lib().da_debug_trace(None)
 t = tr.cpu().numpy()
 base = t[0, 0]
 rel = lambda x: int(x - base) if x else -1  # noqa: E731
-print("global step k: Kissue Vissue MMAwaitK MMAgotK | gemm2#k waitP gotP")
+print("global step k: Kissue Vissue MMAwaitK MMAgotK MMAgotSfree | gemm2#k waitV gotV(waitP) gotP")
 for kk in range(200, 232):
-    print(f"k={kk:4d}: {rel(t[0, kk]):9d} {rel(t[1, kk]):9d} {rel(t[15, kk]):9d} {rel(t[2, kk]):9d} | "
-          f"{rel(t[3, kk]):9d} {rel(t[4, kk]):9d}")
+    print(f"k={kk:4d}: {rel(t[0, kk]):9d} {rel(t[1, kk]):9d} {rel(t[15, kk]):9d} {rel(t[2, kk]):9d} "
+          f"{rel(t[12, kk]):9d} | {rel(t[13, kk]):9d} {rel(t[3, kk]):9d} {rel(t[4, kk]):9d}")
 for wg, (ws, gs, pw, pa) in enumerate([(11, 5, 6, 7), (14, 8, 9, 10)]):
     print(f"WG{wg} step G: waitS gotS beforePwait arrivedP")
     for G in range(100, 116):
@@ -49,5 +49,6 @@ print("avg cycles/global step (K issue):", float(np.mean(np.diff(t[0, 100:900]))
 print("avg cycles/WG0 step:", float(np.mean(np.diff(t[7, 100:450]))))
 print("WG0 softmax: gotS->arrivedP", avg(5, 7, 100, 450), " waitS->gotS", avg(11, 5, 100, 450),
       " beforePwait->arrivedP", avg(6, 7, 100, 450))
-print("MMA: waitK->gotK", avg(15, 2), " gemm2 waitP->gotP", avg(3, 4))
+print("MMA: waitK->gotK", avg(15, 2), " gotK->gotSfree", avg(2, 12), " gemm2 waitV->gotV", avg(13, 3),
+      " gemm2 waitP->gotP", avg(3, 4))
 print("producer K lead over MMA (K issue -> MMA got K)", avg(0, 2))
