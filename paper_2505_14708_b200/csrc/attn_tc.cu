@@ -28,6 +28,9 @@
 // regions are zero-filled), so the patch permutation of padding.py:139-143
 // costs no extra pass; the epilogue writes rows back in original order
 // (padding.py:157 fused).
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -673,7 +676,27 @@ bool tc_supported(const da_attn_args& a, const Geo& g) {
   return (long long)a.heads * g.g < (1ll << 31);
 }
 
+bool make_kv_maps(const da_attn_args& a, const Geo& g, CUtensorMap* mk, CUtensorMap* mv) {
+  if (a.layout == DA_LAYOUT_REORDERED) {
+    const long long rows = (long long)a.heads * g.n_pad;
+    return make_map_2d(mk, a.k, rows) && make_map_2d(mv, a.v, rows);
+  }
+  return make_map_5d(mk, a.k, a.k_head_stride, a.k_row_stride, g, a.heads) &&
+         make_map_5d(mv, a.v, a.v_head_stride, a.v_row_stride, g, a.heads);
+}
+
+cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
+                             long long* trace);
+
+// Default: region-pair kernel (attn_pair.cu). DA_K4=transposed selects the
+// single-region transposed kernel below (kept for A/B measurements).
 cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why) {
+  static int variant = -1;
+  if (variant < 0) {
+    const char* env = getenv("DA_K4");
+    variant = (env && strcmp(env, "transposed") == 0) ? 1 : 0;
+  }
+  if (variant == 0) return launch_pair_attn(a, g, st, why, g_trace);
   CUtensorMap mq, mk, mv;
   bool ok;
   if (a.layout == DA_LAYOUT_REORDERED) {

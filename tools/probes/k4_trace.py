@@ -1,16 +1,15 @@
 """Probe: per-step pipeline timeline of the tcgen05 kernel (CTA 0, clock64).
 
-Events (rows of the trace buffer, index = step counter of that role):
+Region-pair kernel events (row, index = step counter of that role):
   0 K producer issues K(k)      1 V producer issues V(k)
-  15 MMA waits K(k)             2 MMA got K(k) (GEMM1 issue)
-  3 MMA GEMM2 #v waits P        4 MMA got P (GEMM2 issue)
-  11/14 WG0/WG1 waits S(G)      5/8 WG0/WG1 got S(G)
-  6/9 WG0/WG1 before P-buffer wait   7/10 WG0/WG1 arrived P(G)
+  2 MMA got K(k) (GEMM1 issue)  4 MMA GEMM2 #k issue (after V and P)
+  5 softmax waits S(G)          6 softmax got S(G)          7 softmax arrived P(G)
 """
 import ctypes
 import sys
 from pathlib import Path
 
+import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
@@ -31,24 +30,18 @@ _lib.lib().da_debug_trace(None)
 t = tr.cpu().numpy()
 base = t[0, 0]
 rel = lambda x: int(x - base) if x else -1  # noqa: E731
-print("global step k: Kissue Vissue MMAwaitK MMAgotK MMAgotSfree | gemm2#k waitV gotV(waitP) gotP")
-for kk in range(200, 232):
-    print(f"k={kk:4d}: {rel(t[0, kk]):9d} {rel(t[1, kk]):9d} {rel(t[15, kk]):9d} {rel(t[2, kk]):9d} "
-          f"{rel(t[12, kk]):9d} | {rel(t[13, kk]):9d} {rel(t[3, kk]):9d} {rel(t[4, kk]):9d}")
-for wg, (ws, gs, pw, pa) in enumerate([(11, 5, 6, 7), (14, 8, 9, 10)]):
-    print(f"WG{wg} step G: waitS gotS beforePwait arrivedP")
-    for G in range(100, 116):
-        print(f"G={G:4d}: {rel(t[ws, G]):9d} {rel(t[gs, G]):9d} {rel(t[pw, G]):9d} {rel(t[pa, G]):9d}")
-# averages over steps 100..900
-import numpy as np  # noqa: E402
+print("step: Kissue Vissue MMAgotK GEMM2issue | SMwaitS SMgotS SMarrP")
+for s in range(200, 232):
+    print(f"{s:4d}: {rel(t[0, s]):9d} {rel(t[1, s]):9d} {rel(t[2, s]):9d} {rel(t[4, s]):9d} | "
+          f"{rel(t[5, s]):9d} {rel(t[6, s]):9d} {rel(t[7, s]):9d}")
+
 
 def avg(a, b, lo=100, hi=900):
     return float(np.mean(t[b, lo:hi] - t[a, lo:hi]))
 
-print("avg cycles/global step (K issue):", float(np.mean(np.diff(t[0, 100:900]))))
-print("avg cycles/WG0 step:", float(np.mean(np.diff(t[7, 100:450]))))
-print("WG0 softmax: gotS->arrivedP", avg(5, 7, 100, 450), " waitS->gotS", avg(11, 5, 100, 450),
-      " beforePwait->arrivedP", avg(6, 7, 100, 450))
-print("MMA: waitK->gotK", avg(15, 2), " gotK->gotSfree", avg(2, 12), " gemm2 waitV->gotV", avg(13, 3),
-      " gemm2 waitP->gotP", avg(3, 4))
-print("producer K lead over MMA (K issue -> MMA got K)", avg(0, 2))
+
+print("avg cycles/step (K issue):", float(np.mean(np.diff(t[0, 100:900]))))
+print("avg cycles/step (GEMM1 issue):", float(np.mean(np.diff(t[2, 100:900]))))
+print("softmax: gotS->arrivedP", avg(6, 7), " waitS->gotS", avg(5, 6))
+print("GEMM1 issue -> softmax got S", avg(2, 6), "  arrivedP -> GEMM2 issue", avg(7, 4))
+print("producer K lead (K issue -> GEMM1 issue)", avg(0, 2), " V issue -> GEMM2 issue", avg(1, 4))
