@@ -351,6 +351,36 @@ __global__ void __launch_bounds__(256, 1)
     const float sl2 = p.scale_log2;
     long long G = 0;
     int qi = 0;
+    // Q row of (item, my row) -> TMEM columns [0, 64) as packed bf16 pairs. The
+    // Q of the next nonempty item is written as soon as the current item's last
+    // GEMM1 is done (before this item's epilogue), so the MMA warp can start
+    // the next item while the epilogue runs.
+    auto load_q = [&](const PairItem& itm, int wait_parity) {
+      const int region = half ? itm.b : itm.a;
+      const long long qrow = region < p.geo.g ? token_row(p, region, r) : -1;
+      uint32_t qv[64];
+      if (qrow >= 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + qrow * p.qr);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const uint4 w = __ldg(src + c);
+          qv[4 * c] = w.x; qv[4 * c + 1] = w.y; qv[4 * c + 2] = w.z; qv[4 * c + 3] = w.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) qv[c] = 0u;
+      }
+      if (wait_parity >= 0) mbar_wait(&B.q_empty, (uint32_t)wait_parity);
+      tc_fence_after();
+      tmem_st16u(tq + COL_Q, *reinterpret_cast<uint32_t(*)[16]>(&qv[0]));
+      tmem_st16u(tq + COL_Q + 16, *reinterpret_cast<uint32_t(*)[16]>(&qv[16]));
+      tmem_st16u(tq + COL_Q + 32, *reinterpret_cast<uint32_t(*)[16]>(&qv[32]));
+      tmem_st16u(tq + COL_Q + 48, *reinterpret_cast<uint32_t(*)[16]>(&qv[48]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&B.q_full);
+    };
+    bool have_q = false;
     for (long long it = blockIdx.x;; it += gridDim.x) {
       PairItem itm;
       if (!fetch_pair(p, it, items, itm)) break;
@@ -365,30 +395,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         continue;
       }
-      // ---- Q row -> TMEM columns [0, 64) (packed bf16 pairs), once the previous item's GEMM1s are done
-      {
-        uint32_t qv[64];
-        if (row >= 0) {
-          const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + row * p.qr);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const uint4 w = __ldg(src + c);
-            qv[4 * c] = w.x; qv[4 * c + 1] = w.y; qv[4 * c + 2] = w.z; qv[4 * c + 3] = w.w;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 64; ++c) qv[c] = 0u;
-        }
-        if (qi > 0) mbar_wait(&B.q_empty, (qi - 1) & 1);
-        tc_fence_after();
-        tmem_st16u(tq + COL_Q, *reinterpret_cast<uint32_t(*)[16]>(&qv[0]));
-        tmem_st16u(tq + COL_Q + 16, *reinterpret_cast<uint32_t(*)[16]>(&qv[16]));
-        tmem_st16u(tq + COL_Q + 32, *reinterpret_cast<uint32_t(*)[16]>(&qv[32]));
-        tmem_st16u(tq + COL_Q + 48, *reinterpret_cast<uint32_t(*)[16]>(&qv[48]));
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&B.q_full);
-      }
+      if (!have_q) load_q(itm, -1);  // first nonempty item of this CTA
       float m = -INFINITY, l = 0.f;
       bool mvalid = false;
       UnionWalk u;
@@ -473,6 +480,16 @@ __global__ void __launch_bounds__(256, 1)
         if (t == 0) PAIR_TRACE(7, G);
         first_step = false;
         ++G;
+      }
+      // ---- next nonempty item's Q (its GEMM1s overlap this epilogue)
+      have_q = false;
+      for (long long it2 = it + gridDim.x;; it2 += gridDim.x) {
+        PairItem nx;
+        if (!fetch_pair(p, it2, items, nx)) break;
+        if (nx.na + nx.nb == 0) continue;
+        load_q(nx, qi & 1);  // q_empty completion #qi = this item's last GEMM1
+        have_q = true;
+        break;
       }
       // ------------------------------ epilogue ------------------------------
       mbar_wait(&B.o_full, qi & 1);
