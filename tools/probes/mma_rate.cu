@@ -46,6 +46,58 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int reps, long long* out) {
   }
 }
 
+// A from TMEM (K-major, packed bf16 pairs), B from shared memory.
+template <int N, int BMN>
+__global__ void __launch_bounds__(128, 1) mma_rate_ts(int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tmem_base;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    constexpr uint32_t IDESC = umma_idesc_bf16(128, N, 0, BMN);
+    const uint32_t b = smem_u32(smem);
+    const uint64_t db = umma_desc_sw128(b, BMN ? 8192 : 16, 1024);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t bo = BMN ? (uint64_t)((k * 2048) >> 4) : (uint64_t)((k >> 2) * (16384 >> 4) + (k & 3) * 2);
+        umma_bf16_ts(tmem_base + 256, tmem_base + k * 8, db + bo, IDESC, (r | k) ? 1u : 0u);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem_base);
+  }
+}
+
+template <int N, int BMN>
+void run_ts(const char* name, int sms, long long* d_out) {
+  const int reps = 2000;
+  cudaFuncSetAttribute(mma_rate_ts<N, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  mma_rate_ts<N, BMN><<<sms, 128, 64 * 1024>>>(reps, d_out);
+  cudaDeviceSynchronize();
+  long long cyc = 0;
+  cudaMemcpy(&cyc, d_out, 8, cudaMemcpyDeviceToHost);
+  double per = (double)cyc / (reps * 8);
+  printf("%-28s N=%3d: %7.1f cycles/MMA  %7.0f MAC/clk/SM  (%s)\n", name, N, per, 128.0 * N * 16 / per,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int N, int AMN, int BMN>
 void run(const char* name, int sms, long long* d_out) {
   const int reps = 2000;
@@ -70,6 +122,10 @@ int main() {
   run<128, 0, 0>("K-major A, K-major B", sms, d_out);
   run<128, 1, 1>("MN-major A, MN-major B", sms, d_out);
   run<256, 0, 0>("K-major A, K-major B", sms, d_out);
+  run_ts<128, 0>("TS: A tmem, B K-major", sms, d_out);
+  run_ts<128, 1>("TS: A tmem, B MN-major", sms, d_out);
+  run_ts<64, 0>("TS: A tmem, B K-major", sms, d_out);
+  run_ts<256, 0>("TS: A tmem, B K-major", sms, d_out);
   run<64, 0, 0>("K/K single CTA", 1, d_out);
   run<64, 1, 1>("MN/MN single CTA", 1, d_out);
   return 0;
