@@ -431,27 +431,33 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int c = 1; c < 64; ++c) bm = fmaxf(bm, x[c]);
             bm *= sl2;  // block max, log2 units (-inf if no valid key)
+            float alpha = 1.f;
+            bool raise = false;
             if (!mvalid) {
               if (bm != -INFINITY) { m = bm; mvalid = true; }
             } else if (bm > m + TAU) {
-              // raise the running max: rescale l and this row of O (GEMM2 of the previous step must be done)
-              const float alpha = exp2f(m - bm);
+              // raise the running max: rescale l and this row of O
+              alpha = exp2f(m - bm);
               l *= alpha;
-              if (!first_step) {
-                mbar_wait(&B.o_step, (uint32_t)((G - 1) & 1));
-                tc_fence_after();
-#pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                  float o[32];
-                  tmem_ld32(tq + COL_O + c4 * 32, o);
-                  tmem_ld_wait();
-#pragma unroll
-                  for (int c = 0; c < 32; ++c) o[c] *= alpha;
-                  tmem_st32(tq + COL_O + c4 * 32, o);
-                }
-                tmem_st_wait();
-              }
               m = bm;
+              raise = true;
+            }
+            // the O rescale is warp-wide (tcgen05.ld/st are .sync.aligned); rows
+            // that did not raise their max scale by 1. GEMM2 of the previous
+            // step must have landed in O first.
+            if (__any_sync(0xffffffffu, raise) && !first_step) {
+              mbar_wait(&B.o_step, (uint32_t)((G - 1) & 1));
+              tc_fence_after();
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) {
+                float o[32];
+                tmem_ld32(tq + COL_O + c4 * 32, o);
+                tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) o[c] *= alpha;
+                tmem_st32(tq + COL_O + c4 * 32, o);
+              }
+              tmem_st_wait();
             }
             if (mvalid) {
               const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
