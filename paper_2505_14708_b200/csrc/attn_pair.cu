@@ -410,71 +410,81 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&B.s_full[b], (uint32_t)((G >> 1) & 1));
         if (t == 0) PAIR_TRACE(6, G);
         tc_fence_after();
+        // scores of both key regions of this step (only those my region keeps;
+        // the flags are warp-uniform because a warp's rows share one region)
+        const bool keep0 = (fl[0] >> half) & 1, keep1 = (fl[1] >> half) & 1;
+        float x[128];
+        if (keep0) {
+          tmem_ld32_at<0>(cs, x);
+          tmem_ld32_at<32>(cs + 32, x);
+        }
+        if (keep1) {
+          tmem_ld32_at<64>(cs + 64, x);
+          tmem_ld32_at<96>(cs + 96, x);
+        }
+        const unsigned long long vm0 = keep0 ? key_mask(p, j[0]) : 0ull;
+        const unsigned long long vm1 = keep1 ? key_mask(p, j[1]) : 0ull;
+        tmem_ld_wait();
+        // masked scores -> -inf (dropped region or padded key)
+        if (vm0 != ~0ull) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) x[c] = ((vm0 >> c) & 1ull) ? x[c] : -INFINITY;
+        }
+        if (vm1 != ~0ull) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) x[64 + c] = ((vm1 >> c) & 1ull) ? x[64 + c] : -INFINITY;
+        }
+        // step max (log2 units): the running max is raised only when this step
+        // exceeds it by more than TAU, so P <= 2^TAU without rescaling O
+        float bm = x[0];
+#pragma unroll
+        for (int c = 1; c < 128; ++c) bm = fmaxf(bm, x[c]);
+        bm *= sl2;
+        float alpha = 1.f;
+        bool raise = false;
+        if (!mvalid) {
+          if (bm != -INFINITY) { m = bm; mvalid = true; }
+        } else if (bm > m + TAU) {
+          alpha = exp2f(m - bm);
+          l *= alpha;
+          m = bm;
+          raise = true;
+        }
+        // O rescale is warp-wide (tcgen05.ld/st are .sync.aligned; rows that did
+        // not raise scale by 1) and needs the previous step's GEMM2 in O first
+        if (__any_sync(0xffffffffu, raise) && !first_step) {
+          mbar_wait(&B.o_step, (uint32_t)((G - 1) & 1));
+          tc_fence_after();
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            float o[32];
+            tmem_ld32(tq + COL_O + c4 * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] *= alpha;
+            tmem_st32(tq + COL_O + c4 * 32, o);
+          }
+          tmem_st_wait();
+        }
 #pragma unroll
         for (int blk = 0; blk < 2; ++blk) {
-          const bool keep = (fl[blk] >> half) & 1;  // warp-uniform: a warp's rows share one region
+          const bool keep = blk ? keep1 : keep0;
           uint32_t pk[32];
-          if (!keep) {
+          if (keep && mvalid) {
+            const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+              const float2 e = ffma2(make_float2(x[blk * 64 + c], x[blk * 64 + c + 1]), sc, nm);
+              const float p0 = fast_exp2(e.x), p1 = fast_exp2(e.y);
+              acc.x += p0;
+              acc.y += p1;
+              pk[c / 2] = pack_bf16(p0, p1);
+            }
+            l += acc.x + acc.y;
+          } else {
 #pragma unroll
             for (int c = 0; c < 32; ++c) pk[c] = 0u;
-          } else {
-            float x[64];
-            tmem_ld32_at<0>(cs + blk * 64, x);
-            tmem_ld32_at<32>(cs + blk * 64 + 32, x);
-            const unsigned long long vm = key_mask(p, j[blk]);
-            tmem_ld_wait();
-            if (vm != ~0ull) {
-#pragma unroll
-              for (int c = 0; c < 64; ++c) x[c] = ((vm >> c) & 1ull) ? x[c] : -INFINITY;
-            }
-            float bm = x[0];
-#pragma unroll
-            for (int c = 1; c < 64; ++c) bm = fmaxf(bm, x[c]);
-            bm *= sl2;  // block max, log2 units (-inf if no valid key)
-            float alpha = 1.f;
-            bool raise = false;
-            if (!mvalid) {
-              if (bm != -INFINITY) { m = bm; mvalid = true; }
-            } else if (bm > m + TAU) {
-              // raise the running max: rescale l and this row of O
-              alpha = exp2f(m - bm);
-              l *= alpha;
-              m = bm;
-              raise = true;
-            }
-            // the O rescale is warp-wide (tcgen05.ld/st are .sync.aligned); rows
-            // that did not raise their max scale by 1. GEMM2 of the previous
-            // step must have landed in O first.
-            if (__any_sync(0xffffffffu, raise) && !first_step) {
-              mbar_wait(&B.o_step, (uint32_t)((G - 1) & 1));
-              tc_fence_after();
-#pragma unroll
-              for (int c4 = 0; c4 < 4; ++c4) {
-                float o[32];
-                tmem_ld32(tq + COL_O + c4 * 32, o);
-                tmem_ld_wait();
-#pragma unroll
-                for (int c = 0; c < 32; ++c) o[c] *= alpha;
-                tmem_st32(tq + COL_O + c4 * 32, o);
-              }
-              tmem_st_wait();
-            }
-            if (mvalid) {
-              const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
-              float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-              for (int c = 0; c < 64; c += 2) {
-                const float2 e = ffma2(make_float2(x[c], x[c + 1]), sc, nm);
-                const float p0 = fast_exp2(e.x), p1 = fast_exp2(e.y);
-                acc.x += p0;
-                acc.y += p1;
-                pk[c / 2] = pack_bf16(p0, p1);
-              }
-              l += acc.x + acc.y;
-            } else {
-#pragma unroll
-              for (int c = 0; c < 32; ++c) pk[c] = 0u;
-            }
           }
           // P (bf16 pairs) over the first half of this S buffer: keys 64*blk.. -> columns 32*blk..
           tmem_st16u(cs + blk * 32, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
