@@ -21,9 +21,10 @@
 // m (log2 units, lazily raised when a score exceeds it by > TAU, with an O-row
 // rescale) and running sum l. P is written back over S in TMEM as packed bf16.
 //
-// Roles (256 threads): warp 0 = TMA producer for K (and owner of the item
-// walk), warp 2 = TMA producer for V, warp 1 = MMA issuer + TMEM owner,
-// warps 4-7 = softmax / Q loader / epilogue. TMEM: Q [0,64), S0 [64,192),
+// Roles (384 threads): warp 0 = TMA producer for K, warp 2 = TMA producer
+// for V, warp 1 = MMA issuer + TMEM owner, warps 4-7 and 8-11 = two
+// softmax / Q-loader / epilogue warpgroups that split each step's two key
+// regions (and the feature halves of Q and O) between them. TMEM: Q [0,64), S0 [64,192),
 // S1 [192,320) (double-buffered so GEMM1 of step t+1 overlaps the softmax of
 // step t), O [320,448).
 //
@@ -84,6 +85,8 @@ struct __align__(8) Bars {
 struct SmemAux {
   Bars bars;
   uint32_t tmem_base;
+  float xch[2][2 * 128];  // [step parity][warpgroup x row] block maxima
+  float lsum[2][128];     // [warpgroup][row] partial row sums
 };
 constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
 static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
@@ -195,7 +198,7 @@ DA_DEV unsigned long long key_mask(const Params& p, int j) {
   return m;
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     sparse_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                             const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -208,11 +211,11 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 128); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 256); }
     mbar_init(&B.o_step, 1);
     mbar_init(&B.o_full, 1);
-    mbar_init(&B.o_empty, 128);
-    mbar_init(&B.q_full, 128);
+    mbar_init(&B.o_empty, 256);
+    mbar_init(&B.q_full, 256);
     mbar_init(&B.q_empty, 1);
     fence_barrier_init();
     tma_prefetch(&tm_k);
@@ -342,40 +345,41 @@ __global__ void __launch_bounds__(256, 1)
       if (pend.valid) gemm2(pend);
     }
   } else if (warp >= 4) {
-    // =============== softmax / Q loader / epilogue (one thread per query row) ===============
-    const int t = threadIdx.x - 128;
-    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    // ============ softmax / Q loader / epilogue: two warpgroups split the step ============
+    // Warpgroup wg handles key region wg of each step (S columns [64*wg, 64*wg+64))
+    // and feature half wg of Q and O; thread t of a warpgroup owns query row t.
+    // The two threads of a row agree on the running max through shared memory.
+    const int wg = (warp - 4) >> 2;
+    const int t = (threadIdx.x - 128) & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t tq = tmem + lane_off;
     const int half = t >> 6;  // 0: rows of region a, 1: rows of region b
     const int r = t & 63;
     const float sl2 = p.scale_log2;
     long long G = 0;
     int qi = 0;
-    // Q row of (item, my row) -> TMEM columns [0, 64) as packed bf16 pairs. The
-    // Q of the next nonempty item is written as soon as the current item's last
-    // GEMM1 is done (before this item's epilogue), so the MMA warp can start
-    // the next item while the epilogue runs.
+    // my half of the Q row of (item, row) -> TMEM columns [32*wg, 32*wg+32) as
+    // packed bf16 pairs. The next nonempty item's Q is written as soon as the
+    // current item's last GEMM1 is done, before this item's epilogue.
     auto load_q = [&](const PairItem& itm, int wait_parity) {
       const int region = half ? itm.b : itm.a;
       const long long qrow = region < p.geo.g ? token_row(p, region, r) : -1;
-      uint32_t qv[64];
+      uint32_t qv[32];
       if (qrow >= 0) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + qrow * p.qr);
+        const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + qrow * p.qr) + wg * 8;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < 8; ++c) {
           const uint4 w = __ldg(src + c);
           qv[4 * c] = w.x; qv[4 * c + 1] = w.y; qv[4 * c + 2] = w.z; qv[4 * c + 3] = w.w;
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) qv[c] = 0u;
+        for (int c = 0; c < 32; ++c) qv[c] = 0u;
       }
       if (wait_parity >= 0) mbar_wait(&B.q_empty, (uint32_t)wait_parity);
       tc_fence_after();
-      tmem_st16u(tq + COL_Q, *reinterpret_cast<uint32_t(*)[16]>(&qv[0]));
-      tmem_st16u(tq + COL_Q + 16, *reinterpret_cast<uint32_t(*)[16]>(&qv[16]));
-      tmem_st16u(tq + COL_Q + 32, *reinterpret_cast<uint32_t(*)[16]>(&qv[32]));
-      tmem_st16u(tq + COL_Q + 48, *reinterpret_cast<uint32_t(*)[16]>(&qv[48]));
+      tmem_st16u(tq + COL_Q + wg * 32, *reinterpret_cast<uint32_t(*)[16]>(&qv[0]));
+      tmem_st16u(tq + COL_Q + wg * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&qv[16]));
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&B.q_full);
@@ -387,16 +391,16 @@ __global__ void __launch_bounds__(256, 1)
       const int region = half ? itm.b : itm.a;
       const bool region_ok = region < p.geo.g;
       const long long row = region_ok ? token_row(p, region, r) : -1;
-      __nv_bfloat16* orow = row >= 0 ? p.out + itm.h * p.oh + row * p.orow : nullptr;
+      __nv_bfloat16* orow = row >= 0 ? p.out + itm.h * p.oh + row * p.orow + wg * 64 : nullptr;
       if (itm.na + itm.nb == 0) {
         if (orow) {
 #pragma unroll
-          for (int c = 0; c < D / 8; ++c) reinterpret_cast<uint4*>(orow)[c] = make_uint4(0, 0, 0, 0);
+          for (int c = 0; c < 8; ++c) reinterpret_cast<uint4*>(orow)[c] = make_uint4(0, 0, 0, 0);
         }
         continue;
       }
       if (!have_q) load_q(itm, -1);  // first nonempty item of this CTA
-      float m = -INFINITY, l = 0.f;
+      float m = -INFINITY, l = 0.f;  // running max (both threads of a row agree), my partial sum
       bool mvalid = false;
       UnionWalk u;
       u.init(itm);
@@ -406,40 +410,34 @@ __global__ void __launch_bounds__(256, 1)
         if (!u.next(j[1], fl[1])) { j[1] = j[0]; fl[1] = 0; }
         const int b = (int)(G & 1);
         const uint32_t cs = tq + (b ? COL_S1 : COL_S0);
-        if (t == 0) PAIR_TRACE(5, G);
+        if (t == 0 && wg == 0) PAIR_TRACE(5, G);
         mbar_wait(&B.s_full[b], (uint32_t)((G >> 1) & 1));
-        if (t == 0) PAIR_TRACE(6, G);
+        if (t == 0 && wg == 0) PAIR_TRACE(6, G);
         tc_fence_after();
-        // scores of both key regions of this step (only those my region keeps;
-        // the flags are warp-uniform because a warp's rows share one region)
-        const bool keep0 = (fl[0] >> half) & 1, keep1 = (fl[1] >> half) & 1;
-        float x[128];
-        if (keep0) {
-          tmem_ld32_at<0>(cs, x);
-          tmem_ld32_at<32>(cs + 32, x);
-        }
-        if (keep1) {
-          tmem_ld32_at<64>(cs + 64, x);
-          tmem_ld32_at<96>(cs + 96, x);
-        }
-        const unsigned long long vm0 = keep0 ? key_mask(p, j[0]) : 0ull;
-        const unsigned long long vm1 = keep1 ? key_mask(p, j[1]) : 0ull;
-        tmem_ld_wait();
-        // masked scores -> -inf (dropped region or padded key)
-        if (vm0 != ~0ull) {
+        // my key region's scores (warp-uniform: a warp's rows share one query region)
+        const bool keep = (fl[wg] >> half) & 1;
+        float x[64];
+        float bm_own = -INFINITY;
+        if (keep) {
+          tmem_ld32_at<0>(cs + wg * 64, x);
+          tmem_ld32_at<32>(cs + wg * 64 + 32, x);
+          const unsigned long long vm = key_mask(p, j[wg]);
+          tmem_ld_wait();
+          if (vm != ~0ull) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) x[c] = ((vm0 >> c) & 1ull) ? x[c] : -INFINITY;
-        }
-        if (vm1 != ~0ull) {
+            for (int c = 0; c < 64; ++c) x[c] = ((vm >> c) & 1ull) ? x[c] : -INFINITY;
+          }
+          float mx = x[0];
 #pragma unroll
-          for (int c = 0; c < 64; ++c) x[64 + c] = ((vm1 >> c) & 1ull) ? x[64 + c] : -INFINITY;
+          for (int c = 1; c < 64; ++c) mx = fmaxf(mx, x[c]);
+          bm_own = mx * sl2;
         }
-        // step max (log2 units): the running max is raised only when this step
-        // exceeds it by more than TAU, so P <= 2^TAU without rescaling O
-        float bm = x[0];
-#pragma unroll
-        for (int c = 1; c < 128; ++c) bm = fmaxf(bm, x[c]);
-        bm *= sl2;
+        // step max of the row over both key regions (log2 units); the running
+        // max is raised only when the step exceeds it by more than TAU
+        float* xb = aux.xch[G & 1];
+        xb[wg * 128 + t] = bm_own;
+        bar_sync(1, 256);
+        const float bm = fmaxf(bm_own, xb[(wg ^ 1) * 128 + t]);
         float alpha = 1.f;
         bool raise = false;
         if (!mvalid) {
@@ -450,9 +448,10 @@ __global__ void __launch_bounds__(256, 1)
           m = bm;
           raise = true;
         }
-        // O rescale is warp-wide (tcgen05.ld/st are .sync.aligned; rows that did
-        // not raise scale by 1) and needs the previous step's GEMM2 in O first
-        if (__any_sync(0xffffffffu, raise) && !first_step) {
+        // warpgroup 0 rescales the O rows (warp-wide: tcgen05.ld/st are
+        // .sync.aligned; rows that did not raise scale by 1) once the previous
+        // step's GEMM2 has landed
+        if (wg == 0 && __any_sync(0xffffffffu, raise) && !first_step) {
           mbar_wait(&B.o_step, (uint32_t)((G - 1) & 1));
           tc_fence_after();
 #pragma unroll
@@ -466,34 +465,30 @@ __global__ void __launch_bounds__(256, 1)
           }
           tmem_st_wait();
         }
+        uint32_t pk[32];
+        if (keep && mvalid) {
+          const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+          float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int blk = 0; blk < 2; ++blk) {
-          const bool keep = blk ? keep1 : keep0;
-          uint32_t pk[32];
-          if (keep && mvalid) {
-            const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
-            float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int c = 0; c < 64; c += 2) {
-              const float2 e = ffma2(make_float2(x[blk * 64 + c], x[blk * 64 + c + 1]), sc, nm);
-              const float p0 = fast_exp2(e.x), p1 = fast_exp2(e.y);
-              acc.x += p0;
-              acc.y += p1;
-              pk[c / 2] = pack_bf16(p0, p1);
-            }
-            l += acc.x + acc.y;
-          } else {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) pk[c] = 0u;
+          for (int c = 0; c < 64; c += 2) {
+            const float2 e = ffma2(make_float2(x[c], x[c + 1]), sc, nm);
+            const float p0 = fast_exp2(e.x), p1 = fast_exp2(e.y);
+            acc.x += p0;
+            acc.y += p1;
+            pk[c / 2] = pack_bf16(p0, p1);
           }
-          // P (bf16 pairs) over the first half of this S buffer: keys 64*blk.. -> columns 32*blk..
-          tmem_st16u(cs + blk * 32, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-          tmem_st16u(cs + blk * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
+          l += acc.x + acc.y;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) pk[c] = 0u;
         }
+        // P (bf16 pairs) over the first half of this S buffer: keys 64*wg.. -> columns 32*wg..
+        tmem_st16u(cs + wg * 32, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        tmem_st16u(cs + wg * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&B.p_full[b]);
-        if (t == 0) PAIR_TRACE(7, G);
+        if (t == 0 && wg == 0) PAIR_TRACE(7, G);
         first_step = false;
         ++G;
       }
@@ -508,19 +503,22 @@ __global__ void __launch_bounds__(256, 1)
         break;
       }
       // ------------------------------ epilogue ------------------------------
+      aux.lsum[wg][t] = l;
+      bar_sync(1, 256);
+      const float lt = l + aux.lsum[wg ^ 1][t];
       mbar_wait(&B.o_full, qi & 1);
       tc_fence_after();
-      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
+      for (int c2 = 0; c2 < 2; ++c2) {
         float o[32];
-        tmem_ld32(tq + COL_O + c4 * 32, o);
+        tmem_ld32(tq + COL_O + wg * 64 + c2 * 32, o);
         tmem_ld_wait();
         if (orow) {
           uint32_t w[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) w[c] = pack_bf16(o[2 * c] * inv, o[2 * c + 1] * inv);
-          uint4* dst = reinterpret_cast<uint4*>(orow) + c4 * 4;
+          uint4* dst = reinterpret_cast<uint4*>(orow) + c2 * 4;
 #pragma unroll
           for (int c = 0; c < 4; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
         }
@@ -581,7 +579,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   if (e != cudaSuccess) return e;
   const long long items = (long long)a.heads * p.npairs;
   const int grid = (int)(items < num_sms ? items : num_sms);
-  pairk::sparse_attn_pair_kernel<<<grid, 256, pairk::SMEM_ALLOC, st>>>(mk, mv, p);
+  pairk::sparse_attn_pair_kernel<<<grid, 384, pairk::SMEM_ALLOC, st>>>(mk, mv, p);
   return cudaGetLastError();
 }
 
