@@ -190,11 +190,10 @@ DA_DEV unsigned long long key_mask(const Params& p, int j) {
   const RegionXY rc = p.dec(j);
   const int vy = min(p.geo.ph, p.geo.H - rc.y0), vx = min(p.geo.pw, p.geo.W - rc.x0);
   if (vy == p.geo.ph && vx == p.geo.pw) return ~0ull;
+  // key r = u*pw + v is valid iff u < vy and v < vx: vy copies of the row mask
+  const unsigned long long rowm = (1ull << vx) - 1ull;
   unsigned long long m = 0;
-  for (int r = 0; r < P; ++r) {
-    const int u = r / p.geo.pw, v = r - u * p.geo.pw;
-    if (u < vy && v < vx) m |= 1ull << r;
-  }
+  for (int u = 0; u < vy; ++u) m |= rowm << (u * p.geo.pw);
   return m;
 }
 

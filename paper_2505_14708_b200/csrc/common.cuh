@@ -124,10 +124,12 @@ DA_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 DA_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+  // with a suspend-time hint the warp sleeps in hardware until the phase
+  // completes (or the hint expires) instead of spinning on issue slots
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, 1000000;\n"
       "selp.u32 %0, 1, 0, P1;\n"
       "}\n"
       : "=r"(ok)
