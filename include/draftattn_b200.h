@@ -142,7 +142,10 @@ typedef struct da_attn_args {
   int32_t shared_mask;    /* nonzero: every head uses head 0's row_ptr/col_idx
                              (multi_head_sparse_attention shared_head_mask, sparse.py:281-301) */
   int32_t force_portable; /* nonzero: use the CUDA-core kernel even when tcgen05 applies */
+  void* workspace;        /* da_attn_workspace_size(heads, grid) bytes of device memory (caller-owned;
+                             required by the tcgen05 path, ignored by the portable one) */
 } da_attn_args;
+size_t da_attn_workspace_size(int32_t heads, const da_grid* grid);
 int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* stream);
 
 /* ---- Whole pipeline ---------------------------------------------------------
@@ -177,7 +180,7 @@ int da_sparse_attention(const da_pipeline_args* args, const da_grid* grid, void*
 
 /* ---- Diagnostics -------------------------------------------------------------
  * While set, the tcgen05 kernel of CTA 0 records clock64() stamps of its
- * pipeline events (16 event rows x 1024 steps, int64) into this device buffer.
+ * pipeline events (20 event rows x 1024 steps, int64) into this device buffer.
  * NULL disables. Not thread-safe; for profiling only. */
 int da_debug_trace(void* device_buffer);
 

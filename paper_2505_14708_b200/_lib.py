@@ -38,6 +38,7 @@ class DaAttnArgs(ctypes.Structure):
         ("row_ptr", c_vp), ("col_idx", c_vp), ("mask_cap", c_i64),
         ("key_valid", c_vp),
         ("shared_mask", c_i32), ("force_portable", c_i32),
+        ("workspace", c_vp),
     ]
 
 
@@ -68,6 +69,7 @@ SIGNATURES = {
     "da_select_workspace_size": (ctypes.c_size_t, [c_i32, c_i32]),
     "da_select": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_vp, c_vp, c_vp, c_vp]),
+    "da_attn_workspace_size": (ctypes.c_size_t, [c_i32, ctypes.POINTER(DaGrid)]),
     "da_block_sparse_fwd": (ctypes.c_int, [ctypes.POINTER(DaAttnArgs), ctypes.POINTER(DaGrid), c_vp]),
     "da_pipeline_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(DaGrid), c_i32, c_i32]),
     "da_pipeline_launches": (c_i32, [c_i32, c_i32]),

@@ -657,6 +657,9 @@ def block_sparse_attention(q_r, k_r, v_r, mask: RegionMask, scale=None, key_vali
     a.key_valid = kv_ptr
     a.shared_mask = 1 if mask.heads == 1 else 0
     a.force_portable = 1 if force_portable else 0
+    ws = torch.empty(max(1, lib().da_attn_workspace_size(heads, ctypes.byref(grid))), dtype=torch.uint8,
+                     device=q3.device)
+    a.workspace = ws.data_ptr()
     with torch.cuda.device(q3.device):
         check(lib().da_block_sparse_fwd(ctypes.byref(a), ctypes.byref(grid), _stream_ptr(q3.device)),
               "block_sparse_fwd")

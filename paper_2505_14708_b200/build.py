@@ -37,8 +37,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     """Build libdraftattn_b200.so for sm_100a unless it is up to date."""
     if not force and not _stale():
         return OUT
+    extra = os.environ.get("DA_NVCC_FLAGS", "").split()  # experiments only (e.g. -DDA_MBAR_NOHINT)
     cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-o", str(OUT)] + [str(CSRC / s) for s in SOURCES]
+           "-o", str(OUT)] + extra + [str(CSRC / s) for s in SOURCES]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)

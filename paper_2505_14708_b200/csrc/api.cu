@@ -141,12 +141,19 @@ static int check_attn(const da_attn_args* a, const da_grid* grid) {
   return DA_OK;
 }
 
+size_t da_attn_workspace_size(int32_t heads, const da_grid* grid) {
+  if (!grid_ok(grid) || heads < 1) return 0;
+  return da::pair_attn_workspace_size(heads, da::make_geo(*grid));
+}
+
 int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* stream) {
   int rc = check_attn(args, grid);
   if (rc) return rc;
   da::Geo g = da::make_geo(*grid);
   cudaStream_t st = (cudaStream_t)stream;
   if (!args->force_portable && da::tc_supported(*args, g)) {
+    if (!args->workspace)
+      return fail(DA_EINVAL, "block_sparse_fwd: the tcgen05 path needs a workspace (da_attn_workspace_size)");
     const char* why = "";
     cudaError_t e = da::launch_tc_attn(*args, g, st, &why);
     if (e == cudaErrorInvalidValue && why[0]) return fail(DA_ECUDA, "block_sparse_fwd (tcgen05): %s", why);
@@ -166,6 +173,7 @@ struct PipeWs {
   double* kp;
   double* scores;
   void* sel;
+  void* attn;
   size_t total;
 };
 
@@ -178,6 +186,7 @@ static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
   w.kp = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * d));
   w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * g.g));
   w.sel = take(da::select_workspace_size(heads, g.g));
+  w.attn = take(da::pair_attn_workspace_size(heads, g));
   w.total = off;
   return w;
 }
@@ -203,9 +212,10 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // pool (Q and K), draft GEMM (+ row softmax) [+ head mean], selection: init,
   // digit histograms (digit 0 fused into the GEMM on the per-head logits path)
   // and scans, candidate compaction + finish, tie counts + scan, mark, row
-  // scan, collect, threshold, kept totals, packbits (bitmap requested); attention
+  // scan, collect, threshold, kept totals, packbits (bitmap requested);
+  // attention: key norms, tcgen05 kernel, fallback list
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
-  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 1;
+  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 3;
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
@@ -260,6 +270,7 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   aa.mask_cap = da_mask_capacity(g.g, pa->m);
   aa.key_valid = nullptr;
   aa.shared_mask = pa->shared_head_mask ? 1 : 0;
+  aa.workspace = w.attn;
   if (pa->ev_attn_begin) cudaEventRecord((cudaEvent_t)pa->ev_attn_begin, st);
   rc = da_block_sparse_fwd(&aa, grid, stream);
   if (pa->ev_attn_end) cudaEventRecord((cudaEvent_t)pa->ev_attn_end, st);

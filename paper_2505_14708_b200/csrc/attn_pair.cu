@@ -17,9 +17,11 @@
 // MMA work of the kept pairs for i.i.d. data, but each K/V tile is fetched once
 // for 128 queries.
 //
-// Softmax is the classic per-row form: each thread owns its row's running max
-// m (log2 units, lazily raised when a score exceeds it by > TAU, with an O-row
-// rescale) and running sum l. P is written back over S in TMEM as packed bf16.
+// Softmax is per row with a FIXED offset per (row, item) instead of a running
+// max (see the softmax warpgroups below), so O is never rescaled and the two
+// softmax warpgroups meet once per item. P is written back over S in TMEM as
+// packed bf16. Rows whose fixed offset underflows are redone by the portable
+// kernel (launch_pair_attn).
 //
 // Roles (384 threads): warp 0 = TMA producer for K, warp 2 = TMA producer
 // for V, warp 1 = MMA issuer + TMEM owner, warps 4-7 and 8-11 = two
@@ -33,10 +35,15 @@
 // 8x8 region (ragged rows zero-filled), so the permutation of
 // padding.py:139-143 is free; Q rows are read straight from the original order
 // and output rows are written back to it (padding.py:157).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace da {
+
+static inline size_t pair_align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
 namespace pairk {
 
 constexpr int P = 64;
@@ -45,7 +52,7 @@ constexpr int KST = 3;
 constexpr int VST = 3;
 constexpr int BOX = 64 * 128;       // 64 rows x 64 bf16 = 8 KB
 constexpr int KV_BYTES = 4 * BOX;   // two key regions x two feature halves
-constexpr float TAU = 8.0f;
+constexpr int KBLK = 32;              // key_norm_kernel blocks per head
 
 constexpr int SMEM_K = 0;
 constexpr int SMEM_V = SMEM_K + KST * KV_BYTES;
@@ -72,6 +79,11 @@ struct Params {
   FastDiv per_head;  // pairs per head
   int npairs;
   long long n_pad;
+  const float* kpart;  // [heads][KBLK] per-block maxima of the key row norms (key_norm_kernel)
+  int* fb_count;       // rows whose fixed softmax offset underflowed: their (head, region)
+  int* fb_items;       //   items are recomputed by the portable kernel afterwards
+  int fake_load;           // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies
+  uint64_t pol_kv, pol_q, pol_o;  // L2 cache policies of the K/V tiles, Q rows, output rows
   long long* trace;
 };
 
@@ -79,19 +91,31 @@ struct __align__(8) Bars {
   uint64_t k_full[KST], k_empty[KST];
   uint64_t v_full[VST], v_empty[VST];
   uint64_t s_full[2], p_full[2];
-  uint64_t o_step, o_full, o_empty;
+  uint64_t o_full, o_empty;
   uint64_t q_full, q_empty;
+  uint64_t info_full[8];
+  uint64_t sch_full[16], sch_empty[16];
 };
 struct SmemAux {
   Bars bars;
+  int4 info[8];           // per step: key regions j0, j1, membership flags, last/first (K producer)
+  int4 sched[16];         // step schedule (warp 3) for the K and V producers
   uint32_t tmem_base;
-  float xch[2][2 * 128];  // [step parity][warpgroup x row] block maxima
+  float xch[2][2][128];   // [item parity][warpgroup][row] first-step block maxima
+  float xq[2][2][128];    // [item parity][warpgroup][row] partial |q|^2
   float lsum[2][128];     // [warpgroup][row] partial row sums
+  int had[2][128];        // [warpgroup][row] saw a kept valid key
 };
 constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
 static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
 
 constexpr int TRACE_N = 1024;
+// waits on the MMA <-> softmax critical path
+#ifdef DA_CRIT_SLEEP
+#define DA_WAITC mbar_wait
+#else
+#define DA_WAITC mbar_wait_spin
+#endif
 #define PAIR_TRACE(ev, idx)                                                   \
   do {                                                                        \
     if (p.trace != nullptr && blockIdx.x == 0 && (idx) < TRACE_N)             \
@@ -130,41 +154,36 @@ DA_DEV bool fetch_pair(const Params& p, long long it, long long items, PairItem&
   return true;
 }
 
-// Ascending merge of the two kept lists, with membership flags.
-struct UnionWalk {
-  const int* a;
-  const int* b;
-  int na, nb, ia, ib;
-  DA_DEV void init(const PairItem& it) {
-    a = it.la; b = it.lb; na = it.na; nb = it.nb; ia = 0; ib = 0;
+// Elements of sorted list x that are (or are not) in sorted list y, ascending.
+struct MemberStream {
+  const int* x;
+  const int* y;
+  int nx, ny, ix, iy;
+  DA_DEV void init(const int* x_, int nx_, const int* y_, int ny_) {
+    x = x_; nx = nx_; y = y_; ny = ny_; ix = 0; iy = 0;
   }
-  DA_DEV bool done() const { return ia >= na && ib >= nb; }
-  // next key region and its membership (bit 0: kept by a, bit 1: kept by b)
-  DA_DEV bool next(int& j, int& flags) {
-    const int va = ia < na ? __ldg(a + ia) : 0x7fffffff;
-    const int vb = ib < nb ? __ldg(b + ib) : 0x7fffffff;
-    if (va == 0x7fffffff && vb == 0x7fffffff) return false;
-    if (va <= vb) {
-      j = va;
-      flags = 1;
-      ++ia;
-      if (vb == va) { flags |= 2; ++ib; }
-    } else {
-      j = vb;
-      flags = 2;
-      ++ib;
+  DA_DEV bool next(bool want_in_y, int& out) {
+    while (ix < nx) {
+      const int v = __ldg(x + ix);
+      ++ix;
+      while (iy < ny && __ldg(y + iy) < v) ++iy;
+      const bool in = iy < ny && __ldg(y + iy) == v;
+      if (in == want_in_y) {
+        out = v;
+        return true;
+      }
     }
-    return true;
+    return false;
   }
 };
 
 DA_DEV void load_region(const CUtensorMap* map, void* dst, uint64_t* bar, const Params& p, int h, int region,
                         int half) {
   if (p.layout == DA_LAYOUT_REORDERED) {
-    tma_load_2d(dst, map, bar, half * 64, (int)(h * p.n_pad + (long long)region * P));
+    tma_load_2d(dst, map, bar, half * 64, (int)(h * p.n_pad + (long long)region * P), p.pol_kv);
   } else {
     const RegionXY rc = p.dec(region);
-    tma_load_5d(dst, map, bar, half * 64, rc.x0, rc.y0, rc.f, h);
+    tma_load_5d(dst, map, bar, half * 64, rc.x0, rc.y0, rc.f, h, p.pol_kv);
   }
 }
 
@@ -197,6 +216,52 @@ DA_DEV unsigned long long key_mask(const Params& p, int j) {
   return m;
 }
 
+// Per-head maximum key row norm, as KBLK per-block partial maxima (the
+// softmax offset bound); block (0, 0) also clears the fallback counter.
+// grid (KBLK, heads), 256 threads: each warp reads two 256-byte rows per load.
+__global__ void __launch_bounds__(256) key_norm_kernel(const __nv_bfloat16* __restrict__ k, long long kh, long long kr,
+                                                       long long rows, float* __restrict__ kpart, int* fb_count) {
+  __shared__ float red[8];
+  const int h = blockIdx.y;
+  if (blockIdx.x == 0 && h == 0 && threadIdx.x == 0) *fb_count = 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int sub = lane >> 4, c = lane & 15;
+  const uint4* base = reinterpret_cast<const uint4*>(k + h * kh);
+  const long long kr8 = kr / 8;
+  const long long step = (long long)KBLK * 8 * 2;
+  float mx = 0.f;
+  for (long long r0 = ((long long)blockIdx.x * 8 + w) * 2 + sub; r0 < rows; r0 += 4 * step) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long rr = r0 + u * step;
+      v[u] = rr < rows ? __ldg(base + rr * kr8 + c) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+      float s2 = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+        s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+      }
+#pragma unroll
+      for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      mx = fmaxf(mx, s2);
+    }
+  }
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  if (lane == 0) red[w] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = red[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) b = fmaxf(b, red[i]);
+    kpart[(long long)h * KBLK + blockIdx.x] = sqrtf(b);
+  }
+}
+
 __global__ void __launch_bounds__(384, 1)
     sparse_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                             const Params p) {
@@ -211,14 +276,19 @@ __global__ void __launch_bounds__(384, 1)
     for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 256); }
-    mbar_init(&B.o_step, 1);
     mbar_init(&B.o_full, 1);
     mbar_init(&B.o_empty, 256);
     mbar_init(&B.q_full, 256);
     mbar_init(&B.q_empty, 1);
+    for (int s = 0; s < 8; ++s) mbar_init(&B.info_full[s], 1);
+    for (int s = 0; s < 16; ++s) { mbar_init(&B.sch_full[s], 1); mbar_init(&B.sch_empty[s], 2); }
     fence_barrier_init();
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
+  }
+  if (p.fake_load) {  // diagnostics: defined (zero) K/V tiles when copies are skipped
+    for (int i = threadIdx.x; i < SMEM_END / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
   }
   if (warp == 1) tmem_alloc<TMEM_COLS>(&aux.tmem_base);
   tc_fence_before();
@@ -228,7 +298,62 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sK = smem + SMEM_K;
   uint8_t* sV = smem + SMEM_V;
 
-  if (warp == 0 || warp == 2) {
+  if (warp == 3) {
+    // ======================= step scheduler (one thread) =======================
+    // Each step is two key regions of the item's union. Regions kept by only one
+    // query region of the pair are paired across the two (one kept by a, one by
+    // b) so both halves of the softmax warpgroups (rows of a on SMSPs 0-1, rows
+    // of b on SMSPs 2-3) get one region's exponentials per step; the excess of
+    // one side, then regions kept by both, are paired among themselves. The
+    // order of key regions inside a row's softmax is immaterial (fixed offset,
+    // fp32 sums).
+    if (lane == 0) {
+      int sq = 0;
+      int4 pend = make_int4(0, 0, 0, 0);
+      bool have = false, first = true;
+      auto emit = [&](int4 e, bool last) {
+        const int sl = sq & 15;
+        if (sq >= 16) mbar_wait(&B.sch_empty[sl], ((sq >> 4) - 1) & 1);
+        e.w = (last ? 1 : 0) | (first ? 2 : 0);
+        aux.sched[sl] = e;
+        mbar_arrive(&B.sch_full[sl]);
+        first = false;
+        ++sq;
+      };
+      auto step = [&](int j0, int f0, int j1, int f1) {
+        if (have) emit(pend, false);
+        pend = make_int4(j0, j1, f0 | (f1 << 2), 0);
+        have = true;
+      };
+      for (long long it = blockIdx.x;; it += gridDim.x) {
+        PairItem itm;
+        if (!fetch_pair(p, it, items, itm)) break;
+        if (itm.na + itm.nb == 0) continue;
+        MemberStream sa, sb, sc;
+        sa.init(itm.la, itm.na, itm.lb, itm.nb);
+        sb.init(itm.lb, itm.nb, itm.la, itm.na);
+        sc.init(itm.la, itm.na, itm.lb, itm.nb);
+        first = true;
+        have = false;
+        int x = 0, y = 0, z = 0;
+        bool hx = sa.next(false, x), hy = sb.next(false, y);
+        while (hx && hy) {
+          step(x, 1, y, 2);
+          hx = sa.next(false, x);
+          hy = sb.next(false, y);
+        }
+        int lj = -1, lf = 0;
+        auto single = [&](int j, int f) {
+          if (lj < 0) { lj = j; lf = f; } else { step(lj, lf, j, f); lj = -1; }
+        };
+        while (hx) { single(x, 1); hx = sa.next(false, x); }
+        while (hy) { single(y, 2); hy = sb.next(false, y); }
+        while (sc.next(true, z)) single(z, 3);
+        if (lj >= 0) step(lj, lf, lj, 0);
+        emit(pend, true);
+      }
+    }
+  } else if (warp == 0 || warp == 2) {
     // ===================== TMA producers (warp 0: K, warp 2: V) =====================
     if (lane == 0) {
       const bool is_k = warp == 0;
@@ -238,18 +363,34 @@ __global__ void __launch_bounds__(384, 1)
       uint64_t* empty = is_k ? B.k_empty : B.v_empty;
       const CUtensorMap* map = is_k ? &tm_k : &tm_v;
       int kq = 0;
+      int sq = 0;
       for (long long it = blockIdx.x;; it += gridDim.x) {
         PairItem itm;
         if (!fetch_pair(p, it, items, itm)) break;
-        UnionWalk u;
-        u.init(itm);
-        int j0, j1, f;
-        while (u.next(j0, f)) {
-          if (!u.next(j1, f)) j1 = j0;
+        if (itm.na + itm.nb == 0) continue;
+        for (bool last = false; !last;) {
+          const int sl = sq & 15;
+          mbar_wait(&B.sch_full[sl], (uint32_t)((sq >> 4) & 1));
+          const int4 e = aux.sched[sl];
+          mbar_arrive(&B.sch_empty[sl]);
+          ++sq;
+          last = (e.w & 1) != 0;
+          const int j0 = e.x, j1 = e.y;
           const int s = kq % ST;
           if (kq >= ST) mbar_wait(&empty[s], ((kq / ST) - 1) & 1);
           PAIR_TRACE(is_k ? 0 : 1, kq);
+          if (is_k) {
+            // step info for the MMA issuer and the softmax warpgroups (the K
+            // producer runs at most 5 steps ahead of the softmax: 8 entries)
+            aux.info[kq & 7] = e;
+            mbar_arrive(&B.info_full[kq & 7]);
+          }
           uint8_t* st = ring + s * KV_BYTES;
+          if (p.fake_load & (is_k ? 1 : 2)) {  // diagnostics: skip the copy (timing only)
+            mbar_arrive(&full[s]);
+            ++kq;
+            continue;
+          }
           mbar_expect_tx(&full[s], KV_BYTES);
           if (is_k) {  // [half][slot][64 x 128B]: B operand rows 0..127 = keys of j0 then j1
             load_region(map, st, &full[s], p, itm.h, j0, 0);
@@ -284,9 +425,9 @@ __global__ void __launch_bounds__(384, 1)
       pend.valid = false;
       auto gemm2 = [&](const Pend& s) {
         const int vs = vq % VST;
-        mbar_wait(&B.v_full[vs], (vq / VST) & 1);
+        DA_WAITC(&B.v_full[vs], (vq / VST) & 1);
         const int b = (int)(s.step & 1);
-        mbar_wait(&B.p_full[b], (uint32_t)((s.step >> 1) & 1));
+        DA_WAITC(&B.p_full[b], (uint32_t)((s.step >> 1) & 1));
         if (s.first && s.qi > 0) mbar_wait(&B.o_empty, (s.qi - 1) & 1);
         PAIR_TRACE(4, vq);
         tc_fence_after();
@@ -295,10 +436,12 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t bv = dV + (uint64_t)(vbase + (kk >> 2) * (2 * BOX >> 4) + (kk & 3) * (2048 >> 4));
-          umma_bf16_ts(tmem + COL_O, aP + kk * 8, bv, IDESC2, (s.first && kk == 0) ? 0u : 1u);
+          // P of keys 16c.. of key region k sits at column 64k + 32(c/2) + 8(c%2)
+          umma_bf16_ts(tmem + COL_O, aP + (kk >> 2) * 64 + ((kk >> 1) & 1) * 32 + (kk & 1) * 8, bv, IDESC2,
+                       (s.first && kk == 0) ? 0u : 1u);
         }
+        PAIR_TRACE(5, vq);
         umma_commit(&B.v_empty[vs]);
-        umma_commit(&B.o_step);
         if (s.last) umma_commit(&B.o_full);
         ++vq;
       };
@@ -306,16 +449,12 @@ __global__ void __launch_bounds__(384, 1)
         PairItem itm;
         if (!fetch_pair(p, it, items, itm)) break;
         if (itm.na + itm.nb == 0) continue;
-        UnionWalk u;
-        u.init(itm);
         mbar_wait(&B.q_full, qi & 1);
         bool first = true;
-        int j0, j1, f;
-        while (u.next(j0, f)) {
-          u.next(j1, f);
-          const bool last = u.done();
+        for (;;) {
           const int ks = kq % KST;
-          mbar_wait(&B.k_full[ks], (kq / KST) & 1);
+          DA_WAITC(&B.k_full[ks], (kq / KST) & 1);
+          const bool last = (aux.info[kq & 7].w & 1) != 0;  // written before the K copy was issued
           PAIR_TRACE(2, kq);
           tc_fence_after();
           const uint32_t kbase = aK + ks * (KV_BYTES >> 4);
@@ -326,6 +465,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint64_t bk = dK + (uint64_t)(kbase + (kk >> 2) * (2 * BOX >> 4) + (kk & 3) * 2);
             umma_bf16_ts(dS, tmem + COL_Q + kk * 8, bk, IDESC1, kk > 0 ? 1u : 0u);
           }
+          PAIR_TRACE(3, kq);
           umma_commit(&B.k_empty[ks]);
           umma_commit(&B.s_full[b]);
           if (last) umma_commit(&B.q_empty);
@@ -338,6 +478,7 @@ __global__ void __launch_bounds__(384, 1)
           pend.valid = true;
           first = false;
           ++G;
+          if (last) break;
         }
         ++qi;
       }
@@ -347,16 +488,24 @@ __global__ void __launch_bounds__(384, 1)
     // ============ softmax / Q loader / epilogue: two warpgroups split the step ============
     // Warpgroup wg handles key region wg of each step (S columns [64*wg, 64*wg+64))
     // and feature half wg of Q and O; thread t of a warpgroup owns query row t.
-    // The two threads of a row agree on the running max through shared memory.
+    //
+    // Fixed per-row offset instead of a running max: at an item's first step
+    // the row fixes m = max(first-step row max, |q| * max|k| * scale - 64)
+    // (log2 units). Cauchy-Schwarz bounds every later score by |q| max|k| scale,
+    // so no exponent exceeds 2^64 (no overflow in fp32 / bf16) and O is never
+    // rescaled; the two warpgroups only meet once per item. A row whose sum
+    // ends below 2^-80 (its true max sits > ~80 below the bound) is handed to
+    // the portable kernel, which redoes its region with the streaming softmax.
     const int wg = (warp - 4) >> 2;
     const int t = (threadIdx.x - 128) & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t tq = tmem + lane_off;
     const int half = t >> 6;  // 0: rows of region a, 1: rows of region b
     const int r = t & 63;
-    const float sl2 = p.scale_log2;
+    const float sl2 = p.scale_log2;  // > 0 (tc_supported)
     long long G = 0;
     int qi = 0;
+    float qn2_next = 0.f;  // my half of |q|^2 of the row whose Q was loaded last
     // my half of the Q row of (item, row) -> TMEM columns [32*wg, 32*wg+32) as
     // packed bf16 pairs. The next nonempty item's Q is written as soon as the
     // current item's last GEMM1 is done, before this item's epilogue.
@@ -368,13 +517,20 @@ __global__ void __launch_bounds__(384, 1)
         const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + qrow * p.qr) + wg * 8;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint4 w = __ldg(src + c);
+          const uint4 w = ldg128_hint(src + c, p.pol_q);
           qv[4 * c] = w.x; qv[4 * c + 1] = w.y; qv[4 * c + 2] = w.z; qv[4 * c + 3] = w.w;
         }
       } else {
 #pragma unroll
         for (int c = 0; c < 32; ++c) qv[c] = 0u;
       }
+      float s2 = 0.f;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qv[c]));
+        s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+      }
+      qn2_next = s2;
       if (wait_parity >= 0) mbar_wait(&B.q_empty, (uint32_t)wait_parity);
       tc_fence_after();
       tmem_st16u(tq + COL_Q + wg * 32, *reinterpret_cast<uint32_t(*)[16]>(&qv[0]));
@@ -384,6 +540,8 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive(&B.q_full);
     };
     bool have_q = false;
+    int cur_head = -1;
+    float kmax = 0.f;
     for (long long it = blockIdx.x;; it += gridDim.x) {
       PairItem itm;
       if (!fetch_pair(p, it, items, itm)) break;
@@ -399,96 +557,126 @@ __global__ void __launch_bounds__(384, 1)
         continue;
       }
       if (!have_q) load_q(itm, -1);  // first nonempty item of this CTA
-      float m = -INFINITY, l = 0.f;  // running max (both threads of a row agree), my partial sum
-      bool mvalid = false;
-      UnionWalk u;
-      u.init(itm);
+      const float qn2_own = qn2_next;
+      if (itm.h != cur_head) {
+        cur_head = itm.h;
+        const float* kp = p.kpart + (long long)itm.h * KBLK;
+        float mx = 0.f;
+#pragma unroll 8
+        for (int c = 0; c < KBLK; ++c) mx = fmaxf(mx, __ldg(kp + c));
+        kmax = mx;
+      }
+      float m = 0.f, l = 0.f;
+      bool had = false;
       int j[2], fl[2];
       bool first_step = true;
-      while (u.next(j[0], fl[0])) {
-        if (!u.next(j[1], fl[1])) { j[1] = j[0]; fl[1] = 0; }
+      for (bool last = false; !last;) {
+        DA_WAITC(&B.info_full[G & 7], (uint32_t)((G >> 3) & 1));
+        const int4 inf = aux.info[G & 7];
+        j[0] = inf.x;
+        j[1] = inf.y;
+        fl[0] = inf.z & 3;
+        fl[1] = inf.z >> 2;
+        last = (inf.w & 1) != 0;
         const int b = (int)(G & 1);
         const uint32_t cs = tq + (b ? COL_S1 : COL_S0);
-        if (t == 0 && wg == 0) PAIR_TRACE(5, G);
-        mbar_wait(&B.s_full[b], (uint32_t)((G >> 1) & 1));
+        if (t == 0 && wg == 0) PAIR_TRACE(15, G);
+        DA_WAITC(&B.s_full[b], (uint32_t)((G >> 1) & 1));
         if (t == 0 && wg == 0) PAIR_TRACE(6, G);
         tc_fence_after();
-        // my key region's scores (warp-uniform: a warp's rows share one query region)
-        const bool keep = (fl[wg] >> half) & 1;
-        float x[64];
-        float bm_own = -INFINITY;
-        if (keep) {
-          tmem_ld32_at<0>(cs + wg * 64, x);
-          tmem_ld32_at<32>(cs + wg * 64 + 32, x);
-          const unsigned long long vm = key_mask(p, j[wg]);
+        // keys [32*wg, 32*wg+32) of each of the step's two key regions (so the
+        // two warps of an SMSP always split a row's exponentials evenly);
+        // warp-uniform: a warp's rows share one query region
+        const bool kp0 = (fl[0] >> half) & 1, kp1 = (fl[1] >> half) & 1;
+        float x0[32], x1[32];
+        if (kp0) tmem_ld32(cs + 32 * wg, x0);
+        if (kp1) tmem_ld32(cs + 64 + 32 * wg, x1);
+        if (kp0 || kp1) {
+          const unsigned vm0 = kp0 ? (unsigned)(key_mask(p, j[0]) >> (32 * wg)) : 0u;
+          const unsigned vm1 = kp1 ? (unsigned)(key_mask(p, j[1]) >> (32 * wg)) : 0u;
           tmem_ld_wait();
-          if (vm != ~0ull) {
+          if (kp0 && vm0 != ~0u) {
 #pragma unroll
-            for (int c = 0; c < 64; ++c) x[c] = ((vm >> c) & 1ull) ? x[c] : -INFINITY;
+            for (int c = 0; c < 32; ++c) x0[c] = ((vm0 >> c) & 1u) ? x0[c] : -INFINITY;
           }
-          float mx = x[0];
+          if (kp1 && vm1 != ~0u) {
 #pragma unroll
-          for (int c = 1; c < 64; ++c) mx = fmaxf(mx, x[c]);
-          bm_own = mx * sl2;
-        }
-        // step max of the row over both key regions (log2 units); the running
-        // max is raised only when the step exceeds it by more than TAU
-        float* xb = aux.xch[G & 1];
-        xb[wg * 128 + t] = bm_own;
-        bar_sync(1, 256);
-        const float bm = fmaxf(bm_own, xb[(wg ^ 1) * 128 + t]);
-        float alpha = 1.f;
-        bool raise = false;
-        if (!mvalid) {
-          if (bm != -INFINITY) { m = bm; mvalid = true; }
-        } else if (bm > m + TAU) {
-          alpha = exp2f(m - bm);
-          l *= alpha;
-          m = bm;
-          raise = true;
-        }
-        // warpgroup 0 rescales the O rows (warp-wide: tcgen05.ld/st are
-        // .sync.aligned; rows that did not raise scale by 1) once the previous
-        // step's GEMM2 has landed
-        if (wg == 0 && __any_sync(0xffffffffu, raise) && !first_step) {
-          mbar_wait(&B.o_step, (uint32_t)((G - 1) & 1));
-          tc_fence_after();
-#pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            float o[32];
-            tmem_ld32(tq + COL_O + c4 * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] *= alpha;
-            tmem_st32(tq + COL_O + c4 * 32, o);
+            for (int c = 0; c < 32; ++c) x1[c] = ((vm1 >> c) & 1u) ? x1[c] : -INFINITY;
           }
-          tmem_st_wait();
+          had |= (vm0 | vm1) != 0u;
         }
-        uint32_t pk[32];
-        if (keep && mvalid) {
-          const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
-          float2 acc = make_float2(0.f, 0.f);
+        if (t == 0 && wg == 0) PAIR_TRACE(16, G);
+        if (first_step) {
+          float mx[8];
 #pragma unroll
-          for (int c = 0; c < 64; c += 2) {
-            const float2 e = ffma2(make_float2(x[c], x[c + 1]), sc, nm);
-            const float p0 = fast_exp2(e.x), p1 = fast_exp2(e.y);
-            acc.x += p0;
-            acc.y += p1;
-            pk[c / 2] = pack_bf16(p0, p1);
+          for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+          if (kp0) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], x0[c + e]);
+            }
           }
-          l += acc.x + acc.y;
-        } else {
+          if (kp1) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) pk[c] = 0u;
+            for (int c = 0; c < 32; c += 8) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], x1[c + e]);
+            }
+          }
+          const float bm_own = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+          aux.xch[qi & 1][wg][t] = bm_own;
+          aux.xq[qi & 1][wg][t] = qn2_own;
+          bar_sync(1, 256);
+          const float bm = fmaxf(bm_own, aux.xch[qi & 1][wg ^ 1][t]);
+          const float bound = sqrtf(qn2_own + aux.xq[qi & 1][wg ^ 1][t]) * kmax * sl2 * 1.0001f;
+          m = fmaxf(bm, bound - 64.f);
+          first_step = false;
         }
-        // P (bf16 pairs) over the first half of this S buffer: keys 64*wg.. -> columns 32*wg..
-        tmem_st16u(cs + wg * 32, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-        tmem_st16u(cs + wg * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
+        // P (bf16 pairs) of my 32 keys of key region k -> columns 64k + 32wg
+        // .. +15: inside MY S columns, which the other warpgroup never reads
+        const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+        float2 acc = make_float2(0.f, 0.f);
+        {
+          uint32_t pk[16];
+          if (kp0) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+              const float2 e = ffma2(make_float2(x0[c], x0[c + 1]), sc, nm);
+              const float2 pe = make_float2(fast_exp2(e.x), fast_exp2(e.y));
+              acc = fadd2(acc, pe);
+              pk[c / 2] = pack_bf16(pe.x, pe.y);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          }
+          tmem_st16u(cs + 32 * wg, pk);
+        }
+        {
+          uint32_t pk[16];
+          if (kp1) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+              const float2 e = ffma2(make_float2(x1[c], x1[c + 1]), sc, nm);
+              const float2 pe = make_float2(fast_exp2(e.x), fast_exp2(e.y));
+              acc = fadd2(acc, pe);
+              pk[c / 2] = pack_bf16(pe.x, pe.y);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          }
+          if (t == 0 && wg == 0) PAIR_TRACE(17, G);
+          tmem_st16u(cs + 64 + 32 * wg, pk);
+        }
+        l += acc.x + acc.y;
         tmem_st_wait();
+        if (t == 0 && wg == 0) PAIR_TRACE(18, G);
         tc_fence_before();
         mbar_arrive(&B.p_full[b]);
-        if (t == 0 && wg == 0) PAIR_TRACE(7, G);
-        first_step = false;
+        if ((threadIdx.x & 31) == 0) PAIR_TRACE(7 + (warp - 4), G);
         ++G;
       }
       // ---- next nonempty item's Q (its GEMM1s overlap this epilogue)
@@ -503,8 +691,10 @@ __global__ void __launch_bounds__(384, 1)
       }
       // ------------------------------ epilogue ------------------------------
       aux.lsum[wg][t] = l;
+      aux.had[wg][t] = had ? 1 : 0;
       bar_sync(1, 256);
       const float lt = l + aux.lsum[wg ^ 1][t];
+      const bool bad = (had || aux.had[wg ^ 1][t]) && !(lt >= 0x1p-80f);
       mbar_wait(&B.o_full, qi & 1);
       tc_fence_after();
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
@@ -519,11 +709,19 @@ __global__ void __launch_bounds__(384, 1)
           for (int c = 0; c < 16; ++c) w[c] = pack_bf16(o[2 * c] * inv, o[2 * c + 1] * inv);
           uint4* dst = reinterpret_cast<uint4*>(orow) + c2 * 4;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+          for (int c = 0; c < 4; ++c)
+            stg128_hint(dst + c, make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]), p.pol_o);
         }
       }
       tc_fence_before();
       mbar_arrive(&B.o_empty);
+      if (wg == 0) {
+        const unsigned bal = __ballot_sync(0xffffffffu, bad && row >= 0);
+        if (bal != 0u && (threadIdx.x & 31) == 0) {
+          const int slot = atomicAdd(p.fb_count, 1);
+          p.fb_items[slot] = itm.h * p.geo.g + region;
+        }
+      }
       ++qi;
     }
   }
@@ -567,6 +765,31 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   p.per_head = make_fastdiv((uint32_t)p.npairs);
   p.n_pad = g.n_pad;
   p.trace = trace;
+  {
+    static int pol = -1;
+    if (pol < 0) {
+      const char* env = getenv("DA_L2POL");
+      pol = env ? atoi(env) : 0;
+    }
+    p.pol_kv = (pol & 1) ? L2_EVICT_LAST : L2_EVICT_NORMAL;
+    p.pol_q = (pol & 2) ? L2_EVICT_FIRST : L2_EVICT_NORMAL;
+    p.pol_o = (pol & 4) ? L2_EVICT_FIRST : L2_EVICT_NORMAL;
+    static int fk = -1;
+    if (fk < 0) {
+      const char* env = getenv("DA_FAKELOAD");
+      fk = env ? atoi(env) : 0;
+    }
+    p.fake_load = fk;
+  }
+  // workspace: fallback counter | per-block key norm maxima | fallback items
+  char* ws = static_cast<char*>(a.workspace);
+  p.fb_count = reinterpret_cast<int*>(ws);
+  p.kpart = reinterpret_cast<float*>(ws + 256);
+  p.fb_items = reinterpret_cast<int*>(ws + 256 + pair_align256(sizeof(float) * a.heads * pairk::KBLK));
+  const long long key_rows = a.layout == DA_LAYOUT_REORDERED ? g.n_pad : g.n_real;
+  pairk::key_norm_kernel<<<dim3(pairk::KBLK, a.heads), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(a.k), a.k_head_stride, a.k_row_stride, key_rows,
+      const_cast<float*>(p.kpart), p.fb_count);
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;
@@ -579,7 +802,13 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   const long long items = (long long)a.heads * p.npairs;
   const int grid = (int)(items < num_sms ? items : num_sms);
   pairk::sparse_attn_pair_kernel<<<grid, 384, pairk::SMEM_ALLOC, st>>>(mk, mv, p);
-  return cudaGetLastError();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // rows whose fixed softmax offset underflowed: redo their regions exactly
+  return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * num_sms);
+}
+
+size_t pair_attn_workspace_size(int heads, const Geo& g) {
+  return 256 + pair_align256(sizeof(float) * heads * pairk::KBLK) + pair_align256(sizeof(int) * 2 * (size_t)heads * g.g);
 }
 
 }  // namespace da

@@ -38,8 +38,8 @@ DA_DEV bool key_ok(const PortableArgs& a, int region, int r) {
   return key_is_valid(a.geo, region, r);
 }
 
-__global__ void __launch_bounds__(256) portable_attn_kernel(PortableArgs a) {
-  extern __shared__ float sm[];
+// One query region i of head h (the whole block; block-uniform control flow).
+__device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) {
   const int p = a.geo.p, d = a.d, dv = a.dv;
   float* Qs = sm;                 // p*d
   float* Ks = Qs + p * d;         // p*d
@@ -51,7 +51,6 @@ __global__ void __launch_bounds__(256) portable_attn_kernel(PortableArgs a) {
   float* alpha = L + p;           // p
   int* kval = reinterpret_cast<int*>(alpha + p);  // p
 
-  const int i = blockIdx.x, h = blockIdx.y;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int g = a.geo.g;
   const int* rp = a.row_ptr + (long long)(h * a.mask_h) * (g + 1);
@@ -139,13 +138,30 @@ __global__ void __launch_bounds__(256) portable_attn_kernel(PortableArgs a) {
     float o = l > 0.f ? O[e] / l : 0.f;
     a.out[h * a.oh + row * a.orow + c] = __float2bfloat16_rn(o);
   }
+  __syncthreads();  // shared tiles are reused by the block's next region
+}
+
+__global__ void __launch_bounds__(256) portable_attn_kernel(PortableArgs a) {
+  extern __shared__ float sm[];
+  portable_region(a, blockIdx.x, blockIdx.y, sm);
+}
+
+// Regions listed in items[0 .. *count): the tcgen05 kernel's fallback rows.
+__global__ void __launch_bounds__(256) portable_list_kernel(PortableArgs a, const int* __restrict__ items,
+                                                            const int* __restrict__ count) {
+  extern __shared__ float sm[];
+  const int n = *count;
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const int it = items[b];
+    portable_region(a, it % a.geo.g, it / a.geo.g, sm);
+  }
 }
 
 size_t portable_smem_bytes(int p, int d, int dv) {
   return sizeof(float) * ((size_t)p * d * 2 + (size_t)p * dv * 2 + (size_t)p * p + 3 * (size_t)p) + sizeof(int) * p;
 }
 
-cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st) {
+static PortableArgs portable_args(const da_attn_args& args, const Geo& geo) {
   PortableArgs a;
   a.q = static_cast<const __nv_bfloat16*>(args.q);
   a.k = static_cast<const __nv_bfloat16*>(args.k);
@@ -161,11 +177,26 @@ cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaS
   a.key_valid = args.key_valid;
   a.mask_h = args.shared_mask ? 0 : 1;
   a.geo = geo;
+  return a;
+}
+
+cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st) {
+  const PortableArgs a = portable_args(args, geo);
   size_t smem = portable_smem_bytes(geo.p, args.d, args.dv);
   cudaError_t e = cudaFuncSetAttribute(portable_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(geo.g, args.heads);
   portable_attn_kernel<<<grid, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_portable_list(const da_attn_args& args, const Geo& geo, cudaStream_t st, const int* items,
+                                 const int* count, int blocks) {
+  const PortableArgs a = portable_args(args, geo);
+  size_t smem = portable_smem_bytes(geo.p, args.d, args.dv);
+  cudaError_t e = cudaFuncSetAttribute(portable_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  portable_list_kernel<<<blocks, 256, smem, st>>>(a, items, count);
   return cudaGetLastError();
 }
 

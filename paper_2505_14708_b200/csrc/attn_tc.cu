@@ -660,6 +660,7 @@ static bool make_map_5d(CUtensorMap* m, const void* base, long long head_stride,
 
 bool tc_supported(const da_attn_args& a, const Geo& g) {
   if (a.d != 128 || a.dv != 128 || g.p != 64) return false;
+  if (!(a.scale > 0.0)) return false;  // the fixed softmax offset bounds scale * |q| |k| from above
   if (a.layout == DA_LAYOUT_ORIGINAL && (g.ph != 8 || g.pw != 8)) return false;
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   if (!al16(a.q) || !al16(a.k) || !al16(a.v) || !al16(a.out)) return false;

@@ -126,6 +126,17 @@ DA_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   // with a suspend-time hint the warp sleeps in hardware until the phase
   // completes (or the hint expires) instead of spinning on issue slots
+#ifdef DA_MBAR_NOHINT
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -135,6 +146,7 @@ DA_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 // Blocking wait with a watchdog: a pipeline bug traps (kernel error) after
@@ -144,6 +156,30 @@ DA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(addr, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(addr, parity)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
+
+// Latency-critical wait: non-blocking test_wait in a tight loop (no suspend),
+// for waits on the MMA <-> softmax critical path.
+DA_DEV bool mbar_test_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+DA_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_test_wait(addr, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_test_wait(addr, parity)) {
     if (clock64() - t0 > (1ll << 34)) __trap();
   }
 }
@@ -175,6 +211,28 @@ DA_DEV void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
       "l"(policy)
       : "memory");
+}
+// 16-byte global load / store with an L2 cache-policy operand (L1 bypassed on the load).
+DA_DEV uint4 ldg128_hint(const void* p, uint64_t policy) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(policy));
+  return v;
+}
+DA_DEV void stg128_hint(void* p, uint4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(policy)
+               : "memory");
+}
+// 16-byte cp.async (L2 only); src_bytes = 0 zero-fills the destination.
+DA_DEV void cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes) : "memory");
+}
+DA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+DA_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 DA_DEV void sts128(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
@@ -337,6 +395,15 @@ DA_DEV float2 ffma2(float2 a, float2 b, float2 c) {
       : "=l"(d)
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// Packed fp32x2 add (Blackwell FADD2).
+DA_DEV float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
   return *reinterpret_cast<float2*>(&d);
 }
 

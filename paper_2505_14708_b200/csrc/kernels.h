@@ -33,6 +33,10 @@ cudaError_t launch_select(const double* scores, int heads, int g, long long m, i
 
 size_t portable_smem_bytes(int p, int d, int dv);
 cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st);
+// regions listed in items[0 .. *count) (entries h * g + i; count read on the device)
+cudaError_t launch_portable_list(const da_attn_args& args, const Geo& geo, cudaStream_t st, const int* items,
+                                 const int* count, int blocks);
+size_t pair_attn_workspace_size(int heads, const Geo& g);
 
 void set_tc_trace(void* buf);
 bool tc_supported(const da_attn_args& a, const Geo& g);

@@ -1,9 +1,11 @@
-"""Probe: per-step pipeline timeline of the tcgen05 kernel (CTA 0, clock64).
+"""Probe: per-step pipeline timeline of the region-pair tcgen05 kernel (CTA 0, clock64).
 
-Region-pair kernel events (row, index = step counter of that role):
-  0 K producer issues K(k)      1 V producer issues V(k)
-  2 MMA got K(k) (GEMM1 issue)  4 MMA GEMM2 #k issue (after V and P)
-  5 softmax waits S(G)          6 softmax got S(G)          7 softmax arrived P(G)
+Event rows (index = step counter of that role):
+  0 K producer issues K(t)     1 V producer issues V(t)
+  2 MMA got K(t)               3 MMA issued GEMM1(t)
+  4 MMA passed GEMM2(t) waits  5 MMA issued GEMM2(t)
+  6 softmax warp 4 got S(t)    7..14 softmax warps 4..11 arrived P(t)
+  15 softmax warp 4 starts waiting for S(t)
 """
 import ctypes
 import sys
@@ -22,26 +24,34 @@ n, d = plan.num_valid, 128
 g = torch.Generator(device="cuda").manual_seed(0)
 q, k, v = (torch.randn(heads, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
 api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(d), "average", "logits", True, False, "hnd")
-tr = torch.zeros(16, 1024, dtype=torch.int64, device="cuda")
+tr = torch.zeros(20, 1024, dtype=torch.int64, device="cuda")
 _lib.lib().da_debug_trace(ctypes.c_void_p(tr.data_ptr()))
 api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(d), "average", "logits", True, False, "hnd")
 torch.cuda.synchronize()
 _lib.lib().da_debug_trace(None)
-t = tr.cpu().numpy()
-base = t[0, 0]
-rel = lambda x: int(x - base) if x else -1  # noqa: E731
-print("step: Kissue Vissue MMAgotK GEMM2issue | SMwaitS SMgotS SMarrP")
-for s in range(200, 232):
-    print(f"{s:4d}: {rel(t[0, s]):9d} {rel(t[1, s]):9d} {rel(t[2, s]):9d} {rel(t[4, s]):9d} | "
-          f"{rel(t[5, s]):9d} {rel(t[6, s]):9d} {rel(t[7, s]):9d}")
+t = tr.cpu().numpy().astype(np.float64)
+lo, hi = 100, 900
+last_p = t[7:15, :].max(axis=0)
+first_p = t[7:15, :].min(axis=0)
+base = t[0, lo]
+print("step | Kiss  gotK  G1done  G2pass G2done | S4got  Pfirst Plast   (cycles rel. to K issue of step 100)")
+for s in range(200, 224):
+    print(f"{s:4d} | " + " ".join(f"{int(t[r, s] - base):7d}" for r in (0, 2, 3, 4, 5)) + " | " +
+          " ".join(f"{int(x - base):7d}" for x in (t[6, s], first_p[s], last_p[s])))
 
 
-def avg(a, b, lo=100, hi=900):
-    return float(np.mean(t[b, lo:hi] - t[a, lo:hi]))
+def m(x):
+    return float(np.mean(x[lo:hi]))
 
 
-print("avg cycles/step (K issue):", float(np.mean(np.diff(t[0, 100:900]))))
-print("avg cycles/step (GEMM1 issue):", float(np.mean(np.diff(t[2, 100:900]))))
-print("softmax: gotS->arrivedP", avg(6, 7), " waitS->gotS", avg(5, 6))
-print("GEMM1 issue -> softmax got S", avg(2, 6), "  arrivedP -> GEMM2 issue", avg(7, 4))
-print("producer K lead (K issue -> GEMM1 issue)", avg(0, 2), " V issue -> GEMM2 issue", avg(1, 4))
+print("cycles/step (GEMM1 issue):", m(np.diff(t[2], prepend=0)))
+print("G1 issue duration (gotK->G1done):", m(t[3] - t[2]), "  G2 issue duration:", m(t[5] - t[4]))
+print("softmax spread (last P - first P):", m(last_p - first_p))
+print("last P(t) -> G2(t) passes waits:", m(t[4] - last_p))
+print("G2(t) done -> gotK(t+2):", float(np.mean(t[2, lo + 2:hi + 2] - t[5, lo:hi])))
+print("G1(t) issued -> S(t) got by warp 4:", m(t[6] - t[3]))
+print("S got -> last P:", m(last_p - t[6]), " per-warp S got -> P:",
+      [round(m(t[7 + w] - t[6]), 0) for w in range(8)])
+print("warp4 waiting for S:", m(t[6] - t[15]))
+print("warp4: S got -> ld done", m(t[16] - t[6]), " ld done -> exps done", m(t[17] - t[16]),
+      " exps done -> st waited", m(t[18] - t[17]), " st waited -> P arrive", m(t[7] - t[18]))

@@ -91,6 +91,28 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   constexpr int BLK = 16384;
+  auto run_bulk = [&](auto kern, int stages, size_t nblocks) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, stages * BLK);
+    int grid = prop.multiProcessorCount;
+    int iters = 4000;
+    kern<<<grid, 32, stages * BLK>>>(buf, nblocks, 200, sink);
+    cudaEventRecord(e0);
+    kern<<<grid, 32, stages * BLK>>>(buf, nblocks, iters, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double bytes = double(grid) * iters * BLK;
+    printf("bulk stages %2d (%3d KB in flight/SM) 64 MB buf: %.1f GB/s err=%s\n", stages, stages * 16,
+           bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+  };
+  {
+    size_t nb = (size_t(64) << 20) / BLK;
+    run_bulk(l2bw_kernel<4, BLK>, 4, nb);
+    run_bulk(l2bw_kernel<8, BLK>, 8, nb);
+    run_bulk(l2bw_kernel<10, BLK>, 10, nb);
+    run_bulk(l2bw_kernel<13, BLK>, 13, nb);
+  }
   constexpr int STAGES = 8;
   cudaFuncSetAttribute(l2bw_kernel<STAGES, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, STAGES * BLK);
   size_t sizes_mb[] = {32, 64, 96, 2048};
