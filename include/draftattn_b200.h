@@ -180,7 +180,7 @@ int da_sparse_attention(const da_pipeline_args* args, const da_grid* grid, void*
 
 /* ---- Diagnostics -------------------------------------------------------------
  * While set, the tcgen05 kernel of CTA 0 records clock64() stamps of its
- * pipeline events (20 event rows x 1024 steps, int64) into this device buffer.
+ * pipeline events (24 event rows x 1024 steps, int64) into this device buffer.
  * NULL disables. Not thread-safe; for profiling only. */
 int da_debug_trace(void* device_buffer);
 

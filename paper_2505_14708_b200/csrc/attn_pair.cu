@@ -1,34 +1,37 @@
 // K4: block-sparse FlashAttention forward on tcgen05 / TMEM / TMA (sm_100a),
-// region-pair tiles.
+// region-pair tiles with a deep MMA pipeline.
 //
 // Shape: region size p = 64 (8x8 pool), d = dv = 128, bf16 in, fp32 accumulate.
 //
 // A work item is a PAIR of query regions (2i, 2i+1) of one head: 128 query
-// rows, one per TMEM lane and one per softmax thread. The item walks the
-// ascending UNION of the two kept key-region lists, two key regions (128 keys)
-// per step; a key region kept by only one of the two query regions is masked
-// for the other region's rows (whole-warp predicate). Per step:
-//     GEMM1  S[128 q x 128 k]  = Q[128 x 128d] . K_pair^T      A = Q in TMEM, B = K (smem, K-major)
-//     GEMM2  O[128 q x 128 d] += P[128 x 128k] . V_pair        A = P in TMEM, B = V (smem, MN-major)
-// Q and P live in TMEM, so shared memory only carries the K/V tiles: an SS
-// MMA at N = 64 streams 6 KB of operands per 32-cycle instruction and is
-// shared-memory bound (measured 48 cycles, tools/probes/mma_rate.cu), whereas
-// these TS MMAs read 4 KB per 64-cycle instruction. The union costs ~1.9x the
-// MMA work of the kept pairs for i.i.d. data, but each K/V tile is fetched once
-// for 128 queries.
+// rows, one per TMEM lane. The item walks the UNION of the two kept key-region
+// lists, one key region (64 keys) per step; a key region kept by only one of
+// the two query regions is masked (P = 0) for the other region's rows. Per step:
+//     GEMM1  S[128 q x 64 k]   = Q[128 x 128d] . K_j^T     A = Q in TMEM, B = K (smem, K-major)
+//     GEMM2  O[128 q x 128 d] += P[128 x 64k] . V_j        A = P in TMEM, B = V (smem, MN-major)
+// Q and P live in TMEM, so shared memory only carries the K/V tiles. The union
+// costs ~1.9x the MMA work of the kept blocks for i.i.d. data, but each K/V
+// tile is fetched once for 128 queries and every MMA runs at M = 128.
+//
+// Pipeline: five 64-column S buffers let GEMM1 run LOOK = 3 steps ahead of
+// GEMM2, so the softmax of a step has ~3 steps of MMA time to finish (tcgen05
+// issue is effectively synchronous with the tensor pipe; with one S buffer of
+// look-ahead the MMA warp stalled on every softmax). A scheduler warp orders
+// each item's key regions so steps alternate between regions kept only by the
+// first and only by the second query region (their rows live on different
+// SMSPs), then the regions kept by both; a row's softmax is order-free because
+// its offset is fixed (below).
 //
 // Softmax is per row with a FIXED offset per (row, item) instead of a running
-// max (see the softmax warpgroups below), so O is never rescaled and the two
-// softmax warpgroups meet once per item. P is written back over S in TMEM as
-// packed bf16. Rows whose fixed offset underflows are redone by the portable
-// kernel (launch_pair_attn).
+// max, so O is never rescaled and the two softmax warpgroups meet once per
+// item. P is written back over S in TMEM as packed bf16. Rows whose fixed
+// offset underflows are redone by the portable kernel (launch_pair_attn).
 //
-// Roles (384 threads): warp 0 = TMA producer for K, warp 2 = TMA producer
-// for V, warp 1 = MMA issuer + TMEM owner, warps 4-7 and 8-11 = two
-// softmax / Q-loader / epilogue warpgroups that split each step's two key
-// regions (and the feature halves of Q and O) between them. TMEM: Q [0,64), S0 [64,192),
-// S1 [192,320) (double-buffered so GEMM1 of step t+1 overlaps the softmax of
-// step t), O [320,448).
+// Roles (384 threads): warp 0 = TMA producer for K (+ step info ring), warp 1
+// = MMA issuer + TMEM owner, warp 2 = TMA producer for V, warp 3 = step
+// scheduler, warps 4-7 and 8-11 = two softmax / Q-loader / epilogue
+// warpgroups; warpgroup wg takes keys [32wg, 32wg+32) of every step and
+// feature half wg of Q and O. TMEM: Q [0,64), S0..S4 [64,384), O [384,512).
 //
 // K/V tiles come from TMA: 2-D maps over reordered (heads, n_pad, 128) tensors
 // or 5-D maps (d, x, y, f, head) over the ORIGINAL token order whose box is one
@@ -48,18 +51,23 @@ namespace pairk {
 
 constexpr int P = 64;
 constexpr int D = 128;
-constexpr int KST = 3;
-constexpr int VST = 3;
+constexpr int KST = 6;              // K ring stages (one key region each)
+constexpr int VST = 6;              // V ring stages
 constexpr int BOX = 64 * 128;       // 64 rows x 64 bf16 = 8 KB
-constexpr int KV_BYTES = 4 * BOX;   // two key regions x two feature halves
-constexpr int KBLK = 32;              // key_norm_kernel blocks per head
+constexpr int TILE = 2 * BOX;       // one key region, two feature halves
+constexpr int NS = 5;               // S buffers
+constexpr int LOOK = 3;             // GEMM1 runs LOOK steps ahead of GEMM2 (LOOK <= NS - 1)
+constexpr int INFO = 16;            // step info ring (K producer -> MMA, softmax)
+constexpr int SCH = 16;             // schedule ring (scheduler -> K, V producers)
+constexpr int KBLK = 32;            // key_norm_kernel blocks per head
+static_assert(LOOK <= NS - 1, "S buffer reuse");
 
 constexpr int SMEM_K = 0;
-constexpr int SMEM_V = SMEM_K + KST * KV_BYTES;
-constexpr int SMEM_END = SMEM_V + VST * KV_BYTES;
+constexpr int SMEM_V = SMEM_K + KST * TILE;
+constexpr int SMEM_END = SMEM_V + VST * TILE;
 
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t COL_Q = 0, COL_S0 = 64, COL_S1 = 192, COL_O = 320;
+constexpr uint32_t COL_Q = 0, COL_S = 64, COL_O = 384;
 
 struct Params {
   const __nv_bfloat16* q;
@@ -82,7 +90,7 @@ struct Params {
   const float* kpart;  // [heads][KBLK] per-block maxima of the key row norms (key_norm_kernel)
   int* fb_count;       // rows whose fixed softmax offset underflowed: their (head, region)
   int* fb_items;       //   items are recomputed by the portable kernel afterwards
-  int fake_load;           // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies
+  int fake_load;       // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies
   uint64_t pol_kv, pol_q, pol_o;  // L2 cache policies of the K/V tiles, Q rows, output rows
   long long* trace;
 };
@@ -90,16 +98,16 @@ struct Params {
 struct __align__(8) Bars {
   uint64_t k_full[KST], k_empty[KST];
   uint64_t v_full[VST], v_empty[VST];
-  uint64_t s_full[2], p_full[2];
+  uint64_t s_full[NS], p_full[NS];
   uint64_t o_full, o_empty;
   uint64_t q_full, q_empty;
-  uint64_t info_full[8];
-  uint64_t sch_full[16], sch_empty[16];
+  uint64_t info_full[INFO];
+  uint64_t sch_full[SCH], sch_empty[SCH];
 };
 struct SmemAux {
   Bars bars;
-  int4 info[8];           // per step: key regions j0, j1, membership flags, last/first (K producer)
-  int4 sched[16];         // step schedule (warp 3) for the K and V producers
+  int4 info[INFO];        // per step: key region, -, membership flags, last/first (K producer)
+  int4 sched[SCH];        // step schedule (warp 3) for the K and V producers
   uint32_t tmem_base;
   float xch[2][2][128];   // [item parity][warpgroup][row] first-step block maxima
   float xq[2][2][128];    // [item parity][warpgroup][row] partial |q|^2
@@ -110,17 +118,27 @@ constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
 static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
 
 constexpr int TRACE_N = 1024;
+#ifndef TRACE_T
+#define TRACE_T 128  // softmax thread whose step timeline is traced (rows 6, 15-18)
+#endif
 // waits on the MMA <-> softmax critical path
 #ifdef DA_CRIT_SLEEP
 #define DA_WAITC mbar_wait
 #else
 #define DA_WAITC mbar_wait_spin
 #endif
+// pipeline timeline (tools/probes/k4_trace.py): compiled in with -DDA_TRACE only
+#ifdef DA_TRACE
 #define PAIR_TRACE(ev, idx)                                                   \
   do {                                                                        \
     if (p.trace != nullptr && blockIdx.x == 0 && (idx) < TRACE_N)             \
       p.trace[(ev) * TRACE_N + (idx)] = (long long)clock64();                 \
   } while (0)
+#else
+#define PAIR_TRACE(ev, idx) \
+  do {                      \
+  } while (0)
+#endif
 
 // An item: query regions a = 2*ip and b = 2*ip + 1 (b may not exist) of head h.
 struct PairItem {
@@ -275,13 +293,13 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 256); }
+    for (int s = 0; s < NS; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 256); }
     mbar_init(&B.o_full, 1);
     mbar_init(&B.o_empty, 256);
     mbar_init(&B.q_full, 256);
     mbar_init(&B.q_empty, 1);
-    for (int s = 0; s < 8; ++s) mbar_init(&B.info_full[s], 1);
-    for (int s = 0; s < 16; ++s) { mbar_init(&B.sch_full[s], 1); mbar_init(&B.sch_empty[s], 2); }
+    for (int s = 0; s < INFO; ++s) mbar_init(&B.info_full[s], 1);
+    for (int s = 0; s < SCH; ++s) { mbar_init(&B.sch_full[s], 1); mbar_init(&B.sch_empty[s], 2); }
     fence_barrier_init();
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
@@ -300,29 +318,24 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 3) {
     // ======================= step scheduler (one thread) =======================
-    // Each step is two key regions of the item's union. Regions kept by only one
-    // query region of the pair are paired across the two (one kept by a, one by
-    // b) so both halves of the softmax warpgroups (rows of a on SMSPs 0-1, rows
-    // of b on SMSPs 2-3) get one region's exponentials per step; the excess of
-    // one side, then regions kept by both, are paired among themselves. The
-    // order of key regions inside a row's softmax is immaterial (fixed offset,
-    // fp32 sums).
+    // Key regions kept only by query region a and only by b alternate (their
+    // exponentials land on different SMSPs), then the regions kept by both.
     if (lane == 0) {
       int sq = 0;
       int4 pend = make_int4(0, 0, 0, 0);
       bool have = false, first = true;
       auto emit = [&](int4 e, bool last) {
-        const int sl = sq & 15;
-        if (sq >= 16) mbar_wait(&B.sch_empty[sl], ((sq >> 4) - 1) & 1);
+        const int sl = sq % SCH;
+        if (sq >= SCH) mbar_wait(&B.sch_empty[sl], ((sq / SCH) - 1) & 1);
         e.w = (last ? 1 : 0) | (first ? 2 : 0);
         aux.sched[sl] = e;
         mbar_arrive(&B.sch_full[sl]);
         first = false;
         ++sq;
       };
-      auto step = [&](int j0, int f0, int j1, int f1) {
+      auto step = [&](int j, int f) {
         if (have) emit(pend, false);
-        pend = make_int4(j0, j1, f0 | (f1 << 2), 0);
+        pend = make_int4(j, 0, f, 0);
         have = true;
       };
       for (long long it = blockIdx.x;; it += gridDim.x) {
@@ -337,19 +350,11 @@ __global__ void __launch_bounds__(384, 1)
         have = false;
         int x = 0, y = 0, z = 0;
         bool hx = sa.next(false, x), hy = sb.next(false, y);
-        while (hx && hy) {
-          step(x, 1, y, 2);
-          hx = sa.next(false, x);
-          hy = sb.next(false, y);
+        while (hx || hy) {
+          if (hx) { step(x, 1); hx = sa.next(false, x); }
+          if (hy) { step(y, 2); hy = sb.next(false, y); }
         }
-        int lj = -1, lf = 0;
-        auto single = [&](int j, int f) {
-          if (lj < 0) { lj = j; lf = f; } else { step(lj, lf, j, f); lj = -1; }
-        };
-        while (hx) { single(x, 1); hx = sa.next(false, x); }
-        while (hy) { single(y, 2); hy = sb.next(false, y); }
-        while (sc.next(true, z)) single(z, 3);
-        if (lj >= 0) step(lj, lf, lj, 0);
+        while (sc.next(true, z)) step(z, 3);
         emit(pend, true);
       }
     }
@@ -362,140 +367,145 @@ __global__ void __launch_bounds__(384, 1)
       uint64_t* full = is_k ? B.k_full : B.v_full;
       uint64_t* empty = is_k ? B.k_empty : B.v_empty;
       const CUtensorMap* map = is_k ? &tm_k : &tm_v;
-      int kq = 0;
-      int sq = 0;
+      int kq = 0, sq = 0;
       for (long long it = blockIdx.x;; it += gridDim.x) {
         PairItem itm;
         if (!fetch_pair(p, it, items, itm)) break;
         if (itm.na + itm.nb == 0) continue;
         for (bool last = false; !last;) {
-          const int sl = sq & 15;
-          mbar_wait(&B.sch_full[sl], (uint32_t)((sq >> 4) & 1));
+          const int sl = sq % SCH;
+          mbar_wait(&B.sch_full[sl], (uint32_t)((sq / SCH) & 1));
           const int4 e = aux.sched[sl];
           mbar_arrive(&B.sch_empty[sl]);
           ++sq;
           last = (e.w & 1) != 0;
-          const int j0 = e.x, j1 = e.y;
           const int s = kq % ST;
           if (kq >= ST) mbar_wait(&empty[s], ((kq / ST) - 1) & 1);
           PAIR_TRACE(is_k ? 0 : 1, kq);
           if (is_k) {
             // step info for the MMA issuer and the softmax warpgroups (the K
-            // producer runs at most 5 steps ahead of the softmax: 8 entries)
-            aux.info[kq & 7] = e;
-            mbar_arrive(&B.info_full[kq & 7]);
+            // producer runs at most KST + NS steps ahead of the softmax)
+            aux.info[kq % INFO] = e;
+            mbar_arrive(&B.info_full[kq % INFO]);
           }
-          uint8_t* st = ring + s * KV_BYTES;
+          uint8_t* st = ring + s * TILE;
           if (p.fake_load & (is_k ? 1 : 2)) {  // diagnostics: skip the copy (timing only)
             mbar_arrive(&full[s]);
             ++kq;
             continue;
           }
-          mbar_expect_tx(&full[s], KV_BYTES);
-          if (is_k) {  // [half][slot][64 x 128B]: B operand rows 0..127 = keys of j0 then j1
-            load_region(map, st, &full[s], p, itm.h, j0, 0);
-            load_region(map, st + BOX, &full[s], p, itm.h, j1, 0);
-            load_region(map, st + 2 * BOX, &full[s], p, itm.h, j0, 1);
-            load_region(map, st + 3 * BOX, &full[s], p, itm.h, j1, 1);
-          } else {     // [slot][half][64 x 128B]: MN-major B, keys = K dimension
-            load_region(map, st, &full[s], p, itm.h, j0, 0);
-            load_region(map, st + BOX, &full[s], p, itm.h, j0, 1);
-            load_region(map, st + 2 * BOX, &full[s], p, itm.h, j1, 0);
-            load_region(map, st + 3 * BOX, &full[s], p, itm.h, j1, 1);
-          }
+          // [feature half][64 rows x 128 B]: K-major B of GEMM1 / MN-major B of GEMM2
+          mbar_expect_tx(&full[s], TILE);
+          load_region(map, st, &full[s], p, itm.h, e.x, 0);
+          load_region(map, st + BOX, &full[s], p, itm.h, e.x, 1);
           ++kq;
         }
       }
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ==============================
-    if (lane == 0) {
-      constexpr uint32_t IDESC1 = umma_idesc_bf16(128, 128, 0, 0);  // A (TMEM) K-major, B K-major
+    // The whole warp runs the loop (so descriptors and counters are warp-uniform
+    // and live in uniform registers); one elected lane issues the MMAs. The
+    // loop is kept lean: this warp shares its SMSP with two softmax warps, and
+    // every instruction here delays the tensor pipe.
+    {
+      constexpr uint32_t IDESC1 = umma_idesc_bf16(128, 64, 0, 0);   // A (TMEM) K-major, B K-major
       constexpr uint32_t IDESC2 = umma_idesc_bf16(128, 128, 0, 1);  // A (TMEM) K-major, B MN-major
-      const uint64_t dK = umma_desc_sw128(0, 16, 1024);
-      const uint64_t dV = umma_desc_sw128(0, BOX, 1024);
-      const uint32_t aK = smem_u32(sK) >> 4, aV = smem_u32(sV) >> 4;
-      int kq = 0, vq = 0, qi = 0;
-      long long G = 0;
-      struct Pend {
-        long long step;
-        int qi;
-        bool first, last, valid;
-      } pend;
-      pend.valid = false;
-      auto gemm2 = [&](const Pend& s) {
-        const int vs = vq % VST;
-        DA_WAITC(&B.v_full[vs], (vq / VST) & 1);
-        const int b = (int)(s.step & 1);
-        DA_WAITC(&B.p_full[b], (uint32_t)((s.step >> 1) & 1));
-        if (s.first && s.qi > 0) mbar_wait(&B.o_empty, (s.qi - 1) & 1);
-        PAIR_TRACE(4, vq);
+      const uint64_t dK = umma_desc_sw128(0, 16, 1024) + (smem_u32(sK) >> 4);
+      const uint64_t dV = umma_desc_sw128(0, BOX, 1024) + (smem_u32(sV) >> 4);
+      int kidx = 0, sidx = 0, iidx = 0, vidx = 0, pidx = 0;
+      uint32_t kph = 0, vph = 0, pph = 0;
+      int pend0 = 0, pend1 = 0, pend2 = 0, nq = 0;  // steps awaiting GEMM2: qi << 2 | last << 1 | first
+      static_assert(LOOK == 3, "pend registers");
+      int qi = 0, kq = 0, vq = 0;  // step counters (trace indices)
+      auto gemm2 = [&](int fl) {
+        if (lane == 0) PAIR_TRACE(20, vq);
+        DA_WAITC(&B.v_full[vidx], vph);
+        if (lane == 0) PAIR_TRACE(21, vq);
+        DA_WAITC(&B.p_full[pidx], pph);
+        const int q = fl >> 2;
+        if ((fl & 1) && q > 0) mbar_wait(&B.o_empty, (q - 1) & 1);
+        if (lane == 0) PAIR_TRACE(4, vq);
         tc_fence_after();
-        const uint32_t vbase = aV + vs * (KV_BYTES >> 4);
-        const uint32_t aP = tmem + (b ? COL_S1 : COL_S0);
+        if (elect_one_sync()) {
+          const uint32_t aP = tmem + COL_S + 64 * pidx;
+          const uint64_t bv = dV + (uint64_t)(vidx * (TILE >> 4));
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t bv = dV + (uint64_t)(vbase + (kk >> 2) * (2 * BOX >> 4) + (kk & 3) * (2048 >> 4));
-          // P of keys 16c.. of key region k sits at column 64k + 32(c/2) + 8(c%2)
-          umma_bf16_ts(tmem + COL_O, aP + (kk >> 2) * 64 + ((kk >> 1) & 1) * 32 + (kk & 1) * 8, bv, IDESC2,
-                       (s.first && kk == 0) ? 0u : 1u);
+          for (int kk = 0; kk < 4; ++kk) {
+            // P of keys 16kk.. sits at column 32(kk/2) + 8(kk%2) of the S buffer
+            umma_bf16_ts(tmem + COL_O, aP + (kk >> 1) * 32 + (kk & 1) * 8, bv + (uint64_t)(kk * (2048 >> 4)), IDESC2,
+                         ((fl & 1) && kk == 0) ? 0u : 1u);
+          }
+          umma_commit(&B.v_empty[vidx]);
+          if (fl & 2) umma_commit(&B.o_full);
+          PAIR_TRACE(5, vq);
         }
-        PAIR_TRACE(5, vq);
-        umma_commit(&B.v_empty[vs]);
-        if (s.last) umma_commit(&B.o_full);
+        __syncwarp();
         ++vq;
+        if (++vidx == VST) { vidx = 0; vph ^= 1u; }
+        if (++pidx == NS) { pidx = 0; pph ^= 1u; }
+      };
+      auto pop = [&]() {
+        const int fl = pend0;
+        pend0 = pend1;
+        pend1 = pend2;
+        --nq;
+        gemm2(fl);
       };
       for (long long it = blockIdx.x;; it += gridDim.x) {
         PairItem itm;
         if (!fetch_pair(p, it, items, itm)) break;
         if (itm.na + itm.nb == 0) continue;
+        // the softmax reaches this item's Q only after the epilogue of item
+        // qi - 2, which needs all of that item's GEMM2s
+        while (nq > 0 && (pend0 >> 2) <= qi - 2) pop();
         mbar_wait(&B.q_full, qi & 1);
-        bool first = true;
+        int first = 1;
         for (;;) {
-          const int ks = kq % KST;
-          DA_WAITC(&B.k_full[ks], (kq / KST) & 1);
-          const bool last = (aux.info[kq & 7].w & 1) != 0;  // written before the K copy was issued
-          PAIR_TRACE(2, kq);
+          DA_WAITC(&B.k_full[kidx], kph);
+          if (lane == 0) PAIR_TRACE(2, kq);
+          const int last = aux.info[iidx].w & 1;  // written before the K copy was issued
           tc_fence_after();
-          const uint32_t kbase = aK + ks * (KV_BYTES >> 4);
-          const int b = (int)(G & 1);
-          const uint32_t dS = tmem + (b ? COL_S1 : COL_S0);
+          if (elect_one_sync()) {
+            const uint32_t dS = tmem + COL_S + 64 * sidx;
+            const uint64_t bk = dK + (uint64_t)(kidx * (TILE >> 4));
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t bk = dK + (uint64_t)(kbase + (kk >> 2) * (2 * BOX >> 4) + (kk & 3) * 2);
-            umma_bf16_ts(dS, tmem + COL_Q + kk * 8, bk, IDESC1, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < 8; ++kk)
+              umma_bf16_ts(dS, tmem + COL_Q + kk * 8, bk + (uint64_t)((kk >> 2) * (BOX >> 4) + (kk & 3) * 2), IDESC1,
+                           kk > 0 ? 1u : 0u);
+            umma_commit(&B.k_empty[kidx]);
+            umma_commit(&B.s_full[sidx]);
+            if (last) umma_commit(&B.q_empty);
+            PAIR_TRACE(3, kq);
           }
-          PAIR_TRACE(3, kq);
-          umma_commit(&B.k_empty[ks]);
-          umma_commit(&B.s_full[b]);
-          if (last) umma_commit(&B.q_empty);
+          __syncwarp();
           ++kq;
-          if (pend.valid) gemm2(pend);
-          pend.step = G;
-          pend.qi = qi;
-          pend.first = first;
-          pend.last = last;
-          pend.valid = true;
-          first = false;
-          ++G;
+          if (++kidx == KST) { kidx = 0; kph ^= 1u; }
+          if (++sidx == NS) sidx = 0;
+          if (++iidx == INFO) iidx = 0;
+          if (nq == LOOK) pop();  // GEMM2 of the step LOOK back, after this GEMM1
+          const int fl = (qi << 2) | (last << 1) | first;
+          if (nq == 0) pend0 = fl; else if (nq == 1) pend1 = fl; else pend2 = fl;
+          ++nq;
+          first = 0;
           if (last) break;
         }
         ++qi;
       }
-      if (pend.valid) gemm2(pend);
+      while (nq > 0) pop();
     }
   } else if (warp >= 4) {
     // ============ softmax / Q loader / epilogue: two warpgroups split the step ============
-    // Warpgroup wg handles key region wg of each step (S columns [64*wg, 64*wg+64))
-    // and feature half wg of Q and O; thread t of a warpgroup owns query row t.
+    // Warpgroup wg handles keys [32wg, 32wg+32) of each step and feature half
+    // wg of Q and O; thread t of a warpgroup owns query row t.
     //
     // Fixed per-row offset instead of a running max: at an item's first step
     // the row fixes m = max(first-step row max, |q| * max|k| * scale - 64)
     // (log2 units). Cauchy-Schwarz bounds every later score by |q| max|k| scale,
     // so no exponent exceeds 2^64 (no overflow in fp32 / bf16) and O is never
-    // rescaled; the two warpgroups only meet once per item. A row whose sum
-    // ends below 2^-80 (its true max sits > ~80 below the bound) is handed to
-    // the portable kernel, which redoes its region with the streaming softmax.
+    // rescaled. A row whose sum ends below 2^-80 (its true max sits > ~80 below
+    // the bound) is handed to the portable kernel, which redoes its region
+    // with the streaming softmax.
     const int wg = (warp - 4) >> 2;
     const int t = (threadIdx.x - 128) & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -503,7 +513,9 @@ __global__ void __launch_bounds__(384, 1)
     const int half = t >> 6;  // 0: rows of region a, 1: rows of region b
     const int r = t & 63;
     const float sl2 = p.scale_log2;  // > 0 (tc_supported)
-    long long G = 0;
+    int G = 0;
+    int iidx = 0, sidx = 0;
+    uint32_t iph = 0, sph = 0;
     int qi = 0;
     float qn2_next = 0.f;  // my half of |q|^2 of the row whose Q was loaded last
     // my half of the Q row of (item, row) -> TMEM columns [32*wg, 32*wg+32) as
@@ -568,64 +580,41 @@ __global__ void __launch_bounds__(384, 1)
       }
       float m = 0.f, l = 0.f;
       bool had = false;
-      int j[2], fl[2];
       bool first_step = true;
       for (bool last = false; !last;) {
-        DA_WAITC(&B.info_full[G & 7], (uint32_t)((G >> 3) & 1));
-        const int4 inf = aux.info[G & 7];
-        j[0] = inf.x;
-        j[1] = inf.y;
-        fl[0] = inf.z & 3;
-        fl[1] = inf.z >> 2;
+        DA_WAITC(&B.info_full[iidx], iph);
+        const int4 inf = aux.info[iidx];
         last = (inf.w & 1) != 0;
-        const int b = (int)(G & 1);
-        const uint32_t cs = tq + (b ? COL_S1 : COL_S0);
-        if (t == 0 && wg == 0) PAIR_TRACE(15, G);
-        DA_WAITC(&B.s_full[b], (uint32_t)((G >> 1) & 1));
-        if (t == 0 && wg == 0) PAIR_TRACE(6, G);
+        const int sb = sidx;
+        const uint32_t cs = tq + COL_S + 64 * sb;
+        if (threadIdx.x == TRACE_T) PAIR_TRACE(15, G);
+        DA_WAITC(&B.s_full[sb], sph);
+        if (threadIdx.x == TRACE_T) PAIR_TRACE(6, G);
         tc_fence_after();
-        // keys [32*wg, 32*wg+32) of each of the step's two key regions (so the
-        // two warps of an SMSP always split a row's exponentials evenly);
-        // warp-uniform: a warp's rows share one query region
-        const bool kp0 = (fl[0] >> half) & 1, kp1 = (fl[1] >> half) & 1;
-        float x0[32], x1[32];
-        if (kp0) tmem_ld32(cs + 32 * wg, x0);
-        if (kp1) tmem_ld32(cs + 64 + 32 * wg, x1);
-        if (kp0 || kp1) {
-          const unsigned vm0 = kp0 ? (unsigned)(key_mask(p, j[0]) >> (32 * wg)) : 0u;
-          const unsigned vm1 = kp1 ? (unsigned)(key_mask(p, j[1]) >> (32 * wg)) : 0u;
+        // my 32 keys of the step's key region (warp-uniform: a warp's rows
+        // share one query region)
+        const bool kp = (inf.z >> half) & 1;
+        float x[32];
+        if (kp) {
+          tmem_ld32(cs + 32 * wg, x);
+          const unsigned vm = (unsigned)(key_mask(p, inf.x) >> (32 * wg));
           tmem_ld_wait();
-          if (kp0 && vm0 != ~0u) {
+          if (vm != ~0u) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) x0[c] = ((vm0 >> c) & 1u) ? x0[c] : -INFINITY;
+            for (int c = 0; c < 32; ++c) x[c] = ((vm >> c) & 1u) ? x[c] : -INFINITY;
           }
-          if (kp1 && vm1 != ~0u) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) x1[c] = ((vm1 >> c) & 1u) ? x1[c] : -INFINITY;
-          }
-          had |= (vm0 | vm1) != 0u;
+          had |= vm != 0u;
         }
-        if (t == 0 && wg == 0) PAIR_TRACE(16, G);
+        if (threadIdx.x == TRACE_T) PAIR_TRACE(16, G);
         if (first_step) {
-          float mx[8];
+          float bm_own = -INFINITY;
+          if (kp) {
+            float mx[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
-          if (kp0) {
-#pragma unroll
-            for (int c = 0; c < 32; c += 8) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], x0[c + e]);
-            }
+            for (int e = 0; e < 8; ++e) mx[e] = fmaxf(fmaxf(x[e], x[e + 8]), fmaxf(x[e + 16], x[e + 24]));
+            bm_own = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
           }
-          if (kp1) {
-#pragma unroll
-            for (int c = 0; c < 32; c += 8) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], x1[c + e]);
-            }
-          }
-          const float bm_own = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
           aux.xch[qi & 1][wg][t] = bm_own;
           aux.xq[qi & 1][wg][t] = qn2_own;
           bar_sync(1, 256);
@@ -634,50 +623,34 @@ __global__ void __launch_bounds__(384, 1)
           m = fmaxf(bm, bound - 64.f);
           first_step = false;
         }
-        // P (bf16 pairs) of my 32 keys of key region k -> columns 64k + 32wg
-        // .. +15: inside MY S columns, which the other warpgroup never reads
-        const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
-        float2 acc = make_float2(0.f, 0.f);
-        {
-          uint32_t pk[16];
-          if (kp0) {
+        // P (bf16 pairs) of my 32 keys -> columns 32wg .. 32wg+15 of the S
+        // buffer: inside MY S columns, which the other warpgroup never reads
+        uint32_t pk[16];
+        if (kp) {
+          const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+          float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-              const float2 e = ffma2(make_float2(x0[c], x0[c + 1]), sc, nm);
-              const float2 pe = make_float2(fast_exp2(e.x), fast_exp2(e.y));
-              acc = fadd2(acc, pe);
-              pk[c / 2] = pack_bf16(pe.x, pe.y);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          for (int c = 0; c < 32; c += 2) {
+            const float2 e = ffma2(make_float2(x[c], x[c + 1]), sc, nm);
+            const float2 pe = make_float2(fast_exp2(e.x), fast_exp2(e.y));
+            acc = fadd2(acc, pe);
+            pk[c / 2] = pack_bf16(pe.x, pe.y);
           }
-          tmem_st16u(cs + 32 * wg, pk);
-        }
-        {
-          uint32_t pk[16];
-          if (kp1) {
+          l += acc.x + acc.y;
+        } else {
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-              const float2 e = ffma2(make_float2(x1[c], x1[c + 1]), sc, nm);
-              const float2 pe = make_float2(fast_exp2(e.x), fast_exp2(e.y));
-              acc = fadd2(acc, pe);
-              pk[c / 2] = pack_bf16(pe.x, pe.y);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) pk[c] = 0u;
-          }
-          if (t == 0 && wg == 0) PAIR_TRACE(17, G);
-          tmem_st16u(cs + 64 + 32 * wg, pk);
+          for (int c = 0; c < 16; ++c) pk[c] = 0u;
         }
-        l += acc.x + acc.y;
+        if (threadIdx.x == TRACE_T) PAIR_TRACE(17, G);
+        tmem_st16u(cs + 32 * wg, pk);
         tmem_st_wait();
-        if (t == 0 && wg == 0) PAIR_TRACE(18, G);
+        if (threadIdx.x == TRACE_T) PAIR_TRACE(18, G);
         tc_fence_before();
-        mbar_arrive(&B.p_full[b]);
+        mbar_arrive(&B.p_full[sb]);
         if ((threadIdx.x & 31) == 0) PAIR_TRACE(7 + (warp - 4), G);
         ++G;
+        if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
+        if (++sidx == NS) { sidx = 0; sph ^= 1u; }
       }
       // ---- next nonempty item's Q (its GEMM1s overlap this epilogue)
       have_q = false;

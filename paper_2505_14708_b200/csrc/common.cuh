@@ -286,6 +286,21 @@ DA_DEV void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u));
 }
 
+// One lane of a converged warp (elect.sync): lets a whole warp run the MMA
+// issue loop (descriptors stay warp-uniform, in uniform registers) while one
+// lane issues.
+DA_DEV bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "elect.sync _|P1, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 DA_DEV void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");

@@ -24,7 +24,7 @@ n, d = plan.num_valid, 128
 g = torch.Generator(device="cuda").manual_seed(0)
 q, k, v = (torch.randn(heads, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
 api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(d), "average", "logits", True, False, "hnd")
-tr = torch.zeros(20, 1024, dtype=torch.int64, device="cuda")
+tr = torch.zeros(24, 1024, dtype=torch.int64, device="cuda")
 _lib.lib().da_debug_trace(ctypes.c_void_p(tr.data_ptr()))
 api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(d), "average", "logits", True, False, "hnd")
 torch.cuda.synchronize()
@@ -55,3 +55,7 @@ print("S got -> last P:", m(last_p - t[6]), " per-warp S got -> P:",
 print("warp4 waiting for S:", m(t[6] - t[15]))
 print("warp4: S got -> ld done", m(t[16] - t[6]), " ld done -> exps done", m(t[17] - t[16]),
       " exps done -> st waited", m(t[18] - t[17]), " st waited -> P arrive", m(t[7] - t[18]))
+print("MMA warp: gotK -> G1 issued+committed", m(t[3] - t[2]))
+print("  G1(t+3) committed -> enter gemm2(t)", float(np.mean(t[20, lo:hi] - t[3, lo + 3:hi + 3])))
+print("  v_full wait", m(t[21] - t[20]), " p_full+o_empty wait", m(t[4] - t[21]), " G2 issue+commit", m(t[5] - t[4]))
+print("  G2(t) committed -> gotK(t+4)", float(np.mean(t[2, lo + 4:hi + 4] - t[5, lo:hi])))

@@ -1,0 +1,2 @@
+DA_NVCC_FLAGS=-DDA_TRACE python -m paper_2505_14708_b200.build --force >/dev/null 2>&1
+timeout 300 python tools/probes/k4_trace.py 24 | tail -13
