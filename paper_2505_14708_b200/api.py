@@ -385,6 +385,70 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     return out, mask, squeeze
 
 
+def _cat_masks(masks) -> RegionMask:
+    """Stack per-head-group masks of one call (same g, keep ratio, capacity)."""
+    if len(masks) == 1:
+        return masks[0]
+    m0 = masks[0]
+    cat = lambda name: torch.cat([getattr(m, name) for m in masks], 0)  # noqa: E731
+    return RegionMask(m0.g, m0.keep_ratio, cat("bitmap"), cat("row_ptr"), cat("col_idx"), cat("thresholds"),
+                      cat("forced"), cat("kept_counts"), single=False)
+
+
+def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                   shared_head_mask, qkv_layout, group_heads=None):
+    """Host (CPU) inputs, the reference's calling convention: the call stages
+    Q/K/V to the GPU in head groups on a copy stream, runs each group's
+    pipeline on the current stream while the next group uploads, copies each
+    group's output back on a third stream, and returns once the output is in
+    (pinned) host memory. Heads are independent (per-head masks), so the
+    result equals one all-head call. Compute stays on the GPU: without CUDA
+    this raises (there is no CPU path)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("host inputs are staged to the GPU; no CUDA device is available (no CPU fallback)")
+    q3, squeeze = _as_heads(q, qkv_layout, "q")
+    k3, _ = _as_heads(k, qkv_layout, "k")
+    v3, _ = _as_heads(v, qkv_layout, "v")
+    heads, n, _ = q3.shape
+    dv = v3.shape[2]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out_dtype = _out_dtype(q, k, v)
+    main = torch.cuda.current_stream(dev)
+    contiguous = all(x.is_contiguous() for x in (q3, k3, v3))
+    hg = group_heads or max(1, -(-heads // 12))
+    if shared_head_mask or heads == 1 or not contiguous:
+        groups = [(0, heads)]  # the head-mean mask needs every head at once
+    else:
+        groups = [(h0, min(heads, h0 + hg)) for h0 in range(0, heads, hg)]
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in.wait_stream(main)
+    out_host = torch.empty((heads, n, dv), dtype=out_dtype, pin_memory=True)
+    masks = []
+    for h0, h1 in groups:
+        with torch.cuda.stream(s_in):
+            qd, kd, vd = (x[h0:h1].to(dev, non_blocking=True) for x in (q3, k3, v3))
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+        main.wait_event(ev_in)
+        for t in (qd, kd, vd):
+            t.record_stream(main)
+        out_g, mask_g, _ = _pipeline(qd, kd, vd, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                                     shared_head_mask, "hnd")
+        if out_g.dtype != out_dtype:
+            out_g = out_g.to(out_dtype)
+        ev_c = torch.cuda.Event()
+        ev_c.record(main)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_c)
+            out_host[h0:h1].copy_(out_g, non_blocking=True)
+        out_g.record_stream(s_out)
+        masks.append(mask_g)
+    main.wait_stream(s_out)
+    s_out.synchronize()
+    out = out_host[0] if squeeze else (out_host.transpose(0, 1) if qkv_layout == "nhd" else out_host)
+    return out, _cat_masks(masks), squeeze
+
+
 def _details(out, mask: RegionMask, layout: LatentLayout, d: int):
     if mask.single:
         return PipelineResult(out, mask, flops_count(layout, d, kept_count=int(mask.kept_count)),
@@ -420,8 +484,9 @@ def padded_sparse_attention(q, k, v, frames, height, width, patch_h, patch_w, sp
     d = q3.shape[2]
     if scale is None:
         scale = head_dim_scale(d)
-    out, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                             False, qkv_layout)
+    run = _pipeline_host if not q.is_cuda else _pipeline
+    out, mask, _ = run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                       False, qkv_layout)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)
@@ -440,8 +505,9 @@ def draft_sparse_attention(q, k, v, layout: LatentLayout, sparsity, scale=None, 
     if scale is None:
         scale = head_dim_scale(d)
     plan = PadPlan(layout.frames, layout.height, layout.width, layout)
-    out, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                             False, qkv_layout)
+    run = _pipeline_host if not q.is_cuda else _pipeline
+    out, mask, _ = run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                       False, qkv_layout)
     if not return_details:
         return out
     return _details(out, mask, layout, d)
@@ -468,8 +534,9 @@ def multi_head_sparse_attention(q, k, v, layout: LatentLayout, sparsity, shared_
     d = q3.shape[2]
     if scale is None:
         scale = head_dim_scale(d)
-    out, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                             shared_head_mask, qkv_layout)
+    run = _pipeline_host if not q.is_cuda else _pipeline
+    out, mask, _ = run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                       shared_head_mask, qkv_layout)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)

@@ -375,3 +375,19 @@ def test_deterministic():
     a = da.multi_head_sparse_attention(q, k, v, plan, 0.9)
     b = da.multi_head_sparse_attention(q, k, v, plan, 0.9)
     assert torch.equal(a, b)
+
+
+def test_host_inputs_pipelined_by_head_group_match_device_call():
+    # reference calling convention: host tensors in, host tensor out; head
+    # groups overlap upload / compute / download and must not change results
+    grid, (q, k, v), _ = _inputs((2, 45, 80, 8, 8, 128, 6, 0), head_ids=None)
+    plan = da.pad_plan(2, 45, 80, 8, 8)
+    dev = da.multi_head_sparse_attention(q, k, v, plan, 0.9, return_details=True)
+    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+    host = da.multi_head_sparse_attention(qh, kh, vh, plan, 0.9, return_details=True)
+    assert host.output.device.type == "cpu"
+    assert torch.equal(host.output, dev.output.cpu())
+    assert torch.equal(host.mask.bitmap, dev.mask.bitmap)
+    assert host.mask.kept_count == dev.mask.kept_count
+    single = da.padded_sparse_attention(qh[1], kh[1], vh[1], 2, 45, 80, 8, 8, 0.9)
+    assert torch.equal(single, dev.output[1].cpu())
