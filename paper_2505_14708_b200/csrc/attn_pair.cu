@@ -13,10 +13,10 @@
 // costs ~1.9x the MMA work of the kept blocks for i.i.d. data, but each K/V
 // tile is fetched once for 128 queries and every MMA runs at M = 128.
 //
-// Pipeline: five 64-column S buffers let GEMM1 run LOOK = 3 steps ahead of
-// GEMM2, so the softmax of a step has ~3 steps of MMA time to finish (tcgen05
-// issue is effectively synchronous with the tensor pipe; with one S buffer of
-// look-ahead the MMA warp stalled on every softmax). A scheduler warp orders
+// Pipeline: five 64-column S buffers let GEMM1 run up to four steps ahead of
+// GEMM2, so the softmax of a step has several steps of MMA time to finish;
+// GEMM1 and GEMM2 are issued by two warps so neither issue loop's waits stall
+// the other's MMAs. A scheduler warp orders
 // each item's key regions so steps alternate between regions kept only by the
 // first and only by the second query region (their rows live on different
 // SMSPs), then the regions kept by both; a row's softmax is order-free because
@@ -27,10 +27,10 @@
 // item. P is written back over S in TMEM as packed bf16. Rows whose fixed
 // offset underflows are redone by the portable kernel (launch_pair_attn).
 //
-// Roles (384 threads): warp 0 = TMA producer for K (+ step info ring), warp 1
-// = MMA issuer + TMEM owner, warp 2 = TMA producer for V, warp 3 = step
+// Roles (416 threads): warp 0 = TMA producer for K (+ step info ring), warp 1
+// = GEMM1 issuer + TMEM owner, warp 2 = TMA producer for V, warp 3 = step
 // scheduler, warps 4-7 and 8-11 = two softmax / Q-loader / epilogue
-// warpgroups; warpgroup wg takes keys [32wg, 32wg+32) of every step and
+// warpgroups, warp 12 = GEMM2 issuer; warpgroup wg takes keys [32wg, 32wg+32) of every step and
 // feature half wg of Q and O. TMEM: Q [0,64), S0..S4 [64,384), O [384,512).
 //
 // K/V tiles come from TMA: 2-D maps over reordered (heads, n_pad, 128) tensors
@@ -56,11 +56,9 @@ constexpr int VST = 6;              // V ring stages
 constexpr int BOX = 64 * 128;       // 64 rows x 64 bf16 = 8 KB
 constexpr int TILE = 2 * BOX;       // one key region, two feature halves
 constexpr int NS = 5;               // S buffers
-constexpr int LOOK = 3;             // GEMM1 runs LOOK steps ahead of GEMM2 (LOOK <= NS - 1)
 constexpr int INFO = 16;            // step info ring (K producer -> MMA, softmax)
 constexpr int SCH = 16;             // schedule ring (scheduler -> K, V producers)
 constexpr int KBLK = 32;            // key_norm_kernel blocks per head
-static_assert(LOOK <= NS - 1, "S buffer reuse");
 
 constexpr int SMEM_K = 0;
 constexpr int SMEM_V = SMEM_K + KST * TILE;
@@ -90,7 +88,8 @@ struct Params {
   const float* kpart;  // [heads][KBLK] per-block maxima of the key row norms (key_norm_kernel)
   int* fb_count;       // rows whose fixed softmax offset underflowed: their (head, region)
   int* fb_items;       //   items are recomputed by the portable kernel afterwards
-  int fake_load;       // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies
+  int sched_mode;      // 1 (default): ascending union, 0: alternate a-only / b-only regions (DA_SCHED)
+  int fake_load;       // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies, bit 2 softmax work
   uint64_t pol_kv, pol_q, pol_o;  // L2 cache policies of the K/V tiles, Q rows, output rows
   long long* trace;
 };
@@ -98,7 +97,7 @@ struct Params {
 struct __align__(8) Bars {
   uint64_t k_full[KST], k_empty[KST];
   uint64_t v_full[VST], v_empty[VST];
-  uint64_t s_full[NS], p_full[NS];
+  uint64_t s_full[NS], p_full[NS], s_free[NS];
   uint64_t o_full, o_empty;
   uint64_t q_full, q_empty;
   uint64_t info_full[INFO];
@@ -280,7 +279,7 @@ __global__ void __launch_bounds__(256) key_norm_kernel(const __nv_bfloat16* __re
   }
 }
 
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(416, 1)
     sparse_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                             const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -293,7 +292,11 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
-    for (int s = 0; s < NS; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 256); }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&B.s_full[s], 1);
+      mbar_init(&B.p_full[s], 256);
+      mbar_init(&B.s_free[s], 1);
+    }
     mbar_init(&B.o_full, 1);
     mbar_init(&B.o_empty, 256);
     mbar_init(&B.q_full, 256);
@@ -330,6 +333,7 @@ __global__ void __launch_bounds__(384, 1)
         e.w = (last ? 1 : 0) | (first ? 2 : 0);
         aux.sched[sl] = e;
         mbar_arrive(&B.sch_full[sl]);
+        PAIR_TRACE(23, sq);
         first = false;
         ++sq;
       };
@@ -349,12 +353,22 @@ __global__ void __launch_bounds__(384, 1)
         first = true;
         have = false;
         int x = 0, y = 0, z = 0;
-        bool hx = sa.next(false, x), hy = sb.next(false, y);
-        while (hx || hy) {
-          if (hx) { step(x, 1); hx = sa.next(false, x); }
-          if (hy) { step(y, 2); hy = sb.next(false, y); }
+        if (p.sched_mode == 1) {  // ascending union order (the reference's key order)
+          bool hx = sa.next(false, x), hz = sc.next(true, z), hy = sb.next(false, y);
+          while (hx || hy || hz) {
+            const int vx = hx ? x : 0x7fffffff, vy = hy ? y : 0x7fffffff, vz = hz ? z : 0x7fffffff;
+            if (vx < vy && vx < vz) { step(x, 1); hx = sa.next(false, x); }
+            else if (vy < vz) { step(y, 2); hy = sb.next(false, y); }
+            else { step(z, 3); hz = sc.next(true, z); }
+          }
+        } else {
+          bool hx = sa.next(false, x), hy = sb.next(false, y);
+          while (hx || hy) {
+            if (hx) { step(x, 1); hx = sa.next(false, x); }
+            if (hy) { step(y, 2); hy = sb.next(false, y); }
+          }
+          while (sc.next(true, z)) step(z, 3);
         }
-        while (sc.next(true, z)) step(z, 3);
         emit(pend, true);
       }
     }
@@ -403,68 +417,29 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    // ============================ MMA issuer ==============================
-    // The whole warp runs the loop (so descriptors and counters are warp-uniform
-    // and live in uniform registers); one elected lane issues the MMAs. The
-    // loop is kept lean: this warp shares its SMSP with two softmax warps, and
-    // every instruction here delays the tensor pipe.
+    // ========================= GEMM1 issuer (warp 1) =========================
+    // Two issuer warps (GEMM1 here, GEMM2 in warp 12) run their loops
+    // concurrently: each loop's waits and bookkeeping take about as long as
+    // the MMAs they feed, so one warp issuing both could not keep the tensor
+    // pipe busy. Each whole warp runs its loop (descriptors and counters stay
+    // warp-uniform, in uniform registers); one elected lane issues.
     {
-      constexpr uint32_t IDESC1 = umma_idesc_bf16(128, 64, 0, 0);   // A (TMEM) K-major, B K-major
-      constexpr uint32_t IDESC2 = umma_idesc_bf16(128, 128, 0, 1);  // A (TMEM) K-major, B MN-major
+      constexpr uint32_t IDESC1 = umma_idesc_bf16(128, 64, 0, 0);  // A (TMEM) K-major, B K-major
       const uint64_t dK = umma_desc_sw128(0, 16, 1024) + (smem_u32(sK) >> 4);
-      const uint64_t dV = umma_desc_sw128(0, BOX, 1024) + (smem_u32(sV) >> 4);
-      int kidx = 0, sidx = 0, iidx = 0, vidx = 0, pidx = 0;
-      uint32_t kph = 0, vph = 0, pph = 0;
-      int pend0 = 0, pend1 = 0, pend2 = 0, nq = 0;  // steps awaiting GEMM2: qi << 2 | last << 1 | first
-      static_assert(LOOK == 3, "pend registers");
-      int qi = 0, kq = 0, vq = 0;  // step counters (trace indices)
-      auto gemm2 = [&](int fl) {
-        if (lane == 0) PAIR_TRACE(20, vq);
-        DA_WAITC(&B.v_full[vidx], vph);
-        if (lane == 0) PAIR_TRACE(21, vq);
-        DA_WAITC(&B.p_full[pidx], pph);
-        const int q = fl >> 2;
-        if ((fl & 1) && q > 0) mbar_wait(&B.o_empty, (q - 1) & 1);
-        if (lane == 0) PAIR_TRACE(4, vq);
-        tc_fence_after();
-        if (elect_one_sync()) {
-          const uint32_t aP = tmem + COL_S + 64 * pidx;
-          const uint64_t bv = dV + (uint64_t)(vidx * (TILE >> 4));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            // P of keys 16kk.. sits at column 32(kk/2) + 8(kk%2) of the S buffer
-            umma_bf16_ts(tmem + COL_O, aP + (kk >> 1) * 32 + (kk & 1) * 8, bv + (uint64_t)(kk * (2048 >> 4)), IDESC2,
-                         ((fl & 1) && kk == 0) ? 0u : 1u);
-          }
-          umma_commit(&B.v_empty[vidx]);
-          if (fl & 2) umma_commit(&B.o_full);
-          PAIR_TRACE(5, vq);
-        }
-        __syncwarp();
-        ++vq;
-        if (++vidx == VST) { vidx = 0; vph ^= 1u; }
-        if (++pidx == NS) { pidx = 0; pph ^= 1u; }
-      };
-      auto pop = [&]() {
-        const int fl = pend0;
-        pend0 = pend1;
-        pend1 = pend2;
-        --nq;
-        gemm2(fl);
-      };
+      int kidx = 0, sidx = 0, iidx = 0;
+      uint32_t kph = 0, fph = 0;
+      int qi = 0, kq = 0;
       for (long long it = blockIdx.x;; it += gridDim.x) {
         PairItem itm;
         if (!fetch_pair(p, it, items, itm)) break;
         if (itm.na + itm.nb == 0) continue;
-        // the softmax reaches this item's Q only after the epilogue of item
-        // qi - 2, which needs all of that item's GEMM2s
-        while (nq > 0 && (pend0 >> 2) <= qi - 2) pop();
         mbar_wait(&B.q_full, qi & 1);
-        int first = 1;
         for (;;) {
           DA_WAITC(&B.k_full[kidx], kph);
           if (lane == 0) PAIR_TRACE(2, kq);
           const int last = aux.info[iidx].w & 1;  // written before the K copy was issued
+          // S buffer free: GEMM2 of step kq - NS has read its P
+          if (kq >= NS) DA_WAITC(&B.s_free[sidx], fph);
           tc_fence_after();
           if (elect_one_sync()) {
             const uint32_t dS = tmem + COL_S + 64 * sidx;
@@ -481,20 +456,62 @@ __global__ void __launch_bounds__(384, 1)
           __syncwarp();
           ++kq;
           if (++kidx == KST) { kidx = 0; kph ^= 1u; }
+          if (kq > NS && sidx == NS - 1) fph ^= 1u;
           if (++sidx == NS) sidx = 0;
           if (++iidx == INFO) iidx = 0;
-          if (nq == LOOK) pop();  // GEMM2 of the step LOOK back, after this GEMM1
-          const int fl = (qi << 2) | (last << 1) | first;
-          if (nq == 0) pend0 = fl; else if (nq == 1) pend1 = fl; else pend2 = fl;
-          ++nq;
-          first = 0;
           if (last) break;
         }
         ++qi;
       }
-      while (nq > 0) pop();
     }
-  } else if (warp >= 4) {
+  } else if (warp == 12) {
+    // ========================= GEMM2 issuer (warp 12) =========================
+    // O += P . V for every step in order, as soon as the step's P and V are in.
+    {
+      constexpr uint32_t IDESC2 = umma_idesc_bf16(128, 128, 0, 1);  // A (TMEM) K-major, B MN-major
+      const uint64_t dV = umma_desc_sw128(0, BOX, 1024) + (smem_u32(sV) >> 4);
+      int vidx = 0, pidx = 0, iidx = 0;
+      uint32_t vph = 0, pph = 0, iph = 0;
+      int qi = 0, vq = 0;
+      for (long long it = blockIdx.x;; it += gridDim.x) {
+        PairItem itm;
+        if (!fetch_pair(p, it, items, itm)) break;
+        if (itm.na + itm.nb == 0) continue;
+        for (bool first = true;; first = false) {
+          DA_WAITC(&B.info_full[iidx], iph);
+          const int last = aux.info[iidx].w & 1;
+          if (lane == 0) PAIR_TRACE(20, vq);
+          DA_WAITC(&B.v_full[vidx], vph);
+          if (lane == 0) PAIR_TRACE(21, vq);
+          DA_WAITC(&B.p_full[pidx], pph);
+          if (first && qi > 0) mbar_wait(&B.o_empty, (qi - 1) & 1);
+          if (lane == 0) PAIR_TRACE(4, vq);
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint32_t aP = tmem + COL_S + 64 * pidx;
+            const uint64_t bv = dV + (uint64_t)(vidx * (TILE >> 4));
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              // P of keys 16kk.. sits at column 32(kk/2) + 8(kk%2) of the S buffer
+              umma_bf16_ts(tmem + COL_O, aP + (kk >> 1) * 32 + (kk & 1) * 8, bv + (uint64_t)(kk * (2048 >> 4)),
+                           IDESC2, (first && kk == 0) ? 0u : 1u);
+            }
+            umma_commit(&B.v_empty[vidx]);
+            umma_commit(&B.s_free[pidx]);
+            if (last) umma_commit(&B.o_full);
+            PAIR_TRACE(5, vq);
+          }
+          __syncwarp();
+          ++vq;
+          if (++vidx == VST) { vidx = 0; vph ^= 1u; }
+          if (++pidx == NS) { pidx = 0; pph ^= 1u; }
+          if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
+          if (last) break;
+        }
+        ++qi;
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
     // ============ softmax / Q loader / epilogue: two warpgroups split the step ============
     // Warpgroup wg handles keys [32wg, 32wg+32) of each step and feature half
     // wg of Q and O; thread t of a warpgroup owns query row t.
@@ -581,22 +598,33 @@ __global__ void __launch_bounds__(384, 1)
       float m = 0.f, l = 0.f;
       bool had = false;
       bool first_step = true;
-      for (bool last = false; !last;) {
+      // The next step's S is waited for and its TMEM load issued before this
+      // step's P is published, so the load latency overlaps the store, the
+      // barrier arrive and the loop overhead (within an item).
+      float x[32];
+      int4 inf;
+      int sb;
+      bool kp;
+      auto acquire = [&]() {  // wait for step G's info and S; start loading my scores
+        if (threadIdx.x == TRACE_T) PAIR_TRACE(22, G);
         DA_WAITC(&B.info_full[iidx], iph);
-        const int4 inf = aux.info[iidx];
-        last = (inf.w & 1) != 0;
-        const int sb = sidx;
-        const uint32_t cs = tq + COL_S + 64 * sb;
+        inf = aux.info[iidx];
+        sb = sidx;
         if (threadIdx.x == TRACE_T) PAIR_TRACE(15, G);
         DA_WAITC(&B.s_full[sb], sph);
         if (threadIdx.x == TRACE_T) PAIR_TRACE(6, G);
         tc_fence_after();
-        // my 32 keys of the step's key region (warp-uniform: a warp's rows
-        // share one query region)
-        const bool kp = (inf.z >> half) & 1;
-        float x[32];
-        if (kp) {
-          tmem_ld32(cs + 32 * wg, x);
+        // my 32 keys of the step's key region (warp-uniform: a warp's rows share one query region)
+        kp = ((inf.z >> half) & 1) && !(p.fake_load & 4);
+        if (kp) tmem_ld32(tq + COL_S + 64 * sb + 32 * wg, x);
+      };
+      acquire();
+      for (bool last = false; !last;) {
+        last = (inf.w & 1) != 0;
+        const int sb_cur = sb;
+        const bool kp_cur = kp;
+        uint32_t pk[16];
+        if (kp_cur) {
           const unsigned vm = (unsigned)(key_mask(p, inf.x) >> (32 * wg));
           tmem_ld_wait();
           if (vm != ~0u) {
@@ -608,7 +636,7 @@ __global__ void __launch_bounds__(384, 1)
         if (threadIdx.x == TRACE_T) PAIR_TRACE(16, G);
         if (first_step) {
           float bm_own = -INFINITY;
-          if (kp) {
+          if (kp_cur) {
             float mx[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) mx[e] = fmaxf(fmaxf(x[e], x[e + 8]), fmaxf(x[e + 16], x[e + 24]));
@@ -624,15 +652,16 @@ __global__ void __launch_bounds__(384, 1)
           first_step = false;
         }
         // P (bf16 pairs) of my 32 keys -> columns 32wg .. 32wg+15 of the S
-        // buffer: inside MY S columns, which the other warpgroup never reads
-        uint32_t pk[16];
-        if (kp) {
+        // buffer: inside MY S columns, which the other warpgroup never reads.
+        // A quarter of the exponentials run as a polynomial on the FMA pipe
+        // (exp2_poly) to unload MUFU.
+        if (kp_cur) {
           const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
           float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
           for (int c = 0; c < 32; c += 2) {
             const float2 e = ffma2(make_float2(x[c], x[c + 1]), sc, nm);
-            const float2 pe = make_float2(fast_exp2(e.x), fast_exp2(e.y));
+            const float2 pe = (c % 8 == 6) ? exp2_poly2(e) : make_float2(fast_exp2(e.x), fast_exp2(e.y));
             acc = fadd2(acc, pe);
             pk[c / 2] = pack_bf16(pe.x, pe.y);
           }
@@ -642,15 +671,16 @@ __global__ void __launch_bounds__(384, 1)
           for (int c = 0; c < 16; ++c) pk[c] = 0u;
         }
         if (threadIdx.x == TRACE_T) PAIR_TRACE(17, G);
-        tmem_st16u(cs + 32 * wg, pk);
-        tmem_st_wait();
-        if (threadIdx.x == TRACE_T) PAIR_TRACE(18, G);
-        tc_fence_before();
-        mbar_arrive(&B.p_full[sb]);
-        if ((threadIdx.x & 31) == 0) PAIR_TRACE(7 + (warp - 4), G);
         ++G;
         if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
         if (++sidx == NS) { sidx = 0; sph ^= 1u; }
+        if (!last) acquire();  // x is free again: prefetch the next step's scores
+        tmem_st16u(tq + COL_S + 64 * sb_cur + 32 * wg, pk);
+        tmem_st_wait();
+        if (threadIdx.x == TRACE_T) PAIR_TRACE(18, G - 1);
+        tc_fence_before();
+        mbar_arrive(&B.p_full[sb_cur]);
+        if ((threadIdx.x & 31) == 0) PAIR_TRACE(7 + (warp - 4), G - 1);
       }
       // ---- next nonempty item's Q (its GEMM1s overlap this epilogue)
       have_q = false;
@@ -753,6 +783,12 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
       fk = env ? atoi(env) : 0;
     }
     p.fake_load = fk;
+    static int sm = -1;
+    if (sm < 0) {
+      const char* env = getenv("DA_SCHED");
+      sm = env ? atoi(env) : 1;
+    }
+    p.sched_mode = sm;
   }
   // workspace: fallback counter | per-block key norm maxima | fallback items
   char* ws = static_cast<char*>(a.workspace);
@@ -774,7 +810,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   if (e != cudaSuccess) return e;
   const long long items = (long long)a.heads * p.npairs;
   const int grid = (int)(items < num_sms ? items : num_sms);
-  pairk::sparse_attn_pair_kernel<<<grid, 384, pairk::SMEM_ALLOC, st>>>(mk, mv, p);
+  pairk::sparse_attn_pair_kernel<<<grid, 416, pairk::SMEM_ALLOC, st>>>(mk, mv, p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // rows whose fixed softmax offset underflowed: redo their regions exactly
   return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * num_sms);

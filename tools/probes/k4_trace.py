@@ -59,3 +59,5 @@ print("MMA warp: gotK -> G1 issued+committed", m(t[3] - t[2]))
 print("  G1(t+3) committed -> enter gemm2(t)", float(np.mean(t[20, lo:hi] - t[3, lo + 3:hi + 3])))
 print("  v_full wait", m(t[21] - t[20]), " p_full+o_empty wait", m(t[4] - t[21]), " G2 issue+commit", m(t[5] - t[4]))
 print("  G2(t) committed -> gotK(t+4)", float(np.mean(t[2, lo + 4:hi + 4] - t[5, lo:hi])))
+print("scheduler emit period", m(np.diff(t[23], prepend=0)), " emit(t) -> K producer issue(t)", m(t[0] - t[23]),
+      " K issue(t) -> MMA gotK(t)", m(t[2] - t[0]))
