@@ -1,26 +1,26 @@
 // K4: block-sparse FlashAttention forward on tcgen05 / TMEM / TMA (sm_100a),
-// region-pair tiles with a deep MMA pipeline.
+// two query regions per CTA item as two M = 64 tiles in lockstep.
 //
 // Shape: region size p = 64 (8x8 pool), d = dv = 128, bf16 in, fp32 accumulate.
 //
-// A work item is a PAIR of query regions (2i, 2i+1) of one head: 128 query
-// rows, one per TMEM lane. The item walks the UNION of the two kept key-region
-// lists, one key region (64 keys) per step; a key region kept by only one of
-// the two query regions is masked (P = 0) for the other region's rows. Per step:
-//     GEMM1  S[128 q x 64 k]   = Q[128 x 128d] . K_j^T     A = Q in TMEM, B = K (smem, K-major)
-//     GEMM2  O[128 q x 128 d] += P[128 x 64k] . V_j        A = P in TMEM, B = V (smem, MN-major)
-// Q and P live in TMEM, so shared memory only carries the K/V tiles. The union
-// costs ~1.9x the MMA work of the kept blocks for i.i.d. data, but each K/V
-// tile is fetched once for 128 queries and every MMA runs at M = 128.
+// A work item is a pair of query regions (2i, 2i+1) of one head. Each region
+// is its own M = 64 MMA tile: an M = 64 tcgen05 tile occupies TMEM lanes
+// {0-15, 32-47, 64-79, 96-111} at lane offset 0 (tile A) or the other
+// half-subpartitions at lane offset 16 (tile B), so both tiles share the same
+// TMEM columns and every warp holds 16 rows of each (tools/probes/m64_probe.cu).
+// Step t visits the t-th kept key region of each region's own list (ascending,
+// the reference's order): no union, no masked MMA rows; every softmax lane works
+// on every step while both lists last.
+//     GEMM1  S_T[64 q x 64 k]   = Q_T[64 x 128d] . K_j^T   A = Q in TMEM, B = K (smem, K-major)
+//     GEMM2  O_T[64 q x 128 d] += P_T[64 x 64k] . V_j      A = P in TMEM, B = V (smem, MN-major)
+// An M = 64 MMA costs the cycles of an M = 128 one, so per kept block the tensor
+// work equals a 128-row union tile's, while the exponentials are spread over all
+// four SMSPs instead of the two that hold one region's rows.
 //
 // Pipeline: five 64-column S buffers let GEMM1 run up to four steps ahead of
-// GEMM2, so the softmax of a step has several steps of MMA time to finish;
-// GEMM1 and GEMM2 are issued by two warps so neither issue loop's waits stall
-// the other's MMAs. A scheduler warp orders
-// each item's key regions so steps alternate between regions kept only by the
-// first and only by the second query region (their rows live on different
-// SMSPs), then the regions kept by both; a row's softmax is order-free because
-// its offset is fixed (below).
+// GEMM2; GEMM1 and GEMM2 are issued by two warps so neither issue loop's waits
+// stall the other's MMAs. The softmax issues the next step's TMEM load before
+// publishing the current P.
 //
 // Softmax is per row with a FIXED offset per (row, item) instead of a running
 // max, so O is never rescaled and the two softmax warpgroups meet once per
@@ -30,8 +30,9 @@
 // Roles (416 threads): warp 0 = TMA producer for K (+ step info ring), warp 1
 // = GEMM1 issuer + TMEM owner, warp 2 = TMA producer for V, warp 3 = step
 // scheduler, warps 4-7 and 8-11 = two softmax / Q-loader / epilogue
-// warpgroups, warp 12 = GEMM2 issuer; warpgroup wg takes keys [32wg, 32wg+32) of every step and
-// feature half wg of Q and O. TMEM: Q [0,64), S0..S4 [64,384), O [384,512).
+// warpgroups, warp 12 = GEMM2 issuer; warpgroup wg takes keys [32wg, 32wg+32)
+// of every step and feature half wg of Q and O. TMEM: Q [0,64), S0..S4
+// [64,384), O [384,512), each column range holding both tiles.
 //
 // K/V tiles come from TMA: 2-D maps over reordered (heads, n_pad, 128) tensors
 // or 5-D maps (d, x, y, f, head) over the ORIGINAL token order whose box is one
@@ -51,21 +52,23 @@ namespace pairk {
 
 constexpr int P = 64;
 constexpr int D = 128;
-constexpr int KST = 6;              // K ring stages (one key region each)
-constexpr int VST = 6;              // V ring stages
+constexpr int KST = 3;              // K ring stages (one step: a key region per tile)
+constexpr int VST = 3;              // V ring stages
 constexpr int BOX = 64 * 128;       // 64 rows x 64 bf16 = 8 KB
 constexpr int TILE = 2 * BOX;       // one key region, two feature halves
+constexpr int STAGE = 2 * TILE;     // the step's two key regions (tile A, tile B)
 constexpr int NS = 5;               // S buffers
 constexpr int INFO = 16;            // step info ring (K producer -> MMA, softmax)
 constexpr int SCH = 16;             // schedule ring (scheduler -> K, V producers)
 constexpr int KBLK = 32;            // key_norm_kernel blocks per head
 
 constexpr int SMEM_K = 0;
-constexpr int SMEM_V = SMEM_K + KST * TILE;
-constexpr int SMEM_END = SMEM_V + VST * TILE;
+constexpr int SMEM_V = SMEM_K + KST * STAGE;
+constexpr int SMEM_END = SMEM_V + VST * STAGE;
 
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t COL_Q = 0, COL_S = 64, COL_O = 384;
+constexpr uint32_t LANE_B = 16u << 16;  // TMEM address offset of tile B (lane 16)
 
 struct Params {
   const __nv_bfloat16* q;
@@ -88,7 +91,6 @@ struct Params {
   const float* kpart;  // [heads][KBLK] per-block maxima of the key row norms (key_norm_kernel)
   int* fb_count;       // rows whose fixed softmax offset underflowed: their (head, region)
   int* fb_items;       //   items are recomputed by the portable kernel afterwards
-  int sched_mode;      // 1 (default): ascending union, 0: alternate a-only / b-only regions (DA_SCHED)
   int fake_load;       // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies, bit 2 softmax work
   uint64_t pol_kv, pol_q, pol_o;  // L2 cache policies of the K/V tiles, Q rows, output rows
   long long* trace;
@@ -170,29 +172,6 @@ DA_DEV bool fetch_pair(const Params& p, long long it, long long items, PairItem&
   }
   return true;
 }
-
-// Elements of sorted list x that are (or are not) in sorted list y, ascending.
-struct MemberStream {
-  const int* x;
-  const int* y;
-  int nx, ny, ix, iy;
-  DA_DEV void init(const int* x_, int nx_, const int* y_, int ny_) {
-    x = x_; nx = nx_; y = y_; ny = ny_; ix = 0; iy = 0;
-  }
-  DA_DEV bool next(bool want_in_y, int& out) {
-    while (ix < nx) {
-      const int v = __ldg(x + ix);
-      ++ix;
-      while (iy < ny && __ldg(y + iy) < v) ++iy;
-      const bool in = iy < ny && __ldg(y + iy) == v;
-      if (in == want_in_y) {
-        out = v;
-        return true;
-      }
-    }
-    return false;
-  }
-};
 
 DA_DEV void load_region(const CUtensorMap* map, void* dst, uint64_t* bar, const Params& p, int h, int region,
                         int half) {
@@ -321,55 +300,25 @@ __global__ void __launch_bounds__(416, 1)
 
   if (warp == 3) {
     // ======================= step scheduler (one thread) =======================
-    // Key regions kept only by query region a and only by b alternate (their
-    // exponentials land on different SMSPs), then the regions kept by both.
+    // Step t of an item = (t-th kept key region of region a, t-th of region b);
+    // flags bit T = tile T still has a key region. Entries run ahead of the
+    // producers through a 16-deep ring.
     if (lane == 0) {
       int sq = 0;
-      int4 pend = make_int4(0, 0, 0, 0);
-      bool have = false, first = true;
-      auto emit = [&](int4 e, bool last) {
-        const int sl = sq % SCH;
-        if (sq >= SCH) mbar_wait(&B.sch_empty[sl], ((sq / SCH) - 1) & 1);
-        e.w = (last ? 1 : 0) | (first ? 2 : 0);
-        aux.sched[sl] = e;
-        mbar_arrive(&B.sch_full[sl]);
-        PAIR_TRACE(23, sq);
-        first = false;
-        ++sq;
-      };
-      auto step = [&](int j, int f) {
-        if (have) emit(pend, false);
-        pend = make_int4(j, 0, f, 0);
-        have = true;
-      };
       for (long long it = blockIdx.x;; it += gridDim.x) {
         PairItem itm;
         if (!fetch_pair(p, it, items, itm)) break;
-        if (itm.na + itm.nb == 0) continue;
-        MemberStream sa, sb, sc;
-        sa.init(itm.la, itm.na, itm.lb, itm.nb);
-        sb.init(itm.lb, itm.nb, itm.la, itm.na);
-        sc.init(itm.la, itm.na, itm.lb, itm.nb);
-        first = true;
-        have = false;
-        int x = 0, y = 0, z = 0;
-        if (p.sched_mode == 1) {  // ascending union order (the reference's key order)
-          bool hx = sa.next(false, x), hz = sc.next(true, z), hy = sb.next(false, y);
-          while (hx || hy || hz) {
-            const int vx = hx ? x : 0x7fffffff, vy = hy ? y : 0x7fffffff, vz = hz ? z : 0x7fffffff;
-            if (vx < vy && vx < vz) { step(x, 1); hx = sa.next(false, x); }
-            else if (vy < vz) { step(y, 2); hy = sb.next(false, y); }
-            else { step(z, 3); hz = sc.next(true, z); }
-          }
-        } else {
-          bool hx = sa.next(false, x), hy = sb.next(false, y);
-          while (hx || hy) {
-            if (hx) { step(x, 1); hx = sa.next(false, x); }
-            if (hy) { step(y, 2); hy = sb.next(false, y); }
-          }
-          while (sc.next(true, z)) step(z, 3);
+        const int n = max(itm.na, itm.nb);
+        for (int t = 0; t < n; ++t) {
+          const int sl = sq % SCH;
+          const int x = t < itm.na ? __ldg(itm.la + t) : -1;
+          const int y = t < itm.nb ? __ldg(itm.lb + t) : -1;
+          if (sq >= SCH) mbar_wait(&B.sch_empty[sl], ((sq / SCH) - 1) & 1);
+          aux.sched[sl] = make_int4(x, y, (x >= 0 ? 1 : 0) | (y >= 0 ? 2 : 0), (t == n - 1 ? 1 : 0) | (t == 0 ? 2 : 0));
+          mbar_arrive(&B.sch_full[sl]);
+          PAIR_TRACE(23, sq);
+          ++sq;
         }
-        emit(pend, true);
       }
     }
   } else if (warp == 0 || warp == 2) {
@@ -397,124 +346,140 @@ __global__ void __launch_bounds__(416, 1)
           if (kq >= ST) mbar_wait(&empty[s], ((kq / ST) - 1) & 1);
           PAIR_TRACE(is_k ? 0 : 1, kq);
           if (is_k) {
-            // step info for the MMA issuer and the softmax warpgroups (the K
+            // step info for the MMA issuers and the softmax warpgroups (the K
             // producer runs at most KST + NS steps ahead of the softmax)
             aux.info[kq % INFO] = e;
             mbar_arrive(&B.info_full[kq % INFO]);
           }
-          uint8_t* st = ring + s * TILE;
+          uint8_t* st = ring + s * STAGE;
           if (p.fake_load & (is_k ? 1 : 2)) {  // diagnostics: skip the copy (timing only)
             mbar_arrive(&full[s]);
             ++kq;
             continue;
           }
-          // [feature half][64 rows x 128 B]: K-major B of GEMM1 / MN-major B of GEMM2
-          mbar_expect_tx(&full[s], TILE);
-          load_region(map, st, &full[s], p, itm.h, e.x, 0);
-          load_region(map, st + BOX, &full[s], p, itm.h, e.x, 1);
+          // [tile][feature half][64 rows x 128 B]: K-major B of GEMM1 / MN-major B of GEMM2
+          mbar_expect_tx(&full[s], TILE * ((e.z & 1) + ((e.z >> 1) & 1)));
+          if (e.z & 1) {
+            load_region(map, st, &full[s], p, itm.h, e.x, 0);
+            load_region(map, st + BOX, &full[s], p, itm.h, e.x, 1);
+          }
+          if (e.z & 2) {
+            load_region(map, st + TILE, &full[s], p, itm.h, e.y, 0);
+            load_region(map, st + TILE + BOX, &full[s], p, itm.h, e.y, 1);
+          }
           ++kq;
         }
       }
     }
   } else if (warp == 1) {
     // ========================= GEMM1 issuer (warp 1) =========================
-    // Two issuer warps (GEMM1 here, GEMM2 in warp 12) run their loops
-    // concurrently: each loop's waits and bookkeeping take about as long as
-    // the MMAs they feed, so one warp issuing both could not keep the tensor
-    // pipe busy. Each whole warp runs its loop (descriptors and counters stay
-    // warp-uniform, in uniform registers); one elected lane issues.
-    {
-      constexpr uint32_t IDESC1 = umma_idesc_bf16(128, 64, 0, 0);  // A (TMEM) K-major, B K-major
-      const uint64_t dK = umma_desc_sw128(0, 16, 1024) + (smem_u32(sK) >> 4);
-      int kidx = 0, sidx = 0, iidx = 0;
-      uint32_t kph = 0, fph = 0;
-      int qi = 0, kq = 0;
-      for (long long it = blockIdx.x;; it += gridDim.x) {
-        PairItem itm;
-        if (!fetch_pair(p, it, items, itm)) break;
-        if (itm.na + itm.nb == 0) continue;
-        mbar_wait(&B.q_full, qi & 1);
-        for (;;) {
-          DA_WAITC(&B.k_full[kidx], kph);
-          if (lane == 0) PAIR_TRACE(2, kq);
-          const int last = aux.info[iidx].w & 1;  // written before the K copy was issued
-          // S buffer free: GEMM2 of step kq - NS has read its P
-          if (kq >= NS) DA_WAITC(&B.s_free[sidx], fph);
-          tc_fence_after();
-          if (elect_one_sync()) {
-            const uint32_t dS = tmem + COL_S + 64 * sidx;
-            const uint64_t bk = dK + (uint64_t)(kidx * (TILE >> 4));
+    // The whole warp runs the loop (descriptors and counters stay warp-uniform,
+    // in uniform registers); one elected lane issues.
+    constexpr uint32_t IDESC1 = umma_idesc_bf16(64, 64, 0, 0);  // A (TMEM) K-major, B K-major
+    const uint64_t dK = umma_desc_sw128(0, 16, 1024) + (smem_u32(sK) >> 4);
+    int kidx = 0, sidx = 0, iidx = 0;
+    uint32_t kph = 0, fph = 0;
+    int qi = 0, kq = 0;
+    for (long long it = blockIdx.x;; it += gridDim.x) {
+      PairItem itm;
+      if (!fetch_pair(p, it, items, itm)) break;
+      if (itm.na + itm.nb == 0) continue;
+      mbar_wait(&B.q_full, qi & 1);
+      for (;;) {
+        DA_WAITC(&B.k_full[kidx], kph);
+        if (lane == 0) PAIR_TRACE(2, kq);
+        const int4 e = aux.info[iidx];  // written before the K copy was issued
+        const int last = e.w & 1;
+        // S buffer free: GEMM2 of step kq - NS has read its P
+        if (kq >= NS) DA_WAITC(&B.s_free[sidx], fph);
+        tc_fence_after();
+        if (elect_one_sync()) {
+          const uint32_t dS = tmem + COL_S + 64 * sidx;
+          const uint64_t bk = dK + (uint64_t)(kidx * (STAGE >> 4));
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_bf16_ts(dS, tmem + COL_Q + kk * 8, bk + (uint64_t)((kk >> 2) * (BOX >> 4) + (kk & 3) * 2), IDESC1,
-                           kk > 0 ? 1u : 0u);
-            umma_commit(&B.k_empty[kidx]);
-            umma_commit(&B.s_full[sidx]);
-            if (last) umma_commit(&B.q_empty);
-            PAIR_TRACE(3, kq);
+          for (int T = 0; T < 2; ++T) {
+            if (e.z & (1 << T)) {
+              const uint32_t lo = T ? LANE_B : 0u;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                umma_bf16_ts(dS + lo, tmem + lo + COL_Q + kk * 8,
+                             bk + (uint64_t)(T * (TILE >> 4) + (kk >> 2) * (BOX >> 4) + (kk & 3) * 2), IDESC1,
+                             kk > 0 ? 1u : 0u);
+            }
           }
-          __syncwarp();
-          ++kq;
-          if (++kidx == KST) { kidx = 0; kph ^= 1u; }
-          if (kq > NS && sidx == NS - 1) fph ^= 1u;
-          if (++sidx == NS) sidx = 0;
-          if (++iidx == INFO) iidx = 0;
-          if (last) break;
+          umma_commit(&B.k_empty[kidx]);
+          umma_commit(&B.s_full[sidx]);
+          if (last) umma_commit(&B.q_empty);
+          PAIR_TRACE(3, kq);
         }
-        ++qi;
+        __syncwarp();
+        ++kq;
+        if (++kidx == KST) { kidx = 0; kph ^= 1u; }
+        if (kq > NS && sidx == NS - 1) fph ^= 1u;
+        if (++sidx == NS) sidx = 0;
+        if (++iidx == INFO) iidx = 0;
+        if (last) break;
       }
+      ++qi;
     }
   } else if (warp == 12) {
     // ========================= GEMM2 issuer (warp 12) =========================
-    // O += P . V for every step in order, as soon as the step's P and V are in.
-    {
-      constexpr uint32_t IDESC2 = umma_idesc_bf16(128, 128, 0, 1);  // A (TMEM) K-major, B MN-major
-      const uint64_t dV = umma_desc_sw128(0, BOX, 1024) + (smem_u32(sV) >> 4);
-      int vidx = 0, pidx = 0, iidx = 0;
-      uint32_t vph = 0, pph = 0, iph = 0;
-      int qi = 0, vq = 0;
-      for (long long it = blockIdx.x;; it += gridDim.x) {
-        PairItem itm;
-        if (!fetch_pair(p, it, items, itm)) break;
-        if (itm.na + itm.nb == 0) continue;
-        for (bool first = true;; first = false) {
-          DA_WAITC(&B.info_full[iidx], iph);
-          const int last = aux.info[iidx].w & 1;
-          if (lane == 0) PAIR_TRACE(20, vq);
-          DA_WAITC(&B.v_full[vidx], vph);
-          if (lane == 0) PAIR_TRACE(21, vq);
-          DA_WAITC(&B.p_full[pidx], pph);
-          if (first && qi > 0) mbar_wait(&B.o_empty, (qi - 1) & 1);
-          if (lane == 0) PAIR_TRACE(4, vq);
-          tc_fence_after();
-          if (elect_one_sync()) {
-            const uint32_t aP = tmem + COL_S + 64 * pidx;
-            const uint64_t bv = dV + (uint64_t)(vidx * (TILE >> 4));
+    // O_T += P_T . V for every step in order, as soon as the step's P and V are in.
+    constexpr uint32_t IDESC2 = umma_idesc_bf16(64, 128, 0, 1);  // A (TMEM) K-major, B MN-major
+    const uint64_t dV = umma_desc_sw128(0, BOX, 1024) + (smem_u32(sV) >> 4);
+    int vidx = 0, pidx = 0, iidx = 0;
+    uint32_t vph = 0, pph = 0, iph = 0;
+    int qi = 0, vq = 0;
+    for (long long it = blockIdx.x;; it += gridDim.x) {
+      PairItem itm;
+      if (!fetch_pair(p, it, items, itm)) break;
+      if (itm.na + itm.nb == 0) continue;
+      for (;;) {
+        DA_WAITC(&B.info_full[iidx], iph);
+        const int4 e = aux.info[iidx];
+        const int last = e.w & 1, first = (e.w >> 1) & 1;
+        if (lane == 0) PAIR_TRACE(20, vq);
+        DA_WAITC(&B.v_full[vidx], vph);
+        if (lane == 0) PAIR_TRACE(21, vq);
+        DA_WAITC(&B.p_full[pidx], pph);
+        if (first && qi > 0) mbar_wait(&B.o_empty, (qi - 1) & 1);
+        if (lane == 0) PAIR_TRACE(4, vq);
+        tc_fence_after();
+        if (elect_one_sync()) {
+          const uint32_t aP = tmem + COL_S + 64 * pidx;
+          const uint64_t bv = dV + (uint64_t)(vidx * (STAGE >> 4));
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              // P of keys 16kk.. sits at column 32(kk/2) + 8(kk%2) of the S buffer
-              umma_bf16_ts(tmem + COL_O, aP + (kk >> 1) * 32 + (kk & 1) * 8, bv + (uint64_t)(kk * (2048 >> 4)),
-                           IDESC2, (first && kk == 0) ? 0u : 1u);
+          for (int T = 0; T < 2; ++T) {
+            if (e.z & (1 << T)) {
+              const uint32_t lo = T ? LANE_B : 0u;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                // P of keys 16kk.. sits at column 32(kk/2) + 8(kk%2) of the S buffer
+                umma_bf16_ts(tmem + lo + COL_O, aP + lo + (kk >> 1) * 32 + (kk & 1) * 8,
+                             bv + (uint64_t)(T * (TILE >> 4) + kk * (2048 >> 4)), IDESC2, (first && kk == 0) ? 0u : 1u);
+              }
             }
-            umma_commit(&B.v_empty[vidx]);
-            umma_commit(&B.s_free[pidx]);
-            if (last) umma_commit(&B.o_full);
-            PAIR_TRACE(5, vq);
           }
-          __syncwarp();
-          ++vq;
-          if (++vidx == VST) { vidx = 0; vph ^= 1u; }
-          if (++pidx == NS) { pidx = 0; pph ^= 1u; }
-          if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
-          if (last) break;
+          umma_commit(&B.v_empty[vidx]);
+          umma_commit(&B.s_free[pidx]);
+          if (last) umma_commit(&B.o_full);
+          PAIR_TRACE(5, vq);
         }
-        ++qi;
+        __syncwarp();
+        ++vq;
+        if (++vidx == VST) { vidx = 0; vph ^= 1u; }
+        if (++pidx == NS) { pidx = 0; pph ^= 1u; }
+        if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
+        if (last) break;
       }
+      ++qi;
     }
   } else if (warp >= 4 && warp < 12) {
     // ============ softmax / Q loader / epilogue: two warpgroups split the step ============
-    // Warpgroup wg handles keys [32wg, 32wg+32) of each step and feature half
-    // wg of Q and O; thread t of a warpgroup owns query row t.
+    // Thread (warp, lane) owns TMEM lane L = 32 (warp % 4) + lane: tile T =
+    // lane / 16 (region a or b), row r = 16 (warp % 4) + lane % 16 of that
+    // region. Warpgroup wg handles keys [32wg, 32wg+32) of each step and feature
+    // half wg of Q and O.
     //
     // Fixed per-row offset instead of a running max: at an item's first step
     // the row fixes m = max(first-step row max, |q| * max|k| * scale - 64)
@@ -524,11 +489,10 @@ __global__ void __launch_bounds__(416, 1)
     // the bound) is handed to the portable kernel, which redoes its region
     // with the streaming softmax.
     const int wg = (warp - 4) >> 2;
-    const int t = (threadIdx.x - 128) & 127;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tq = tmem + lane_off;
-    const int half = t >> 6;  // 0: rows of region a, 1: rows of region b
-    const int r = t & 63;
+    const int L = 32 * (warp & 3) + lane;
+    const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int tile = lane >> 4;
+    const int r = 16 * (warp & 3) + (lane & 15);
     const float sl2 = p.scale_log2;  // > 0 (tc_supported)
     int G = 0;
     int iidx = 0, sidx = 0;
@@ -539,7 +503,7 @@ __global__ void __launch_bounds__(416, 1)
     // packed bf16 pairs. The next nonempty item's Q is written as soon as the
     // current item's last GEMM1 is done, before this item's epilogue.
     auto load_q = [&](const PairItem& itm, int wait_parity) {
-      const int region = half ? itm.b : itm.a;
+      const int region = tile ? itm.b : itm.a;
       const long long qrow = region < p.geo.g ? token_row(p, region, r) : -1;
       uint32_t qv[32];
       if (qrow >= 0) {
@@ -574,9 +538,10 @@ __global__ void __launch_bounds__(416, 1)
     for (long long it = blockIdx.x;; it += gridDim.x) {
       PairItem itm;
       if (!fetch_pair(p, it, items, itm)) break;
-      const int region = half ? itm.b : itm.a;
+      const int region = tile ? itm.b : itm.a;
       const bool region_ok = region < p.geo.g;
       const long long row = region_ok ? token_row(p, region, r) : -1;
+      const bool tile_has_keys = (tile ? itm.nb : itm.na) > 0;
       __nv_bfloat16* orow = row >= 0 ? p.out + itm.h * p.oh + row * p.orow + wg * 64 : nullptr;
       if (itm.na + itm.nb == 0) {
         if (orow) {
@@ -604,28 +569,27 @@ __global__ void __launch_bounds__(416, 1)
       float x[32];
       int4 inf;
       int sb;
-      bool kp;
       auto acquire = [&]() {  // wait for step G's info and S; start loading my scores
-        if (threadIdx.x == TRACE_T) PAIR_TRACE(22, G);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(22, G);
         DA_WAITC(&B.info_full[iidx], iph);
         inf = aux.info[iidx];
         sb = sidx;
-        if (threadIdx.x == TRACE_T) PAIR_TRACE(15, G);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(15, G);
         DA_WAITC(&B.s_full[sb], sph);
-        if (threadIdx.x == TRACE_T) PAIR_TRACE(6, G);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(6, G);
         tc_fence_after();
-        // my 32 keys of the step's key region (warp-uniform: a warp's rows share one query region)
-        kp = ((inf.z >> half) & 1) && !(p.fake_load & 4);
-        if (kp) tmem_ld32(tq + COL_S + 64 * sb + 32 * wg, x);
+        // the whole warp loads (tcgen05.ld is warp-wide); lanes of an idle tile ignore it
+        if (!(p.fake_load & 4)) tmem_ld32(tq + COL_S + 64 * sb + 32 * wg, x);
       };
       acquire();
       for (bool last = false; !last;) {
         last = (inf.w & 1) != 0;
         const int sb_cur = sb;
-        const bool kp_cur = kp;
+        const bool kp = ((inf.z >> tile) & 1) && !(p.fake_load & 4);
         uint32_t pk[16];
-        if (kp_cur) {
-          const unsigned vm = (unsigned)(key_mask(p, inf.x) >> (32 * wg));
+        if (!(p.fake_load & 4)) {
+          const int j = tile ? inf.y : inf.x;
+          const unsigned vm = kp ? (unsigned)(key_mask(p, j) >> (32 * wg)) : 0u;
           tmem_ld_wait();
           if (vm != ~0u) {
 #pragma unroll
@@ -633,29 +597,29 @@ __global__ void __launch_bounds__(416, 1)
           }
           had |= vm != 0u;
         }
-        if (threadIdx.x == TRACE_T) PAIR_TRACE(16, G);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(16, G);
         if (first_step) {
           float bm_own = -INFINITY;
-          if (kp_cur) {
+          if (kp) {
             float mx[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) mx[e] = fmaxf(fmaxf(x[e], x[e + 8]), fmaxf(x[e + 16], x[e + 24]));
             bm_own = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                            fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
           }
-          aux.xch[qi & 1][wg][t] = bm_own;
-          aux.xq[qi & 1][wg][t] = qn2_own;
+          aux.xch[qi & 1][wg][L] = bm_own;
+          aux.xq[qi & 1][wg][L] = qn2_own;
           bar_sync(1, 256);
-          const float bm = fmaxf(bm_own, aux.xch[qi & 1][wg ^ 1][t]);
-          const float bound = sqrtf(qn2_own + aux.xq[qi & 1][wg ^ 1][t]) * kmax * sl2 * 1.0001f;
+          const float bm = fmaxf(bm_own, aux.xch[qi & 1][wg ^ 1][L]);
+          const float bound = sqrtf(qn2_own + aux.xq[qi & 1][wg ^ 1][L]) * kmax * sl2 * 1.0001f;
           m = fmaxf(bm, bound - 64.f);
           first_step = false;
         }
         // P (bf16 pairs) of my 32 keys -> columns 32wg .. 32wg+15 of the S
         // buffer: inside MY S columns, which the other warpgroup never reads.
-        // A quarter of the exponentials run as a polynomial on the FMA pipe
-        // (exp2_poly) to unload MUFU.
-        if (kp_cur) {
+        // Lanes of a tile without a key region this step hold x = -inf (P = 0).
+        // A quarter of the exponentials run as a polynomial on the FMA pipe.
+        {
           const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
           float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
@@ -665,19 +629,20 @@ __global__ void __launch_bounds__(416, 1)
             acc = fadd2(acc, pe);
             pk[c / 2] = pack_bf16(pe.x, pe.y);
           }
-          l += acc.x + acc.y;
-        } else {
+          if (kp) l += acc.x + acc.y;
+          if (!kp) {
 #pragma unroll
-          for (int c = 0; c < 16; ++c) pk[c] = 0u;
+            for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          }
         }
-        if (threadIdx.x == TRACE_T) PAIR_TRACE(17, G);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(17, G);
         ++G;
         if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
         if (++sidx == NS) { sidx = 0; sph ^= 1u; }
         if (!last) acquire();  // x is free again: prefetch the next step's scores
         tmem_st16u(tq + COL_S + 64 * sb_cur + 32 * wg, pk);
         tmem_st_wait();
-        if (threadIdx.x == TRACE_T) PAIR_TRACE(18, G - 1);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(18, G - 1);
         tc_fence_before();
         mbar_arrive(&B.p_full[sb_cur]);
         if ((threadIdx.x & 31) == 0) PAIR_TRACE(7 + (warp - 4), G - 1);
@@ -693,14 +658,15 @@ __global__ void __launch_bounds__(416, 1)
         break;
       }
       // ------------------------------ epilogue ------------------------------
-      aux.lsum[wg][t] = l;
-      aux.had[wg][t] = had ? 1 : 0;
+      aux.lsum[wg][L] = l;
+      aux.had[wg][L] = had ? 1 : 0;
       bar_sync(1, 256);
-      const float lt = l + aux.lsum[wg ^ 1][t];
-      const bool bad = (had || aux.had[wg ^ 1][t]) && !(lt >= 0x1p-80f);
+      const float lt = l + aux.lsum[wg ^ 1][L];
+      const bool bad = (had || aux.had[wg ^ 1][L]) && !(lt >= 0x1p-80f);
       mbar_wait(&B.o_full, qi & 1);
       tc_fence_after();
-      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      // a tile without any kept key region never accumulated O: its rows are 0
+      const float inv = (lt > 0.f && tile_has_keys) ? 1.f / lt : 0.f;
 #pragma unroll
       for (int c2 = 0; c2 < 2; ++c2) {
         float o[32];
@@ -709,7 +675,8 @@ __global__ void __launch_bounds__(416, 1)
         if (orow) {
           uint32_t w[16];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) w[c] = pack_bf16(o[2 * c] * inv, o[2 * c + 1] * inv);
+          for (int c = 0; c < 16; ++c)
+            w[c] = tile_has_keys ? pack_bf16(o[2 * c] * inv, o[2 * c + 1] * inv) : 0u;
           uint4* dst = reinterpret_cast<uint4*>(orow) + c2 * 4;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
@@ -719,8 +686,10 @@ __global__ void __launch_bounds__(416, 1)
       tc_fence_before();
       mbar_arrive(&B.o_empty);
       if (wg == 0) {
+        // one push per (warp, tile) with a bad row; duplicates are harmless
         const unsigned bal = __ballot_sync(0xffffffffu, bad && row >= 0);
-        if (bal != 0u && (threadIdx.x & 31) == 0) {
+        const unsigned mine = tile ? (bal >> 16) : (bal & 0xffffu);
+        if (mine != 0u && (lane & 15) == 0) {
           const int slot = atomicAdd(p.fb_count, 1);
           p.fb_items[slot] = itm.h * p.geo.g + region;
         }
@@ -783,12 +752,6 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
       fk = env ? atoi(env) : 0;
     }
     p.fake_load = fk;
-    static int sm = -1;
-    if (sm < 0) {
-      const char* env = getenv("DA_SCHED");
-      sm = env ? atoi(env) : 1;
-    }
-    p.sched_mode = sm;
   }
   // workspace: fallback counter | per-block key norm maxima | fallback items
   char* ws = static_cast<char*>(a.workspace);
@@ -817,7 +780,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
 }
 
 size_t pair_attn_workspace_size(int heads, const Geo& g) {
-  return 256 + pair_align256(sizeof(float) * heads * pairk::KBLK) + pair_align256(sizeof(int) * 2 * (size_t)heads * g.g);
+  return 256 + pair_align256(sizeof(float) * heads * pairk::KBLK) + pair_align256(sizeof(int) * 4 * (size_t)heads * g.g);
 }
 
 }  // namespace da

@@ -431,22 +431,19 @@ DA_DEV float2 fadd2(float2 a, float2 b) {
 }
 
 // 2^x for a pair, on the FMA pipe (no MUFU): round-to-nearest split
-// x = j + f (|f| <= 1/2) by the 1.5 * 2^23 trick, degree-4 polynomial for 2^f
-// (relative error < 4e-6, far below the bf16 rounding of P), exponent add.
-// Inputs are clamped at -125 (2^-125 for -inf scores: below every kept term
-// by > 60 binades, so it only perturbs sums at the 1e-19 level).
+// x = j + f (|f| <= 1/2) by the 1.5 * 2^23 trick, degree-3 near-minimax
+// polynomial for 2^f (relative error < 7.5e-5, far below the bf16 rounding of
+// P), exponent add. Inputs are clamped at -125 (2^-125 for -inf scores:
+// below every kept term by > 60 binades, so it only perturbs sums at ~1e-19).
 DA_DEV float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -125.f);
   x.y = fmaxf(x.y, -125.f);
-  const float2 magic = make_float2(12582912.f, 12582912.f);
-  const float2 t = fadd2(x, magic);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
   const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = fadd2(x, make_float2(-j.x, -j.y));
-  float2 p = ffma2(f, make_float2(1.3333558e-3f, 1.3333558e-3f), make_float2(9.6181291e-3f, 9.6181291e-3f));
-  p = ffma2(p, f, make_float2(5.5504109e-2f, 5.5504109e-2f));
-  p = ffma2(p, f, make_float2(2.4022650e-1f, 2.4022650e-1f));
-  p = ffma2(p, f, make_float2(6.9314718e-1f, 6.9314718e-1f));
-  p = ffma2(p, f, make_float2(1.f, 1.f));
+  float2 p = ffma2(f, make_float2(0.05517167f, 0.05517167f), make_float2(0.24261115f, 0.24261115f));
+  p = ffma2(p, f, make_float2(0.69326097f, 0.69326097f));
+  p = ffma2(p, f, make_float2(0.99992806f, 0.99992806f));
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }

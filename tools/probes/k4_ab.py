@@ -23,7 +23,7 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--config", default="hv720")
 args = ap.parse_args()
 
-f, h, w = (33, 45, 80) if args.config == "hv720" else (21, 45, 80)
+f, h, w = {"hv720": (33, 45, 80), "wan720": (21, 45, 80), "hv16": (16, 45, 80), "hv8": (8, 45, 80)}[args.config]
 plan = da.pad_plan(f, h, w, 8, 8)
 n, d, H = plan.num_valid, 128, args.heads
 
@@ -56,6 +56,7 @@ for mode in args.data.split(","):
             b = set(ci[hh, rp[hh, i + 1]:rp[hh, i + 2]].tolist())
             uni += len(a | b)
     kept2 = int(mask.kept_counts[:min(H, 2)].sum().item())
+    steps_est = uni / min(H, 2) * H  # union steps of the whole call (one key region per step)
     flops = 4.0 * 64 * 64 * d * kept
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     for e in ev:
@@ -73,4 +74,5 @@ for mode in args.data.split(","):
     ms = sorted(ts)[len(ts) // 2]
     print(f"K4={os.environ.get('DA_K4', 'pair'):10s} data={mode:8s} sp={args.sparsity} k4={ms:8.3f} ms "
           f"call={sorted(tot)[len(tot) // 2]:8.3f} ms  {flops / ms / 1e9:7.1f} TFLOP/s  "
-          f"pair-union/kept={2 * uni / kept2:.3f}", flush=True)
+          f"pair-union/kept={2 * uni / kept2:.3f}  ~{ms * 1e-3 * 1.8e9 * 148 / steps_est:.0f} cycles/step @1.8GHz",
+          flush=True)
