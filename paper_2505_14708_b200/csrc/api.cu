@@ -213,9 +213,9 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // digit histograms (digit 0 fused into the GEMM on the per-head logits path)
   // and scans, candidate compaction + finish, tie counts + scan, mark, row
   // scan, collect, threshold, kept totals, packbits (bitmap requested);
-  // attention: key norms, tcgen05 kernel, fallback list
+  // attention: key norms, pair plan, tcgen05 kernel, fallback list
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
-  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 3;
+  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 4;
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {

@@ -88,6 +88,7 @@ struct Params {
   FastDiv per_head;  // pairs per head
   int npairs;
   long long n_pad;
+  const int2* pairs;   // [heads][npairs] query regions (a, b) of each item, by kept count (pair_plan_kernel)
   const float* kpart;  // [heads][KBLK] per-block maxima of the key row norms (key_norm_kernel)
   int* fb_count;       // rows whose fixed softmax offset underflowed: their (head, region)
   int* fb_items;       //   items are recomputed by the portable kernel afterwards
@@ -141,7 +142,7 @@ constexpr int TRACE_N = 1024;
   } while (0)
 #endif
 
-// An item: query regions a = 2*ip and b = 2*ip + 1 (b may not exist) of head h.
+// An item: query regions a and b (b may be g: no region) of head h; pairs by kept count when planned.
 struct PairItem {
   int h, a, b;
   const int* la;
@@ -155,8 +156,14 @@ DA_DEV bool fetch_pair(const Params& p, long long it, long long items, PairItem&
   const int h = (int)fdiv((uint32_t)it, p.per_head);
   const int ip = (int)(it - (long long)h * p.npairs);
   o.h = h;
-  o.a = 2 * ip;
-  o.b = 2 * ip + 1;
+  if (p.pairs != nullptr) {
+    const int2 ab = __ldg(p.pairs + it);
+    o.a = ab.x;
+    o.b = ab.y;
+  } else {
+    o.a = 2 * ip;
+    o.b = 2 * ip + 1;
+  }
   const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
   const int* base = p.col_idx + (long long)(h * p.mask_h) * p.cap;
   const int a0 = rp[o.a];
@@ -210,6 +217,44 @@ DA_DEV unsigned long long key_mask(const Params& p, int j) {
   unsigned long long m = 0;
   for (int u = 0; u < vy; ++u) m |= rowm << (u * p.geo.pw);
   return m;
+}
+
+// Per head: query regions sorted by kept count (descending, ties by index) and
+// paired neighbour with neighbour, so the two lockstep tiles of an item walk
+// lists of nearly equal length (the shorter list's tile idles for the
+// difference), heaviest pairs first. Counting sort over counts 0..g in shared
+// memory; one block per head.
+__global__ void __launch_bounds__(1024) pair_plan_kernel(const int* __restrict__ row_ptr, int g, int npairs,
+                                                         int mask_h, int2* __restrict__ pairs) {
+  extern __shared__ int sh[];  // [g + 1] bins, then [g] order
+  int* bins = sh;
+  int* order = sh + g + 1;
+  const int h = blockIdx.x;
+  const int* rp = row_ptr + (long long)(h * mask_h) * (g + 1);
+  for (int i = threadIdx.x; i <= g; i += blockDim.x) bins[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < g; i += blockDim.x) atomicAdd(&bins[g - (rp[i + 1] - rp[i])], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive prefix over descending counts
+    int run = 0;
+    for (int c = 0; c <= g; ++c) {
+      const int v = bins[c];
+      bins[c] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  // stable placement: each thread walks its strided indices in order; ranks
+  // within a bin come from a warp-sequential pass to keep index order
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < g; ++i) order[bins[g - (rp[i + 1] - rp[i])]++] = i;
+  }
+  __syncthreads();
+  for (int ip = threadIdx.x; ip < npairs; ip += blockDim.x) {
+    const int a = order[2 * ip];
+    const int b = 2 * ip + 1 < g ? order[2 * ip + 1] : g;
+    pairs[(long long)h * npairs + ip] = make_int2(a, b);
+  }
 }
 
 // Per-head maximum key row norm, as KBLK per-block partial maxima (the
@@ -758,10 +803,23 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   p.fb_count = reinterpret_cast<int*>(ws);
   p.kpart = reinterpret_cast<float*>(ws + 256);
   p.fb_items = reinterpret_cast<int*>(ws + 256 + pair_align256(sizeof(float) * a.heads * pairk::KBLK));
+  int2* pairs = reinterpret_cast<int2*>(reinterpret_cast<char*>(p.fb_items) +
+                                        pair_align256(sizeof(int) * 4 * (size_t)a.heads * g.g));
   const long long key_rows = a.layout == DA_LAYOUT_REORDERED ? g.n_pad : g.n_real;
   pairk::key_norm_kernel<<<dim3(pairk::KBLK, a.heads), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(a.k), a.k_head_stride, a.k_row_stride, key_rows,
       const_cast<float*>(p.kpart), p.fb_count);
+  {
+    const size_t plan_smem = sizeof(int) * (2 * (size_t)g.g + 1);
+    const int npairs = (g.g + 1) / 2;
+    if (plan_smem <= 200 * 1024) {
+      cudaFuncSetAttribute(pairk::pair_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan_smem);
+      pairk::pair_plan_kernel<<<a.heads, 1024, plan_smem, st>>>(a.row_ptr, g.g, npairs, a.shared_mask ? 0 : 1, pairs);
+      p.pairs = pairs;
+    } else {
+      p.pairs = nullptr;  // natural pairs (2i, 2i+1)
+    }
+  }
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;
@@ -780,7 +838,8 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
 }
 
 size_t pair_attn_workspace_size(int heads, const Geo& g) {
-  return 256 + pair_align256(sizeof(float) * heads * pairk::KBLK) + pair_align256(sizeof(int) * 4 * (size_t)heads * g.g);
+  return 256 + pair_align256(sizeof(float) * heads * pairk::KBLK) + pair_align256(sizeof(int) * 4 * (size_t)heads * g.g) +
+         pair_align256(sizeof(int2) * (size_t)heads * ((g.g + 1) / 2));
 }
 
 }  // namespace da
