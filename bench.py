@@ -306,17 +306,18 @@ def _e2e(da, plan, cfg, dev, args):
     f, h, w, ph, pw, heads, d, sp = cfg
     n = plan.num_valid
     host = [torch.randn(heads, n, d, dtype=torch.float32).to(torch.bfloat16).pin_memory() for _ in range(3)]
+    out_host = torch.empty(heads, n, d, dtype=torch.bfloat16).pin_memory()
 
     def once():
         # host tensors in, host tensor out (the reference's calling convention):
         # the API uploads head groups while earlier groups compute and download
-        return da.multi_head_sparse_attention(host[0], host[1], host[2], plan, sp)
+        return da.multi_head_sparse_attention(host[0], host[1], host[2], plan, sp, out=out_host)
 
-    for _ in range(2):
+    for _ in range(3):
         once()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(2, min(args.steps, 5))
+    steps = max(3, min(args.steps, 5))
     s.record()
     for _ in range(steps):
         once()

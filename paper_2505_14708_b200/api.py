@@ -385,6 +385,21 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     return out, mask, squeeze
 
 
+def _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask, qkv_layout, out):
+    """Device tensors run on their GPU; host tensors (the reference's calling
+    convention) go through the pipelined upload/compute/download path, which
+    may write into a caller-provided host ``out``."""
+    if q.is_cuda:
+        if out is not None:
+            raise ValueError("out= is for host inputs; device calls return a fresh tensor")
+        o, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                               shared_head_mask, qkv_layout)
+    else:
+        o, mask, _ = _pipeline_host(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                                    shared_head_mask, qkv_layout, out=out)
+    return o, mask
+
+
 def _cat_masks(masks) -> RegionMask:
     """Stack per-head-group masks of one call (same g, keep ratio, capacity)."""
     if len(masks) == 1:
@@ -396,7 +411,7 @@ def _cat_masks(masks) -> RegionMask:
 
 
 def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                   shared_head_mask, qkv_layout, group_heads=None):
+                   shared_head_mask, qkv_layout, group_heads=None, out=None):
     """Host (CPU) inputs, the reference's calling convention: the call stages
     Q/K/V to the GPU in head groups on a copy stream, runs each group's
     pipeline on the current stream while the next group uploads, copies each
@@ -422,7 +437,15 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
         groups = [(h0, min(heads, h0 + hg)) for h0 in range(0, heads, hg)]
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     s_in.wait_stream(main)
-    out_host = torch.empty((heads, n, dv), dtype=out_dtype, pin_memory=True)
+    if out is not None:
+        o3, _ = _as_heads(out, qkv_layout, "out")
+        if o3.device.type != "cpu" or tuple(o3.shape) != (heads, n, dv) or o3.dtype != out_dtype or \
+                not o3.is_contiguous():
+            raise ValueError(f"out must be a contiguous CPU tensor of shape {(heads, n, dv)} and dtype {out_dtype}")
+        out_host = o3
+    else:
+        # pinned so the per-group downloads are asynchronous (pass out= to reuse a buffer)
+        out_host = torch.empty((heads, n, dv), dtype=out_dtype, pin_memory=True)
     masks = []
     for h0, h1 in groups:
         with torch.cuda.stream(s_in):
@@ -445,8 +468,8 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
         masks.append(mask_g)
     main.wait_stream(s_out)
     s_out.synchronize()
-    out = out_host[0] if squeeze else (out_host.transpose(0, 1) if qkv_layout == "nhd" else out_host)
-    return out, _cat_masks(masks), squeeze
+    res = out_host[0] if squeeze else (out_host.transpose(0, 1) if qkv_layout == "nhd" else out_host)
+    return res, _cat_masks(masks), squeeze
 
 
 def _details(out, mask: RegionMask, layout: LatentLayout, d: int):
@@ -465,7 +488,7 @@ def _details(out, mask: RegionMask, layout: LatentLayout, d: int):
 def padded_sparse_attention(q, k, v, frames, height, width, patch_h, patch_w, sparsity,
                             scale=None, pool_mode="average", select_on="logits",
                             force_row_keep=True, two_pass=False, return_details=False,
-                            *, qkv_layout="hnd"):
+                            *, qkv_layout="hnd", out=None):
     """Draft-guided block-sparse attention on any grid (padding.py:95-165).
 
     Ragged grids are padded inside the kernels: pooling averages over real
@@ -484,9 +507,7 @@ def padded_sparse_attention(q, k, v, frames, height, width, patch_h, patch_w, sp
     d = q3.shape[2]
     if scale is None:
         scale = head_dim_scale(d)
-    run = _pipeline_host if not q.is_cuda else _pipeline
-    out, mask, _ = run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                       False, qkv_layout)
+    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)
@@ -494,7 +515,7 @@ def padded_sparse_attention(q, k, v, frames, height, width, patch_h, patch_w, sp
 
 def draft_sparse_attention(q, k, v, layout: LatentLayout, sparsity, scale=None, pool_mode="average",
                            select_on="logits", force_row_keep=True, two_pass=False,
-                           return_details=False, *, qkv_layout="hnd"):
+                           return_details=False, *, qkv_layout="hnd", out=None):
     """Full pipeline on a divisible grid (sparse.py:193-246)."""
     del two_pass
     _validate_pipeline_args(sparsity, select_on, pool_mode)
@@ -505,9 +526,7 @@ def draft_sparse_attention(q, k, v, layout: LatentLayout, sparsity, scale=None, 
     if scale is None:
         scale = head_dim_scale(d)
     plan = PadPlan(layout.frames, layout.height, layout.width, layout)
-    run = _pipeline_host if not q.is_cuda else _pipeline
-    out, mask, _ = run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                       False, qkv_layout)
+    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out)
     if not return_details:
         return out
     return _details(out, mask, layout, d)
@@ -515,7 +534,7 @@ def draft_sparse_attention(q, k, v, layout: LatentLayout, sparsity, scale=None, 
 
 def multi_head_sparse_attention(q, k, v, layout: LatentLayout, sparsity, shared_head_mask=False,
                                 scale=None, pool_mode="average", select_on="logits",
-                                force_row_keep=True, *, qkv_layout="hnd", return_details=False):
+                                force_row_keep=True, *, qkv_layout="hnd", return_details=False, out=None):
     """Stacked (heads, n, d) inputs (sparse.py:249-302); all heads in one launch per stage.
 
     ``layout`` may also be a PadPlan for ragged grids (the reference has no
@@ -534,9 +553,8 @@ def multi_head_sparse_attention(q, k, v, layout: LatentLayout, sparsity, shared_
     d = q3.shape[2]
     if scale is None:
         scale = head_dim_scale(d)
-    run = _pipeline_host if not q.is_cuda else _pipeline
-    out, mask, _ = run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                       shared_head_mask, qkv_layout)
+    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask,
+                     qkv_layout, out)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)

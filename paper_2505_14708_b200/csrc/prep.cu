@@ -94,6 +94,27 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode,
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = init;
   // rows of the region: (u, v) with u < vy, v < vx, visited as r = u*pw + v
+  if (mode == 0 && g.p == 4 * RG) {
+    // common case (8x8 pool, d = 128: four rows per thread): all four 16-byte
+    // loads in flight before any accumulation
+    uint4 q[4];
+    bool ok[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = rg + i * RG;
+      const int u = r / g.pw, v = r - u * g.pw;
+      ok[i] = u < rc.vy && v < rc.vx;
+      const long long row = ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
+      q[i] = ok[i] ? __ldg(reinterpret_cast<const uint4*>(base + row * rs) + k) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (!ok[i]) continue;  // padding rows are not summed (keeps -0.0 sums bit-exact)
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&q[i]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += (double)__bfloat162float(b[e]);
+    }
+  } else
   for (int r = rg; r < g.p; r += RG) {
     const int u = r / g.pw, v = r - u * g.pw;
     if (u >= rc.vy || v >= rc.vx) continue;
