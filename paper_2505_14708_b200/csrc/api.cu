@@ -146,7 +146,15 @@ size_t da_attn_workspace_size(int32_t heads, const da_grid* grid) {
   return da::pair_attn_workspace_size(heads, da::make_geo(*grid));
 }
 
+static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, void* stream, const float* kpart,
+                                 int kblk);
+
 int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* stream) {
+  return block_sparse_fwd_impl(args, grid, stream, nullptr, 0);
+}
+
+static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, void* stream, const float* kpart,
+                                 int kblk) {
   int rc = check_attn(args, grid);
   if (rc) return rc;
   da::Geo g = da::make_geo(*grid);
@@ -155,7 +163,7 @@ int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* str
     if (!args->workspace)
       return fail(DA_EINVAL, "block_sparse_fwd: the tcgen05 path needs a workspace (da_attn_workspace_size)");
     const char* why = "";
-    cudaError_t e = da::launch_tc_attn(*args, g, st, &why);
+    cudaError_t e = da::launch_tc_attn(*args, g, st, &why, kpart, kblk);
     if (e == cudaErrorInvalidValue && why[0]) return fail(DA_ECUDA, "block_sparse_fwd (tcgen05): %s", why);
     return cuda_status(e, "block_sparse_fwd (tcgen05)");
   }
@@ -174,6 +182,7 @@ struct PipeWs {
   double* scores;
   void* sel;
   void* attn;
+  float* kpart;
   size_t total;
 };
 
@@ -187,6 +196,7 @@ static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
   w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * g.g));
   w.sel = take(da::select_workspace_size(heads, g.g));
   w.attn = take(da::pair_attn_workspace_size(heads, g));
+  w.kpart = reinterpret_cast<float*>(take(sizeof(float) * (size_t)heads * (da::pool_norm_blocks(d, g) + 1)));
   w.total = off;
   return w;
 }
@@ -213,9 +223,9 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // digit histograms (digit 0 fused into the GEMM on the per-head logits path)
   // and scans, candidate compaction + finish, tie counts + scan, mark, row
   // scan, collect, threshold, kept totals, packbits (bitmap requested);
-  // attention: key norms, pair plan, tcgen05 kernel, fallback list
+  // attention: pair plan, tcgen05 kernel, fallback list (key norms come from pooling)
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
-  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 4;
+  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 3;
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
@@ -235,8 +245,11 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
       a.k_row_stride % 8 || (reinterpret_cast<uintptr_t>(a.q) & 15) || (reinterpret_cast<uintptr_t>(a.k) & 15))
     return fail(DA_EINVAL, "sparse_attention: q/k need d %% 8 == 0 and 16-byte aligned rows");
   // K2: pool Q and K in one launch
+  // (average pooling also records K's row-norm maxima for the attention kernel)
+  const int kblk = pa->pool_mode == 0 ? da::pool_norm_blocks(a.d, g) : 0;
   if ((rc = cuda_status(da::launch_pool2(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.k, a.k_head_stride,
-                                         a.k_row_stride, w.kp, a.heads, a.d, pa->pool_mode, g, st),
+                                         a.k_row_stride, w.kp, a.heads, a.d, pa->pool_mode, g, st,
+                                         kblk > 0 ? w.kpart : nullptr),
                         "pool")))
     return rc;
   // K3a: draft scores; when the selection runs per head on raw logits, the
@@ -272,7 +285,7 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   aa.shared_mask = pa->shared_head_mask ? 1 : 0;
   aa.workspace = w.attn;
   if (pa->ev_attn_begin) cudaEventRecord((cudaEvent_t)pa->ev_attn_begin, st);
-  rc = da_block_sparse_fwd(&aa, grid, stream);
+  rc = block_sparse_fwd_impl(&aa, grid, stream, kblk > 0 ? w.kpart : nullptr, kblk);
   if (pa->ev_attn_end) cudaEventRecord((cudaEvent_t)pa->ev_attn_end, st);
   return rc;
 }

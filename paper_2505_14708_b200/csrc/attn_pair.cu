@@ -89,7 +89,8 @@ struct Params {
   int npairs;
   long long n_pad;
   const int2* pairs;   // [heads][npairs] query regions (a, b) of each item, by kept count (pair_plan_kernel)
-  const float* kpart;  // [heads][KBLK] per-block maxima of the key row norms (key_norm_kernel)
+  const float* kpart;  // [heads][kblk] per-block maxima of the key row norms (pooling or key_norm_kernel)
+  int kblk;
   int* fb_count;       // rows whose fixed softmax offset underflowed: their (head, region)
   int* fb_items;       //   items are recomputed by the portable kernel afterwards
   int fake_load;       // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies, bit 2 softmax work
@@ -599,10 +600,10 @@ __global__ void __launch_bounds__(416, 1)
       const float qn2_own = qn2_next;
       if (itm.h != cur_head) {
         cur_head = itm.h;
-        const float* kp = p.kpart + (long long)itm.h * KBLK;
+        const float* kp = p.kpart + (long long)itm.h * p.kblk;
         float mx = 0.f;
 #pragma unroll 8
-        for (int c = 0; c < KBLK; ++c) mx = fmaxf(mx, __ldg(kp + c));
+        for (int c = 0; c < p.kblk; ++c) mx = fmaxf(mx, __ldg(kp + c));
         kmax = mx;
       }
       float m = 0.f, l = 0.f;
@@ -755,7 +756,7 @@ __global__ void __launch_bounds__(416, 1)
 bool make_kv_maps(const da_attn_args& a, const Geo& g, CUtensorMap* mk, CUtensorMap* mv);
 
 cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                             long long* trace) {
+                             long long* trace, const float* kpart, int kblk) {
   CUtensorMap mk, mv;
   if (!make_kv_maps(a, g, &mk, &mv)) {
     *why = "cuTensorMapEncodeTiled failed";
@@ -805,10 +806,17 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   p.fb_items = reinterpret_cast<int*>(ws + 256 + pair_align256(sizeof(float) * a.heads * pairk::KBLK));
   int2* pairs = reinterpret_cast<int2*>(reinterpret_cast<char*>(p.fb_items) +
                                         pair_align256(sizeof(int) * 4 * (size_t)a.heads * g.g));
-  const long long key_rows = a.layout == DA_LAYOUT_REORDERED ? g.n_pad : g.n_real;
-  pairk::key_norm_kernel<<<dim3(pairk::KBLK, a.heads), 256, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(a.k), a.k_head_stride, a.k_row_stride, key_rows,
-      const_cast<float*>(p.kpart), p.fb_count);
+  if (kpart != nullptr) {  // norms from the pooling pass; only the fallback counter needs clearing
+    p.kpart = kpart;
+    p.kblk = kblk;
+    cudaMemsetAsync(p.fb_count, 0, sizeof(int), st);
+  } else {
+    p.kblk = pairk::KBLK;
+    const long long key_rows = a.layout == DA_LAYOUT_REORDERED ? g.n_pad : g.n_real;
+    pairk::key_norm_kernel<<<dim3(pairk::KBLK, a.heads), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(a.k), a.k_head_stride, a.k_row_stride, key_rows,
+        const_cast<float*>(p.kpart), p.fb_count);
+  }
   {
     const size_t plan_smem = sizeof(int) * (2 * (size_t)g.g + 1);
     const int npairs = (g.g + 1) / 2;

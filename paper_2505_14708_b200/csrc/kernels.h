@@ -16,9 +16,13 @@ cudaError_t launch_permute_out(const void* o_r, void* out, long long hs, long lo
                                const Geo& g, cudaStream_t st);
 cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
                         const Geo& g, cudaStream_t st);
-// pools two tensors (Q and K) in one launch
+// pools two tensors (Q and K) in one launch; kpart (optional, average mode with
+// pool_norm_blocks(d, g) > 0) receives per-block maxima of K's row norms,
+// [heads][pool_norm_blocks(d, g)]
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
-                         long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st);
+                         long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
+                         float* kpart);
+int pool_norm_blocks(int d, const Geo& g);
 // hist0 (optional): per-head 2048-bin histogram of the top 11 key bits, filled in the epilogue
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
                                 double scale, int softmax, cudaStream_t st, unsigned int* hist0 = nullptr);
@@ -40,6 +44,9 @@ size_t pair_attn_workspace_size(int heads, const Geo& g);
 
 void set_tc_trace(void* buf);
 bool tc_supported(const da_attn_args& a, const Geo& g);
-cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why);
+// kpart/kblk: per-head key row norm maxima already computed by the pooling
+// pass ([heads][kblk]); null = the attention launch computes them itself
+cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
+                           const float* kpart = nullptr, int kblk = 0);
 
 }  // namespace da

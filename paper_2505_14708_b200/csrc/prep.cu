@@ -265,8 +265,109 @@ cudaError_t launch_permute_out(const void* o_r, void* out, long long hs, long lo
   return cudaGetLastError();
 }
 
+// Average pooling with one thread per (region, 8-feature chunk): the TPR = d/8
+// threads of a region read its rows whole (256 B per row at d = 128, coalesced),
+// eight rows in flight, and keep exact float64 sums in registers (no shared-
+// memory reduction); one division by the valid count (padding.py:91-92). For
+// the second tensor (K) the kernel also records the largest key row norm per
+// block (kpart[h][blockIdx.x]), the bound the attention kernel's fixed softmax
+// offset needs, so K is read once.
+template <int TPR>
+__global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g, float* __restrict__ kpart) {
+  constexpr int RPB = 256 / TPR;  // regions per block
+  __shared__ float wmax[8];
+  const int h = blockIdx.y, z = blockIdx.z;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * RPB + threadIdx.x / TPR;
+  const int k = threadIdx.x % TPR;
+  const bool live = i < g.g;
+  const RegionCoord rc = region_coord(g, live ? i : 0);
+  const uint4* base = reinterpret_cast<const uint4*>(src.x[z] + h * src.hs[z]) + k;
+  const long long rs8 = src.rs[z] / 8;
+  const bool norms = z == 1 && kpart != nullptr;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  float nmax = 0.f;
+  for (int r0 = 0; r0 < g.p; r0 += 8) {
+    uint4 q[8];
+    bool ok[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = r0 + t;
+      const int u = r / g.pw, v = r - u * g.pw;
+      ok[t] = live && r < g.p && u < rc.vy && v < rc.vx;
+      const long long row = ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
+      q[t] = ok[t] ? __ldg(base + row * rs8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&q[t]);
+      if (ok[t]) {  // padding rows are not summed (keeps -0.0 sums bit-exact)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += (double)__bfloat162float(b[e]);
+      }
+      if (norms) {
+        float s2 = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float x = __bfloat162float(b[e]);
+          s2 = fmaf(x, x, s2);
+        }
+#pragma unroll
+        for (int o = TPR / 2; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        nmax = fmaxf(nmax, s2);
+      }
+    }
+  }
+  if (live) {
+    const int cnt = rc.vy * rc.vx;
+    const double div = (double)(cnt > 1 ? cnt : 1);
+    double* o = src.out[z] + ((long long)h * g.g + i) * d + k * 8;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = acc[e] / div;
+  }
+  if (norms) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nmax = fmaxf(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    if (lane == 0) wmax[w] = nmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float b = wmax[0];
+      for (int j = 1; j < 8; ++j) b = fmaxf(b, wmax[j]);
+      kpart[(long long)h * gridDim.x + blockIdx.x] = sqrtf(b);
+    }
+  }
+}
+
+int pool_norm_blocks(int d, const Geo& g) {
+  const int tpr = d / 8;
+  return (tpr >= 1 && tpr <= 32 && (tpr & (tpr - 1)) == 0 && d % 8 == 0) ? (g.g + 256 / tpr - 1) / (256 / tpr) : 0;
+}
+
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
-                         long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st) {
+                         long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
+                         float* kpart) {
+  if (mode == 0 && pool_norm_blocks(d, g) > 0 && rs0 % 8 == 0 && (!x1 || rs1 % 8 == 0)) {
+    PoolSrc src;
+    src.x[0] = static_cast<const __nv_bfloat16*>(x0);
+    src.hs[0] = hs0; src.rs[0] = rs0; src.out[0] = out0;
+    src.x[1] = static_cast<const __nv_bfloat16*>(x1 ? x1 : x0);
+    src.hs[1] = x1 ? hs1 : hs0; src.rs[1] = x1 ? rs1 : rs0; src.out[1] = x1 ? out1 : out0;
+    dim3 grid(pool_norm_blocks(d, g), heads, x1 ? 2 : 1);
+    float* kp = x1 ? kpart : nullptr;
+    switch (d / 8) {
+      case 1: pool_avg_kernel<1><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+      case 2: pool_avg_kernel<2><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+      case 4: pool_avg_kernel<4><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+      case 8: pool_avg_kernel<8><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+      case 16: pool_avg_kernel<16><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+      default: pool_avg_kernel<32><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+    }
+    return cudaGetLastError();
+  }
+  if (kpart) return cudaErrorInvalidValue;  // norms only on the fast path
+
   PoolSrc src;
   src.x[0] = static_cast<const __nv_bfloat16*>(x0);
   src.hs[0] = hs0; src.rs[0] = rs0; src.out[0] = out0;
@@ -288,7 +389,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
 
 cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
                         const Geo& g, cudaStream_t st) {
-  return launch_pool2(x, hs, rs, pooled, nullptr, 0, 0, nullptr, heads, d, mode, g, st);
+  return launch_pool2(x, hs, rs, pooled, nullptr, 0, 0, nullptr, heads, d, mode, g, st, nullptr);
 }
 
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
