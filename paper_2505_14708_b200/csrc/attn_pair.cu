@@ -88,6 +88,8 @@ struct Params {
   FastDiv per_head;  // pairs per head
   int npairs;
   long long n_pad;
+  const uint8_t* kt;   // pre-tiled K / V ([head][region][half][64 rows x 128 B], SW128 image) or null
+  const uint8_t* vt;
   const int2* pairs;   // [heads][npairs] query regions (a, b) of each item, by kept count (pair_plan_kernel)
   const float* kpart;  // [heads][kblk] per-block maxima of the key row norms (pooling or key_norm_kernel)
   int kblk;
@@ -258,6 +260,40 @@ __global__ void __launch_bounds__(1024) pair_plan_kernel(const int* __restrict__
   }
 }
 
+// K and V re-laid out once per call as per-region tiles that are byte-for-byte
+// the shared-memory image the MMAs read ([half][64 rows x 128 B], 128-byte
+// swizzle, padding rows zero): the attention kernel then fetches each tile
+// with one contiguous bulk copy, a faster L2->SM path than two 64-row tensor
+// boxes (tools/probes/tma_rate.cu). grid (g, heads, 2 tensors), 256 threads.
+struct KvTileArgs {
+  const __nv_bfloat16* x[2];
+  long long hs[2], rs[2];
+  uint8_t* out[2];
+  int layout;
+};
+__global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, RegionDecoder dec) {
+  const int j = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
+  const RegionXY rc = dec(j);
+  const uint4* src = reinterpret_cast<const uint4*>(a.x[z] + h * a.hs[z]);
+  const long long rs8 = a.rs[z] / 8;
+  uint8_t* dst = a.out[z] + ((long long)h * g.g + j) * TILE;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = threadIdx.x + 256 * i;
+    const int r = idx >> 4, c = idx & 15;
+    long long row;
+    if (a.layout == DA_LAYOUT_REORDERED) {
+      row = (long long)j * P + r;
+    } else {
+      const int u = r >> 3, v = r & 7;
+      row = (rc.y0 + u < g.H && rc.x0 + v < g.W) ? ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v : -1;
+    }
+    const uint4 val = row >= 0 ? __ldg(src + row * rs8 + c) : make_uint4(0, 0, 0, 0);
+    const int hf = c >> 3, cc = c & 7;
+    *reinterpret_cast<uint4*>(dst + hf * BOX + r * 128 + ((cc ^ (r & 7)) << 4)) = val;
+  }
+}
+
 // Per-head maximum key row norm, as KBLK per-block partial maxima (the
 // softmax offset bound); block (0, 0) also clears the fallback counter.
 // grid (KBLK, heads), 256 threads: each warp reads two 256-byte rows per load.
@@ -405,13 +441,20 @@ __global__ void __launch_bounds__(416, 1)
           }
           // [tile][feature half][64 rows x 128 B]: K-major B of GEMM1 / MN-major B of GEMM2
           mbar_expect_tx(&full[s], TILE * ((e.z & 1) + ((e.z >> 1) & 1)));
-          if (e.z & 1) {
-            load_region(map, st, &full[s], p, itm.h, e.x, 0);
-            load_region(map, st + BOX, &full[s], p, itm.h, e.x, 1);
-          }
-          if (e.z & 2) {
-            load_region(map, st + TILE, &full[s], p, itm.h, e.y, 0);
-            load_region(map, st + TILE + BOX, &full[s], p, itm.h, e.y, 1);
+          const uint8_t* tiles = is_k ? p.kt : p.vt;
+          if (tiles != nullptr) {  // pre-tiled: one contiguous 16 KB bulk copy per key region
+            const uint8_t* hb = tiles + (long long)itm.h * p.geo.g * TILE;
+            if (e.z & 1) bulk_g2s(st, hb + (long long)e.x * TILE, TILE, &full[s], p.pol_kv);
+            if (e.z & 2) bulk_g2s(st + TILE, hb + (long long)e.y * TILE, TILE, &full[s], p.pol_kv);
+          } else {
+            if (e.z & 1) {
+              load_region(map, st, &full[s], p, itm.h, e.x, 0);
+              load_region(map, st + BOX, &full[s], p, itm.h, e.x, 1);
+            }
+            if (e.z & 2) {
+              load_region(map, st + TILE, &full[s], p, itm.h, e.y, 0);
+              load_region(map, st + TILE + BOX, &full[s], p, itm.h, e.y, 1);
+            }
           }
           ++kq;
         }
@@ -828,6 +871,28 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
       p.pairs = nullptr;  // natural pairs (2i, 2i+1)
     }
   }
+  p.kt = p.vt = nullptr;
+  {
+    static int kvt = -1;
+    if (kvt < 0) {
+      const char* env = getenv("DA_KVTILE");
+      kvt = env ? atoi(env) : 1;
+    }
+    if (kvt && (a.layout == DA_LAYOUT_REORDERED || (g.ph == 8 && g.pw == 8))) {
+      uint8_t* tiles = reinterpret_cast<uint8_t*>(pairs) + pair_align256(sizeof(int2) * (size_t)a.heads * ((g.g + 1) / 2));
+      pairk::KvTileArgs ta;
+      ta.x[0] = static_cast<const __nv_bfloat16*>(a.k);
+      ta.x[1] = static_cast<const __nv_bfloat16*>(a.v);
+      ta.hs[0] = a.k_head_stride; ta.hs[1] = a.v_head_stride;
+      ta.rs[0] = a.k_row_stride; ta.rs[1] = a.v_row_stride;
+      ta.out[0] = tiles;
+      ta.out[1] = tiles + (size_t)a.heads * g.g * pairk::TILE;
+      ta.layout = a.layout;
+      pairk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
+      p.kt = ta.out[0];
+      p.vt = ta.out[1];
+    }
+  }
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;
@@ -847,7 +912,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
 
 size_t pair_attn_workspace_size(int heads, const Geo& g) {
   return 256 + pair_align256(sizeof(float) * heads * pairk::KBLK) + pair_align256(sizeof(int) * 4 * (size_t)heads * g.g) +
-         pair_align256(sizeof(int2) * (size_t)heads * ((g.g + 1) / 2));
+         pair_align256(sizeof(int2) * (size_t)heads * ((g.g + 1) / 2)) + 2 * (size_t)heads * g.g * pairk::TILE;
 }
 
 }  // namespace da
