@@ -396,7 +396,12 @@ __global__ void __launch_bounds__(416, 1)
           const int x = t < itm.na ? __ldg(itm.la + t) : -1;
           const int y = t < itm.nb ? __ldg(itm.lb + t) : -1;
           if (sq >= SCH) mbar_wait(&B.sch_empty[sl], ((sq / SCH) - 1) & 1);
-          aux.sched[sl] = make_int4(x, y, (x >= 0 ? 1 : 0) | (y >= 0 ? 2 : 0), (t == n - 1 ? 1 : 0) | (t == 0 ? 2 : 0));
+          // bits 2/3 of .z: the key region of tile A / B has padding keys (its mask
+          // is computed by the softmax threads only then)
+          const int rx = x >= 0 && key_mask(p, x) != ~0ull ? 4 : 0;
+          const int ry = y >= 0 && key_mask(p, y) != ~0ull ? 8 : 0;
+          aux.sched[sl] = make_int4(x, y, (x >= 0 ? 1 : 0) | (y >= 0 ? 2 : 0) | rx | ry,
+                                    (t == n - 1 ? 1 : 0) | (t == 0 ? 2 : 0));
           mbar_arrive(&B.sch_full[sl]);
           PAIR_TRACE(23, sq);
           ++sq;
@@ -678,7 +683,8 @@ __global__ void __launch_bounds__(416, 1)
         uint32_t pk[16];
         if (!(p.fake_load & 4)) {
           const int j = tile ? inf.y : inf.x;
-          const unsigned vm = kp ? (unsigned)(key_mask(p, j) >> (32 * wg)) : 0u;
+          const bool ragged = (inf.z >> (2 + tile)) & 1;
+          const unsigned vm = kp ? (ragged ? (unsigned)(key_mask(p, j) >> (32 * wg)) : ~0u) : 0u;
           tmem_ld_wait();
           if (vm != ~0u) {
 #pragma unroll
