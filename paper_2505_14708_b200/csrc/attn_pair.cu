@@ -19,19 +19,19 @@
 //
 // Pipeline: five 64-column S buffers let GEMM1 run up to four steps ahead of
 // GEMM2; GEMM1 and GEMM2 are issued by two warps so neither issue loop's waits
-// stall the other's MMAs. The softmax issues the next step's TMEM load before
-// publishing the current P.
+// stall the other's MMAs. The two softmax warpgroups take alternate steps and
+// issue their next step's TMEM load before publishing the current P.
 //
 // Softmax is per row with a FIXED offset per (row, item) instead of a running
 // max, so O is never rescaled and the two softmax warpgroups meet once per
 // item. P is written back over S in TMEM as packed bf16. Rows whose fixed
 // offset underflows are redone by the portable kernel (launch_pair_attn).
 //
-// Roles (416 threads): warp 0 = TMA producer for K (+ step info ring), warp 1
-// = GEMM1 issuer + TMEM owner, warp 2 = TMA producer for V, warp 3 = step
-// scheduler, warps 4-7 and 8-11 = two softmax / Q-loader / epilogue
-// warpgroups, warp 12 = GEMM2 issuer; warpgroup wg takes keys [32wg, 32wg+32)
-// of every step and feature half wg of Q and O. TMEM: Q [0,64), S0..S4
+// Roles (384 threads): warp 0 = TMA producer for K (walks both kept lists and
+// fills the step info ring), warp 1 = GEMM1 issuer + TMEM owner, warp 2 = TMA
+// producer for V, warp 3 = GEMM2 issuer, warps 4-7 and 8-11 = two softmax /
+// Q-loader / epilogue warpgroups (alternate steps; feature half wg of Q and O).
+// 12 warps keep 3 per SMSP, so each thread may use up to 168 registers. TMEM: Q [0,64), S0..S4
 // [64,384), O [384,512), each column range holding both tiles.
 //
 // K/V tiles come from TMA: 2-D maps over reordered (heads, n_pad, 128) tensors
@@ -59,8 +59,9 @@ constexpr int TILE = 2 * BOX;       // one key region, two feature halves
 constexpr int STAGE = 2 * TILE;     // the step's two key regions (tile A, tile B)
 constexpr int NS = 5;               // S buffers
 constexpr int INFO = 16;            // step info ring (K producer -> MMA, softmax)
-constexpr int SCH = 16;             // schedule ring (scheduler -> K, V producers)
 constexpr int KBLK = 32;            // key_norm_kernel blocks per head
+constexpr int RAGW = 512;           // ragged-region bitmap words (g <= 16384)
+constexpr int LISTCAP = 4096;       // staged kept-list entries per item (else read from global)
 
 constexpr int SMEM_K = 0;
 constexpr int SMEM_V = SMEM_K + KST * STAGE;
@@ -107,17 +108,17 @@ struct __align__(8) Bars {
   uint64_t o_full, o_empty;
   uint64_t q_full, q_empty;
   uint64_t info_full[INFO];
-  uint64_t sch_full[SCH], sch_empty[SCH];
 };
 struct SmemAux {
   Bars bars;
   int4 info[INFO];        // per step: key region, -, membership flags, last/first (K producer)
-  int4 sched[SCH];        // step schedule (warp 3) for the K and V producers
   uint32_t tmem_base;
   float xch[2][2][128];   // [item parity][warpgroup][row] first-step block maxima
   float xq[2][2][128];    // [item parity][warpgroup][row] partial |q|^2
   float lsum[2][128];     // [warpgroup][row] partial row sums
   int had[2][128];        // [warpgroup][row] saw a kept valid key
+  uint32_t ragged[RAGW];  // bit j: key region j has padding keys (when g <= 32 * RAGW)
+  int lists[LISTCAP];     // the K producer's copy of the current item's two kept lists
 };
 constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
 static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(256) key_norm_kernel(const __nv_bfloat16* __re
   }
 }
 
-__global__ void __launch_bounds__(416, 1)
+__global__ void __launch_bounds__(384, 1)
     sparse_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                             const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(416, 1)
     for (int s = 0; s < VST; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&B.s_full[s], 1);
-      mbar_init(&B.p_full[s], 256);
+      mbar_init(&B.p_full[s], 128);  // one softmax warpgroup per step
       mbar_init(&B.s_free[s], 1);
     }
     mbar_init(&B.o_full, 1);
@@ -363,7 +364,6 @@ __global__ void __launch_bounds__(416, 1)
     mbar_init(&B.q_full, 256);
     mbar_init(&B.q_empty, 1);
     for (int s = 0; s < INFO; ++s) mbar_init(&B.info_full[s], 1);
-    for (int s = 0; s < SCH; ++s) { mbar_init(&B.sch_full[s], 1); mbar_init(&B.sch_empty[s], 2); }
     fence_barrier_init();
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
@@ -371,6 +371,16 @@ __global__ void __launch_bounds__(416, 1)
   if (p.fake_load) {  // diagnostics: defined (zero) K/V tiles when copies are skipped
     for (int i = threadIdx.x; i < SMEM_END / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
+  }
+  if (p.key_valid == nullptr && p.geo.g <= 32 * RAGW) {
+    for (int wd = threadIdx.x; wd < (p.geo.g + 31) / 32; wd += blockDim.x) {
+      uint32_t bits = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int j = wd * 32 + b;
+        if (j < p.geo.g && key_mask(p, j) != ~0ull) bits |= 1u << b;
+      }
+      aux.ragged[wd] = bits;
+    }
   }
   if (warp == 1) tmem_alloc<TMEM_COLS>(&aux.tmem_base);
   tc_fence_before();
@@ -380,63 +390,55 @@ __global__ void __launch_bounds__(416, 1)
   uint8_t* sK = smem + SMEM_K;
   uint8_t* sV = smem + SMEM_V;
 
-  if (warp == 3) {
-    // ======================= step scheduler (one thread) =======================
-    // Step t of an item = (t-th kept key region of region a, t-th of region b);
-    // flags bit T = tile T still has a key region. Entries run ahead of the
-    // producers through a 16-deep ring.
-    if (lane == 0) {
-      int sq = 0;
-      for (long long it = blockIdx.x;; it += gridDim.x) {
-        PairItem itm;
-        if (!fetch_pair(p, it, items, itm)) break;
+  if (warp == 0 || warp == 2) {
+    // ===================== TMA producers (warp 0: K, warp 2: V) =====================
+    // The K warp stages each item's two kept lists in shared memory (all 32
+    // lanes, coalesced), then its lane 0 emits step t = (t-th kept key region
+    // of region a, t-th of region b) into the info ring and issues the K copies;
+    // the V warp follows the info ring. Info flags: bit T = tile T still has a
+    // key region; bits 2/3 = that key region has padding keys (its mask is
+    // computed by the softmax threads only then).
+    const bool is_k = warp == 0;
+    const int ST = is_k ? KST : VST;
+    uint8_t* ring = is_k ? sK : sV;
+    uint64_t* full = is_k ? B.k_full : B.v_full;
+    uint64_t* empty = is_k ? B.k_empty : B.v_empty;
+    const CUtensorMap* map = is_k ? &tm_k : &tm_v;
+    const bool bitmap = p.key_valid == nullptr && p.geo.g <= 32 * RAGW;
+    int kq = 0;
+    for (long long it = blockIdx.x;; it += gridDim.x) {
+      PairItem itm;
+      if (!fetch_pair(p, it, items, itm)) break;
+      if (itm.na + itm.nb == 0) continue;
+      const bool staged = is_k && itm.na + itm.nb <= LISTCAP;
+      if (staged) {
+        __syncwarp();  // lane 0 is done with the previous item's lists
+        for (int e = lane; e < itm.na; e += 32) aux.lists[e] = __ldg(itm.la + e);
+        for (int e = lane; e < itm.nb; e += 32) aux.lists[itm.na + e] = __ldg(itm.lb + e);
+        __syncwarp();
+      }
+      if (lane == 0) {
         const int n = max(itm.na, itm.nb);
         for (int t = 0; t < n; ++t) {
-          const int sl = sq % SCH;
-          const int x = t < itm.na ? __ldg(itm.la + t) : -1;
-          const int y = t < itm.nb ? __ldg(itm.lb + t) : -1;
-          if (sq >= SCH) mbar_wait(&B.sch_empty[sl], ((sq / SCH) - 1) & 1);
-          // bits 2/3 of .z: the key region of tile A / B has padding keys (its mask
-          // is computed by the softmax threads only then)
-          const int rx = x >= 0 && key_mask(p, x) != ~0ull ? 4 : 0;
-          const int ry = y >= 0 && key_mask(p, y) != ~0ull ? 8 : 0;
-          aux.sched[sl] = make_int4(x, y, (x >= 0 ? 1 : 0) | (y >= 0 ? 2 : 0) | rx | ry,
-                                    (t == n - 1 ? 1 : 0) | (t == 0 ? 2 : 0));
-          mbar_arrive(&B.sch_full[sl]);
-          PAIR_TRACE(23, sq);
-          ++sq;
-        }
-      }
-    }
-  } else if (warp == 0 || warp == 2) {
-    // ===================== TMA producers (warp 0: K, warp 2: V) =====================
-    if (lane == 0) {
-      const bool is_k = warp == 0;
-      const int ST = is_k ? KST : VST;
-      uint8_t* ring = is_k ? sK : sV;
-      uint64_t* full = is_k ? B.k_full : B.v_full;
-      uint64_t* empty = is_k ? B.k_empty : B.v_empty;
-      const CUtensorMap* map = is_k ? &tm_k : &tm_v;
-      int kq = 0, sq = 0;
-      for (long long it = blockIdx.x;; it += gridDim.x) {
-        PairItem itm;
-        if (!fetch_pair(p, it, items, itm)) break;
-        if (itm.na + itm.nb == 0) continue;
-        for (bool last = false; !last;) {
-          const int sl = sq % SCH;
-          mbar_wait(&B.sch_full[sl], (uint32_t)((sq / SCH) & 1));
-          const int4 e = aux.sched[sl];
-          mbar_arrive(&B.sch_empty[sl]);
-          ++sq;
-          last = (e.w & 1) != 0;
+          int4 e;
+          if (is_k) {
+            const int x = t < itm.na ? (staged ? aux.lists[t] : __ldg(itm.la + t)) : -1;
+            const int y = t < itm.nb ? (staged ? aux.lists[itm.na + t] : __ldg(itm.lb + t)) : -1;
+            e = make_int4(x, y, (x >= 0 ? 1 : 0) | (y >= 0 ? 2 : 0), (t == n - 1 ? 1 : 0) | (t == 0 ? 2 : 0));
+            if (x >= 0 && (bitmap ? (aux.ragged[x >> 5] >> (x & 31)) & 1 : key_mask(p, x) != ~0ull)) e.z |= 4;
+            if (y >= 0 && (bitmap ? (aux.ragged[y >> 5] >> (y & 31)) & 1 : key_mask(p, y) != ~0ull)) e.z |= 8;
+          }
           const int s = kq % ST;
           if (kq >= ST) mbar_wait(&empty[s], ((kq / ST) - 1) & 1);
           PAIR_TRACE(is_k ? 0 : 1, kq);
           if (is_k) {
-            // step info for the MMA issuers and the softmax warpgroups (the K
-            // producer runs at most KST + NS steps ahead of the softmax)
+            // step info for the V producer, the MMA issuers and the softmax
+            // warpgroups (the K producer runs at most KST + NS steps ahead)
             aux.info[kq % INFO] = e;
             mbar_arrive(&B.info_full[kq % INFO]);
+          } else {
+            mbar_wait(&B.info_full[kq % INFO], (uint32_t)((kq / INFO) & 1));
+            e = aux.info[kq % INFO];
           }
           uint8_t* st = ring + s * STAGE;
           if (p.fake_load & (is_k ? 1 : 2)) {  // diagnostics: skip the copy (timing only)
@@ -516,8 +518,8 @@ __global__ void __launch_bounds__(416, 1)
       }
       ++qi;
     }
-  } else if (warp == 12) {
-    // ========================= GEMM2 issuer (warp 12) =========================
+  } else if (warp == 3) {
+    // ========================= GEMM2 issuer (warp 3) =========================
     // O_T += P_T . V for every step in order, as soon as the step's P and V are in.
     constexpr uint32_t IDESC2 = umma_idesc_bf16(64, 128, 0, 1);  // A (TMEM) K-major, B MN-major
     const uint64_t dV = umma_desc_sw128(0, BOX, 1024) + (smem_u32(sV) >> 4);
@@ -548,8 +550,8 @@ __global__ void __launch_bounds__(416, 1)
               const uint32_t lo = T ? LANE_B : 0u;
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
-                // P of keys 16kk.. sits at column 32(kk/2) + 8(kk%2) of the S buffer
-                umma_bf16_ts(tmem + lo + COL_O, aP + lo + (kk >> 1) * 32 + (kk & 1) * 8,
+                // P of keys 16kk.. sits at column 8kk of the S buffer
+                umma_bf16_ts(tmem + lo + COL_O, aP + lo + kk * 8,
                              bv + (uint64_t)(T * (TILE >> 4) + kk * (2048 >> 4)), IDESC2, (first && kk == 0) ? 0u : 1u);
               }
             }
@@ -568,29 +570,30 @@ __global__ void __launch_bounds__(416, 1)
       }
       ++qi;
     }
-  } else if (warp >= 4 && warp < 12) {
-    // ============ softmax / Q loader / epilogue: two warpgroups split the step ============
+  } else if (warp >= 4) {
+    // ============ softmax / Q loader / epilogue: two warpgroups take alternate steps ============
     // Thread (warp, lane) owns TMEM lane L = 32 (warp % 4) + lane: tile T =
     // lane / 16 (region a or b), row r = 16 (warp % 4) + lane % 16 of that
-    // region. Warpgroup wg handles keys [32wg, 32wg+32) of each step and feature
-    // half wg of Q and O.
+    // region. Warpgroup wg takes the steps t = wg, wg + 2, ... of every item
+    // (all 64 keys of its row), so each warp pays the per-step waits and
+    // barrier traffic every other step and has two steps of time to hide its
+    // TMEM load; wg also owns feature half wg of Q and O.
     //
     // Fixed per-row offset instead of a running max: at an item's first step
-    // the row fixes m = max(first-step row max, |q| * max|k| * scale - 64)
-    // (log2 units). Cauchy-Schwarz bounds every later score by |q| max|k| scale,
-    // so no exponent exceeds 2^64 (no overflow in fp32 / bf16) and O is never
-    // rescaled. A row whose sum ends below 2^-80 (its true max sits > ~80 below
-    // the bound) is handed to the portable kernel, which redoes its region
-    // with the streaming softmax.
+    // (warpgroup 0) the row fixes m = max(first-step row max,
+    // |q| * max|k| * scale - 64) (log2 units) and hands it to warpgroup 1.
+    // Cauchy-Schwarz bounds every later score by |q| max|k| scale, so no
+    // exponent exceeds 2^64 (no overflow in fp32 / bf16) and O is never
+    // rescaled. A row whose sum ends below 2^-80 (its true max sits > ~80
+    // below the bound) is handed to the portable kernel, which redoes its
+    // region with the streaming softmax.
     const int wg = (warp - 4) >> 2;
     const int L = 32 * (warp & 3) + lane;
     const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const int tile = lane >> 4;
     const int r = 16 * (warp & 3) + (lane & 15);
     const float sl2 = p.scale_log2;  // > 0 (tc_supported)
-    int G = 0;
-    int iidx = 0, sidx = 0;
-    uint32_t iph = 0, sph = 0;
+    int G = 0;  // global step index of the current item's first step
     int qi = 0;
     float qn2_next = 0.f;  // my half of |q|^2 of the row whose Q was loaded last
     // my half of the Q row of (item, row) -> TMEM columns [32*wg, 32*wg+32) as
@@ -644,6 +647,7 @@ __global__ void __launch_bounds__(416, 1)
         }
         continue;
       }
+      const int nsteps = max(itm.na, itm.nb);
       if (!have_q) load_q(itm, -1);  // first nonempty item of this CTA
       const float qn2_own = qn2_next;
       if (itm.h != cur_head) {
@@ -654,94 +658,97 @@ __global__ void __launch_bounds__(416, 1)
         for (int c = 0; c < p.kblk; ++c) mx = fmaxf(mx, __ldg(kp + c));
         kmax = mx;
       }
+      // warpgroup 1's half of |q|^2 -> warpgroup 0 (which fixes the offset)
+      if (wg == 1) aux.xq[qi & 1][1][L] = qn2_own;
+      bar_sync(1, 256);
       float m = 0.f, l = 0.f;
       bool had = false;
-      bool first_step = true;
-      // The next step's S is waited for and its TMEM load issued before this
-      // step's P is published, so the load latency overlaps the store, the
-      // barrier arrive and the loop overhead (within an item).
-      float x[32];
+      float x[64];
       int4 inf;
-      int sb;
-      auto acquire = [&]() {  // wait for step G's info and S; start loading my scores
-        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(22, G);
-        DA_WAITC(&B.info_full[iidx], iph);
-        inf = aux.info[iidx];
-        sb = sidx;
-        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(15, G);
-        DA_WAITC(&B.s_full[sb], sph);
-        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(6, G);
+      int sb = 0;
+      auto acquire = [&](int gs) {  // wait for global step gs's info and S; start my load
+        const int ii = gs & (INFO - 1), si = gs % NS;
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(22, gs);
+        DA_WAITC(&B.info_full[ii], (uint32_t)((gs / INFO) & 1));
+        inf = aux.info[ii];
+        sb = si;
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(15, gs);
+        DA_WAITC(&B.s_full[si], (uint32_t)((gs / NS) & 1));
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(6, gs);
         tc_fence_after();
         // the whole warp loads (tcgen05.ld is warp-wide); lanes of an idle tile ignore it
-        if (!(p.fake_load & 4)) tmem_ld32(tq + COL_S + 64 * sb + 32 * wg, x);
+        if (!(p.fake_load & 4)) {
+          tmem_ld32_at<0>(tq + COL_S + 64 * si, x);
+          tmem_ld32_at<32>(tq + COL_S + 64 * si + 32, x);
+        }
       };
-      acquire();
-      for (bool last = false; !last;) {
-        last = (inf.w & 1) != 0;
+      if (wg < nsteps) acquire(G + wg);
+      for (int t = wg; t < nsteps; t += 2) {
+        const int gs = G + t;
         const int sb_cur = sb;
         const bool kp = ((inf.z >> tile) & 1) && !(p.fake_load & 4);
-        uint32_t pk[16];
+        uint32_t pk[32];
         if (!(p.fake_load & 4)) {
           const int j = tile ? inf.y : inf.x;
           const bool ragged = (inf.z >> (2 + tile)) & 1;
-          const unsigned vm = kp ? (ragged ? (unsigned)(key_mask(p, j) >> (32 * wg)) : ~0u) : 0u;
+          const unsigned long long vm = kp ? (ragged ? key_mask(p, j) : ~0ull) : 0ull;
           tmem_ld_wait();
-          if (vm != ~0u) {
+          if (vm != ~0ull) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) x[c] = ((vm >> c) & 1u) ? x[c] : -INFINITY;
+            for (int c = 0; c < 64; ++c) x[c] = ((vm >> c) & 1ull) ? x[c] : -INFINITY;
           }
-          had |= vm != 0u;
+          had |= vm != 0ull;
         }
-        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(16, G);
-        if (first_step) {
-          float bm_own = -INFINITY;
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(16, gs);
+        if (t == 0) {  // warpgroup 0: fix the row's offset and publish it
+          float bm = -INFINITY;
           if (kp) {
             float mx[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) mx[e] = fmaxf(fmaxf(x[e], x[e + 8]), fmaxf(x[e + 16], x[e + 24]));
-            bm_own = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+            for (int e = 0; e < 8; ++e)
+              mx[e] = fmaxf(fmaxf(fmaxf(x[e], x[e + 8]), fmaxf(x[e + 16], x[e + 24])),
+                            fmaxf(fmaxf(x[e + 32], x[e + 40]), fmaxf(x[e + 48], x[e + 56])));
+            bm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
           }
-          aux.xch[qi & 1][wg][L] = bm_own;
-          aux.xq[qi & 1][wg][L] = qn2_own;
-          bar_sync(1, 256);
-          const float bm = fmaxf(bm_own, aux.xch[qi & 1][wg ^ 1][L]);
-          const float bound = sqrtf(qn2_own + aux.xq[qi & 1][wg ^ 1][L]) * kmax * sl2 * 1.0001f;
+          const float bound = sqrtf(qn2_own + aux.xq[qi & 1][1][L]) * kmax * sl2 * 1.0001f;
           m = fmaxf(bm, bound - 64.f);
-          first_step = false;
+          aux.xch[qi & 1][0][L] = m;
+          bar_arrive(2, 256);
+        } else if (t == 1) {  // warpgroup 1: take the offset fixed at step 0
+          bar_sync(2, 256);
+          m = aux.xch[qi & 1][0][L];
         }
-        // P (bf16 pairs) of my 32 keys -> columns 32wg .. 32wg+15 of the S
-        // buffer: inside MY S columns, which the other warpgroup never reads.
-        // Lanes of a tile without a key region this step hold x = -inf (P = 0).
-        // A quarter of the exponentials run as a polynomial on the FMA pipe.
+        // P (bf16 pairs) of the 64 keys -> columns 0..31 of the S buffer (this
+        // warpgroup already holds the scores in registers). Lanes of a tile
+        // without a key region this step hold x = -inf (P = 0). A quarter of
+        // the exponentials run as a polynomial on the FMA pipe.
         {
           const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
           float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
+          for (int c = 0; c < 64; c += 2) {
             const float2 e = ffma2(make_float2(x[c], x[c + 1]), sc, nm);
             const float2 pe = (c % 8 == 6) ? exp2_poly2(e) : make_float2(fast_exp2(e.x), fast_exp2(e.y));
             acc = fadd2(acc, pe);
-            pk[c / 2] = pack_bf16(pe.x, pe.y);
+            pk[c / 2] = kp ? pack_bf16(pe.x, pe.y) : 0u;
           }
           if (kp) l += acc.x + acc.y;
-          if (!kp) {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) pk[c] = 0u;
-          }
         }
-        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(17, G);
-        ++G;
-        if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
-        if (++sidx == NS) { sidx = 0; sph ^= 1u; }
-        if (!last) acquire();  // x is free again: prefetch the next step's scores
-        tmem_st16u(tq + COL_S + 64 * sb_cur + 32 * wg, pk);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(17, gs);
+        if (t + 2 < nsteps) acquire(gs + 2);  // x is free again: prefetch my next step
+        tmem_st16u(tq + COL_S + 64 * sb_cur, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        tmem_st16u(tq + COL_S + 64 * sb_cur + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
         tmem_st_wait();
-        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(18, G - 1);
+        if (L == TRACE_T - 128 && wg == 0) PAIR_TRACE(18, gs);
         tc_fence_before();
         mbar_arrive(&B.p_full[sb_cur]);
-        if ((threadIdx.x & 31) == 0) PAIR_TRACE(7 + (warp - 4), G - 1);
+        if ((threadIdx.x & 31) == 0) PAIR_TRACE(7 + (warp - 4), gs);
       }
+      if (wg == 1 && nsteps == 1) {  // warpgroup 1 had no step: still consume the offset handoff
+        bar_sync(2, 256);
+      }
+      G += nsteps;
       // ---- next nonempty item's Q (its GEMM1s overlap this epilogue)
       have_q = false;
       for (long long it2 = it + gridDim.x;; it2 += gridDim.x) {
@@ -910,7 +917,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   if (e != cudaSuccess) return e;
   const long long items = (long long)a.heads * p.npairs;
   const int grid = (int)(items < num_sms ? items : num_sms);
-  pairk::sparse_attn_pair_kernel<<<grid, 416, pairk::SMEM_ALLOC, st>>>(mk, mv, p);
+  pairk::sparse_attn_pair_kernel<<<grid, 384, pairk::SMEM_ALLOC, st>>>(mk, mv, p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // rows whose fixed softmax offset underflowed: redo their regions exactly
   return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * num_sms);

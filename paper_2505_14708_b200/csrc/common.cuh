@@ -406,6 +406,9 @@ DA_DEV bool bar_red_or(int id, int nthreads, bool pred) {
       : "memory");
   return out != 0;
 }
+DA_DEV void bar_arrive(int id, int nthreads) {
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 DA_DEV void bar_sync(int id, int nthreads) { asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
 DA_DEV uint32_t pack_bf16(float lo, float hi) {
