@@ -208,7 +208,7 @@ def run_ours(args, cfg, name):
 
         def step(events=None):
             return da.api._pipeline(q, k, v, plan, sp, da.head_dim_scale(d), "average", "logits", True, False,
-                                    "hnd", attn_events=events)
+                                    "hnd", attn_events=events, want_bitmap=False)
     else:
         from paper_2505_14708_b200.headpar import HeadParallelAttention
 

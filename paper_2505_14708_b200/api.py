@@ -142,7 +142,7 @@ class RegionMask:
 
     g: int
     keep_ratio: float
-    bitmap: torch.Tensor          # (heads, ceil(g*g/8)) uint8
+    packed: torch.Tensor | None   # (heads, ceil(g*g/8)) uint8, or None: packed from the lists on first use
     row_ptr: torch.Tensor         # (heads, g+1) int32
     col_idx: torch.Tensor         # (heads, cap) int32
     thresholds: torch.Tensor      # (heads,) float64
@@ -154,6 +154,26 @@ class RegionMask:
     @property
     def heads(self) -> int:
         return int(self.row_ptr.shape[0])
+
+    @property
+    def bitmap(self) -> torch.Tensor:
+        """Packed bitmap (heads, ceil(g*g/8)) uint8; calls that did not ask for
+        details skip the packing kernel, and it is built here from the lists."""
+        if self.packed is not None:
+            return self.packed
+        if "bitmap" not in self._host:
+            g, dev = self.g, self.row_ptr.device
+            nbytes = (g * g + 7) // 8
+            bits = torch.zeros((self.heads, nbytes * 8), dtype=torch.uint8, device=dev)
+            counts = (self.row_ptr[:, 1:] - self.row_ptr[:, :-1]).to(torch.int64)
+            rows = torch.arange(g, device=dev, dtype=torch.int64)
+            for h in range(self.heads):
+                tot = int(self.row_ptr[h, g].item())
+                flat = torch.repeat_interleave(rows, counts[h]) * g + self.col_idx[h, :tot].to(torch.int64)
+                bits[h, flat] = 1
+            w = torch.tensor([128, 64, 32, 16, 8, 4, 2, 1], dtype=torch.int32, device=dev)
+            self._host["bitmap"] = (bits.view(self.heads, nbytes, 8).to(torch.int32) * w).sum(-1).to(torch.uint8)
+        return self._host["bitmap"]
 
     def _scalars(self):
         if "s" not in self._host:
@@ -194,7 +214,8 @@ class RegionMask:
         return self.bitmap[head].cpu().numpy().tobytes()
 
     def head(self, h: int) -> "RegionMask":
-        return RegionMask(self.g, self.keep_ratio, self.bitmap[h:h + 1], self.row_ptr[h:h + 1],
+        return RegionMask(self.g, self.keep_ratio, None if self.packed is None else self.packed[h:h + 1],
+                          self.row_ptr[h:h + 1],
                           self.col_idx[h:h + 1], self.thresholds[h:h + 1], self.forced[h:h + 1],
                           self.kept_counts[h:h + 1], single=True)
 
@@ -332,7 +353,7 @@ def _validate_pipeline_args(sparsity, select_on, pool_mode):
 
 
 def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
-              shared_head_mask, qkv_layout, force_portable=False, attn_events=None):
+              shared_head_mask, qkv_layout, force_portable=False, attn_events=None, want_bitmap=True):
     """Run the fused C-ABI pipeline; returns (output, mask, squeeze)."""
     q3, squeeze = _as_heads(q, qkv_layout, "q")
     k3, _ = _as_heads(k, qkv_layout, "k")
@@ -353,7 +374,7 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     cap = m + g
     row_ptr = torch.empty((mheads, g + 1), dtype=torch.int32, device=dev)
     col_idx = torch.empty((mheads, cap), dtype=torch.int32, device=dev)
-    bitmap = torch.empty((mheads, (g * g + 7) // 8), dtype=torch.uint8, device=dev)
+    bitmap = torch.empty((mheads, (g * g + 7) // 8), dtype=torch.uint8, device=dev) if want_bitmap else None
     thr = torch.empty(mheads, dtype=torch.float64, device=dev)
     forced = torch.empty(mheads, dtype=torch.int64, device=dev)
     kept = torch.empty(mheads, dtype=torch.int64, device=dev)
@@ -368,7 +389,8 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     pa.pool_mode = POOL_MODES.index(pool_mode)
     pa.select_softmax = 1 if select_on == "softmax" else 0
     pa.shared_head_mask = 1 if shared_head_mask else 0
-    pa.row_ptr, pa.col_idx, pa.bitmap = row_ptr.data_ptr(), col_idx.data_ptr(), bitmap.data_ptr()
+    pa.row_ptr, pa.col_idx = row_ptr.data_ptr(), col_idx.data_ptr()
+    pa.bitmap = bitmap.data_ptr() if bitmap is not None else None
     pa.threshold, pa.forced, pa.kept = thr.data_ptr(), forced.data_ptr(), kept.data_ptr()
     pa.workspace = ws.data_ptr()
     if attn_events is not None:  # (begin, end) torch.cuda.Event pair around the K4 launch
@@ -385,7 +407,8 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     return out, mask, squeeze
 
 
-def _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask, qkv_layout, out):
+def _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask, qkv_layout, out,
+         details=True):
     """Device tensors run on their GPU; host tensors (the reference's calling
     convention) go through the pipelined upload/compute/download path, which
     may write into a caller-provided host ``out``."""
@@ -393,10 +416,10 @@ def _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, s
         if out is not None:
             raise ValueError("out= is for host inputs; device calls return a fresh tensor")
         o, mask, _ = _pipeline(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                               shared_head_mask, qkv_layout)
+                               shared_head_mask, qkv_layout, want_bitmap=details)
     else:
         o, mask, _ = _pipeline_host(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                                    shared_head_mask, qkv_layout, out=out)
+                                    shared_head_mask, qkv_layout, out=out, details=details)
     return o, mask
 
 
@@ -406,12 +429,13 @@ def _cat_masks(masks) -> RegionMask:
         return masks[0]
     m0 = masks[0]
     cat = lambda name: torch.cat([getattr(m, name) for m in masks], 0)  # noqa: E731
-    return RegionMask(m0.g, m0.keep_ratio, cat("bitmap"), cat("row_ptr"), cat("col_idx"), cat("thresholds"),
+    packed = None if any(m.packed is None for m in masks) else cat("packed")
+    return RegionMask(m0.g, m0.keep_ratio, packed, cat("row_ptr"), cat("col_idx"), cat("thresholds"),
                       cat("forced"), cat("kept_counts"), single=False)
 
 
 def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                   shared_head_mask, qkv_layout, group_heads=None, out=None):
+                   shared_head_mask, qkv_layout, group_heads=None, out=None, details=True):
     """Host (CPU) inputs, the reference's calling convention: the call stages
     Q/K/V to the GPU in head groups on a copy stream, runs each group's
     pipeline on the current stream while the next group uploads, copies each
@@ -456,7 +480,7 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
         for t in (qd, kd, vd):
             t.record_stream(main)
         out_g, mask_g, _ = _pipeline(qd, kd, vd, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                                     shared_head_mask, "hnd")
+                                     shared_head_mask, "hnd", want_bitmap=details)
         if out_g.dtype != out_dtype:
             out_g = out_g.to(out_dtype)
         ev_c = torch.cuda.Event()
@@ -507,7 +531,8 @@ def padded_sparse_attention(q, k, v, frames, height, width, patch_h, patch_w, sp
     d = q3.shape[2]
     if scale is None:
         scale = head_dim_scale(d)
-    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out)
+    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out,
+                     return_details)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)
@@ -526,7 +551,8 @@ def draft_sparse_attention(q, k, v, layout: LatentLayout, sparsity, scale=None, 
     if scale is None:
         scale = head_dim_scale(d)
     plan = PadPlan(layout.frames, layout.height, layout.width, layout)
-    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out)
+    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out,
+                     return_details)
     if not return_details:
         return out
     return _details(out, mask, layout, d)
@@ -554,7 +580,7 @@ def multi_head_sparse_attention(q, k, v, layout: LatentLayout, sparsity, shared_
     if scale is None:
         scale = head_dim_scale(d)
     out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask,
-                     qkv_layout, out)
+                     qkv_layout, out, return_details)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)

@@ -182,6 +182,7 @@ struct PipeWs {
   double* scores;
   void* sel;
   void* attn;
+  void* sel32;
   float* kpart;
   size_t total;
 };
@@ -196,6 +197,7 @@ static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
   w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * g.g));
   w.sel = take(da::select_workspace_size(heads, g.g));
   w.attn = take(da::pair_attn_workspace_size(heads, g));
+  w.sel32 = take(da::select32_workspace_size(heads, g.g));
   w.kpart = reinterpret_cast<float*>(take(sizeof(float) * (size_t)heads * (da::pool_norm_blocks(d, g) + 1)));
   w.total = off;
   return w;
@@ -224,8 +226,13 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // and scans, candidate compaction + finish, tie counts + scan, mark, row
   // scan, collect, threshold, kept totals, packbits (bitmap requested);
   // attention: pair plan, tcgen05 kernel, fallback list (key norms come from pooling)
+  // (per-head logits path: the fp32 guard-band selection — init, eps, GEMM,
+  // 2 digit histograms + 3 scans, mark, band finish, force, row scan, collect,
+  // kept totals, packbits — followed by the gated fp64 launches, which exit
+  // at once unless the fp32 path flagged a fallback)
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
-  return 1 + 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1 + 3;
+  const int fp64_path = 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1;
+  return 1 + (fused ? 15 : 0) + fp64_path + 3 + 1;  // + pair plan, tcgen05 kernel, fallback list, K/V tiling
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
@@ -252,12 +259,28 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
                                          kblk > 0 ? w.kpart : nullptr),
                         "pool")))
     return rc;
-  // K3a: draft scores; when the selection runs per head on raw logits, the
-  // GEMM epilogue also histograms digit 0 of the selection keys
+  // K3: per-head selection on raw logits (the default) runs on fp32 draft
+  // scores with an exact fp64 guard band (launch_select32); the fp64 GEMM and
+  // radix selection below then only run (gated on the device) if that path
+  // flags non-finite inputs or an oversized band. softmax selection and the
+  // shared-head mask always take the fp64 path.
   const bool fuse_digit0 = !pa->select_softmax && !pa->shared_head_mask;
-  if (fuse_digit0) da::select_init(w.sel, a.heads, g.g, pa->m, st);
+  const int* gate = nullptr;
+  if (fuse_digit0) {
+    if ((rc = cuda_status(da::launch_select32(w.qp, w.kp, reinterpret_cast<float*>(w.scores), a.heads, g.g, a.d,
+                                              a.scale, pa->m, pa->force_row_keep, w.sel32, pa->row_ptr, pa->col_idx,
+                                              pa->bitmap, pa->threshold, pa->forced, pa->kept,
+                                              da_mask_capacity(g.g, pa->m), st),
+                          "select32")))
+      return rc;
+    gate = da::select32_fallback_flag(w.sel32, a.heads, g.g);
+  }
+  // fp64 draft scores; on the per-head logits path the GEMM epilogue also
+  // histograms digit 0 of the selection keys
+  if (fuse_digit0) da::select_init(w.sel, a.heads, g.g, pa->m, st, gate);
   if ((rc = cuda_status(da::launch_draft_scores(w.qp, w.kp, w.scores, a.heads, g.g, a.d, a.scale, pa->select_softmax,
-                                                st, fuse_digit0 ? da::select_hist_buffer(w.sel, a.heads, g.g) : nullptr),
+                                                st, fuse_digit0 ? da::select_hist_buffer(w.sel, a.heads, g.g) : nullptr,
+                                                gate),
                         "draft_scores")))
     return rc;
   const double* sel_scores = w.scores;
@@ -274,7 +297,7 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   // starts inside the real extent), so no dead columns (padding.py:151-153)
   if ((rc = cuda_status(da::launch_select(sel_scores, sel_heads, g.g, pa->m, pa->force_row_keep, nullptr, w.sel,
                                           pa->row_ptr, pa->col_idx, pa->bitmap, pa->threshold, pa->forced, pa->kept,
-                                          da_mask_capacity(g.g, pa->m), st, fuse_digit0),
+                                          da_mask_capacity(g.g, pa->m), st, fuse_digit0, gate),
                         "select")))
     return rc;
   da_attn_args aa = a;

@@ -25,15 +25,25 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
 int pool_norm_blocks(int d, const Geo& g);
 // hist0 (optional): per-head 2048-bin histogram of the top 11 key bits, filled in the epilogue
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
-                                double scale, int softmax, cudaStream_t st, unsigned int* hist0 = nullptr);
+                                double scale, int softmax, cudaStream_t st, unsigned int* hist0 = nullptr,
+                                const int* gate = nullptr);
 
 size_t select_workspace_size(int heads, int g);
 long long bitmap_bytes_per_head(int g);
 unsigned int* select_hist_buffer(void* ws, int heads, int g);
-void select_init(void* ws, int heads, int g, long long m, cudaStream_t st);
+void select_init(void* ws, int heads, int g, long long m, cudaStream_t st, const int* gate = nullptr);
 cudaError_t launch_select(const double* scores, int heads, int g, long long m, int force, const uint8_t* dead,
                           void* ws, int* row_ptr, int* col_idx, uint8_t* bitmap, double* threshold,
-                          int64_t* forced, int64_t* kept, long long cap, cudaStream_t st, bool digit0_done = false);
+                          int64_t* forced, int64_t* kept, long long cap, cudaStream_t st, bool digit0_done = false,
+                          const int* gate = nullptr);
+// fp32 draft scores + exact fp64 guard-band selection (the pipeline default);
+// sets the flag select32_fallback_flag() points to when the fp64 path must run
+size_t select32_workspace_size(int heads, int g);
+const int* select32_fallback_flag(void* ws, int heads, int g);
+cudaError_t launch_select32(const double* qp, const double* kp, float* scores32, int heads, int g, int d,
+                            double scale, long long m, int force, void* ws, int* row_ptr, int* col_idx,
+                            uint8_t* bitmap, double* threshold, int64_t* forced, int64_t* kept, long long cap,
+                            cudaStream_t st);
 
 size_t portable_smem_bytes(int p, int d, int dv);
 cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st);

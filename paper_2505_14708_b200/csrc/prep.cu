@@ -151,9 +151,10 @@ constexpr int DT = 128, DK = 8;
 
 __global__ void __launch_bounds__(256) draft_gemm_kernel(const double* __restrict__ qp, const double* __restrict__ kp,
                                                          double* __restrict__ scores, int g, int d, double scale,
-                                                         unsigned int* __restrict__ hist0) {
-  __shared__ double sq[DK][DT];
-  __shared__ double sk[DK][DT];
+                                                         unsigned int* __restrict__ hist0, const int* __restrict__ gate = nullptr) {
+  if (gate != nullptr && *gate == 0) return;  // fp64 path gated off (fp32 selection succeeded)
+  __shared__ double sq[DK][DT + 1];  // +1: the transposing stores hit distinct banks
+  __shared__ double sk[DK][DT + 1];
   __shared__ unsigned int sh[2048];
   const int h = blockIdx.z;
   const int i0 = blockIdx.y * DT, j0 = blockIdx.x * DT;
@@ -228,7 +229,8 @@ __global__ void __launch_bounds__(256) draft_gemm_kernel(const double* __restric
 }
 
 // Row softmax in float64 (core.py:38-54), one warp per row.
-__global__ void __launch_bounds__(256) row_softmax_kernel(double* __restrict__ scores, int g, long long rows) {
+__global__ void __launch_bounds__(256) row_softmax_kernel(double* __restrict__ scores, int g, long long rows, const int* __restrict__ gate = nullptr) {
+  if (gate != nullptr && *gate == 0) return;
   long long row = (long long)blockIdx.x * 8 + threadIdx.x / 32;
   int lane = threadIdx.x % 32;
   if (row >= rows) return;
@@ -285,9 +287,9 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
   const uint4* base = reinterpret_cast<const uint4*>(src.x[z] + h * src.hs[z]) + k;
   const long long rs8 = src.rs[z] / 8;
   const bool norms = z == 1 && kpart != nullptr;
-  double acc[8];
+  double acc[8], acc2[8];  // even / odd rows: two shorter add chains (fp64 sums of bf16 are exact either way)
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  for (int e = 0; e < 8; ++e) acc[e] = acc2[e] = 0.0;
   float nmax = 0.f;
   for (int r0 = 0; r0 < g.p; r0 += 8) {
     uint4 q[8];
@@ -305,7 +307,10 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
       const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&q[t]);
       if (ok[t]) {  // padding rows are not summed (keeps -0.0 sums bit-exact)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += (double)__bfloat162float(b[e]);
+        for (int e = 0; e < 8; ++e) {
+          if (t & 1) acc2[e] += (double)__bfloat162float(b[e]);
+          else acc[e] += (double)__bfloat162float(b[e]);
+        }
       }
       if (norms) {
         float s2 = 0.f;
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
     const double div = (double)(cnt > 1 ? cnt : 1);
     double* o = src.out[z] + ((long long)h * g.g + i) * d + k * 8;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = acc[e] / div;
+    for (int e = 0; e < 8; ++e) o[e] = (acc[e] + acc2[e]) / div;
   }
   if (norms) {
 #pragma unroll
@@ -393,13 +398,13 @@ cudaError_t launch_pool(const void* x, long long hs, long long rs, double* poole
 }
 
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
-                                double scale, int softmax, cudaStream_t st, unsigned int* hist0) {
+                                double scale, int softmax, cudaStream_t st, unsigned int* hist0, const int* gate) {
   dim3 grid((g + DT - 1) / DT, (g + DT - 1) / DT, heads);
-  draft_gemm_kernel<<<grid, 256, 0, st>>>(qp, kp, scores, g, d, scale, softmax ? nullptr : hist0);
+  draft_gemm_kernel<<<grid, 256, 0, st>>>(qp, kp, scores, g, d, scale, softmax ? nullptr : hist0, gate);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !softmax) return e;
   long long rows = (long long)heads * g;
-  row_softmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(scores, g, rows);
+  row_softmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(scores, g, rows, gate);
   return cudaGetLastError();
 }
 

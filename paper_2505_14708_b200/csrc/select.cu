@@ -37,6 +37,10 @@ struct SelState {
   unsigned int cand_count;
 };
 
+// Launch gate: with `gate` set, a kernel runs only when (*gate != 0) == want
+// (the fp32 selection runs when its fallback flag is clear, the fp64 one when set).
+DA_DEV bool gated_off(const int* gate, int want) { return gate != nullptr && ((*gate != 0) != (want != 0)); }
+
 DA_DEV double key_score(unsigned long long k) {
   unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
   return __longlong_as_double((long long)b);
@@ -45,7 +49,8 @@ DA_DEV double key_score(unsigned long long k) {
 DA_DEV int pass_hi(int pass) { return 64 - RB * pass; }
 DA_DEV int pass_lo(int pass) { int lo = 64 - RB * (pass + 1); return lo < 0 ? 0 : lo; }
 
-__global__ void sel_init_kernel(SelState* st, unsigned int* hist, long long m) {
+__global__ void sel_init_kernel(SelState* st, unsigned int* hist, long long m, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.x;
   if (threadIdx.x == 0) {
     SelState s;
@@ -60,7 +65,8 @@ __global__ void sel_init_kernel(SelState* st, unsigned int* hist, long long m) {
 // still match the resolved prefix). grid: (chunks, heads).
 __global__ void __launch_bounds__(256) sel_hist_kernel(const double* __restrict__ scores, long long n,
                                                        const SelState* __restrict__ st, unsigned int* hist,
-                                                       int pass) {
+                                                       int pass, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.y;
   if (pass >= 2 && st[h].compact) return;
   __shared__ unsigned int sh[NB];
@@ -111,7 +117,8 @@ DA_DEV void pick_bucket(const unsigned int* H, int nb, long long rem, int lane, 
 }
 
 // One warp per head: resolve digit `pass` from the global histogram.
-__global__ void sel_scan_kernel(SelState* st, unsigned int* hist, int pass) {
+__global__ void sel_scan_kernel(SelState* st, unsigned int* hist, int pass, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.x;
   const int lane = threadIdx.x;
   if (pass >= 2 && st[h].compact) return;
@@ -141,7 +148,8 @@ __global__ void sel_scan_kernel(SelState* st, unsigned int* hist, int pass) {
 // Gather the entries of the 22-bit bucket (key, flat index) when it is small.
 __global__ void __launch_bounds__(256) sel_compact_kernel(const double* __restrict__ scores, long long n,
                                                           SelState* st, unsigned long long* cand_key,
-                                                          unsigned int* cand_idx) {
+                                                          unsigned int* cand_idx, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.y;
   if (!st[h].compact) return;
   const unsigned long long prefix = st[h].prefix;
@@ -172,7 +180,8 @@ __global__ void __launch_bounds__(256) sel_compact_kernel(const double* __restri
 }
 
 // One CTA per head: digits 2..5 over the compacted candidates, in shared memory.
-__global__ void __launch_bounds__(1024) sel_cand_finish_kernel(SelState* st, const unsigned long long* cand_key) {
+__global__ void __launch_bounds__(1024) sel_cand_finish_kernel(SelState* st, const unsigned long long* cand_key, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.x;
   if (!st[h].compact) return;
   __shared__ unsigned int sh[NB];
@@ -222,7 +231,8 @@ __global__ void __launch_bounds__(1024) sel_cand_finish_kernel(SelState* st, con
 
 // Per-row equal-key counts (only needed when ties at T straddle the cut).
 __global__ void __launch_bounds__(256) sel_rowcount_eq_kernel(const double* __restrict__ scores, int g,
-                                                              const SelState* __restrict__ st, int* eq_rows) {
+                                                              const SelState* __restrict__ st, int* eq_rows, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.y;
   const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (row >= g) return;
@@ -240,7 +250,9 @@ __global__ void __launch_bounds__(256) sel_rowcount_eq_kernel(const double* __re
 // If `extra` is given, its per-row values are summed into extra_total[h].
 __global__ void __launch_bounds__(1024) scan_rows_kernel(const int* __restrict__ in, int* __restrict__ out, int g,
                                                          int out_stride, const SelState* st, int only_if_ties,
-                                                         const int* __restrict__ extra, long long* extra_total) {
+                                                         const int* __restrict__ extra, long long* extra_total,
+                                                         const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.x;
   if (only_if_ties && st[h].eq_total == st[h].remaining) return;
   __shared__ int warp_tot[32];
@@ -300,7 +312,8 @@ __global__ void __launch_bounds__(1024) scan_rows_kernel(const int* __restrict__
 __global__ void __launch_bounds__(256) sel_mark_kernel(const double* __restrict__ scores, int g, const SelState* st,
                                                        const int* __restrict__ eq_prefix, int force_row_keep,
                                                        const uint8_t* __restrict__ dead, unsigned int* bm, int w32,
-                                                       int* row_counts, int* row_forced) {
+                                                       int* row_counts, int* row_forced, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.y;
   const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (row >= g) return;
@@ -381,7 +394,8 @@ __global__ void __launch_bounds__(256) sel_mark_kernel(const double* __restrict_
 // Expand bitmap rows into ascending column lists at row_ptr offsets.
 __global__ void __launch_bounds__(256) sel_collect_kernel(const unsigned int* __restrict__ bm, int g, int w32,
                                                           const int* __restrict__ row_ptr, int* col_idx,
-                                                          long long cap) {
+                                                          long long cap, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.y;
   const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (row >= g) return;
@@ -397,7 +411,9 @@ __global__ void __launch_bounds__(256) sel_collect_kernel(const unsigned int* __
 
 // np.packbits(kept) (masking.py:168-170): one output byte per thread.
 __global__ void __launch_bounds__(256) sel_packbits_kernel(const unsigned int* __restrict__ bm, int g, int w32,
-                                                           FastDiv gdiv, long long bytes_per_head, uint8_t* out) {
+                                                           FastDiv gdiv, long long bytes_per_head, uint8_t* out,
+                                                           const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.y;
   const long long byte = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (byte >= bytes_per_head) return;
@@ -418,12 +434,14 @@ __global__ void __launch_bounds__(256) sel_packbits_kernel(const unsigned int* _
   out[(long long)h * bytes_per_head + byte] = (uint8_t)v;
 }
 
-__global__ void sel_finish_kernel(const SelState* st, int heads, double* threshold) {
+__global__ void sel_finish_kernel(const SelState* st, int heads, double* threshold, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h < heads) threshold[h] = key_score(st[h].T);
 }
 
-__global__ void copy_total_kernel(const int* row_ptr, int g, int heads, int64_t* kept) {
+__global__ void copy_total_kernel(const int* row_ptr, int g, int heads, int64_t* kept, const int* __restrict__ gate = nullptr, int want = 1) {
+  if (gated_off(gate, want)) return;
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h < heads) kept[h] = row_ptr[(long long)h * (g + 1) + g];
 }
@@ -469,45 +487,500 @@ unsigned int* select_hist_buffer(void* ws, int heads, int g) { return carve_sel(
 
 cudaError_t launch_select(const double* scores, int heads, int g, long long m, int force, const uint8_t* dead,
                           void* ws, int* row_ptr, int* col_idx, uint8_t* bitmap, double* threshold,
-                          int64_t* forced, int64_t* kept, long long cap, cudaStream_t st, bool digit0_done) {
+                          int64_t* forced, int64_t* kept, long long cap, cudaStream_t st, bool digit0_done,
+                          const int* gate) {
   SelWs w = carve_sel(ws, heads, g);
   const long long n = (long long)g * g;
   const int w32 = (g + 31) / 32;
-  if (!digit0_done) sel_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, m);
+  if (!digit0_done) sel_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, m, gate);
   int chunks = (int)((n + 256 * 16 - 1) / (256 * 16));
   if (chunks > 256) chunks = 256;
   if (chunks < 1) chunks = 1;
   for (int pass = 0; pass < NPASS; ++pass) {
     if (!(pass == 0 && digit0_done))
-      sel_hist_kernel<<<dim3(chunks, heads), 256, 0, st>>>(scores, n, w.state, w.hist, pass);
-    sel_scan_kernel<<<heads, 32, 0, st>>>(w.state, w.hist, pass);
+      sel_hist_kernel<<<dim3(chunks, heads), 256, 0, st>>>(scores, n, w.state, w.hist, pass, gate);
+    sel_scan_kernel<<<heads, 32, 0, st>>>(w.state, w.hist, pass, gate);
     if (pass == 1) {
-      sel_compact_kernel<<<dim3(chunks, heads), 256, 0, st>>>(scores, n, w.state, w.cand_key, w.cand_idx);
-      sel_cand_finish_kernel<<<heads, 1024, 0, st>>>(w.state, w.cand_key);
+      sel_compact_kernel<<<dim3(chunks, heads), 256, 0, st>>>(scores, n, w.state, w.cand_key, w.cand_idx, gate);
+      sel_cand_finish_kernel<<<heads, 1024, 0, st>>>(w.state, w.cand_key, gate);
     }
   }
   dim3 rows_grid((g + 7) / 8, heads);
-  sel_rowcount_eq_kernel<<<rows_grid, 256, 0, st>>>(scores, g, w.state, w.eq_rows);
-  scan_rows_kernel<<<heads, 1024, 0, st>>>(w.eq_rows, w.eq_prefix, g, g + 1, w.state, 1, nullptr, nullptr);
+  sel_rowcount_eq_kernel<<<rows_grid, 256, 0, st>>>(scores, g, w.state, w.eq_rows, gate);
+  scan_rows_kernel<<<heads, 1024, 0, st>>>(w.eq_rows, w.eq_prefix, g, g + 1, w.state, 1, nullptr, nullptr, gate);
   sel_mark_kernel<<<rows_grid, 256, 0, st>>>(scores, g, w.state, w.eq_prefix, force, dead, w.bm, w32, w.row_counts,
-                                             w.row_forced);
+                                             w.row_forced, gate);
   scan_rows_kernel<<<heads, 1024, 0, st>>>(w.row_counts, row_ptr, g, g + 1, w.state, 0, w.row_forced,
-                                           reinterpret_cast<long long*>(forced));
-  sel_collect_kernel<<<rows_grid, 256, 0, st>>>(w.bm, g, w32, row_ptr, col_idx, cap);
-  sel_finish_kernel<<<(heads + 127) / 128, 128, 0, st>>>(w.state, heads, threshold);
-  copy_total_kernel<<<(heads + 127) / 128, 128, 0, st>>>(row_ptr, g, heads, kept);
+                                           reinterpret_cast<long long*>(forced), gate);
+  sel_collect_kernel<<<rows_grid, 256, 0, st>>>(w.bm, g, w32, row_ptr, col_idx, cap, gate);
+  sel_finish_kernel<<<(heads + 127) / 128, 128, 0, st>>>(w.state, heads, threshold, gate);
+  copy_total_kernel<<<(heads + 127) / 128, 128, 0, st>>>(row_ptr, g, heads, kept, gate);
   if (bitmap != nullptr) {
     const long long bph = bitmap_bytes_per_head(g);
     sel_packbits_kernel<<<dim3((unsigned)((bph + 255) / 256), heads), 256, 0, st>>>(w.bm, g, w32, make_fastdiv(g),
-                                                                                     bph, bitmap);
+                                                                                     bph, bitmap, gate);
   }
   return cudaGetLastError();
 }
 
 // Fused digit-0 histogram support for the draft GEMM epilogue.
-void select_init(void* ws, int heads, int g, long long m, cudaStream_t st) {
+void select_init(void* ws, int heads, int g, long long m, cudaStream_t st, const int* gate) {
   SelWs w = carve_sel(ws, heads, g);
-  sel_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, m);
+  sel_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, m, gate);
+}
+
+
+// ===========================================================================
+// fp32 draft scores with an exact fp64 guard band (the pipeline's default).
+//
+// The ranking must equal the reference's float64 argsort. Scores are computed
+// in fp32 (FFMA GEMM, 4x the fp64 rate), and every fp32 score is within
+// eps = (d + 8) 2^-24 max|q~| max|k~| |scale| of the fp64 score (Cauchy-Schwarz
+// over the fp32 input rounding, FMA accumulation and the scale multiply). With
+// T32 the m-th largest fp32 score, the m-th largest fp64 score t lies in
+// [T32 - eps, T32 + eps], so
+//   s32 > T32 + 2 eps   -> kept (s64 > t),
+//   s32 < T32 - 2 eps   -> dropped (s64 < t),
+// and only the band in between (a few hundred entries per head for real data)
+// is rescored in fp64 and ranked exactly (descending score, ties to the smaller
+// flat index). The row argmax (force_row_keep) is resolved the same way among
+// the entries within 2 eps of the row's fp32 maximum. Non-finite inputs or a
+// band larger than S32_CAP set a flag, and the fp64 GEMM + radix selection
+// then run for the call (their launches are no-ops otherwise).
+// ===========================================================================
+constexpr int S32_CAP = 8192;    // band candidates per head resolved in one CTA
+
+struct Sel32State {
+  unsigned int prefix;           // resolved high bits of T32's key
+  long long remaining;           // entries still to take from the current bucket
+  unsigned long long nq2, nk2;   // largest pooled row norms^2 (double bits; non-negative so uint order)
+  double eps;
+  long long count_hi;            // sure-kept entries
+  int cand_count;
+};
+
+DA_DEV unsigned int key32(float s) {
+  if (s != s) return 0u;
+  if (s == 0.f) s = 0.f;
+  const unsigned int b = __float_as_uint(s);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+DA_DEV float key32_score(unsigned int k) {
+  const unsigned int b = (k >> 31) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(b);
+}
+
+// fp64 score exactly as the fp64 GEMM forms it: sequential FMA over features, then * scale
+DA_DEV double score64(const double* __restrict__ q, const double* __restrict__ k, int d, double scale) {
+  double acc = 0.0;
+  for (int c = 0; c < d; ++c) acc = fma(__ldg(q + c), __ldg(k + c), acc);
+  return acc * scale;
+}
+
+__global__ void s32_init_kernel(Sel32State* st, unsigned int* hist, unsigned int* rowmax, int g, long long m,
+                                int* fallback) {
+  const int h = blockIdx.x;
+  if (threadIdx.x == 0) {
+    Sel32State s;
+    s.prefix = 0; s.remaining = m; s.nq2 = 0; s.nk2 = 0; s.eps = 0.0; s.count_hi = 0; s.cand_count = 0;
+    st[h] = s;
+    if (h == 0) *fallback = 0;
+  }
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) hist[(long long)h * NB + b] = 0;
+  for (int i = threadIdx.x; i < g; i += blockDim.x) rowmax[(long long)h * g + i] = 0u;
+}
+
+// Largest pooled row norms per head (fp64), for eps; grid (heads, EPSB).
+constexpr int EPSB = 16;
+__global__ void __launch_bounds__(256) s32_norm_kernel(const double* __restrict__ qp, const double* __restrict__ kp,
+                                                       int g, int d, Sel32State* st) {
+  const int h = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = 0; t < 2; ++t) {
+    const double* X = (t ? kp : qp) + (long long)h * g * d;
+    double mx = 0.0;
+    for (int i = blockIdx.y * 8 + w; i < g; i += 8 * EPSB) {
+      double s2 = 0.0;
+      for (int c = lane; c < d; c += 32) { const double v = __ldg(X + (long long)i * d + c); s2 = fma(v, v, s2); }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      mx = (s2 != s2) ? s2 : fmax(mx, s2);  // keep NaN visible
+    }
+    if (lane == 0) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(mx);
+      atomicMax(t ? &st[h].nk2 : &st[h].nq2, bits);  // NaN / inf bits sort above every finite value
+    }
+  }
+}
+
+DA_DEV void s32_set_eps(Sel32State& s, int d, double scale, int* fallback) {
+  const double a = __longlong_as_double((long long)s.nq2), b = __longlong_as_double((long long)s.nk2);
+  const double e = (double)(d + 8) * 0x1p-24 * sqrt(a) * sqrt(b) * fabs(scale) * 1.0625 + 1e-300;
+  s.eps = e;
+  if (!(a <= 1e300) || !(b <= 1e300) || !(e <= 1e30)) atomicOr(fallback, 1);
+}
+
+// fp32 draft scores: 128 x 128 tiles, 8 x 8 outputs per thread; epilogue keeps
+// the digit-0 histogram of the 32-bit keys and each row's largest key.
+constexpr int DT32 = 128, DK32 = 16;
+__global__ void __launch_bounds__(256) draft32_gemm_kernel(const double* __restrict__ qp, const double* __restrict__ kp,
+                                                           float* __restrict__ scores, int g, int d, float scale,
+                                                           unsigned int* __restrict__ hist0,
+                                                           unsigned int* __restrict__ rowmax) {
+  __shared__ float sq[DK32][DT32 + 1];  // +1: the transposing stores hit distinct banks
+  __shared__ float sk[DK32][DT32 + 1];
+  __shared__ unsigned int sh[NB];
+  const int h = blockIdx.z;
+  const int i0 = blockIdx.y * DT32, j0 = blockIdx.x * DT32;
+  const double* Q = qp + (long long)h * g * d;
+  const double* K = kp + (long long)h * g * d;
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;
+  for (int b = tid; b < NB; b += 256) sh[b] = 0;
+  float pq[8], pk[8];
+  auto load = [&](int k0) {  // 2048 values per operand chunk -> 8 per thread
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int e = tid + 256 * t;
+      const int r = e / DK32, c = e % DK32;
+      const int kk = k0 + c;
+      pq[t] = (i0 + r < g && kk < d) ? (float)__ldg(Q + (long long)(i0 + r) * d + kk) : 0.f;
+      pk[t] = (j0 + r < g && kk < d) ? (float)__ldg(K + (long long)(j0 + r) * d + kk) : 0.f;
+    }
+  };
+  float2 acc[8][4];  // acc[u][v2] = outputs (u, 2 v2) and (u, 2 v2 + 1)
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = make_float2(0.f, 0.f);
+  load(0);
+  for (int k0 = 0; k0 < d; k0 += DK32) {
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int e = tid + 256 * t;
+      sq[e % DK32][e / DK32] = pq[t];
+      sk[e % DK32][e / DK32] = pk[t];
+    }
+    __syncthreads();
+    if (k0 + DK32 < d) load(k0 + DK32);
+#pragma unroll
+    for (int c = 0; c < DK32; ++c) {
+      float a[8];
+      float2 b[4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = sq[c][ty + 16 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) b[v] = make_float2(sk[c][tx + 32 * v], sk[c][tx + 32 * v + 16]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = ffma2(make_float2(a[u], a[u]), b[v], acc[u][v]);
+    }
+  }
+  float* S = scores + (long long)h * g * g;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int gi = i0 + ty + 16 * u;
+    unsigned int rk = 0u;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int gj = j0 + tx + 16 * v;  // v even: acc[u][v/2].x (col tx + 32(v/2)), odd: .y (+16)
+      if (gi < g && gj < g) {
+        const float sv = ((v & 1) ? acc[u][v >> 1].y : acc[u][v >> 1].x) * scale;
+        S[(long long)gi * g + gj] = sv;
+        const unsigned int k = key32(sv);
+        rk = max(rk, k);
+      }
+      // digit-0 histogram with one shared-memory atomic per distinct bin of
+      // the warp (scores crowd a handful of bins)
+      const bool live = gi < g && gj < g;
+      const unsigned int bin = live ? (key32(((v & 1) ? acc[u][v >> 1].y : acc[u][v >> 1].x) * scale) >> 21) : 0xFFFFFFFFu;
+      const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+      if (live && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bin], (unsigned int)__popc(peers));
+    }
+    // row max over the 16 threads (tx) sharing this row
+#pragma unroll
+    for (int o = 8; o; o >>= 1) rk = max(rk, __shfl_xor_sync(0xffffffffu, rk, o));
+    if (tx == 0 && gi < g) atomicMax(&rowmax[(long long)h * g + gi], rk);
+  }
+  __syncthreads();
+  for (int b = tid; b < NB; b += 256)
+    if (sh[b]) atomicAdd(&hist0[(long long)h * NB + b], sh[b]);
+}
+
+// digits: 0 = bits 21..31 (fused in the GEMM), 1 = bits 10..20, 2 = bits 0..9
+DA_DEV int p32_hi(int pass) { return pass == 0 ? 32 : pass == 1 ? 21 : 10; }
+DA_DEV int p32_lo(int pass) { return pass == 0 ? 21 : pass == 1 ? 10 : 0; }
+
+__global__ void __launch_bounds__(256) s32_hist_kernel(const float* __restrict__ scores, long long n,
+                                                       const Sel32State* __restrict__ st, unsigned int* hist, int pass,
+                                                       const int* __restrict__ fallback) {
+  if (*fallback) return;
+  const int h = blockIdx.y;
+  __shared__ unsigned int sh[NB];
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const int hi = p32_hi(pass), lo = p32_lo(pass);
+  const unsigned int prefix = st[h].prefix;
+  const unsigned int dmask = (1u << (hi - lo)) - 1u;
+  const float4* s4 = reinterpret_cast<const float4*>(scores + (long long)h * n);
+  const long long n4 = n / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n4 + 4; e += stride) {
+    float v[4];
+    int cnt = 4;
+    if (e < n4) {
+      const float4 x = __ldg(s4 + e);
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {  // tail (n % 4 entries)
+      const long long t = n4 * 4 + (e - n4);
+      cnt = t < n ? 1 : 0;
+      if (cnt) v[0] = __ldg(scores + (long long)h * n + t);
+    }
+    for (int q = 0; q < cnt; ++q) {
+      const unsigned int k = key32(v[q]);
+      if ((k >> hi) == prefix) atomicAdd(&sh[(k >> lo) & dmask], 1u);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < NB; b += blockDim.x)
+    if (sh[b]) atomicAdd(&hist[(long long)h * NB + b], sh[b]);
+}
+
+__global__ void s32_scan_kernel(Sel32State* st, unsigned int* hist, int pass, int* fallback, int d, double scale) {
+  if (*fallback) return;
+  const int h = blockIdx.x;
+  const int lane = threadIdx.x;
+  const int hi = p32_hi(pass), lo = p32_lo(pass);
+  unsigned int* H = hist + (long long)h * NB;
+  const long long rem = st[h].remaining;
+  int chosen;
+  long long above, cnt;
+  pick_bucket(H, 1 << (hi - lo), rem, lane, chosen, above, cnt);
+  __syncwarp();
+  for (int b = lane; b < NB; b += 32) H[b] = 0;
+  if (lane == 0) {
+    Sel32State s = st[h];
+    s.remaining = rem - above;
+    s.prefix = (pass == 0 ? 0u : (s.prefix << (hi - lo))) | (unsigned int)chosen;
+    if (pass == 2) s32_set_eps(s, d, scale, fallback);
+    st[h] = s;
+  }
+}
+
+// One warp per row: sure-kept bits into the word-aligned bitmap, band entries
+// into the candidate list, and the row's exact first argmax.
+__global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__ scores, const double* __restrict__ qp,
+                                                       const double* __restrict__ kp, int g, int d, double scale,
+                                                       Sel32State* st, unsigned int* bm, int w32,
+                                                       const unsigned int* __restrict__ rowmax, int* argmax,
+                                                       int* cand, const int* __restrict__ fallback) {
+  if (*fallback) return;
+  const int h = blockIdx.y;
+  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= g) return;
+  const double eps = st[h].eps;
+  const double t32 = (double)key32_score(st[h].prefix);
+  const float hi_f = __double2float_ru(t32 + 2.0 * eps);
+  const float lo_f = __double2float_rd(t32 - 2.0 * eps);
+  const float rmax = key32_score(rowmax[(long long)h * g + row]);
+  const float rlo = __double2float_rd((double)rmax - 2.0 * eps);
+  const float* S = scores + ((long long)h * g + row) * g;
+  unsigned int* B = bm + ((long long)h * g + row) * w32;
+  int* C = cand + (long long)h * S32_CAP;
+  long long hi_cnt = 0;
+  int best = -1, nbest = 0;
+  double bv = 0.0;
+  const double* qrow = qp + ((long long)h * g + row) * d;
+  for (int j0 = 0; j0 < g; j0 += 32) {
+    const int j = j0 + lane;
+    const float v = j < g ? __ldg(S + j) : -INFINITY;
+    const bool sure = v > hi_f;
+    const bool band = !sure && v >= lo_f;
+    const unsigned sw = __ballot_sync(0xffffffffu, sure);
+    if (lane == 0) B[j0 >> 5] = sw;
+    hi_cnt += __popc(sw);
+    const unsigned bw = __ballot_sync(0xffffffffu, band);
+    if (bw) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&st[h].cand_count, __popc(bw));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int slot = base + __popc(bw & ((1u << lane) - 1));
+      if (band && slot < S32_CAP) C[slot] = row * g + j;
+    }
+    // row argmax candidates (within 2 eps of the fp32 row max), resolved in fp64
+    unsigned aw = __ballot_sync(0xffffffffu, j < g && v >= rlo);
+    while (aw) {
+      const int src = __ffs(aw) - 1;
+      aw &= aw - 1;
+      const int jj = j0 + src;
+      ++nbest;
+      const double* krow = kp + ((long long)h * g + jj) * d;
+      // fp64 score, lane-split over features (all candidates of the row alike)
+      double sv = 0.0;
+      for (int c = lane; c < d; c += 32) sv = fma(__ldg(qrow + c), __ldg(krow + c), sv);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      sv *= scale;
+      if (best < 0 || sv > bv) { best = jj; bv = sv; }
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st[h].count_hi), (unsigned long long)hi_cnt);
+    argmax[(long long)h * g + row] = best;
+  }
+}
+
+// One CTA per head: rescore the band in fp64, keep the `need` best (descending
+// score, ties to the smaller flat index), set their bits, emit the threshold.
+__global__ void __launch_bounds__(1024) s32_finish_kernel(const double* __restrict__ qp,
+                                                          const double* __restrict__ kp, int g, int d, double scale,
+                                                          long long m, Sel32State* st, const int* __restrict__ cand,
+                                                          unsigned int* bm, int w32, double* threshold,
+                                                          int* fallback) {
+  extern __shared__ unsigned char smraw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smraw);  // [S32_CAP]
+  int* idx = reinterpret_cast<int*>(key + S32_CAP);                         // [S32_CAP]
+  __shared__ int bad;
+  const int h = blockIdx.x;
+  if (*fallback) return;
+  const int cnt = st[h].cand_count;
+  const long long need = m - st[h].count_hi;
+  if (threadIdx.x == 0) bad = (cnt > S32_CAP || need < 1 || need > cnt) ? 1 : 0;
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) atomicOr(fallback, 1);
+    return;
+  }
+  const int* C = cand + (long long)h * S32_CAP;
+  for (int c = threadIdx.x; c < cnt; c += blockDim.x) {
+    const int f = C[c];
+    const int i = f / g, j = f - i * g;
+    key[c] = score_key(score64(qp + ((long long)h * g + i) * d, kp + ((long long)h * g + j) * d, d, scale));
+    idx[c] = f;
+  }
+  __syncthreads();
+  unsigned int* Bh = bm + (long long)h * g * w32;
+  for (int c = threadIdx.x; c < cnt; c += blockDim.x) {
+    const unsigned long long kc = key[c];
+    const int fc = idx[c];
+    int rank = 0;
+    for (int o = 0; o < cnt; ++o) rank += (key[o] > kc) || (key[o] == kc && idx[o] < fc);
+    if (rank < need) {
+      const int i = fc / g, j = fc - i * g;
+      atomicOr(&Bh[(long long)i * w32 + (j >> 5)], 1u << (j & 31));
+    }
+    if (rank == need - 1) threshold[h] = key_score(kc);
+  }
+}
+
+// Per row: force the first argmax in (force_row_keep) and count the row.
+__global__ void __launch_bounds__(256) s32_force_kernel(unsigned int* bm, int g, int w32,
+                                                        const int* __restrict__ argmax, int force, int* row_counts,
+                                                        int* row_forced, const int* __restrict__ fallback) {
+  if (*fallback) return;
+  const int h = blockIdx.y;
+  const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= g) return;
+  unsigned int* B = bm + ((long long)h * g + row) * w32;
+  int forced = 0;
+  if (force && lane == 0) {
+    const int a = argmax[(long long)h * g + row];
+    if (a >= 0 && !((B[a >> 5] >> (a & 31)) & 1u)) {
+      B[a >> 5] |= 1u << (a & 31);
+      forced = 1;
+    }
+  }
+  __syncwarp();
+  int cnt = 0;
+  for (int c = lane; c < w32; c += 32) cnt += __popc(B[c]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) {
+    row_counts[(long long)h * g + row] = cnt;
+    row_forced[(long long)h * g + row] = forced;
+  }
+}
+
+__global__ void copy_total_guarded_kernel(const int* row_ptr, int g, int heads, int64_t* kept,
+                                          const int* __restrict__ fallback) {
+  if (*fallback) return;
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < heads) kept[h] = row_ptr[(long long)h * (g + 1) + g];
+}
+
+struct Sel32Ws {
+  Sel32State* state;
+  unsigned int* hist;
+  unsigned int* rowmax;
+  int* argmax;
+  int* cand;
+  int* row_counts;
+  int* row_forced;
+  unsigned int* bm;
+  int* fallback;
+  size_t total;
+};
+
+static Sel32Ws carve_sel32(void* base, int heads, int g) {
+  Sel32Ws w;
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* r = p ? p + off : nullptr; off += (bytes + 255) & ~size_t(255); return r; };
+  const int w32 = (g + 31) / 32;
+  w.state = reinterpret_cast<Sel32State*>(take(sizeof(Sel32State) * heads));
+  w.hist = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * NB * heads));
+  w.rowmax = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (size_t)heads * g));
+  w.argmax = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * g));
+  w.cand = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * S32_CAP));
+  w.row_counts = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * g));
+  w.row_forced = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * g));
+  w.bm = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (size_t)heads * g * w32));
+  w.fallback = reinterpret_cast<int*>(take(sizeof(int)));
+  w.total = off;
+  return w;
+}
+
+size_t select32_workspace_size(int heads, int g) { return carve_sel32(nullptr, heads, g).total; }
+const int* select32_fallback_flag(void* ws, int heads, int g) { return carve_sel32(ws, heads, g).fallback; }
+
+cudaError_t launch_select32(const double* qp, const double* kp, float* scores32, int heads, int g, int d,
+                            double scale, long long m, int force, void* ws, int* row_ptr, int* col_idx,
+                            uint8_t* bitmap, double* threshold, int64_t* forced, int64_t* kept, long long cap,
+                            cudaStream_t st) {
+  Sel32Ws w = carve_sel32(ws, heads, g);
+  const long long n = (long long)g * g;
+  const int w32 = (g + 31) / 32;
+  s32_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, w.rowmax, g, m, w.fallback);
+  s32_norm_kernel<<<dim3(heads, EPSB), 256, 0, st>>>(qp, kp, g, d, w.state);
+  dim3 ggrid((g + DT32 - 1) / DT32, (g + DT32 - 1) / DT32, heads);
+  draft32_gemm_kernel<<<ggrid, 256, 0, st>>>(qp, kp, scores32, g, d, (float)scale, w.hist, w.rowmax);
+  int chunks = (int)((n / 4 + 256 * 8 - 1) / (256 * 8));
+  if (chunks > 512) chunks = 512;
+  if (chunks < 1) chunks = 1;
+  for (int pass = 0; pass < 3; ++pass) {
+    if (pass > 0) s32_hist_kernel<<<dim3(chunks, heads), 256, 0, st>>>(scores32, n, w.state, w.hist, pass, w.fallback);
+    s32_scan_kernel<<<heads, 32, 0, st>>>(w.state, w.hist, pass, w.fallback, d, scale);
+  }
+  dim3 rows_grid((g + 7) / 8, heads);
+  s32_mark_kernel<<<rows_grid, 256, 0, st>>>(scores32, qp, kp, g, d, scale, w.state, w.bm, w32, w.rowmax, w.argmax,
+                                             w.cand, w.fallback);
+  const size_t fsmem = (sizeof(unsigned long long) + sizeof(int)) * S32_CAP;
+  cudaFuncSetAttribute(s32_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+  s32_finish_kernel<<<heads, 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bm, w32, threshold,
+                                               w.fallback);
+  s32_force_kernel<<<rows_grid, 256, 0, st>>>(w.bm, g, w32, w.argmax, force, w.row_counts, w.row_forced, w.fallback);
+  scan_rows_kernel<<<heads, 1024, 0, st>>>(w.row_counts, row_ptr, g, g + 1, nullptr, 0, w.row_forced,
+                                           reinterpret_cast<long long*>(forced), w.fallback, 0);
+  sel_collect_kernel<<<rows_grid, 256, 0, st>>>(w.bm, g, w32, row_ptr, col_idx, cap, w.fallback, 0);
+  copy_total_guarded_kernel<<<(heads + 127) / 128, 128, 0, st>>>(row_ptr, g, heads, kept, w.fallback);
+  if (bitmap != nullptr) {
+    const long long bph = bitmap_bytes_per_head(g);
+    sel_packbits_kernel<<<dim3((unsigned)((bph + 255) / 256), heads), 256, 0, st>>>(w.bm, g, w32, make_fastdiv(g),
+                                                                                     bph, bitmap, w.fallback, 0);
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace da

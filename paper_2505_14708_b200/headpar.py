@@ -47,5 +47,5 @@ class HeadParallelAttention:
         qh, kh, vh = (seq_to_head(x, self.world, self.group) for x in (q, k, v))
         scale = self.scale if self.scale is not None else api.head_dim_scale(q.shape[-1])
         out, mask, _ = api._pipeline(qh, kh, vh, self.plan, self.sparsity, scale, self.pool_mode, self.select_on,
-                                     self.force, False, "nhd", attn_events=attn_events)
+                                     self.force, False, "nhd", attn_events=attn_events, want_bitmap=False)
         return head_to_seq(out, self.world, self.group), mask

@@ -391,3 +391,26 @@ def test_host_inputs_pipelined_by_head_group_match_device_call():
     assert host.mask.kept_count == dev.mask.kept_count
     single = da.padded_sparse_attention(qh[1], kh[1], vh[1], 2, 45, 80, 8, 8, 0.9)
     assert torch.equal(single, dev.output[1].cpu())
+
+
+@pytest.mark.parametrize("kind", ["zeros", "constant_rows", "nan_row"])
+def test_pipeline_selection_fallback_cases(kind):
+    # massive ties (every score equal) overflow the fp32 guard band and
+    # non-finite inputs skip it: the gated fp64 selection must then produce
+    # the reference mask (masking.py:59-91 tie rule, np.argmax first max)
+    grid, (q, k, v), _ = _inputs((2, 45, 80, 8, 8, 128, 2, 3), head_ids=None)
+    if kind == "zeros":
+        q = torch.zeros_like(q)
+    elif kind == "constant_rows":
+        k = torch.ones_like(k)
+    plan = da.pad_plan(2, 45, 80, 8, 8)
+    if kind == "nan_row":
+        q = q.clone()
+        q[1, 7] = float("nan")
+    res = da.multi_head_sparse_attention(q, k, v, plan, 0.9, return_details=True)
+    q64, k64, v64 = (t.double().cpu().numpy() for t in (q, k, v))
+    for h in range(2):
+        ref, _ = O.draft_mask(q64[h], k64[h], grid, 0.9)
+        got = res.mask.head(h)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.kept), (kind, h)
+        assert got.kept_count == ref.kept_count and got.forced_row_keeps == ref.forced_row_keeps

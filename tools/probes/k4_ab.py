@@ -66,7 +66,7 @@ for mode in args.data.split(","):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         api._pipeline(q, k, v, plan, args.sparsity, da.head_dim_scale(d), "average", "logits", True,
-                      False, "hnd", attn_events=ev)
+                      False, "hnd", attn_events=ev, want_bitmap=False)
         e.record()
         torch.cuda.synchronize()
         ts.append(ev[0].elapsed_time(ev[1]))
