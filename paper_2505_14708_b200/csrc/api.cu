@@ -147,14 +147,14 @@ size_t da_attn_workspace_size(int32_t heads, const da_grid* grid) {
 }
 
 static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, void* stream, const float* kpart,
-                                 int kblk);
+                                 int kblk, bool tiles_ready);
 
 int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* stream) {
-  return block_sparse_fwd_impl(args, grid, stream, nullptr, 0);
+  return block_sparse_fwd_impl(args, grid, stream, nullptr, 0, false);
 }
 
 static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, void* stream, const float* kpart,
-                                 int kblk) {
+                                 int kblk, bool tiles_ready) {
   int rc = check_attn(args, grid);
   if (rc) return rc;
   da::Geo g = da::make_geo(*grid);
@@ -163,7 +163,7 @@ static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, 
     if (!args->workspace)
       return fail(DA_EINVAL, "block_sparse_fwd: the tcgen05 path needs a workspace (da_attn_workspace_size)");
     const char* why = "";
-    cudaError_t e = da::launch_tc_attn(*args, g, st, &why, kpart, kblk);
+    cudaError_t e = da::launch_tc_attn(*args, g, st, &why, kpart, kblk, tiles_ready);
     if (e == cudaErrorInvalidValue && why[0]) return fail(DA_ECUDA, "block_sparse_fwd (tcgen05): %s", why);
     return cuda_status(e, "block_sparse_fwd (tcgen05)");
   }
@@ -232,7 +232,7 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // at once unless the fp32 path flagged a fallback)
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
   const int fp64_path = 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1;
-  return 1 + (fused ? 15 : 0) + fp64_path + 3 + 1;  // + pair plan, tcgen05 kernel, fallback list, K/V tiling
+  return 1 + (fused ? 15 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
@@ -253,10 +253,15 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
     return fail(DA_EINVAL, "sparse_attention: q/k need d %% 8 == 0 and 16-byte aligned rows");
   // K2: pool Q and K in one launch
   // (average pooling also records K's row-norm maxima for the attention kernel)
+  // (and, on the tcgen05 shape, writes K and V as the attention kernel's region tiles)
   const int kblk = pa->pool_mode == 0 ? da::pool_norm_blocks(a.d, g) : 0;
+  const bool tiles = kblk > 0 && a.d == 128 && a.dv == 128 && g.ph == 8 && g.pw == 8 && a.v_row_stride % 8 == 0 &&
+                     (reinterpret_cast<uintptr_t>(a.v) & 15) == 0;
   if ((rc = cuda_status(da::launch_pool2(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.k, a.k_head_stride,
                                          a.k_row_stride, w.kp, a.heads, a.d, pa->pool_mode, g, st,
-                                         kblk > 0 ? w.kpart : nullptr),
+                                         kblk > 0 ? w.kpart : nullptr, tiles ? a.v : nullptr, a.v_head_stride,
+                                         a.v_row_stride, tiles ? da::pair_attn_tiles(w.attn, a.heads, g, 0) : nullptr,
+                                         tiles ? da::pair_attn_tiles(w.attn, a.heads, g, 1) : nullptr),
                         "pool")))
     return rc;
   // K3: per-head selection on raw logits (the default) runs on fp32 draft
@@ -308,7 +313,7 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   aa.shared_mask = pa->shared_head_mask ? 1 : 0;
   aa.workspace = w.attn;
   if (pa->ev_attn_begin) cudaEventRecord((cudaEvent_t)pa->ev_attn_begin, st);
-  rc = block_sparse_fwd_impl(&aa, grid, stream, kblk > 0 ? w.kpart : nullptr, kblk);
+  rc = block_sparse_fwd_impl(&aa, grid, stream, kblk > 0 ? w.kpart : nullptr, kblk, tiles);
   if (pa->ev_attn_end) cudaEventRecord((cudaEvent_t)pa->ev_attn_end, st);
   return rc;
 }

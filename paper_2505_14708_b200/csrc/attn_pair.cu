@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(384, 1)
 bool make_kv_maps(const da_attn_args& a, const Geo& g, CUtensorMap* mk, CUtensorMap* mv);
 
 cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                             long long* trace, const float* kpart, int kblk) {
+                             long long* trace, const float* kpart, int kblk, bool tiles_ready) {
   CUtensorMap mk, mv;
   if (!make_kv_maps(a, g, &mk, &mv)) {
     *why = "cuTensorMapEncodeTiled failed";
@@ -892,7 +892,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
       kvt = env ? atoi(env) : 1;
     }
     if (kvt && (a.layout == DA_LAYOUT_REORDERED || (g.ph == 8 && g.pw == 8))) {
-      uint8_t* tiles = reinterpret_cast<uint8_t*>(pairs) + pair_align256(sizeof(int2) * (size_t)a.heads * ((g.g + 1) / 2));
+      uint8_t* tiles = pair_attn_tiles(a.workspace, a.heads, g, 0);
       pairk::KvTileArgs ta;
       ta.x[0] = static_cast<const __nv_bfloat16*>(a.k);
       ta.x[1] = static_cast<const __nv_bfloat16*>(a.v);
@@ -901,7 +901,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
       ta.out[0] = tiles;
       ta.out[1] = tiles + (size_t)a.heads * g.g * pairk::TILE;
       ta.layout = a.layout;
-      pairk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
+      if (!tiles_ready) pairk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
       p.kt = ta.out[0];
       p.vt = ta.out[1];
     }
@@ -921,6 +921,13 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // rows whose fixed softmax offset underflowed: redo their regions exactly
   return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * num_sms);
+}
+
+uint8_t* pair_attn_tiles(void* ws, int heads, const Geo& g, int which) {
+  const size_t off = 256 + pair_align256(sizeof(float) * heads * pairk::KBLK) +
+                     pair_align256(sizeof(int) * 4 * (size_t)heads * g.g) +
+                     pair_align256(sizeof(int2) * (size_t)heads * ((g.g + 1) / 2));
+  return static_cast<uint8_t*>(ws) + off + (size_t)which * heads * g.g * pairk::TILE;
 }
 
 size_t pair_attn_workspace_size(int heads, const Geo& g) {

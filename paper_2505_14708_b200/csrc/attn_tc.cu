@@ -687,18 +687,18 @@ bool make_kv_maps(const da_attn_args& a, const Geo& g, CUtensorMap* mk, CUtensor
 }
 
 cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                             long long* trace, const float* kpart, int kblk);
+                             long long* trace, const float* kpart, int kblk, bool tiles_ready);
 
 // Default: region-pair kernel (attn_pair.cu). DA_K4=transposed selects the
 // single-region transposed kernel below (kept for A/B measurements).
 cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                           const float* kpart, int kblk) {
+                           const float* kpart, int kblk, bool tiles_ready) {
   static int variant = -1;
   if (variant < 0) {
     const char* env = getenv("DA_K4");
     variant = (env && strcmp(env, "transposed") == 0) ? 1 : 0;
   }
-  if (variant == 0) return launch_pair_attn(a, g, st, why, g_trace, kpart, kblk);
+  if (variant == 0) return launch_pair_attn(a, g, st, why, g_trace, kpart, kblk, tiles_ready);
   CUtensorMap mq, mk, mv;
   bool ok;
   if (a.layout == DA_LAYOUT_REORDERED) {

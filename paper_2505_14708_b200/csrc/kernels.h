@@ -19,9 +19,14 @@ cudaError_t launch_pool(const void* x, long long hs, long long rs, double* poole
 // pools two tensors (Q and K) in one launch; kpart (optional, average mode with
 // pool_norm_blocks(d, g) > 0) receives per-block maxima of K's row norms,
 // [heads][pool_norm_blocks(d, g)]
+// x2/ktile/vtile (optional, d = 128 and 8x8 pools): the same pass also writes
+// K and V as the attention kernel's region tiles (pair_attn_tiles)
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
                          long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
-                         float* kpart);
+                         float* kpart, const void* x2 = nullptr, long long hs2 = 0, long long rs2 = 0,
+                         uint8_t* ktile = nullptr, uint8_t* vtile = nullptr);
+// K / V tile buffers inside the attention workspace ([heads][g][16 KB] each)
+uint8_t* pair_attn_tiles(void* ws, int heads, const Geo& g, int which);
 int pool_norm_blocks(int d, const Geo& g);
 // hist0 (optional): per-head 2048-bin histogram of the top 11 key bits, filled in the epilogue
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
@@ -57,6 +62,6 @@ bool tc_supported(const da_attn_args& a, const Geo& g);
 // kpart/kblk: per-head key row norm maxima already computed by the pooling
 // pass ([heads][kblk]); null = the attention launch computes them itself
 cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                           const float* kpart = nullptr, int kblk = 0);
+                           const float* kpart = nullptr, int kblk = 0, bool tiles_ready = false);
 
 }  // namespace da

@@ -74,9 +74,10 @@ __global__ void __launch_bounds__(256) permute_out_kernel(const uint4* __restric
 // two tensors (Q and K) per launch.
 // ---------------------------------------------------------------------------
 struct PoolSrc {
-  const __nv_bfloat16* x[2];
-  long long hs[2], rs[2];
+  const __nv_bfloat16* x[3];  // Q, K (pooled) and V (tiled only)
+  long long hs[3], rs[3];
   double* out[2];
+  uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
 };
 
 __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode, Geo g) {
@@ -287,6 +288,10 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
   const uint4* base = reinterpret_cast<const uint4*>(src.x[z] + h * src.hs[z]) + k;
   const long long rs8 = src.rs[z] / 8;
   const bool norms = z == 1 && kpart != nullptr;
+  // K / V tiles ([half][64 rows x 128 B], 128-byte swizzle, zero padding rows):
+  // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
+  uint8_t* tdst = (z >= 1 && src.tile[z - 1] != nullptr && live)
+                      ? src.tile[z - 1] + ((long long)h * g.g + i) * 16384 + (k >> 3) * 8192 : nullptr;
   double acc[8], acc2[8];  // even / odd rows: two shorter add chains (fp64 sums of bf16 are exact either way)
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = acc2[e] = 0.0;
@@ -302,6 +307,14 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
       const long long row = ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
       q[t] = ok[t] ? __ldg(base + row * rs8) : make_uint4(0, 0, 0, 0);
     }
+    if (tdst != nullptr) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int r = r0 + t;
+        *reinterpret_cast<uint4*>(tdst + r * 128 + (((k & 7) ^ (r & 7)) << 4)) = q[t];
+      }
+    }
+    if (z == 2) continue;  // V: tiles only
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&q[t]);
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
       }
     }
   }
-  if (live) {
+  if (live && z < 2) {
     const int cnt = rc.vy * rc.vx;
     const double div = (double)(cnt > 1 ? cnt : 1);
     double* o = src.out[z] + ((long long)h * g.g + i) * d + k * 8;
@@ -352,14 +365,20 @@ int pool_norm_blocks(int d, const Geo& g) {
 
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
                          long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
-                         float* kpart) {
+                         float* kpart, const void* x2, long long hs2, long long rs2, uint8_t* ktile,
+                         uint8_t* vtile) {
   if (mode == 0 && pool_norm_blocks(d, g) > 0 && rs0 % 8 == 0 && (!x1 || rs1 % 8 == 0)) {
     PoolSrc src;
     src.x[0] = static_cast<const __nv_bfloat16*>(x0);
     src.hs[0] = hs0; src.rs[0] = rs0; src.out[0] = out0;
     src.x[1] = static_cast<const __nv_bfloat16*>(x1 ? x1 : x0);
     src.hs[1] = x1 ? hs1 : hs0; src.rs[1] = x1 ? rs1 : rs0; src.out[1] = x1 ? out1 : out0;
-    dim3 grid(pool_norm_blocks(d, g), heads, x1 ? 2 : 1);
+    const bool tiles = x1 && x2 && ktile && vtile && d == 128 && g.p == 64 && rs2 % 8 == 0;
+    src.x[2] = static_cast<const __nv_bfloat16*>(tiles ? x2 : x0);
+    src.hs[2] = tiles ? hs2 : hs0; src.rs[2] = tiles ? rs2 : rs0;
+    src.tile[0] = tiles ? ktile : nullptr;
+    src.tile[1] = tiles ? vtile : nullptr;
+    dim3 grid(pool_norm_blocks(d, g), heads, x1 ? (tiles ? 3 : 2) : 1);
     float* kp = x1 ? kpart : nullptr;
     switch (d / 8) {
       case 1: pool_avg_kernel<1><<<grid, 256, 0, st>>>(src, d, g, kp); break;
@@ -394,7 +413,8 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
 
 cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
                         const Geo& g, cudaStream_t st) {
-  return launch_pool2(x, hs, rs, pooled, nullptr, 0, 0, nullptr, heads, d, mode, g, st, nullptr);
+  return launch_pool2(x, hs, rs, pooled, nullptr, 0, 0, nullptr, heads, d, mode, g, st, nullptr, nullptr, 0, 0,
+                      nullptr, nullptr);
 }
 
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
