@@ -197,7 +197,7 @@ static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
   w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * g.g));
   w.sel = take(da::select_workspace_size(heads, g.g));
   w.attn = take(da::pair_attn_workspace_size(heads, g));
-  w.sel32 = take(da::select32_workspace_size(heads, g.g));
+  w.sel32 = take(da::select32_workspace_size(heads, g.g, d));
   w.kpart = reinterpret_cast<float*>(take(sizeof(float) * (size_t)heads * (da::pool_norm_blocks(d, g) + 1)));
   w.total = off;
   return w;
@@ -226,13 +226,13 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // and scans, candidate compaction + finish, tie counts + scan, mark, row
   // scan, collect, threshold, kept totals, packbits (bitmap requested);
   // attention: pair plan, tcgen05 kernel, fallback list (key norms come from pooling)
-  // (per-head logits path: the fp32 guard-band selection — init, eps, GEMM,
+  // (per-head logits path: the fp32 guard-band selection — init, eps, operand pack, GEMM,
   // 2 digit histograms + 3 scans, mark, band finish, force, row scan, collect,
   // kept totals, packbits — followed by the gated fp64 launches, which exit
   // at once unless the fp32 path flagged a fallback)
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
   const int fp64_path = 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1;
-  return 1 + (fused ? 15 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
+  return 1 + (fused ? 16 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {

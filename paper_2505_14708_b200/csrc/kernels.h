@@ -43,7 +43,7 @@ cudaError_t launch_select(const double* scores, int heads, int g, long long m, i
                           const int* gate = nullptr);
 // fp32 draft scores + exact fp64 guard-band selection (the pipeline default);
 // sets the flag select32_fallback_flag() points to when the fp64 path must run
-size_t select32_workspace_size(int heads, int g);
+size_t select32_workspace_size(int heads, int g, int d);
 const int* select32_fallback_flag(void* ws, int heads, int g);
 cudaError_t launch_select32(const double* qp, const double* kp, float* scores32, int heads, int g, int d,
                             double scale, long long m, int force, void* ws, int* row_ptr, int* col_idx,

@@ -622,87 +622,141 @@ DA_DEV void s32_set_eps(Sel32State& s, int d, double scale, int* fallback) {
 
 // fp32 draft scores: 128 x 128 tiles, 8 x 8 outputs per thread; epilogue keeps
 // the digit-0 histogram of the 32-bit keys and each row's largest key.
-constexpr int DT32 = 128, DK32 = 16;
-__global__ void __launch_bounds__(256) draft32_gemm_kernel(const double* __restrict__ qp, const double* __restrict__ kp,
-                                                           float* __restrict__ scores, int g, int d, float scale,
-                                                           unsigned int* __restrict__ hist0,
-                                                           unsigned int* __restrict__ rowmax) {
-  __shared__ float sq[DK32][DT32 + 1];  // +1: the transposing stores hit distinct banks
-  __shared__ float sk[DK32][DT32 + 1];
+// Operands come pre-packed by s32_pack_kernel: fp32, transposed and zero
+// padded, [heads][dp][gp] (dp = d rounded up to DK32, gp = g rounded up to
+// DT32), so each k-chunk is DK32 contiguous 512-byte rows per operand, moved
+// by cp.async through a G32_STAGES-deep ring with no bounds checks.
+constexpr int DT32 = 128, DK32 = 16, G32_TS = DT32 + 4, G32_STAGES = 3;
+constexpr int G32_STAGE_FLOATS = 2 * DK32 * DT32;
+constexpr int G32_SMEM = (DT32 * G32_TS > G32_STAGES * G32_STAGE_FLOATS ? DT32 * G32_TS : G32_STAGES * G32_STAGE_FLOATS) * 4;
+__host__ __device__ inline long long g32_pad(long long x, int to) { return (x + to - 1) / to * to; }
+
+// fp64 pooled [heads][g][d] -> fp32 [heads][dp][gp] (zero padded); grid
+// (gp / 32, dp / 32, 2 * heads), block (32, 8)
+__global__ void __launch_bounds__(256) s32_pack_kernel(const double* __restrict__ qp, const double* __restrict__ kp,
+                                                       int g, int d, float* __restrict__ qt, float* __restrict__ kt) {
+  __shared__ float tile[32][33];
+  const int h = blockIdx.z >> 1, which = blockIdx.z & 1;
+  const int gp = (int)g32_pad(g, DT32), dp = (int)g32_pad(d, DK32);
+  const double* X = (which ? kp : qp) + (long long)h * g * d;
+  float* Y = (which ? kt : qt) + (long long)h * dp * gp;
+  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int r = r0 + y, c = c0 + threadIdx.x;
+    tile[y][threadIdx.x] = (r < g && c < d) ? (float)__ldg(X + (long long)r * d + c) : 0.f;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int c = c0 + y, r = r0 + threadIdx.x;
+    if (c < dp) Y[(long long)c * gp + r] = tile[threadIdx.x][y];
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) draft32_gemm_kernel(const float* __restrict__ qt, const float* __restrict__ kt,
+                                                              float* __restrict__ scores, int g, int d, float scale,
+                                                              unsigned int* __restrict__ hist0,
+                                                              unsigned int* __restrict__ rowmax) {
+  // dynamic shared memory: the operand ring during the main loop, then the
+  // 128 x 128 score tile, which the epilogue writes out row by row (coalesced
+  // 16-byte stores, row maxima and the digit-0 histogram per row)
+  extern __shared__ __align__(16) float g32s[];
+  float (*T)[G32_TS] = reinterpret_cast<float (*)[G32_TS]>(g32s);  // [DT32][G32_TS]
   __shared__ unsigned int sh[NB];
   const int h = blockIdx.z;
   const int i0 = blockIdx.y * DT32, j0 = blockIdx.x * DT32;
-  const double* Q = qp + (long long)h * g * d;
-  const double* K = kp + (long long)h * g * d;
+  const int gp = (int)g32_pad(g, DT32), dp = (int)g32_pad(d, DK32);
+  const float* Q = qt + (long long)h * dp * gp + i0;
+  const float* K = kt + (long long)h * dp * gp + j0;
   const int tid = threadIdx.x;
   const int ty = tid >> 4, tx = tid & 15;
   for (int b = tid; b < NB; b += 256) sh[b] = 0;
-  float pq[8], pk[8];
-  auto load = [&](int k0) {  // 2048 values per operand chunk -> 8 per thread
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(g32s);
+  const int nk = dp / DK32;
+  // chunk kc -> stage kc % G32_STAGES: [operand][DK32][DT32] floats; each
+  // thread moves 4 x 16 bytes (row c = tid / 32 + 8 t, 16-byte column tid % 32)
+  auto issue = [&](int kc) {
+    if (kc < nk) {
+      const uint32_t s = sbase + (uint32_t)((kc % G32_STAGES) * G32_STAGE_FLOATS * 4);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int e = tid + 256 * t;
-      const int r = e / DK32, c = e % DK32;
-      const int kk = k0 + c;
-      pq[t] = (i0 + r < g && kk < d) ? (float)__ldg(Q + (long long)(i0 + r) * d + kk) : 0.f;
-      pk[t] = (j0 + r < g && kk < d) ? (float)__ldg(K + (long long)(j0 + r) * d + kk) : 0.f;
+      for (int t = 0; t < 4; ++t) {
+        const int op = t >> 1, c = (tid >> 5) + 8 * (t & 1), col = (tid & 31) * 4;
+        const float* src = (op ? K : Q) + (long long)(kc * DK32 + c) * gp + col;
+        cp_async16(s + (uint32_t)(((op * DK32 + c) * DT32 + col) * 4), src, 16);
+      }
     }
+    cp_async_commit();
   };
-  float2 acc[8][4];  // acc[u][v2] = outputs (u, 2 v2) and (u, 2 v2 + 1)
+  // thread (ty, tx) owns rows 4 ty + {0..3} and 64 + 4 ty + {0..3} (u = 0..7),
+  // columns 4 tx + {0..3} and 64 + 4 tx + {0..3}; acc[u][v2] = column pair v2
+  float2 acc[8][4];
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v] = make_float2(0.f, 0.f);
-  load(0);
-  for (int k0 = 0; k0 < d; k0 += DK32) {
-    __syncthreads();
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int e = tid + 256 * t;
-      sq[e % DK32][e / DK32] = pq[t];
-      sk[e % DK32][e / DK32] = pk[t];
-    }
-    __syncthreads();
-    if (k0 + DK32 < d) load(k0 + DK32);
+  for (int s = 0; s < G32_STAGES - 1; ++s) issue(s);
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<G32_STAGES - 2>();
+    __syncthreads();  // chunk kc visible to all; stage (kc - 1) % STAGES free
+    issue(kc + G32_STAGES - 1);
+    const float* sq = g32s + (kc % G32_STAGES) * G32_STAGE_FLOATS;
+    const float* sk = sq + DK32 * DT32;
 #pragma unroll
     for (int c = 0; c < DK32; ++c) {
-      float a[8];
-      float2 b[4];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] = sq[c][ty + 16 * u];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) b[v] = make_float2(sk[c][tx + 32 * v], sk[c][tx + 32 * v + 16]);
+      const float4 a0 = *reinterpret_cast<const float4*>(sq + c * DT32 + 4 * ty);
+      const float4 a1 = *reinterpret_cast<const float4*>(sq + c * DT32 + 64 + 4 * ty);
+      const float4 b0 = *reinterpret_cast<const float4*>(sk + c * DT32 + 4 * tx);
+      const float4 b1 = *reinterpret_cast<const float4*>(sk + c * DT32 + 64 + 4 * tx);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                           make_float2(b1.z, b1.w)};
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = ffma2(make_float2(a[u], a[u]), b[v], acc[u][v]);
     }
   }
+  cp_async_wait<0>();
   float* S = scores + (long long)h * g * g;
+  __syncthreads();  // operands no longer needed: the tile reuses the space
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    const int gi = i0 + ty + 16 * u;
+    const int r = (u < 4 ? 0 : 60) + 4 * ty + u;
+    *reinterpret_cast<float4*>(&T[r][4 * tx]) =
+        make_float4(acc[u][0].x * scale, acc[u][0].y * scale, acc[u][1].x * scale, acc[u][1].y * scale);
+    *reinterpret_cast<float4*>(&T[r][64 + 4 * tx]) =
+        make_float4(acc[u][2].x * scale, acc[u][2].y * scale, acc[u][3].x * scale, acc[u][3].y * scale);
+  }
+  __syncthreads();
+  const int lane = tid & 31, wp = tid >> 5;
+  const bool vec = (g & 3) == 0;  // 16-byte aligned rows
+  for (int rr = wp; rr < DT32; rr += 8) {
+    const int gi = i0 + rr;
+    if (gi >= g) break;
+    const float4 o = *reinterpret_cast<const float4*>(&T[rr][4 * lane]);
+    const int gj = j0 + 4 * lane;
+    const float ov[4] = {o.x, o.y, o.z, o.w};
+    if (vec && gj + 3 < g) {
+      *reinterpret_cast<float4*>(S + (long long)gi * g + gj) = o;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (gj + q < g) S[(long long)gi * g + gj + q] = ov[q];
+    }
     unsigned int rk = 0u;
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const int gj = j0 + tx + 16 * v;  // v even: acc[u][v/2].x (col tx + 32(v/2)), odd: .y (+16)
-      if (gi < g && gj < g) {
-        const float sv = ((v & 1) ? acc[u][v >> 1].y : acc[u][v >> 1].x) * scale;
-        S[(long long)gi * g + gj] = sv;
-        const unsigned int k = key32(sv);
-        rk = max(rk, k);
-      }
-      // digit-0 histogram with one shared-memory atomic per distinct bin of
-      // the warp (scores crowd a handful of bins)
-      const bool live = gi < g && gj < g;
-      const unsigned int bin = live ? (key32(((v & 1) ? acc[u][v >> 1].y : acc[u][v >> 1].x) * scale) >> 21) : 0xFFFFFFFFu;
-      const unsigned int peers = __match_any_sync(0xffffffffu, bin);
-      if (live && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bin], (unsigned int)__popc(peers));
+    for (int q = 0; q < 4; ++q) {
+      const bool live = gj + q < g;
+      const unsigned int k = key32(ov[q]);
+      if (live) rk = max(rk, k);
+      const unsigned int bin = live ? (k >> 21) : 0xFFFFFFFFu;
+      // digit-0 histogram: plain shared-memory atomics (measured faster than
+      // warp-aggregating equal bins with match.any, whose latency dominated)
+      if (live) atomicAdd(&sh[bin], 1u);
     }
-    // row max over the 16 threads (tx) sharing this row
 #pragma unroll
-    for (int o = 8; o; o >>= 1) rk = max(rk, __shfl_xor_sync(0xffffffffu, rk, o));
-    if (tx == 0 && gi < g) atomicMax(&rowmax[(long long)h * g + gi], rk);
+    for (int o2 = 16; o2; o2 >>= 1) rk = max(rk, __shfl_xor_sync(0xffffffffu, rk, o2));
+    if (lane == 0) atomicMax(&rowmax[(long long)h * g + gi], rk);
   }
   __syncthreads();
   for (int b = tid; b < NB; b += 256)
@@ -920,10 +974,12 @@ struct Sel32Ws {
   int* row_forced;
   unsigned int* bm;
   int* fallback;
+  float* qt;  // packed fp32 operands of the draft GEMM, [heads][dp][gp]
+  float* kt;
   size_t total;
 };
 
-static Sel32Ws carve_sel32(void* base, int heads, int g) {
+static Sel32Ws carve_sel32(void* base, int heads, int g, int d) {
   Sel32Ws w;
   char* p = static_cast<char*>(base);
   size_t off = 0;
@@ -938,24 +994,30 @@ static Sel32Ws carve_sel32(void* base, int heads, int g) {
   w.row_forced = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * g));
   w.bm = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (size_t)heads * g * w32));
   w.fallback = reinterpret_cast<int*>(take(sizeof(int)));
+  const size_t packed = sizeof(float) * (size_t)heads * g32_pad(d, DK32) * g32_pad(g, DT32);
+  w.qt = reinterpret_cast<float*>(take(packed));
+  w.kt = reinterpret_cast<float*>(take(packed));
   w.total = off;
   return w;
 }
 
-size_t select32_workspace_size(int heads, int g) { return carve_sel32(nullptr, heads, g).total; }
-const int* select32_fallback_flag(void* ws, int heads, int g) { return carve_sel32(ws, heads, g).fallback; }
+size_t select32_workspace_size(int heads, int g, int d) { return carve_sel32(nullptr, heads, g, d).total; }
+const int* select32_fallback_flag(void* ws, int heads, int g) { return carve_sel32(ws, heads, g, 0).fallback; }
 
 cudaError_t launch_select32(const double* qp, const double* kp, float* scores32, int heads, int g, int d,
                             double scale, long long m, int force, void* ws, int* row_ptr, int* col_idx,
                             uint8_t* bitmap, double* threshold, int64_t* forced, int64_t* kept, long long cap,
                             cudaStream_t st) {
-  Sel32Ws w = carve_sel32(ws, heads, g);
+  Sel32Ws w = carve_sel32(ws, heads, g, d);
   const long long n = (long long)g * g;
   const int w32 = (g + 31) / 32;
   s32_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, w.rowmax, g, m, w.fallback);
   s32_norm_kernel<<<dim3(heads, EPSB), 256, 0, st>>>(qp, kp, g, d, w.state);
   dim3 ggrid((g + DT32 - 1) / DT32, (g + DT32 - 1) / DT32, heads);
-  draft32_gemm_kernel<<<ggrid, 256, 0, st>>>(qp, kp, scores32, g, d, (float)scale, w.hist, w.rowmax);
+  cudaFuncSetAttribute(draft32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G32_SMEM);
+  s32_pack_kernel<<<dim3((unsigned)(g32_pad(g, DT32) / 32), (unsigned)g32_pad(d, 32) / 32, 2 * heads), dim3(32, 8), 0,
+                    st>>>(qp, kp, g, d, w.qt, w.kt);
+  draft32_gemm_kernel<<<ggrid, 256, G32_SMEM, st>>>(w.qt, w.kt, scores32, g, d, (float)scale, w.hist, w.rowmax);
   int chunks = (int)((n / 4 + 256 * 8 - 1) / (256 * 8));
   if (chunks > 512) chunks = 512;
   if (chunks < 1) chunks = 1;
