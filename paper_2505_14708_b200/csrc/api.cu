@@ -194,7 +194,8 @@ static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
   auto take = [&](size_t bytes) { char* r = p ? p + off : nullptr; off += align256(bytes); return r; };
   w.qp = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * d));
   w.kp = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * d));
-  w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * g.g * g.g));
+  // fp64 scores, or the fp32 planes of the guard-band path (per-head stride g * g rounded up to 4)
+  w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * ((size_t)g.g * g.g + 2)));
   w.sel = take(da::select_workspace_size(heads, g.g));
   w.attn = take(da::pair_attn_workspace_size(heads, g));
   w.sel32 = take(da::select32_workspace_size(heads, g.g, d));

@@ -630,6 +630,9 @@ constexpr int DT32 = 128, DK32 = 16, G32_TS = DT32 + 4, G32_STAGES = 3;
 constexpr int G32_STAGE_FLOATS = 2 * DK32 * DT32;
 constexpr int G32_SMEM = (DT32 * G32_TS > G32_STAGES * G32_STAGE_FLOATS ? DT32 * G32_TS : G32_STAGES * G32_STAGE_FLOATS) * 4;
 __host__ __device__ inline long long g32_pad(long long x, int to) { return (x + to - 1) / to * to; }
+// per-head stride of the fp32 score planes: g * g rounded up to 4 floats, so
+// every plane starts 16-byte aligned (odd g)
+__host__ __device__ inline long long s32_plane(int g) { return g32_pad((long long)g * g, 4); }
 
 // fp64 pooled [heads][g][d] -> fp32 [heads][dp][gp] (zero padded); grid
 // (gp / 32, dp / 32, 2 * heads), block (32, 8)
@@ -717,7 +720,7 @@ __global__ void __launch_bounds__(256, 2) draft32_gemm_kernel(const float* __res
     }
   }
   cp_async_wait<0>();
-  float* S = scores + (long long)h * g * g;
+  float* S = scores + (long long)h * s32_plane(g);
   __syncthreads();  // operands no longer needed: the tile reuses the space
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
@@ -778,7 +781,8 @@ __global__ void __launch_bounds__(256) s32_hist_kernel(const float* __restrict__
   const int hi = p32_hi(pass), lo = p32_lo(pass);
   const unsigned int prefix = st[h].prefix;
   const unsigned int dmask = (1u << (hi - lo)) - 1u;
-  const float4* s4 = reinterpret_cast<const float4*>(scores + (long long)h * n);
+  const float* plane = scores + (long long)h * g32_pad(n, 4);
+  const float4* s4 = reinterpret_cast<const float4*>(plane);
   const long long n4 = n / 4;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n4 + 4; e += stride) {
@@ -790,7 +794,7 @@ __global__ void __launch_bounds__(256) s32_hist_kernel(const float* __restrict__
     } else {  // tail (n % 4 entries)
       const long long t = n4 * 4 + (e - n4);
       cnt = t < n ? 1 : 0;
-      if (cnt) v[0] = __ldg(scores + (long long)h * n + t);
+      if (cnt) v[0] = __ldg(plane + t);
     }
     for (int q = 0; q < cnt; ++q) {
       const unsigned int k = key32(v[q]);
@@ -840,7 +844,7 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
   const float lo_f = __double2float_rd(t32 - 2.0 * eps);
   const float rmax = key32_score(rowmax[(long long)h * g + row]);
   const float rlo = __double2float_rd((double)rmax - 2.0 * eps);
-  const float* S = scores + ((long long)h * g + row) * g;
+  const float* S = scores + (long long)h * s32_plane(g) + (long long)row * g;
   unsigned int* B = bm + ((long long)h * g + row) * w32;
   int* C = cand + (long long)h * S32_CAP;
   long long hi_cnt = 0;

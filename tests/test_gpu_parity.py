@@ -414,3 +414,21 @@ def test_pipeline_selection_fallback_cases(kind):
         got = res.mask.head(h)
         assert got.bitmap_bytes() == O.mask_bitmap(ref.kept), (kind, h)
         assert got.kept_count == ref.kept_count and got.forced_row_keeps == ref.forced_row_keeps
+
+
+@pytest.mark.parametrize("dims", [(1, 12, 20, 4, 4, 32, 3, 7), (3, 40, 24, 8, 8, 128, 3, 8),
+                                  (3, 17, 20, 8, 8, 128, 2, 9)])
+def test_pipeline_odd_region_counts(dims):
+    # g odd (15, 45, 27 - the last one also ragged on both axes): per-head score
+    # planes are not 16-byte aligned at g * g, and rows are not either
+    grid, (q, k, v), (q64, k64, v64) = _inputs(dims)
+    f, h, w, ph, pw = dims[:5]
+    plan = da.pad_plan(f, h, w, ph, pw)
+    res = da.multi_head_sparse_attention(q, k, v, plan, 0.75, return_details=True)
+    out = res.output.float().cpu().numpy()
+    for hh in range(q.shape[0]):
+        ref = O.padded_sparse_attention(q64[hh], k64[hh], v64[hh], f, h, w, ph, pw, 0.75, return_details=True)
+        got = res.mask.head(hh)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept), hh
+        assert got.kept_count == ref.mask.kept_count and got.forced_row_keeps == ref.mask.forced_row_keeps
+        _close(out[hh], ref.output)
