@@ -784,23 +784,28 @@ __global__ void __launch_bounds__(256) s32_hist_kernel(const float* __restrict__
   const float* plane = scores + (long long)h * g32_pad(n, 4);
   const float4* s4 = reinterpret_cast<const float4*>(plane);
   const long long n4 = n / 4;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n4 + 4; e += stride) {
-    float v[4];
-    int cnt = 4;
-    if (e < n4) {
-      const float4 x = __ldg(s4 + e);
-      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    } else {  // tail (n % 4 entries)
-      const long long t = n4 * 4 + (e - n4);
-      cnt = t < n ? 1 : 0;
-      if (cnt) v[0] = __ldg(plane + t);
+  // each CTA streams a contiguous range of 16-byte groups, 4 loads in flight per thread
+  const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+  const long long b0 = (long long)blockIdx.x * per, b1 = min(n4, b0 + per);
+  auto count = [&](float x) {
+    const unsigned int k = key32(x);
+    if ((k >> hi) == prefix) atomicAdd(&sh[(k >> lo) & dmask], 1u);
+  };
+  for (long long e0 = b0 + threadIdx.x; e0 < b1; e0 += 4 * blockDim.x) {
+    float4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long e = e0 + (long long)u * blockDim.x;
+      if (e < b1) x[u] = __ldg(s4 + e);
     }
-    for (int q = 0; q < cnt; ++q) {
-      const unsigned int k = key32(v[q]);
-      if ((k >> hi) == prefix) atomicAdd(&sh[(k >> lo) & dmask], 1u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (e0 + (long long)u * blockDim.x < b1) {
+        count(x[u].x); count(x[u].y); count(x[u].z); count(x[u].w);
+      }
     }
   }
+  if (blockIdx.x == 0 && threadIdx.x < (int)(n - n4 * 4)) count(__ldg(plane + n4 * 4 + threadIdx.x));  // tail
   __syncthreads();
   for (int b = threadIdx.x; b < NB; b += blockDim.x)
     if (sh[b]) atomicAdd(&hist[(long long)h * NB + b], sh[b]);
@@ -851,37 +856,93 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
   int best = -1, nbest = 0;
   double bv = 0.0;
   const double* qrow = qp + ((long long)h * g + row) * d;
-  for (int j0 = 0; j0 < g; j0 += 32) {
-    const int j = j0 + lane;
-    const float v = j < g ? __ldg(S + j) : -INFINITY;
-    const bool sure = v > hi_f;
-    const bool band = !sure && v >= lo_f;
-    const unsigned sw = __ballot_sync(0xffffffffu, sure);
-    if (lane == 0) B[j0 >> 5] = sw;
-    hi_cnt += __popc(sw);
-    const unsigned bw = __ballot_sync(0xffffffffu, band);
-    if (bw) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&st[h].cand_count, __popc(bw));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      const int slot = base + __popc(bw & ((1u << lane) - 1));
-      if (band && slot < S32_CAP) C[slot] = row * g + j;
-    }
-    // row argmax candidates (within 2 eps of the fp32 row max), resolved in fp64
-    unsigned aw = __ballot_sync(0xffffffffu, j < g && v >= rlo);
-    while (aw) {
-      const int src = __ffs(aw) - 1;
-      aw &= aw - 1;
-      const int jj = j0 + src;
-      ++nbest;
-      const double* krow = kp + ((long long)h * g + jj) * d;
-      // fp64 score, lane-split over features (all candidates of the row alike)
-      double sv = 0.0;
-      for (int c = lane; c < d; c += 32) sv = fma(__ldg(qrow + c), __ldg(krow + c), sv);
+  // fp64 score of candidate column jj (lane-split over features); keeps the
+  // first maximum in ascending column order
+  auto argmax_candidate = [&](int jj) {
+    ++nbest;
+    const double* krow = kp + ((long long)h * g + jj) * d;
+    double sv = 0.0;
+    for (int c = lane; c < d; c += 32) sv = fma(__ldg(qrow + c), __ldg(krow + c), sv);
 #pragma unroll
-      for (int o = 16; o; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-      sv *= scale;
-      if (best < 0 || sv > bv) { best = jj; bv = sv; }
+    for (int o = 16; o; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+    sv *= scale;
+    if (best < 0 || sv > bv) { best = jj; bv = sv; }
+  };
+  if ((g & 3) == 0) {
+    // 16-byte path: lane holds columns j0 + 4 lane .. + 3 (128 per step, the
+    // next step's load in flight); bitmap word w of the step is assembled
+    // from the 4-bit masks of lanes 8 w .. 8 w + 7
+    const float4 ninf = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    float4 nxt = 4 * lane < g ? __ldg(reinterpret_cast<const float4*>(S + 4 * lane)) : ninf;
+    for (int j0 = 0; j0 < g; j0 += 128) {
+      const float4 x = nxt;
+      const int j = j0 + 4 * lane;
+      nxt = j + 128 < g ? __ldg(reinterpret_cast<const float4*>(S + j + 128)) : ninf;
+      const float v[4] = {x.x, x.y, x.z, x.w};
+      unsigned int sn = 0, bn = 0, an = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool sure = v[q] > hi_f;
+        sn |= (unsigned)sure << q;
+        bn |= (unsigned)(!sure && v[q] >= lo_f) << q;
+        an |= (unsigned)(j < g && v[q] >= rlo) << q;
+      }
+      hi_cnt += __popc(sn);
+      unsigned int word = sn << (4 * (lane & 7));
+      word |= __shfl_xor_sync(0xffffffffu, word, 1);
+      word |= __shfl_xor_sync(0xffffffffu, word, 2);
+      word |= __shfl_xor_sync(0xffffffffu, word, 4);
+      const int wi = (j0 >> 5) + (lane >> 3);
+      if ((lane & 7) == 0 && wi < w32) B[wi] = word;
+      if (__any_sync(0xffffffffu, bn != 0)) {
+        const int c = __popc(bn);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        int base = 0;
+        if (lane == 31) base = atomicAdd(&st[h].cand_count, incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        int slot = base + incl - c;
+        for (unsigned int b = bn; b; b &= b - 1, ++slot)
+          if (slot < S32_CAP) C[slot] = row * g + j + __ffs(b) - 1;
+      }
+      unsigned int aw = __ballot_sync(0xffffffffu, an != 0);
+      while (aw) {
+        const int src = __ffs(aw) - 1;
+        aw &= aw - 1;
+        for (unsigned int nib = __shfl_sync(0xffffffffu, an, src); nib; nib &= nib - 1)
+          argmax_candidate(j0 + 4 * src + __ffs(nib) - 1);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) hi_cnt += __shfl_xor_sync(0xffffffffu, hi_cnt, o);  // per-lane counts above
+  } else {
+    for (int j0 = 0; j0 < g; j0 += 32) {
+      const int j = j0 + lane;
+      const float v = j < g ? __ldg(S + j) : -INFINITY;
+      const bool sure = v > hi_f;
+      const bool band = !sure && v >= lo_f;
+      const unsigned sw = __ballot_sync(0xffffffffu, sure);
+      if (lane == 0) B[j0 >> 5] = sw;
+      hi_cnt += __popc(sw);
+      const unsigned bw = __ballot_sync(0xffffffffu, band);
+      if (bw) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&st[h].cand_count, __popc(bw));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const int slot = base + __popc(bw & ((1u << lane) - 1));
+        if (band && slot < S32_CAP) C[slot] = row * g + j;
+      }
+      // row argmax candidates (within 2 eps of the fp32 row max), resolved in fp64
+      unsigned aw = __ballot_sync(0xffffffffu, j < g && v >= rlo);
+      while (aw) {
+        const int src = __ffs(aw) - 1;
+        aw &= aw - 1;
+        argmax_candidate(j0 + src);
+      }
     }
   }
   if (lane == 0) {
