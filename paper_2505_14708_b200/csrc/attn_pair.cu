@@ -62,6 +62,7 @@ constexpr int INFO = 16;            // step info ring (K producer -> MMA, softma
 constexpr int KBLK = 32;            // key_norm_kernel blocks per head
 constexpr int RAGW = 512;           // ragged-region bitmap words (g <= 16384)
 constexpr int LISTCAP = 4096;       // staged kept-list entries per item (else read from global)
+constexpr int IR = 8;               // item ring (K producer -> every other role)
 
 constexpr int SMEM_K = 0;
 constexpr int SMEM_V = SMEM_K + KST * STAGE;
@@ -96,7 +97,9 @@ struct Params {
   int kblk;
   int* fb_count;       // rows whose fixed softmax offset underflowed: their (head, region)
   int* fb_items;       //   items are recomputed by the portable kernel afterwards
-  int fake_load;       // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies, bit 2 softmax work
+  int* work;           // dynamic item counter (zero at launch)
+  int fake_load;       // diagnostics (DA_FAKELOAD): bit 0 skips K copies, bit 1 V copies, bit 2 softmax work,
+                       // bit 3 fetches an L2-resident tile set instead
   uint64_t pol_kv, pol_q, pol_o;  // L2 cache policies of the K/V tiles, Q rows, output rows
   long long* trace;
 };
@@ -108,10 +111,12 @@ struct __align__(8) Bars {
   uint64_t o_full, o_empty;
   uint64_t q_full, q_empty;
   uint64_t info_full[INFO];
+  uint64_t item_full[IR], item_empty[IR];
 };
 struct SmemAux {
   Bars bars;
   int4 info[INFO];        // per step: key region, -, membership flags, last/first (K producer)
+  int items[IR];          // dynamically claimed nonempty items in claim order; items = end
   uint32_t tmem_base;
   float xch[2][2][128];   // [item parity][warpgroup][row] first-step block maxima
   float xq[2][2][128];    // [item parity][warpgroup][row] partial |q|^2
@@ -364,6 +369,10 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(&B.q_full, 256);
     mbar_init(&B.q_empty, 1);
     for (int s = 0; s < INFO; ++s) mbar_init(&B.info_full[s], 1);
+    for (int s = 0; s < IR; ++s) {
+      mbar_init(&B.item_full[s], 1);
+      mbar_init(&B.item_empty[s], 11);  // warps 1, 2, 3 and the 8 softmax warps
+    }
     fence_barrier_init();
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
@@ -389,6 +398,26 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t tmem = aux.tmem_base;
   uint8_t* sK = smem + SMEM_K;
   uint8_t* sV = smem + SMEM_V;
+  // Items are claimed dynamically (an atomic counter) by the K producer and
+  // handed to the other roles through the item ring in claim order: all CTAs
+  // stay within a head or two (the per-head K/V tile set fits L2) and the
+  // heaviest-first order of pair_plan_kernel balances the tail. Every other
+  // warp reads each entry once (next_item) and releases it at once.
+  int ring_i = 0;
+  uint32_t ring_ph = 0;
+  auto peek_item = [&](int k) {  // entry k places ahead of the reader's position
+    const int slot = (ring_i + k) % IR;
+    const uint32_t ph = ring_ph ^ (uint32_t)(((ring_i + k) / IR) & 1);
+    mbar_wait(&B.item_full[slot], ph);
+    return (long long)aux.items[slot];
+  };
+  auto next_item = [&]() {
+    const long long it = peek_item(0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&B.item_empty[ring_i]);
+    if (++ring_i == IR) { ring_i = 0; ring_ph ^= 1u; }
+    return it;
+  };
 
   if (warp == 0 || warp == 2) {
     // ===================== TMA producers (warp 0: K, warp 2: V) =====================
@@ -406,10 +435,39 @@ __global__ void __launch_bounds__(384, 1)
     const CUtensorMap* map = is_k ? &tm_k : &tm_v;
     const bool bitmap = p.key_valid == nullptr && p.geo.g <= 32 * RAGW;
     int kq = 0;
-    for (long long it = blockIdx.x;; it += gridDim.x) {
+    int claimed = 0;
+    for (;;) {
       PairItem itm;
-      if (!fetch_pair(p, it, items, itm)) break;
-      if (itm.na + itm.nb == 0) continue;
+      long long it;
+      if (is_k) {
+        // claim the next nonempty item; items without any kept key region
+        // are finished here (zero output rows) and never published
+        for (;;) {
+          long long c = 0;
+          if (lane == 0) c = atomicAdd(p.work, 1);
+          c = __shfl_sync(0xffffffffu, c, 0);
+          if (!fetch_pair(p, c, items, itm)) { it = items; break; }
+          if (itm.na + itm.nb > 0) { it = c; break; }
+          for (int e = lane; e < 2 * P * (D / 8); e += 32) {
+            const int tt = e / (P * (D / 8)), rr = (e / (D / 8)) % P, cc = e % (D / 8);
+            const int region = tt ? itm.b : itm.a;
+            const long long row = region < p.geo.g ? token_row(p, region, rr) : -1;
+            if (row >= 0)
+              reinterpret_cast<uint4*>(p.out + itm.h * p.oh + row * p.orow)[cc] = make_uint4(0, 0, 0, 0);
+          }
+        }
+        const int slot = claimed % IR;
+        if (claimed >= IR) mbar_wait(&B.item_empty[slot], (uint32_t)(((claimed / IR) - 1) & 1));
+        if (lane == 0) {
+          aux.items[slot] = (int)it;
+          mbar_arrive(&B.item_full[slot]);
+        }
+        ++claimed;
+        if (it >= items) break;
+      } else {
+        it = next_item();
+        if (!fetch_pair(p, it, items, itm)) break;
+      }
       const bool staged = is_k && itm.na + itm.nb <= LISTCAP;
       if (staged) {
         __syncwarp();  // lane 0 is done with the previous item's lists
@@ -451,8 +509,18 @@ __global__ void __launch_bounds__(384, 1)
           const uint8_t* tiles = is_k ? p.kt : p.vt;
           if (tiles != nullptr) {  // pre-tiled: one contiguous 16 KB bulk copy per key region
             const uint8_t* hb = tiles + (long long)itm.h * p.geo.g * TILE;
-            if (e.z & 1) bulk_g2s(st, hb + (long long)e.x * TILE, TILE, &full[s], p.pol_kv);
-            if (e.z & 2) bulk_g2s(st + TILE, hb + (long long)e.y * TILE, TILE, &full[s], p.pol_kv);
+            int jx = e.x, jy = e.y;
+            if (p.fake_load & 8) {  // diagnostics: an L2-resident 2 MB tile set (same bytes, all hits)
+              hb = tiles;
+              jx &= 63;
+              jy &= 63;
+            } else if (p.fake_load & 0x70) {  // diagnostics: per-head working set of 2^(bits 4-6 + 6) key regions
+              const int msk = (64 << ((p.fake_load >> 4) & 7)) - 1;
+              jx &= msk;
+              jy &= msk;
+            }
+            if (e.z & 1) bulk_g2s(st, hb + (long long)jx * TILE, TILE, &full[s], p.pol_kv);
+            if (e.z & 2) bulk_g2s(st + TILE, hb + (long long)jy * TILE, TILE, &full[s], p.pol_kv);
           } else {
             if (e.z & 1) {
               load_region(map, st, &full[s], p, itm.h, e.x, 0);
@@ -476,10 +544,9 @@ __global__ void __launch_bounds__(384, 1)
     int kidx = 0, sidx = 0, iidx = 0;
     uint32_t kph = 0, fph = 0;
     int qi = 0, kq = 0;
-    for (long long it = blockIdx.x;; it += gridDim.x) {
+    for (;;) {
       PairItem itm;
-      if (!fetch_pair(p, it, items, itm)) break;
-      if (itm.na + itm.nb == 0) continue;
+      if (!fetch_pair(p, next_item(), items, itm)) break;
       mbar_wait(&B.q_full, qi & 1);
       for (;;) {
         DA_WAITC(&B.k_full[kidx], kph);
@@ -526,10 +593,9 @@ __global__ void __launch_bounds__(384, 1)
     int vidx = 0, pidx = 0, iidx = 0;
     uint32_t vph = 0, pph = 0, iph = 0;
     int qi = 0, vq = 0;
-    for (long long it = blockIdx.x;; it += gridDim.x) {
+    for (;;) {
       PairItem itm;
-      if (!fetch_pair(p, it, items, itm)) break;
-      if (itm.na + itm.nb == 0) continue;
+      if (!fetch_pair(p, next_item(), items, itm)) break;
       for (;;) {
         DA_WAITC(&B.info_full[iidx], iph);
         const int4 e = aux.info[iidx];
@@ -632,21 +698,14 @@ __global__ void __launch_bounds__(384, 1)
     bool have_q = false;
     int cur_head = -1;
     float kmax = 0.f;
-    for (long long it = blockIdx.x;; it += gridDim.x) {
+    for (;;) {
       PairItem itm;
-      if (!fetch_pair(p, it, items, itm)) break;
+      if (!fetch_pair(p, next_item(), items, itm)) break;
       const int region = tile ? itm.b : itm.a;
       const bool region_ok = region < p.geo.g;
       const long long row = region_ok ? token_row(p, region, r) : -1;
       const bool tile_has_keys = (tile ? itm.nb : itm.na) > 0;
       __nv_bfloat16* orow = row >= 0 ? p.out + itm.h * p.oh + row * p.orow + wg * 64 : nullptr;
-      if (itm.na + itm.nb == 0) {
-        if (orow) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) reinterpret_cast<uint4*>(orow)[c] = make_uint4(0, 0, 0, 0);
-        }
-        continue;
-      }
       const int nsteps = max(itm.na, itm.nb);
       if (!have_q) load_q(itm, -1);  // first nonempty item of this CTA
       const float qn2_own = qn2_next;
@@ -751,13 +810,12 @@ __global__ void __launch_bounds__(384, 1)
       G += nsteps;
       // ---- next nonempty item's Q (its GEMM1s overlap this epilogue)
       have_q = false;
-      for (long long it2 = it + gridDim.x;; it2 += gridDim.x) {
+      {
         PairItem nx;
-        if (!fetch_pair(p, it2, items, nx)) break;
-        if (nx.na + nx.nb == 0) continue;
-        load_q(nx, qi & 1);  // q_empty completion #qi = this item's last GEMM1
-        have_q = true;
-        break;
+        if (fetch_pair(p, peek_item(0), items, nx)) {  // the ring holds nonempty items only
+          load_q(nx, qi & 1);  // q_empty completion #qi = this item's last GEMM1
+          have_q = true;
+        }
       }
       // ------------------------------ epilogue ------------------------------
       aux.lsum[wg][L] = l;
@@ -859,13 +917,13 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   char* ws = static_cast<char*>(a.workspace);
   p.fb_count = reinterpret_cast<int*>(ws);
   p.kpart = reinterpret_cast<float*>(ws + 256);
+  p.work = reinterpret_cast<int*>(ws + 4);
   p.fb_items = reinterpret_cast<int*>(ws + 256 + pair_align256(sizeof(float) * a.heads * pairk::KBLK));
   int2* pairs = reinterpret_cast<int2*>(reinterpret_cast<char*>(p.fb_items) +
                                         pair_align256(sizeof(int) * 4 * (size_t)a.heads * g.g));
   if (kpart != nullptr) {  // norms from the pooling pass; only the fallback counter needs clearing
     p.kpart = kpart;
     p.kblk = kblk;
-    cudaMemsetAsync(p.fb_count, 0, sizeof(int), st);
   } else {
     p.kblk = pairk::KBLK;
     const long long key_rows = a.layout == DA_LAYOUT_REORDERED ? g.n_pad : g.n_real;
@@ -906,6 +964,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
       p.vt = ta.out[1];
     }
   }
+  cudaMemsetAsync(ws, 0, 2 * sizeof(int), st);  // fallback counter, item counter
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;

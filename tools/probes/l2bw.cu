@@ -76,6 +76,95 @@ __global__ void __launch_bounds__(256) ldg_kernel(const int4* __restrict__ buf, 
   if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678) atomicAdd(sink, 1ull);
 }
 
+
+// cp.async (LDGSTS, 16 B per thread) of random 16 KB blocks into a smem ring,
+// NT threads per CTA, STAGES blocks in flight
+template <int STAGES, int NT>
+__global__ void __launch_bounds__(NT, 1) ldgsts_kernel(const uint8_t* __restrict__ buf, size_t nblocks, int iters,
+                                                      unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t x = blockIdx.x * 2654435761u + 999u;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
+  unsigned long long acc = 0;
+  auto issue = [&](int it) {
+    x = x * 1664525u + 1013904223u;
+    const size_t b = (x >> 8) % nblocks;
+    const uint8_t* src = buf + b * 16384;
+    const uint32_t dst = sb + (it % STAGES) * 16384;
+#pragma unroll
+    for (int j = 0; j < 16384 / 16 / NT; ++j) {
+      const int off = (threadIdx.x + j * NT) * 16;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + off), "l"(src + off) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int s = 0; s < STAGES - 1; ++s) issue(s);
+  for (int it = 0; it < iters; ++it) {
+    issue(it + STAGES - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 1) : "memory");
+    acc += smem[(it % STAGES) * 16384 + threadIdx.x * 16];
+  }
+  if (acc == 0x123456789ull) atomicAdd(sink, acc);
+}
+
+// mixed: warp 0 streams random 16 KB blocks with bulk copies (TMA engine),
+// warps 1..NW-1 with cp.async (LSU path), each into its own ring
+template <int NW>
+__global__ void __launch_bounds__(32 * NW, 1) mixed_kernel(const uint8_t* __restrict__ buf, size_t nblocks, int iters,
+                                                          unsigned long long* sink, int use_bulk) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[4];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  uint32_t x = blockIdx.x * 2654435761u + 31u * warp;
+  unsigned long long acc = 0;
+  if (warp == 0) {
+    if (!use_bulk) return;
+    if (lane == 0) {
+      for (int s = 0; s < 4; ++s) {
+        x = x * 1664525u + 1013904223u;
+        mbar_expect_tx(&bars[s], 16384);
+        bulk_g2s(smem + s * 16384, buf + ((x >> 8) % nblocks) * 16384, 16384, &bars[s]);
+      }
+      for (int it = 0; it < iters; ++it) {
+        const int s = it % 4;
+        mbar_wait(&bars[s], (it / 4) & 1);
+        acc += smem[s * 16384 + (it & 1023)];
+        if (it + 4 < iters) {
+          x = x * 1664525u + 1013904223u;
+          mbar_expect_tx(&bars[s], 16384);
+          bulk_g2s(smem + s * 16384, buf + ((x >> 8) % nblocks) * 16384, 16384, &bars[s]);
+        }
+      }
+    }
+  } else {
+    // each cp.async warp: its own 4-stage ring of 16 KB after the bulk ring
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem) + 4 * 16384 + (warp - 1) * 4 * 16384;
+    auto issue = [&](int it) {
+      x = x * 1664525u + 1013904223u;
+      const uint8_t* src = buf + ((x >> 8) % nblocks) * 16384;
+      const uint32_t dst = sb + (it % 4) * 16384;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const int off = (lane + j * 32) * 16;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + off), "l"(src + off) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int s = 0; s < 3; ++s) issue(s);
+    for (int it = 0; it < iters; ++it) {
+      issue(it + 3);
+      asm volatile("cp.async.wait_group 3;" ::: "memory");
+      acc += smem[4 * 16384 + (warp - 1) * 4 * 16384 + (it % 4) * 16384 + lane * 16];
+    }
+  }
+  if (acc == 0x123456789ull) atomicAdd(sink, acc);
+}
+
 int main() {
   int dev = 0;
   cudaDeviceProp prop;
@@ -112,6 +201,55 @@ int main() {
     run_bulk(l2bw_kernel<8, BLK>, 8, nb);
     run_bulk(l2bw_kernel<10, BLK>, 10, nb);
     run_bulk(l2bw_kernel<13, BLK>, 13, nb);
+  }
+
+  {
+    size_t nb = (size_t(64) << 20) / BLK;
+    auto run_ldgsts = [&](auto kern, int stages, int nt, const char* name) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, stages * BLK);
+      int grid = prop.multiProcessorCount;
+      int iters = 4000;
+      kern<<<grid, nt, stages * BLK>>>(buf, nb, 200, sink);
+      cudaEventRecord(e0);
+      kern<<<grid, nt, stages * BLK>>>(buf, nb, iters, sink);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double bytes = double(grid) * iters * BLK;
+      printf("ldgsts %s stages %2d threads %d 64 MB buf: %.1f GB/s err=%s\n", name, stages, nt, bytes / ms / 1e6,
+             cudaGetErrorString(cudaGetLastError()));
+    };
+    run_ldgsts(ldgsts_kernel<4, 128>, 4, 128, "");
+    run_ldgsts(ldgsts_kernel<8, 128>, 8, 128, "");
+    run_ldgsts(ldgsts_kernel<8, 256>, 8, 256, "");
+    run_ldgsts(ldgsts_kernel<12, 256>, 12, 256, "");
+    run_ldgsts(ldgsts_kernel<8, 64>, 8, 64, "");
+    run_ldgsts(ldgsts_kernel<8, 32>, 8, 32, "");
+  }
+
+  {
+    size_t nb = (size_t(64) << 20) / BLK;
+    auto run_mixed = [&](auto kern, int nw, int use_bulk) {
+      const int smem_bytes = (4 + 4 * (nw - 1)) * BLK;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+      int grid = prop.multiProcessorCount;
+      int iters = 2000;
+      kern<<<grid, 32 * nw, smem_bytes>>>(buf, nb, 100, sink, use_bulk);
+      cudaEventRecord(e0);
+      kern<<<grid, 32 * nw, smem_bytes>>>(buf, nb, iters, sink, use_bulk);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double bytes = double(grid) * iters * BLK * ((nw - 1) + use_bulk);
+      printf("mixed bulk=%d + %d cp.async warps: %.1f GB/s err=%s\n", use_bulk, nw - 1, bytes / ms / 1e6,
+             cudaGetErrorString(cudaGetLastError()));
+    };
+    run_mixed(mixed_kernel<2>, 2, 0);
+    run_mixed(mixed_kernel<2>, 2, 1);
+    run_mixed(mixed_kernel<3>, 3, 0);
+    run_mixed(mixed_kernel<3>, 3, 1);
   }
   constexpr int STAGES = 8;
   cudaFuncSetAttribute(l2bw_kernel<STAGES, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, STAGES * BLK);
