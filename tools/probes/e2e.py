@@ -8,10 +8,11 @@ from paper_2505_14708_b200 import api
 plan = da.pad_plan(33, 45, 80, 8, 8)
 H, n, d = 24, plan.num_valid, 128
 host = [torch.randn(H, n, d).to(torch.bfloat16).pin_memory() for _ in range(3)]
-for hg in (None, 1, 2, 4, 6, 24):
+out_host = torch.empty(H, n, d, dtype=torch.bfloat16).pin_memory()
+for hg in (None, 1, 2, 3, 4, 6, 8, 12):
     def once():
         return api._pipeline_host(host[0], host[1], host[2], plan, 0.9, da.head_dim_scale(d), "average", "logits",
-                                  True, False, "hnd", group_heads=hg)
+                                  True, False, "hnd", group_heads=hg, out=out_host, details=False)
     once(); once()
     ts = []
     for _ in range(4):
