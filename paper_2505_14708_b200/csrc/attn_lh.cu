@@ -1,0 +1,721 @@
+// K4 variant "lh" (DA_K4=lh): block-sparse FlashAttention forward with ONE
+// query region per item, two key regions per step (GEMM1 at N = 128), and the
+// two TMEM lane halves of the M = 64 tile used as an even / odd step pipeline.
+//
+// Same semantics as attn_pair.cu (reference sparse.py:88-166): per query
+// region, kept key regions in ascending order, padding keys masked, fixed
+// per-row softmax offset with the portable-kernel fallback for rows whose sum
+// underflows.
+//
+// Why: an M = 64 tcgen05.mma costs the cycles of an M = 128 one and an N = 64
+// one 44.7 cycles per K = 16 against 64 for N = 128 (tools/probes/mma_rate.cu).
+// With two key regions per step GEMM1 issues M = 64, N = 128 MMAs: 512 instead
+// of 614 tensor cycles per kept 64 x 64 block.
+//
+// Layout. Global step s of a CTA runs on TMEM lane half h = s & 1 (lanes
+// {0-15, 32-47, ...} or {16-31, 48-63, ...}); each half holds its own copy of
+// Q, its S buffer, its P buffer and its share of O:
+//     columns [0,64) Q   [64,192) S   [192,256) P   [256,384) O (items of even
+//     parity)   [384,512) O (odd items)
+// so consecutive steps never share S / P / O and each barrier has a single
+// waiter sequence. Softmax warpgroup h takes the steps of half h and reads its
+// 16 lanes per warp with the 16x32bx2 shapes: thread t < 16 holds key region
+// 2s of row t, thread t + 16 key region 2s + 1 of the same row
+// (tools/probes/tmem16x2.cu). O = O_half0 + O_half1 is summed in the epilogue.
+//
+// Shared memory: K and V ring slots of two region tiles each (a step); the
+// tiles are the pooling pass's GROUPED images (kv_tile_offset_grouped), so two
+// adjacent tiles form one 128-row K-major GEMM1 operand.
+//
+//     GEMM1  S[64 q x 128 k]  = Q . [K_j0 ; K_j1]^T   A = Q (TMEM), B = K slot (smem, K-major, SW128, SBO 2 KB)
+//     GEMM2  O[64 q x 128 d] += P . [V_j0 ; V_j1]     A = P (TMEM), B = V tiles (smem, MN-major, SW128)
+//
+// Roles (384 threads): warp 0 claims items (atomic counter), stages the kept
+// list, emits step info and issues K copies; warp 1 GEMM1 issuer + TMEM owner;
+// warp 2 V copies; warp 3 GEMM2 issuer; warps 4-7 / 8-11 softmax warpgroups
+// for lane half 0 / 1 (each also loads half of Q's features into both halves
+// and writes half of the output features).
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace da {
+namespace lhk {
+
+constexpr int P = 64;
+constexpr int D = 128;
+constexpr int TILE = 16384;
+constexpr int SLOT = 2 * TILE;  // a step: key regions j0, j1
+constexpr int KSL = 3;
+constexpr int VSL = 3;
+constexpr int INFO = 16;
+constexpr int RAGW = 512;
+constexpr int LISTCAP = 4096;
+constexpr int IR = 8;
+constexpr int KBLK = 32;
+
+constexpr int SMEM_K = 0;
+constexpr int SMEM_V = SMEM_K + KSL * SLOT;
+constexpr int SMEM_END = SMEM_V + VSL * SLOT;
+
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t COL_Q = 0, COL_S = 64, COL_P = 192, COL_O = 256;
+constexpr uint32_t LANE_H = 16u << 16;  // TMEM address offset of lane half 1
+
+struct Params {
+  const __nv_bfloat16* q;
+  long long qh, qr;
+  __nv_bfloat16* out;
+  long long oh, orow;
+  int heads;
+  int layout;
+  float scale_log2;
+  const int* row_ptr;
+  const int* col_idx;
+  long long cap;
+  const uint8_t* key_valid;
+  int mask_h;
+  Geo geo;
+  RegionDecoder dec;
+  FastDiv per_head;  // g
+  const uint8_t* kt;
+  const uint8_t* vt;
+  const int* order;  // [heads][g] query regions by kept count (descending), or null
+  const float* kpart;
+  int kblk;
+  int* fb_count;
+  int* fb_items;
+  int* work;
+  int fake_load;
+  uint64_t pol_kv, pol_q, pol_o;
+};
+
+struct __align__(8) Bars {
+  uint64_t k_full[KSL], k_empty[KSL];
+  uint64_t v_full[VSL], v_empty[VSL];
+  uint64_t s_full[2], s_free[2], p_full[2], p_free[2];  // per lane half
+  uint64_t o_full[2], o_empty[2];                        // per O buffer (item parity)
+  uint64_t q_full, q_empty;
+  uint64_t info_full[INFO];
+  uint64_t item_full[IR], item_empty[IR];
+};
+struct SmemAux {
+  Bars bars;
+  int4 info[INFO];      // per step: j0, j1, flags (1 j0, 2 j1, 4 j0 ragged, 8 j1 ragged), w (1 last, 2 first)
+  int items[IR];
+  uint32_t tmem_base;
+  float xm[2][64];      // [item parity][row] fixed softmax offset
+  float xq[2][2][64];   // [item parity][warpgroup][row] partial |q|^2
+  float lsum[2][64];    // [warpgroup][row] partial row sums
+  int had[2][64];       // [warpgroup][row] saw a kept valid key
+  uint32_t ragged[RAGW];
+  int list[LISTCAP];
+};
+constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
+static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
+
+struct Item {
+  int h, i;
+  const int* list;
+  int n;
+};
+
+DA_DEV bool fetch_item(const Params& p, long long it, long long items, Item& o) {
+  if (it < 0 || it >= items) return false;
+  const int g = p.geo.g;
+  const int h = (int)fdiv((uint32_t)it, p.per_head);
+  const int k = (int)(it - (long long)h * g);
+  o.h = h;
+  o.i = p.order != nullptr ? __ldg(p.order + it) : k;
+  const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
+  const int b = rp[o.i];
+  o.list = p.col_idx + (long long)(h * p.mask_h) * p.cap + b;
+  o.n = rp[o.i + 1] - b;
+  return true;
+}
+
+DA_DEV long long token_row(const Params& p, int region, int r) {
+  if (p.layout == DA_LAYOUT_REORDERED) return (long long)region * P + r;
+  const RegionXY rc = p.dec(region);
+  const int u = r / p.geo.pw, v = r - u * p.geo.pw;
+  const int y = rc.y0 + u, x = rc.x0 + v;
+  if (y >= p.geo.H || x >= p.geo.W) return -1;
+  return ((long long)rc.f * p.geo.H + y) * p.geo.W + x;
+}
+
+DA_DEV unsigned long long key_mask(const Params& p, int j) {
+  if (p.key_valid != nullptr) {
+    const uint8_t* kv = p.key_valid + (long long)j * P;
+    unsigned long long m = 0;
+#pragma unroll 8
+    for (int r = 0; r < P; ++r) m |= (unsigned long long)(kv[r] != 0) << r;
+    return m;
+  }
+  const RegionXY rc = p.dec(j);
+  const int vy = min(p.geo.ph, p.geo.H - rc.y0), vx = min(p.geo.pw, p.geo.W - rc.x0);
+  if (vy == p.geo.ph && vx == p.geo.pw) return ~0ull;
+  const unsigned long long rowm = (1ull << vx) - 1ull;
+  unsigned long long m = 0;
+  for (int u = 0; u < vy; ++u) m |= rowm << (u * p.geo.pw);
+  return m;
+}
+
+// Per head: query regions by kept count, descending (ties by index): the
+// dynamic item order puts the heaviest items first. One block per head.
+__global__ void __launch_bounds__(1024) region_order_kernel(const int* __restrict__ row_ptr, int g, int mask_h,
+                                                            int* __restrict__ order) {
+  extern __shared__ int bins[];  // [g + 1]
+  const int h = blockIdx.x;
+  const int* rp = row_ptr + (long long)(h * mask_h) * (g + 1);
+  for (int i = threadIdx.x; i <= g; i += blockDim.x) bins[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < g; i += blockDim.x) atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int c = 0; c <= g; ++c) {
+      const int v = bins[c];
+      bins[c] = run;
+      run += v;
+    }
+    for (int i = 0; i < g; ++i) order[(long long)h * g + bins[g - min(g, rp[i + 1] - rp[i])]++] = i;
+  }
+}
+
+__global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  SmemAux& aux = *reinterpret_cast<SmemAux*>(smem + SMEM_END);
+  Bars& B = aux.bars;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long items = (long long)p.heads * p.geo.g;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < KSL; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
+    for (int s = 0; s < VSL; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&B.s_full[h], 1);
+      mbar_init(&B.s_free[h], 128);
+      mbar_init(&B.p_full[h], 128);
+      mbar_init(&B.p_free[h], 1);
+      mbar_init(&B.o_full[h], 1);
+      mbar_init(&B.o_empty[h], 256);
+    }
+    mbar_init(&B.q_full, 256);
+    mbar_init(&B.q_empty, 1);
+    for (int s = 0; s < INFO; ++s) mbar_init(&B.info_full[s], 1);
+    for (int s = 0; s < IR; ++s) {
+      mbar_init(&B.item_full[s], 1);
+      mbar_init(&B.item_empty[s], 11);  // warps 1, 2, 3 and the 8 softmax warps
+    }
+    fence_barrier_init();
+  }
+  if (p.fake_load) {
+    for (int i = threadIdx.x; i < SMEM_END / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
+  if (p.key_valid == nullptr && p.geo.g <= 32 * RAGW) {
+    for (int wd = threadIdx.x; wd < (p.geo.g + 31) / 32; wd += blockDim.x) {
+      uint32_t bits = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int j = wd * 32 + b;
+        if (j < p.geo.g && key_mask(p, j) != ~0ull) bits |= 1u << b;
+      }
+      aux.ragged[wd] = bits;
+    }
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(&aux.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = aux.tmem_base;
+  uint8_t* sK = smem + SMEM_K;
+  uint8_t* sV = smem + SMEM_V;
+
+  int ring_i = 0;
+  uint32_t ring_ph = 0;
+  auto peek_item = [&]() {
+    mbar_wait_spin(&B.item_full[ring_i], ring_ph);
+    return (long long)aux.items[ring_i];
+  };
+  auto next_item = [&]() {
+    const long long it = peek_item();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&B.item_empty[ring_i]);
+    if (++ring_i == IR) { ring_i = 0; ring_ph ^= 1u; }
+    return it;
+  };
+
+  if (warp == 0 || warp == 2) {
+    // ===================== producers (warp 0: items, step info, K; warp 2: V) =====================
+    const bool is_k = warp == 0;
+    const int NSL = is_k ? KSL : VSL;
+    uint8_t* ring = is_k ? sK : sV;
+    uint64_t* full = is_k ? B.k_full : B.v_full;
+    uint64_t* empty = is_k ? B.k_empty : B.v_empty;
+    const bool bitmap = p.key_valid == nullptr && p.geo.g <= 32 * RAGW;
+    int kq = 0, claimed = 0;
+    long long next_claim = 0;
+    if (is_k && lane == 0) next_claim = atomicAdd(p.work, 1);
+    for (;;) {
+      Item itm;
+      long long it;
+      if (is_k) {
+        for (;;) {
+          long long c = 0;
+          if (lane == 0) {
+            c = next_claim;
+            next_claim = atomicAdd(p.work, 1);
+          }
+          c = __shfl_sync(0xffffffffu, c, 0);
+          if (!fetch_item(p, c, items, itm)) { it = items; break; }
+          if (itm.n > 0) { it = c; break; }
+          // no kept key region: the region's output rows are zero
+          for (int e = lane; e < P * (D / 8); e += 32) {
+            const long long row = token_row(p, itm.i, e / (D / 8));
+            if (row >= 0) reinterpret_cast<uint4*>(p.out + itm.h * p.oh + row * p.orow)[e % (D / 8)] = make_uint4(0, 0, 0, 0);
+          }
+        }
+        const int slot = claimed % IR;
+        if (claimed >= IR) mbar_wait(&B.item_empty[slot], (uint32_t)(((claimed / IR) - 1) & 1));
+        if (lane == 0) {
+          aux.items[slot] = (int)it;
+          mbar_arrive(&B.item_full[slot]);
+        }
+        ++claimed;
+        if (it >= items) break;
+      } else {
+        it = next_item();
+        if (!fetch_item(p, it, items, itm)) break;
+      }
+      const bool staged = is_k && itm.n <= LISTCAP;
+      if (staged) {
+        __syncwarp();
+        for (int e = lane; e < itm.n; e += 32) aux.list[e] = __ldg(itm.list + e);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        const int n = (itm.n + 1) / 2;
+        const uint8_t* hb = (is_k ? p.kt : p.vt) + (long long)itm.h * p.geo.g * TILE;
+        for (int t = 0; t < n; ++t) {
+          int4 e;
+          const int ii = kq % INFO;
+          if (is_k) {
+            const int j0 = staged ? aux.list[2 * t] : __ldg(itm.list + 2 * t);
+            const int j1 = 2 * t + 1 < itm.n ? (staged ? aux.list[2 * t + 1] : __ldg(itm.list + 2 * t + 1)) : -1;
+            int fl = 1;
+            if (bitmap ? (aux.ragged[j0 >> 5] >> (j0 & 31)) & 1 : key_mask(p, j0) != ~0ull) fl |= 4;
+            if (j1 >= 0) {
+              fl |= 2;
+              if (bitmap ? (aux.ragged[j1 >> 5] >> (j1 & 31)) & 1 : key_mask(p, j1) != ~0ull) fl |= 8;
+            }
+            e = make_int4(j0, j1, fl, (t == n - 1 ? 1 : 0) | (t == 0 ? 2 : 0));
+            aux.info[ii] = e;
+            mbar_arrive(&B.info_full[ii]);
+          } else {
+            mbar_wait(&B.info_full[ii], (uint32_t)((kq / INFO) & 1));
+            e = aux.info[ii];
+          }
+          const int s = kq % NSL;
+          if (kq >= NSL) mbar_wait(&empty[s], ((kq / NSL) - 1) & 1);
+          ++kq;
+          if (p.fake_load & (is_k ? 1 : 2)) {
+            mbar_arrive(&full[s]);
+            continue;
+          }
+          uint8_t* st = ring + s * SLOT;
+          mbar_expect_tx(&full[s], TILE * (1 + ((e.z >> 1) & 1)));
+          bulk_g2s(st, hb + (long long)e.x * TILE, TILE, &full[s], p.pol_kv);
+          if (e.z & 2) bulk_g2s(st + TILE, hb + (long long)e.y * TILE, TILE, &full[s], p.pol_kv);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ========================= GEMM1 issuer =========================
+    constexpr uint32_t IDESC_N128 = umma_idesc_bf16(64, 128, 0, 0);
+    constexpr uint32_t IDESC_N64 = umma_idesc_bf16(64, 64, 0, 0);
+    const uint64_t dK = umma_desc_sw128(0, 16, 2048) + (smem_u32(sK) >> 4);
+    int gs = 0, iidx = 0;
+    uint32_t iph = 0;
+    int qi = 0;
+    for (;;) {
+      Item itm;
+      if (!fetch_item(p, next_item(), items, itm)) break;
+      mbar_wait(&B.q_full, qi & 1);
+      for (;;) {
+        mbar_wait_spin(&B.info_full[iidx], iph);
+        const int4 e = aux.info[iidx];
+        const int last = e.w & 1;
+        const int h = gs & 1;
+        // this half's S buffer: the softmax has loaded step gs - 2
+        if (gs >= 2) mbar_wait_spin(&B.s_free[h], (uint32_t)(((gs >> 1) - 1) & 1));
+        const int s = gs % KSL;
+        mbar_wait_spin(&B.k_full[s], (uint32_t)((gs / KSL) & 1));
+        tc_fence_after();
+        if (elect_one_sync()) {
+          const uint32_t lo = h ? LANE_H : 0u;
+          const uint32_t idesc = (e.z & 2) ? IDESC_N128 : IDESC_N64;
+          const uint64_t bk = dK + (uint64_t)(s * (SLOT >> 4));
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ts(tmem + lo + COL_S, tmem + lo + COL_Q + kk * 8,
+                         bk + (uint64_t)((kk >> 2) * (1024 >> 4) + (kk & 3) * 2), idesc, kk > 0 ? 1u : 0u);
+          umma_commit(&B.k_empty[s]);
+          umma_commit(&B.s_full[h]);
+          if (last) umma_commit(&B.q_empty);
+        }
+        __syncwarp();
+        ++gs;
+        if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
+        if (last) break;
+      }
+      ++qi;
+    }
+  } else if (warp == 3) {
+    // ========================= GEMM2 issuer =========================
+    constexpr uint32_t IDESC2 = umma_idesc_bf16(64, 128, 0, 1);  // B (V) MN-major
+    const uint64_t dV = umma_desc_sw128(0, 1024, 2048) + (smem_u32(sV) >> 4);
+    int gs = 0, iidx = 0;
+    uint32_t iph = 0;
+    int qi = 0;
+    for (;;) {
+      Item itm;
+      if (!fetch_item(p, next_item(), items, itm)) break;
+      const int ob = qi & 1;
+      int t = 0;
+      for (;;) {
+        mbar_wait_spin(&B.info_full[iidx], iph);
+        const int4 e = aux.info[iidx];
+        const int last = e.w & 1;
+        const int h = gs & 1;
+        const int s = gs % VSL;
+        mbar_wait_spin(&B.v_full[s], (uint32_t)((gs / VSL) & 1));
+        mbar_wait_spin(&B.p_full[h], (uint32_t)((gs >> 1) & 1));
+        if (t == 0 && qi >= 2) mbar_wait(&B.o_empty[ob], (uint32_t)(((qi >> 1) - 1) & 1));
+        tc_fence_after();
+        if (elect_one_sync()) {
+          const uint32_t lo = h ? LANE_H : 0u;
+          const uint64_t bv = dV + (uint64_t)(s * (SLOT >> 4));
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            if (c == 1 && !(e.z & 2)) break;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16_ts(tmem + lo + COL_O + 128 * ob, tmem + lo + COL_P + 32 * c + 8 * kk,
+                           bv + (uint64_t)((c * TILE + kk * 4096) >> 4), IDESC2,
+                           (t < 2 && c == 0 && kk == 0) ? 0u : 1u);
+          }
+          umma_commit(&B.v_empty[s]);
+          umma_commit(&B.p_free[h]);
+          if (last) umma_commit(&B.o_full[ob]);
+        }
+        __syncwarp();
+        ++gs;
+        ++t;
+        if (++iidx == INFO) { iidx = 0; iph ^= 1u; }
+        if (last) break;
+      }
+      ++qi;
+    }
+  } else if (warp >= 4) {
+    // ============ softmax warpgroup wg = lane half wg; Q loader; epilogue ============
+    // Warp w (subpartition sp = w % 4) owns rows 16 sp .. 16 sp + 15: lanes
+    // 32 sp + [0,16) of half 0 and 32 sp + 16 + [0,16) of half 1. In a step
+    // thread lane (< 16 / >= 16) processes key region j0 / j1 of row
+    // 16 sp + lane % 16.
+    const int wg = (warp - 4) >> 2;
+    const int sp = warp & 3;
+    const int c = lane >> 4;            // chunk: key region j0 (0) or j1 (1) of a step
+    const int r = 16 * sp + (lane & 15);
+    const uint32_t tl = tmem + ((uint32_t)(sp * 32) << 16);    // 32x32b lane base (epilogue, Q)
+    const uint32_t th = tl + (wg ? LANE_H : 0u);               // this warpgroup's half (16x32bx2)
+    const float sl2 = p.scale_log2;
+    int G = 0;   // global step index of the current item's first step
+    int qi = 0;
+    float qn2_next = 0.f;
+    // Q row r, feature half wg, into BOTH lane halves of columns [32 wg, 32 wg + 32)
+    // (lane < 16 writes half 0, lane >= 16 half 1: the same row)
+    auto load_q = [&](const Item& itm, int wait_parity) {
+      const long long qrow = token_row(p, itm.i, r);
+      uint32_t qv[32];
+      if (qrow >= 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + qrow * p.qr) + wg * 8;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint4 w = ldg128_hint(src + k, p.pol_q);
+          qv[4 * k] = w.x; qv[4 * k + 1] = w.y; qv[4 * k + 2] = w.z; qv[4 * k + 3] = w.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) qv[k] = 0u;
+      }
+      float s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qv[k]));
+        s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+      }
+      qn2_next = s2;
+      if (wait_parity >= 0) mbar_wait(&B.q_empty, (uint32_t)wait_parity);
+      tc_fence_after();
+      tmem_st16u(tl + COL_Q + wg * 32, *reinterpret_cast<uint32_t(*)[16]>(&qv[0]));
+      tmem_st16u(tl + COL_Q + wg * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&qv[16]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&B.q_full);
+    };
+    bool have_q = false;
+    int cur_head = -1;
+    float kmax = 0.f;
+    for (;;) {
+      Item itm;
+      if (!fetch_item(p, next_item(), items, itm)) break;
+      const long long row = token_row(p, itm.i, r);
+      const int nsteps = (itm.n + 1) / 2;
+      const int ob = qi & 1;
+      if (!have_q) load_q(itm, -1);
+      const float qn2_own = qn2_next;
+      if (itm.h != cur_head) {
+        cur_head = itm.h;
+        const float* kp = p.kpart + (long long)itm.h * p.kblk;
+        float mx = 0.f;
+#pragma unroll 8
+        for (int k = 0; k < p.kblk; ++k) mx = fmaxf(mx, __ldg(kp + k));
+        kmax = mx;
+      }
+      if (lane < 16) aux.xq[qi & 1][wg][r] = qn2_own;
+      bar_sync(1, 256);
+      const float qn2 = aux.xq[qi & 1][0][r] + aux.xq[qi & 1][1][r];
+      const int first_wg = G & 1;  // the warpgroup that runs the item's first step fixes the offsets
+      float m = 0.f, l = 0.f;
+      bool had = false;
+      bool got_m = false;
+      float x[64];
+      for (int t = (wg - first_wg) & 1; t < nsteps; t += 2) {
+        const int gs = G + t;
+        const int ii = gs & (INFO - 1);
+        mbar_wait_spin(&B.info_full[ii], (uint32_t)((gs / INFO) & 1));
+        const int4 e = aux.info[ii];
+        mbar_wait_spin(&B.s_full[wg], (uint32_t)((gs >> 1) & 1));
+        tc_fence_after();
+        const bool kp = ((e.z >> c) & 1) && !(p.fake_load & 4);
+        if (!(p.fake_load & 4)) {
+          tmem_ld16x2_32(th + COL_S, x);
+          tmem_ld16x2_32hi(th + COL_S + 32, x);
+          tmem_ld_wait();
+        }
+        tc_fence_before();
+        mbar_arrive(&B.s_free[wg]);  // scores in registers: GEMM1 may refill this half
+        if (!(p.fake_load & 4)) {
+          const int j = c ? e.y : e.x;
+          const bool rag = (e.z >> (2 + c)) & 1;
+          const unsigned long long vm = kp ? (rag ? key_mask(p, j) : ~0ull) : 0ull;
+          if (vm != ~0ull) {
+#pragma unroll
+            for (int k = 0; k < 64; ++k) x[k] = ((vm >> k) & 1ull) ? x[k] : -INFINITY;
+          }
+          had |= vm != 0ull;
+        }
+        if (!got_m) {
+          if (t == 0) {  // first step of the item: fix the row's offset from its two key regions
+            float bm = -INFINITY;
+            if (kp) {
+              float mx[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                mx[q] = fmaxf(fmaxf(fmaxf(x[q], x[q + 8]), fmaxf(x[q + 16], x[q + 24])),
+                              fmaxf(fmaxf(x[q + 32], x[q + 40]), fmaxf(x[q + 48], x[q + 56])));
+              bm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            }
+            bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16)) * sl2;
+            const float bound = sqrtf(qn2) * kmax * sl2 * 1.0001f;
+            m = fmaxf(bm, bound - 64.f);
+            if (lane < 16) aux.xm[qi & 1][r] = m;
+            bar_arrive(2, 256);
+          } else {
+            bar_sync(2, 256);
+            m = aux.xm[qi & 1][r];
+          }
+          got_m = true;
+        }
+        uint32_t pk[32];
+        {
+          const float2 sc = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < 64; k += 2) {
+            const float2 ev = ffma2(make_float2(x[k], x[k + 1]), sc, nm);
+            const float2 pe = (k % 8 == 6) ? exp2_poly2(ev) : make_float2(fast_exp2(ev.x), fast_exp2(ev.y));
+            acc = fadd2(acc, pe);
+            pk[k / 2] = kp ? pack_bf16(pe.x, pe.y) : 0u;
+          }
+          if (kp) l += acc.x + acc.y;
+        }
+        // this half's P buffer: GEMM2 of step gs - 2 has read it
+        if (gs >= 2) {
+          mbar_wait_spin(&B.p_free[wg], (uint32_t)(((gs >> 1) - 1) & 1));
+          tc_fence_after();
+        }
+        tmem_st16x2_16(th + COL_P, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        tmem_st16x2_16(th + COL_P + 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[16]));
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&B.p_full[wg]);
+      }
+      if (!got_m) {  // this warpgroup had no step: still take part in the offset hand-off
+        if (first_wg == wg) bar_arrive(2, 256);
+        else bar_sync(2, 256);
+      }
+      G += nsteps;
+      // ---- next item's Q
+      have_q = false;
+      {
+        Item nx;
+        if (fetch_item(p, peek_item(), items, nx)) {
+          load_q(nx, qi & 1);
+          have_q = true;
+        }
+      }
+      // ------------------------------ epilogue ------------------------------
+      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      had = __shfl_xor_sync(0xffffffffu, had ? 1 : 0, 16) != 0 || had;
+      if (lane < 16) {
+        aux.lsum[wg][r] = l;
+        aux.had[wg][r] = had ? 1 : 0;
+      }
+      bar_sync(1, 256);
+      const float lt = aux.lsum[0][r] + aux.lsum[1][r];
+      const bool bad = (aux.had[0][r] || aux.had[1][r]) && !(lt >= 0x1p-80f);
+      mbar_wait(&B.o_full[ob], (uint32_t)((qi >> 1) & 1));
+      tc_fence_after();
+      // lane < 16 reads O of half 0, lane >= 16 O of half 1 (same row); a half
+      // without any step of this item holds no O for it
+      const int myhalf = lane >> 4;
+      const bool used = nsteps >= 2 || (G - nsteps + 0) % 2 == myhalf;
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      float o[64];
+      tmem_ld32_at<0>(tl + COL_O + 128 * ob + wg * 64, o);
+      tmem_ld32_at<32>(tl + COL_O + 128 * ob + wg * 64 + 32, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&B.o_empty[ob]);
+      uint32_t w[16];
+#pragma unroll
+      for (int k = 0; k < 32; k += 2) {
+        // lane < 16 writes features wg*64 + [0,32), lane >= 16 wg*64 + [32,64)
+        float a0 = used ? (myhalf ? o[32 + k] : o[k]) : 0.f;
+        float a1 = used ? (myhalf ? o[33 + k] : o[k + 1]) : 0.f;
+        const float s0 = used ? (myhalf ? o[k] : o[32 + k]) : 0.f;
+        const float s1 = used ? (myhalf ? o[k + 1] : o[33 + k]) : 0.f;
+        a0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+        a1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+        w[k / 2] = pack_bf16(a0 * inv, a1 * inv);
+      }
+      if (row >= 0) {
+        uint4* dst = reinterpret_cast<uint4*>(p.out + itm.h * p.oh + row * p.orow + wg * 64 + myhalf * 32);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          stg128_hint(dst + k, make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]), p.pol_o);
+      }
+      if (wg == 0) {  // one push per warp with a bad row; duplicates are harmless
+        const unsigned bal = __ballot_sync(0xffffffffu, bad && row >= 0 && lane < 16);
+        if (bal != 0u && lane == 0) {
+          const int slot = atomicAdd(p.fb_count, 1);
+          p.fb_items[slot] = itm.h * p.geo.g + itm.i;
+        }
+      }
+      ++qi;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<TMEM_COLS>(tmem);
+  }
+}
+
+}  // namespace lhk
+
+cudaError_t launch_lh_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why, long long* trace,
+                           const float* kpart, int kblk, bool tiles_ready) {
+  (void)why;
+  (void)trace;
+  lhk::Params p;
+  p.q = static_cast<const __nv_bfloat16*>(a.q);
+  p.qh = a.q_head_stride;
+  p.qr = a.q_row_stride;
+  p.out = static_cast<__nv_bfloat16*>(a.out);
+  p.oh = a.o_head_stride;
+  p.orow = a.o_row_stride;
+  p.heads = a.heads;
+  p.layout = a.layout;
+  p.scale_log2 = (float)(a.scale * 1.4426950408889634);
+  p.row_ptr = a.row_ptr;
+  p.col_idx = a.col_idx;
+  p.cap = a.mask_cap;
+  p.key_valid = a.key_valid;
+  p.mask_h = a.shared_mask ? 0 : 1;
+  p.geo = g;
+  p.dec = make_decoder(g);
+  p.per_head = make_fastdiv((uint32_t)g.g);
+  p.pol_kv = L2_EVICT_NORMAL;
+  p.pol_q = L2_EVICT_NORMAL;
+  p.pol_o = L2_EVICT_NORMAL;
+  {
+    static int fk = -1;
+    if (fk < 0) {
+      const char* env = getenv("DA_FAKELOAD");
+      fk = env ? atoi(env) : 0;
+    }
+    p.fake_load = fk;
+  }
+  // workspace: the pair kernel's layout (counters | key norm maxima | fallback
+  // items | plan | tiles); the region order fits in the pair plan's space
+  char* ws = static_cast<char*>(a.workspace);
+  p.fb_count = reinterpret_cast<int*>(ws);
+  p.work = reinterpret_cast<int*>(ws + 4);
+  const size_t kb = (sizeof(float) * a.heads * lhk::KBLK + 255) & ~(size_t)255;
+  p.fb_items = reinterpret_cast<int*>(ws + 256 + kb);
+  int* order = reinterpret_cast<int*>(reinterpret_cast<char*>(p.fb_items) +
+                                      ((sizeof(int) * 4 * (size_t)a.heads * g.g + 255) & ~(size_t)255));
+  // the block-sparse seam (no pooling pass, so no key norms / tiles): pair kernel
+  if (kpart == nullptr) return launch_pair_attn(a, g, st, why, trace, kpart, kblk, tiles_ready);
+  p.kpart = kpart;
+  p.kblk = kblk;
+  {
+    const size_t smem = sizeof(int) * ((size_t)g.g + 1);
+    if (smem <= 200 * 1024) {
+      cudaFuncSetAttribute(lhk::region_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      lhk::region_order_kernel<<<a.heads, 1024, smem, st>>>(a.row_ptr, g.g, a.shared_mask ? 0 : 1, order);
+      p.order = order;
+    } else {
+      p.order = nullptr;
+    }
+  }
+  if (!tiles_ready) {
+    cudaError_t e = launch_kv_tiles(a, g, st, 1);
+    if (e != cudaSuccess) return e;
+  }
+  p.kt = pair_attn_tiles(a.workspace, a.heads, g, 0);
+  p.vt = pair_attn_tiles(a.workspace, a.heads, g, 1);
+  cudaMemsetAsync(ws, 0, 2 * sizeof(int), st);
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  cudaError_t e = cudaFuncSetAttribute(lhk::sparse_attn_lh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       lhk::SMEM_ALLOC);
+  if (e != cudaSuccess) return e;
+  const long long items = (long long)a.heads * g.g;
+  const int grid = (int)(items < num_sms ? items : num_sms);
+  lhk::sparse_attn_lh_kernel<<<grid, 384, lhk::SMEM_ALLOC, st>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * num_sms);
+}
+
+}  // namespace da

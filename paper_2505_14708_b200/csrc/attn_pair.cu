@@ -277,6 +277,7 @@ struct KvTileArgs {
   long long hs[2], rs[2];
   uint8_t* out[2];
   int layout;
+  int grouped;  // tile layout (kv_tile_offset_grouped vs kv_tile_offset_halves)
 };
 __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, RegionDecoder dec) {
   const int j = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
@@ -296,8 +297,8 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
       row = (rc.y0 + u < g.H && rc.x0 + v < g.W) ? ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v : -1;
     }
     const uint4 val = row >= 0 ? __ldg(src + row * rs8 + c) : make_uint4(0, 0, 0, 0);
-    const int hf = c >> 3, cc = c & 7;
-    *reinterpret_cast<uint4*>(dst + hf * BOX + r * 128 + ((cc ^ (r & 7)) << 4)) = val;
+    const uint32_t off = a.grouped ? kv_tile_offset_grouped(r, c >> 3, c & 7) : kv_tile_offset_halves(r, c >> 3, c & 7);
+    *reinterpret_cast<uint4*>(dst + off) = val;
   }
 }
 
@@ -973,6 +974,7 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
       ta.out[0] = tiles;
       ta.out[1] = tiles + (size_t)a.heads * g.g * pairk::TILE;
       ta.layout = a.layout;
+      ta.grouped = 0;
       if (!tiles_ready) pairk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
       p.kt = ta.out[0];
       p.vt = ta.out[1];
@@ -994,6 +996,22 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // rows whose fixed softmax offset underflowed: redo their regions exactly
   return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * num_sms);
+}
+
+// K / V region tiles for either K4 kernel (grouped = the lane-half layout)
+cudaError_t launch_kv_tiles(const da_attn_args& a, const Geo& g, cudaStream_t st, int grouped) {
+  uint8_t* tiles = pair_attn_tiles(a.workspace, a.heads, g, 0);
+  pairk::KvTileArgs ta;
+  ta.x[0] = static_cast<const __nv_bfloat16*>(a.k);
+  ta.x[1] = static_cast<const __nv_bfloat16*>(a.v);
+  ta.hs[0] = a.k_head_stride; ta.hs[1] = a.v_head_stride;
+  ta.rs[0] = a.k_row_stride; ta.rs[1] = a.v_row_stride;
+  ta.out[0] = tiles;
+  ta.out[1] = tiles + (size_t)a.heads * g.g * pairk::TILE;
+  ta.layout = a.layout;
+  ta.grouped = grouped;
+  pairk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, make_decoder(g));
+  return cudaGetLastError();
 }
 
 uint8_t* pair_attn_tiles(void* ws, int heads, const Geo& g, int which) {

@@ -691,14 +691,22 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
 
 // Default: region-pair kernel (attn_pair.cu). DA_K4=transposed selects the
 // single-region transposed kernel below (kept for A/B measurements).
-cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                           const float* kpart, int kblk, bool tiles_ready) {
+// K4 variant: 0 pair kernel (default), 1 transposed (DA_K4=transposed), 2 lane-half (DA_K4=lh)
+static int k4_variant() {
   static int variant = -1;
   if (variant < 0) {
     const char* env = getenv("DA_K4");
-    variant = (env && strcmp(env, "transposed") == 0) ? 1 : 0;
+    variant = (env && strcmp(env, "transposed") == 0) ? 1 : (env && strcmp(env, "lh") == 0) ? 2 : 0;
   }
+  return variant;
+}
+bool attn_tiles_grouped() { return k4_variant() == 2; }
+
+cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
+                           const float* kpart, int kblk, bool tiles_ready) {
+  const int variant = k4_variant();
   if (variant == 0) return launch_pair_attn(a, g, st, why, g_trace, kpart, kblk, tiles_ready);
+  if (variant == 2) return launch_lh_attn(a, g, st, why, g_trace, kpart, kblk, tiles_ready);
   CUtensorMap mq, mk, mv;
   bool ok;
   if (a.layout == DA_LAYOUT_REORDERED) {

@@ -257,6 +257,18 @@ DA_DEV void sts128(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t 
 // ---------------------------------------------------------------------------
 // tcgen05 / UMMA
 // ---------------------------------------------------------------------------
+// Byte offset of (row r, feature half h, 16-byte chunk c of the half) in a
+// 64 x 128 bf16 key/value region tile in the GROUPED layout: [8-row group]
+// [half][8 rows x 128 B] with the 128-byte swizzle. Group stride 2048 B, so
+// two tiles 16 KB apart read as one 128-row MMA operand (N = 128 GEMM1 of
+// the lane-half kernel); the halves sit 1 KB apart.
+DA_DEV uint32_t kv_tile_offset_grouped(int r, int h, int c) {
+  return (uint32_t)((((r >> 3) * 2 + h) << 10) + ((r & 7) << 7) + (((c ^ r) & 7) << 4));
+}
+// The same in the HALF-MAJOR layout of the pair kernel: [half][64 rows x 128 B].
+DA_DEV uint32_t kv_tile_offset_halves(int r, int h, int c) {
+  return (uint32_t)((h << 13) + (r << 7) + (((c ^ r) & 7) << 4));
+}
 // Shared-memory matrix descriptor (SM100 "version 1"), SWIZZLE_128B.
 //   start address >> 4 in [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46),
 //   version 1 at bit 46, layout type SWIZZLE_128B (2) in [61,64).
@@ -387,6 +399,42 @@ DA_DEV void tmem_ld32_at(uint32_t taddr, float (&v)[N]) {
       : "r"(taddr));
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[OFF + i] = __uint_as_float(r[i]);
+}
+// 16x32bx2 shapes (tools/probes/tmem16x2.cu): threads 0-15 access TMEM lanes
+// base + t at columns [c, c + N), threads 16-31 lanes base + t - 16 at columns
+// [c + split, c + split + N). Used on M = 64 tiles, whose 64 rows occupy 16
+// lanes of each warp's 32-lane slice.
+DA_DEV void tmem_ld16x2_32(uint32_t taddr, float (&v)[64]) {  // split 64: 32 columns -> v[0..31]
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 64;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+DA_DEV void tmem_ld16x2_32hi(uint32_t taddr, float (&v)[64]) {  // split 64: 32 columns -> v[32..63]
+  uint32_t* r = reinterpret_cast<uint32_t*>(v) + 32;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 64;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+DA_DEV void tmem_st16x2_16(uint32_t taddr, const uint32_t (&r)[16]) {  // split 32: 16 columns
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], 32, "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
 }
 DA_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 DA_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }

@@ -26,6 +26,9 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
                          float* kpart, const void* x2 = nullptr, long long hs2 = 0, long long rs2 = 0,
                          uint8_t* ktile = nullptr, uint8_t* vtile = nullptr);
 // K / V tile buffers inside the attention workspace ([heads][g][16 KB] each)
+// and their layout: grouped (kv_tile_offset_grouped) for the lane-half K4
+// (DA_K4=lh), half-major (kv_tile_offset_halves) for the pair kernel
+bool attn_tiles_grouped();
 uint8_t* pair_attn_tiles(void* ws, int heads, const Geo& g, int which);
 int pool_norm_blocks(int d, const Geo& g);
 // hist0 (optional): per-head 2048-bin histogram of the top 11 key bits, filled in the epilogue
@@ -56,6 +59,11 @@ cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaS
 cudaError_t launch_portable_list(const da_attn_args& args, const Geo& geo, cudaStream_t st, const int* items,
                                  const int* count, int blocks);
 size_t pair_attn_workspace_size(int heads, const Geo& g);
+cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
+                             long long* trace, const float* kpart, int kblk, bool tiles_ready);
+cudaError_t launch_kv_tiles(const da_attn_args& a, const Geo& g, cudaStream_t st, int grouped);
+cudaError_t launch_lh_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
+                           long long* trace, const float* kpart, int kblk, bool tiles_ready);
 
 void set_tc_trace(void* buf);
 bool tc_supported(const da_attn_args& a, const Geo& g);

@@ -78,6 +78,7 @@ struct PoolSrc {
   long long hs[3], rs[3];
   double* out[2];
   uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
+  int grouped;                // tile layout: 1 grouped (lane-half kernel), 0 half-major (pair kernel)
 };
 
 __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode, Geo g) {
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
   // K / V tiles ([half][64 rows x 128 B], 128-byte swizzle, zero padding rows):
   // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
   uint8_t* tdst = (z >= 1 && src.tile[z - 1] != nullptr && live)
-                      ? src.tile[z - 1] + ((long long)h * g.g + i) * 16384 + (k >> 3) * 8192 : nullptr;
+                      ? src.tile[z - 1] + ((long long)h * g.g + i) * 16384 : nullptr;
   double acc[8], acc2[8];  // even / odd rows: two shorter add chains (fp64 sums of bf16 are exact either way)
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = acc2[e] = 0.0;
@@ -311,7 +312,8 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int r = r0 + t;
-        *reinterpret_cast<uint4*>(tdst + r * 128 + (((k & 7) ^ (r & 7)) << 4)) = q[t];
+        const uint32_t off = src.grouped ? kv_tile_offset_grouped(r, k >> 3, k & 7) : kv_tile_offset_halves(r, k >> 3, k & 7);
+        *reinterpret_cast<uint4*>(tdst + off) = q[t];
       }
     }
     if (z == 2) continue;  // V: tiles only
@@ -378,6 +380,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
     src.hs[2] = tiles ? hs2 : hs0; src.rs[2] = tiles ? rs2 : rs0;
     src.tile[0] = tiles ? ktile : nullptr;
     src.tile[1] = tiles ? vtile : nullptr;
+    src.grouped = attn_tiles_grouped() ? 1 : 0;
     dim3 grid(pool_norm_blocks(d, g), heads, x1 ? (tiles ? 3 : 2) : 1);
     float* kp = x1 ? kpart : nullptr;
     switch (d / 8) {
