@@ -691,12 +691,13 @@ cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t s
 
 // Default: region-pair kernel (attn_pair.cu). DA_K4=transposed selects the
 // single-region transposed kernel below (kept for A/B measurements).
-// K4 variant: 0 pair kernel (default), 1 transposed (DA_K4=transposed), 2 lane-half (DA_K4=lh)
+// K4 variant: 2 lane-half kernel (attn_lh.cu, default), 0 pair kernel
+// (DA_K4=pair; also the block-sparse seam), 1 transposed (DA_K4=transposed)
 static int k4_variant() {
   static int variant = -1;
   if (variant < 0) {
     const char* env = getenv("DA_K4");
-    variant = (env && strcmp(env, "transposed") == 0) ? 1 : (env && strcmp(env, "lh") == 0) ? 2 : 0;
+    variant = (env && strcmp(env, "transposed") == 0) ? 1 : (env && strcmp(env, "pair") == 0) ? 0 : 2;
   }
   return variant;
 }

@@ -432,3 +432,46 @@ def test_pipeline_odd_region_counts(dims):
         assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept), hh
         assert got.kept_count == ref.mask.kept_count and got.forced_row_keeps == ref.mask.forced_row_keeps
         _close(out[hh], ref.output)
+
+
+@pytest.mark.parametrize("sparsity", [0.995, 0.97])
+def test_pipeline_without_force_keep_empty_and_short_rows(sparsity):
+    # force_row_keep off at high sparsity: many query regions keep 0, 1 or 2
+    # key regions (empty items are zero-filled by K4's producer, one-step
+    # items leave one TMEM lane half unused)
+    grid, (q, k, v), (q64, k64, v64) = _inputs((3, 45, 80, 8, 8, 128, 2, 11))
+    plan = da.pad_plan(3, 45, 80, 8, 8)
+    res = da.multi_head_sparse_attention(q, k, v, plan, sparsity, force_row_keep=False, return_details=True)
+    out = res.output.float().cpu().numpy()
+    for hh in range(2):
+        ref = O.padded_sparse_attention(q64[hh], k64[hh], v64[hh], 3, 45, 80, 8, 8, sparsity,
+                                        force_row_keep=False, return_details=True)
+        got = res.mask.head(hh)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept)
+        counts = ref.mask.kept.sum(1)
+        assert (counts == 0).any() and (counts == 1).any()
+        _close(out[hh], ref.output)
+
+
+def test_k4_variants_agree():
+    # the lane-half K4 (default) and the pair K4 compute the same function;
+    # run the pair kernel in a subprocess (the variant is fixed per process)
+    import subprocess
+    import sys
+    code = ("import sys, torch; sys.path.insert(0, '.'); import paper_2505_14708_b200 as da; "
+            "g = torch.Generator(device='cuda').manual_seed(5); plan = da.pad_plan(4, 45, 80, 8, 8); "
+            "q, k, v = (torch.randn(3, plan.num_valid, 128, device='cuda', generator=g).to(torch.bfloat16) "
+            "for _ in range(3)); o = da.multi_head_sparse_attention(q, k, v, plan, 0.8); "
+            "torch.save(o.cpu(), sys.argv[1])")
+    import os
+    import tempfile
+    outs = []
+    for var in ("lh", "pair"):
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "o.pt")
+            env = dict(os.environ, DA_K4=var)
+            subprocess.run([sys.executable, "-c", code, path], check=True, env=env,
+                           cwd=str(Path(__file__).resolve().parents[1]))
+            outs.append(torch.load(path).float())
+    err = (outs[0] - outs[1]).abs().max().item()
+    assert err <= 4e-3, err
