@@ -277,7 +277,10 @@ cudaError_t launch_permute_out(const void* o_r, void* out, long long hs, long lo
 // block (kpart[h][blockIdx.x]), the bound the attention kernel's fixed softmax
 // offset needs, so K is read once.
 template <int TPR>
-__global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g, float* __restrict__ kpart) {
+#ifndef DA_POOL_MINB
+#define DA_POOL_MINB 4  // 64 registers: 8 CTAs of 256 threads per SM (memory-latency bound at 2)
+#endif
+__global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src, int d, Geo g, float* __restrict__ kpart) {
   constexpr int RPB = 256 / TPR;  // regions per block
   __shared__ float wmax[8];
   const int h = blockIdx.y, z = blockIdx.z;
@@ -293,15 +296,20 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
   // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
   uint8_t* tdst = (z >= 1 && src.tile[z - 1] != nullptr && live)
                       ? src.tile[z - 1] + ((long long)h * g.g + i) * 16384 : nullptr;
-  double acc[8], acc2[8];  // even / odd rows: two shorter add chains (fp64 sums of bf16 are exact either way)
+  // fp64 sums of bf16 values are exact, in any order
+  double acc[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = acc2[e] = 0.0;
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
   float nmax = 0.f;
-  for (int r0 = 0; r0 < g.p; r0 += 8) {
-    uint4 q[8];
-    bool ok[8];
+#ifndef DA_POOL_RB
+#define DA_POOL_RB 4
+#endif
+  constexpr int RB = DA_POOL_RB;  // rows per batch (loads in flight per thread); occupancy supplies the rest
+  for (int r0 = 0; r0 < g.p; r0 += RB) {
+    uint4 q[RB];
+    bool ok[RB];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < RB; ++t) {
       const int r = r0 + t;
       const int u = r / g.pw, v = r - u * g.pw;
       ok[t] = live && r < g.p && u < rc.vy && v < rc.vx;
@@ -310,29 +318,31 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
     }
     if (tdst != nullptr) {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      for (int t = 0; t < RB; ++t) {
         const int r = r0 + t;
-        const uint32_t off = src.grouped ? kv_tile_offset_grouped(r, k >> 3, k & 7) : kv_tile_offset_halves(r, k >> 3, k & 7);
-        *reinterpret_cast<uint4*>(tdst + off) = q[t];
+        if (r < g.p) {
+          const uint32_t off = src.grouped ? kv_tile_offset_grouped(r, k >> 3, k & 7) : kv_tile_offset_halves(r, k >> 3, k & 7);
+          *reinterpret_cast<uint4*>(tdst + off) = q[t];
+        }
       }
     }
     if (z == 2) continue;  // V: tiles only
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&q[t]);
+    for (int t = 0; t < RB; ++t) {
+      const uint32_t wv[4] = {q[t].x, q[t].y, q[t].z, q[t].w};
       if (ok[t]) {  // padding rows are not summed (keeps -0.0 sums bit-exact)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (t & 1) acc2[e] += (double)__bfloat162float(b[e]);
-          else acc[e] += (double)__bfloat162float(b[e]);
+        for (int e = 0; e < 4; ++e) {
+          acc[2 * e] += (double)__uint_as_float(wv[e] << 16);
+          acc[2 * e + 1] += (double)__uint_as_float(wv[e] & 0xffff0000u);
         }
       }
       if (norms) {
         float s2 = 0.f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float x = __bfloat162float(b[e]);
-          s2 = fmaf(x, x, s2);
+        for (int e = 0; e < 4; ++e) {
+          const float lo = __uint_as_float(wv[e] << 16), hi = __uint_as_float(wv[e] & 0xffff0000u);
+          s2 = fmaf(lo, lo, fmaf(hi, hi, s2));
         }
 #pragma unroll
         for (int o = TPR / 2; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(256) pool_avg_kernel(PoolSrc src, int d, Geo g
     const double div = (double)(cnt > 1 ? cnt : 1);
     double* o = src.out[z] + ((long long)h * g.g + i) * d + k * 8;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = (acc[e] + acc2[e]) / div;
+    for (int e = 0; e < 8; ++e) o[e] = acc[e] / div;
   }
   if (norms) {
 #pragma unroll
