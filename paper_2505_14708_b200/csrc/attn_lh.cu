@@ -161,25 +161,54 @@ DA_DEV unsigned long long key_mask(const Params& p, int j) {
   return m;
 }
 
-// Per head: query regions by kept count, descending (ties by index): the
-// dynamic item order puts the heaviest items first. One block per head.
+// Per head: query regions by kept count, descending: the dynamic item order
+// puts the heaviest items first (the order within a count does not matter:
+// every region's output is computed independently). One block per head:
+// count histogram, block-wide exclusive scan, atomic placement.
 __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restrict__ row_ptr, int g, int mask_h,
                                                             int* __restrict__ order) {
-  extern __shared__ int bins[];  // [g + 1]
-  const int h = blockIdx.x;
+  extern __shared__ int bins[];  // [g + 1], key = g - count
+  __shared__ int wsum[32];
+  const int h = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int* rp = row_ptr + (long long)(h * mask_h) * (g + 1);
-  for (int i = threadIdx.x; i <= g; i += blockDim.x) bins[i] = 0;
+  const int nb = g + 1;
+  for (int i = t; i < nb; i += blockDim.x) bins[i] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < g; i += blockDim.x) atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1);
+  for (int i = t; i < g; i += blockDim.x) atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int c = 0; c <= g; ++c) {
-      const int v = bins[c];
-      bins[c] = run;
-      run += v;
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int k0 = min(nb, t * per), k1 = min(nb, k0 + per);
+  int local = 0;
+  for (int k = k0; k < k1; ++k) local += bins[k];
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x / 32;
+    int v = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
     }
-    for (int i = 0; i < g; ++i) order[(long long)h * g + bins[g - min(g, rp[i + 1] - rp[i])]++] = i;
+    if (lane < nw) wsum[lane] = v;  // inclusive warp totals
+  }
+  __syncthreads();
+  int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
+  for (int k = k0; k < k1; ++k) {
+    const int v = bins[k];
+    bins[k] = run;
+    run += v;
+  }
+  __syncthreads();
+  for (int i = t; i < g; i += blockDim.x) {
+    const int pos = atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1);
+    order[(long long)h * g + pos] = i;
   }
 }
 

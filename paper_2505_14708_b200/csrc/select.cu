@@ -571,9 +571,15 @@ DA_DEV float key32_score(unsigned int k) {
 }
 
 // fp64 score exactly as the fp64 GEMM forms it: sequential FMA over features, then * scale
-DA_DEV double score64(const double* __restrict__ q, const double* __restrict__ k, int d, double scale) {
+// fp64 score of one (query region, key region) pair computed by a whole warp
+// (lanes split the features, coalesced row reads, fixed shuffle tree; the
+// mark kernel's argmax rescoring uses the same order): every lane returns it.
+DA_DEV double score64_warp(const double* __restrict__ q, const double* __restrict__ k, int d, double scale) {
+  const int lane = threadIdx.x & 31;
   double acc = 0.0;
-  for (int c = 0; c < d; ++c) acc = fma(__ldg(q + c), __ldg(k + c), acc);
+  for (int c = lane; c < d; c += 32) acc = fma(__ldg(q + c), __ldg(k + c), acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc * scale;
 }
 
@@ -721,6 +727,33 @@ __global__ void __launch_bounds__(256, 2) draft32_gemm_kernel(const float* __res
   }
   cp_async_wait<0>();
   float* S = scores + (long long)h * s32_plane(g);
+  // each row's largest key, from registers: per thread over its 8 columns,
+  // then across the 16 threads of the row group (8 independent chains)
+  {
+    unsigned int rk[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      rk[u] = 0u;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int col = (v < 4 ? 0 : 64) + 4 * tx + (v & 3);
+        const float2 a2 = acc[u][v >> 1];
+        const float val = ((v & 1) ? a2.y : a2.x) * scale;
+        if (j0 + col < g) rk[u] = max(rk[u], key32(val));
+      }
+    }
+#pragma unroll
+    for (int o2 = 8; o2; o2 >>= 1)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rk[u] = max(rk[u], __shfl_xor_sync(0xffffffffu, rk[u], o2));
+    if (tx == 0) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int gi = i0 + (u < 4 ? 0 : 60) + 4 * ty + u;
+        if (gi < g) atomicMax(&rowmax[(long long)h * g + gi], rk[u]);
+      }
+    }
+  }
   __syncthreads();  // operands no longer needed: the tile reuses the space
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
@@ -739,6 +772,9 @@ __global__ void __launch_bounds__(256, 2) draft32_gemm_kernel(const float* __res
     const float4 o = *reinterpret_cast<const float4*>(&T[rr][4 * lane]);
     const int gj = j0 + 4 * lane;
     const float ov[4] = {o.x, o.y, o.z, o.w};
+#ifdef DA_G32_NOSTORE
+    if (o.x == 12345.f)
+#endif
     if (vec && gj + 3 < g) {
       *reinterpret_cast<float4*>(S + (long long)gi * g + gj) = o;
     } else {
@@ -746,20 +782,14 @@ __global__ void __launch_bounds__(256, 2) draft32_gemm_kernel(const float* __res
       for (int q = 0; q < 4; ++q)
         if (gj + q < g) S[(long long)gi * g + gj + q] = ov[q];
     }
-    unsigned int rk = 0u;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const bool live = gj + q < g;
-      const unsigned int k = key32(ov[q]);
-      if (live) rk = max(rk, k);
-      const unsigned int bin = live ? (k >> 21) : 0xFFFFFFFFu;
       // digit-0 histogram: plain shared-memory atomics (measured faster than
       // warp-aggregating equal bins with match.any, whose latency dominated)
-      if (live) atomicAdd(&sh[bin], 1u);
+#ifndef DA_G32_NOHIST
+      if (gj + q < g) atomicAdd(&sh[key32(ov[q]) >> 21], 1u);
+#endif
     }
-#pragma unroll
-    for (int o2 = 16; o2; o2 >>= 1) rk = max(rk, __shfl_xor_sync(0xffffffffu, rk, o2));
-    if (lane == 0) atomicMax(&rowmax[(long long)h * g + gi], rk);
   }
   __syncthreads();
   for (int b = tid; b < NB; b += 256)
@@ -951,8 +981,10 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
   }
 }
 
-// One CTA per head: rescore the band in fp64, keep the `need` best (descending
-// score, ties to the smaller flat index), set their bits, emit the threshold.
+// Per head (S32_FINISH_SPLIT CTAs, each ranking a slice): rescore the band in
+// fp64, keep the `need` best (descending score, ties to the smaller flat
+// index), set their bits, emit the threshold.
+constexpr int S32_FINISH_SPLIT = 8;
 __global__ void __launch_bounds__(1024) s32_finish_kernel(const double* __restrict__ qp,
                                                           const double* __restrict__ kp, int g, int d, double scale,
                                                           long long m, Sel32State* st, const int* __restrict__ cand,
@@ -973,15 +1005,24 @@ __global__ void __launch_bounds__(1024) s32_finish_kernel(const double* __restri
     return;
   }
   const int* C = cand + (long long)h * S32_CAP;
-  for (int c = threadIdx.x; c < cnt; c += blockDim.x) {
-    const int f = C[c];
-    const int i = f / g, j = f - i * g;
-    key[c] = score_key(score64(qp + ((long long)h * g + i) * d, kp + ((long long)h * g + j) * d, d, scale));
-    idx[c] = f;
+  {  // one warp per candidate: coalesced fp64 row reads (every CTA of the head rescores the whole band)
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c = wp; c < cnt; c += nw) {
+      const int f = C[c];
+      const int i = f / g, j = f - i * g;
+      const double sc = score64_warp(qp + ((long long)h * g + i) * d, kp + ((long long)h * g + j) * d, d, scale);
+      if (lane == 0) {
+        key[c] = score_key(sc);
+        idx[c] = f;
+      }
+    }
   }
   __syncthreads();
   unsigned int* Bh = bm + (long long)h * g * w32;
-  for (int c = threadIdx.x; c < cnt; c += blockDim.x) {
+  // the O(cnt^2) ranking is split over gridDim.y CTAs per head (each rescored the whole band)
+  const int per = (cnt + gridDim.y - 1) / gridDim.y;
+  const int c0 = blockIdx.y * per, c1 = min(cnt, c0 + per);
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
     const unsigned long long kc = key[c];
     const int fc = idx[c];
     int rank = 0;
@@ -1095,7 +1136,7 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
                                              w.cand, w.fallback);
   const size_t fsmem = (sizeof(unsigned long long) + sizeof(int)) * S32_CAP;
   cudaFuncSetAttribute(s32_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-  s32_finish_kernel<<<heads, 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bm, w32, threshold,
+  s32_finish_kernel<<<dim3(heads, S32_FINISH_SPLIT), 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bm, w32, threshold,
                                                w.fallback);
   s32_force_kernel<<<rows_grid, 256, 0, st>>>(w.bm, g, w32, w.argmax, force, w.row_counts, w.row_forced, w.fallback);
   scan_rows_kernel<<<heads, 1024, 0, st>>>(w.row_counts, row_ptr, g, g + 1, nullptr, 0, w.row_forced,
