@@ -353,8 +353,11 @@ def _validate_pipeline_args(sparsity, select_on, pool_mode):
 
 
 def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
-              shared_head_mask, qkv_layout, force_portable=False, attn_events=None, want_bitmap=True):
-    """Run the fused C-ABI pipeline; returns (output, mask, squeeze)."""
+              shared_head_mask, qkv_layout, force_portable=False, attn_events=None, want_bitmap=True,
+              out_dev=None):
+    """Run the fused C-ABI pipeline; returns (output, mask, squeeze). ``out_dev``
+    (internal): a preallocated contiguous (heads, n, dv) bf16 device tensor the
+    output is written into (``hnd`` layout only)."""
     q3, squeeze = _as_heads(q, qkv_layout, "q")
     k3, _ = _as_heads(k, qkv_layout, "k")
     v3, _ = _as_heads(v, qkv_layout, "v")
@@ -380,7 +383,10 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     kept = torch.empty(mheads, dtype=torch.int64, device=dev)
     ws_bytes = lib().da_pipeline_workspace_size(ctypes.byref(grid), heads, d)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    o_base, o3 = _alloc_like_layout(heads, n, dv, qkv_layout if not squeeze else "hnd", dev)
+    if out_dev is not None:
+        o_base = o3 = out_dev
+    else:
+        o_base, o3 = _alloc_like_layout(heads, n, dv, qkv_layout if not squeeze else "hnd", dev)
     pa = DaPipelineArgs()
     pa.attn = _attn_struct(q3, k3, v3, o3, d, dv, _lib.LAYOUT_ORIGINAL, scale)
     pa.attn.force_portable = 1 if force_portable else 0
@@ -460,7 +466,6 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
     else:
         groups = [(h0, min(heads, h0 + hg)) for h0 in range(0, heads, hg)]
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    s_in.wait_stream(main)
     if out is not None:
         o3, _ = _as_heads(out, qkv_layout, "out")
         if o3.device.type != "cpu" or tuple(o3.shape) != (heads, n, dv) or o3.dtype != out_dtype or \
@@ -470,17 +475,26 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
     else:
         # pinned so the per-group downloads are asynchronous (pass out= to reuse a buffer)
         out_host = torch.empty((heads, n, dv), dtype=out_dtype, pin_memory=True)
+    # Device staging for the whole call, allocated once on the compute stream:
+    # the uploads (s_in) and downloads (s_out) only touch slices of these, and
+    # every group's compute waits for its upload, so no cross-stream frees.
+    dev_in = [torch.empty(x.shape, dtype=x.dtype, device=dev) for x in (q3, k3, v3)]
+    direct_out = len(groups) > 1 and out_dtype == torch.bfloat16
+    out_dev = torch.empty((heads, n, dv), dtype=torch.bfloat16, device=dev) if direct_out else None
+    s_in.wait_stream(main)
+    s_out.wait_stream(main)
     masks = []
     for h0, h1 in groups:
         with torch.cuda.stream(s_in):
-            qd, kd, vd = (x[h0:h1].to(dev, non_blocking=True) for x in (q3, k3, v3))
+            for x, y in zip((q3, k3, v3), dev_in):
+                y[h0:h1].copy_(x[h0:h1], non_blocking=True)
             ev_in = torch.cuda.Event()
             ev_in.record(s_in)
         main.wait_event(ev_in)
-        for t in (qd, kd, vd):
-            t.record_stream(main)
+        qd, kd, vd = (y[h0:h1] for y in dev_in)
         out_g, mask_g, _ = _pipeline(qd, kd, vd, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
-                                     shared_head_mask, "hnd", want_bitmap=details)
+                                     shared_head_mask, "hnd", want_bitmap=details,
+                                     out_dev=out_dev[h0:h1] if direct_out else None)
         if out_g.dtype != out_dtype:
             out_g = out_g.to(out_dtype)
         ev_c = torch.cuda.Event()
@@ -488,7 +502,8 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_c)
             out_host[h0:h1].copy_(out_g, non_blocking=True)
-        out_g.record_stream(s_out)
+        if not direct_out:
+            out_g.record_stream(s_out)
         masks.append(mask_g)
     main.wait_stream(s_out)
     s_out.synchronize()
