@@ -278,7 +278,7 @@ def run_ours(args, cfg, name):
             "config": _config_dict(name, cfg, world),
             "effective_tflops_per_gpu": eff_flops / (ms * 1e-3) / 1e12 / world,
             "kept_blocks": kept_total,
-            "roofline": {"bound": "tensor", "kernel": "sparse_attn_tc_kernel (K4)", "achieved": k4_tflops,
+            "roofline": {"bound": "tensor", "kernel": "sparse_attn_lh_kernel (K4)", "achieved": k4_tflops,
                          "peak": peak_tf, "unit": "TFLOP/s", "frac": k4_tflops / peak_tf,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
                          "k4_ms": k4_ms, "k4_share_of_step": k4_ms / ms,
