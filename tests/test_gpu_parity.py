@@ -475,3 +475,18 @@ def test_k4_variants_agree():
             outs.append(torch.load(path).float())
     err = (outs[0] - outs[1]).abs().max().item()
     assert err <= 4e-3, err
+
+
+def test_zero_sparsity_long_lists_equal_dense():
+    # g = 4800 regions (80 frames): every kept list (4800 key regions) exceeds
+    # K4's staged-list capacity, so the producer reads the list from global
+    # memory; at sparsity 0 the result is dense attention
+    f, h, w = 80, 45, 80
+    plan = da.pad_plan(f, h, w, 8, 8)
+    n = plan.num_valid
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(1, n, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    out = da.multi_head_sparse_attention(q, k, v, plan, 0.0).float()
+    # dense reference: bf16 flash attention (fp32 math would need the full n x n matrix)
+    ref = torch.nn.functional.scaled_dot_product_attention(q[None], k[None], v[None])[0].float()
+    _close(out.cpu().numpy(), ref.cpu().numpy())
