@@ -217,9 +217,16 @@ def run_ours(args, cfg, name):
         q, k, v = (torch.randn(nl, heads, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
                    for _ in range(3))
         hp = HeadParallelAttention(plan, sp, world, rank)
+        a2a_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+                  for _ in range(args.steps)]
+        a2a_i = [0]
 
         def step(events=None):
-            return hp(q, k, v, attn_events=events)
+            evs = None
+            if events is not None:
+                evs = a2a_ev[a2a_i[0] % len(a2a_ev)]
+                a2a_i[0] += 1
+            return hp(q, k, v, attn_events=events, a2a_events=evs)
 
     for _ in range(args.warmup):
         step()
@@ -246,10 +253,12 @@ def run_ours(args, cfg, name):
     k4_ms = statistics.mean(b.elapsed_time(e) for b, e in ev)
     mask = res[1]
     kept_total = int(mask.kept_counts.sum().item())
+    a2a_ms = None
     if world > 1:
-        t = torch.tensor([elapsed, k4_ms], device=dev, dtype=torch.float64)
+        a2a_ms = statistics.mean(sum(b.elapsed_time(e) for b, e in pair) for pair in a2a_ev)
+        t = torch.tensor([elapsed, k4_ms, a2a_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed, k4_ms = float(t[0]), float(t[1])
+        elapsed, k4_ms, a2a_ms = float(t[0]), float(t[1]), float(t[2])
         kt = torch.tensor([kept_total], device=dev, dtype=torch.int64)
         dist.all_reduce(kt)
         kept_total = int(kt.item())
@@ -263,6 +272,8 @@ def run_ours(args, cfg, name):
     e2e = None
     cpu_base = None
     dense_ms = None
+    if world > 1:
+        e2e = _e2e_sharded(hp, q.shape, dev, args, world)
     if world == 1:
         e2e = _e2e(da, plan, cfg, dev, args)
         dense_ms = _dense_sdpa_ms(heads, n, d, dev) if args.dense else None
@@ -287,6 +298,8 @@ def run_ours(args, cfg, name):
             "gpu_launches": launches,
             "clocks": clocks.result,
         }
+        if a2a_ms is not None:  # the seq <-> head all-to-alls (NCCL), per call, max over ranks
+            line["collective_ms"] = a2a_ms
         if e2e is not None:
             line["e2e"] = e2e
         if dense_ms is not None:
@@ -297,6 +310,39 @@ def run_ours(args, cfg, name):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _e2e_sharded(hp, shape, dev, args, world):
+    """N > 1: each rank's sequence shard starts in pinned host memory; upload,
+    the head-parallel call (two NCCL all-to-alls around the pipeline) and the
+    download of the output shard are timed; max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    host = [torch.randn(*shape, dtype=torch.float32).to(torch.bfloat16).pin_memory() for _ in range(3)]
+    out_host = torch.empty(*shape, dtype=torch.bfloat16).pin_memory()
+
+    def once():
+        qd, kd, vd = (x.to(dev, non_blocking=True) for x in host)
+        o, _ = hp(qd, kd, vd)
+        out_host.copy_(o, non_blocking=True)
+
+    for _ in range(3):
+        once()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, min(args.steps, 5))
+    s.record()
+    for _ in range(steps):
+        once()
+    e.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([s.elapsed_time(e) / steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nb = shape[0] * shape[1] * shape[2] * 2
+    return {"value": float(t[0]), "unit": "ms/call", "h2d_bytes_per_step": 3 * nb * world,
+            "d2h_bytes_per_step": nb * world}
 
 
 def _e2e(da, plan, cfg, dev, args):

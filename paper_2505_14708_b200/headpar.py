@@ -43,9 +43,20 @@ class HeadParallelAttention:
         self.plan, self.sparsity, self.world, self.rank, self.group = plan, sparsity, world, rank, group
         self.scale, self.pool_mode, self.select_on, self.force = scale, pool_mode, select_on, force_row_keep
 
-    def __call__(self, q, k, v, attn_events=None):
+    def __call__(self, q, k, v, attn_events=None, a2a_events=None):
+        """``a2a_events`` (optional): two (begin, end) CUDA event pairs recorded
+        around the input and output all-to-alls, for timing the collectives."""
+        if a2a_events is not None:
+            a2a_events[0][0].record()
         qh, kh, vh = (seq_to_head(x, self.world, self.group) for x in (q, k, v))
+        if a2a_events is not None:
+            a2a_events[0][1].record()
         scale = self.scale if self.scale is not None else api.head_dim_scale(q.shape[-1])
         out, mask, _ = api._pipeline(qh, kh, vh, self.plan, self.sparsity, scale, self.pool_mode, self.select_on,
                                      self.force, False, "nhd", attn_events=attn_events, want_bitmap=False)
-        return head_to_seq(out, self.world, self.group), mask
+        if a2a_events is not None:
+            a2a_events[1][0].record()
+        res = head_to_seq(out, self.world, self.group)
+        if a2a_events is not None:
+            a2a_events[1][1].record()
+        return res, mask
