@@ -174,6 +174,11 @@ typedef struct da_pipeline_args {
   void* ev_attn_end;
 } da_pipeline_args;
 size_t da_pipeline_workspace_size(const da_grid* grid, int32_t heads, int32_t d);
+/* Byte offset, inside the pipeline workspace, of the int the fp32 guard-band
+ * selection sets when the exact fp64 selection had to run instead (non-finite
+ * inputs, massive ties); 0 after a call means the fast path decided the mask.
+ * Diagnostics / tests; -1 on invalid arguments. */
+int64_t da_pipeline_fallback_offset(const da_grid* grid, int32_t heads, int32_t d);
 /* Kernel launches one da_sparse_attention call issues (for launch accounting). */
 int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask);
 int da_sparse_attention(const da_pipeline_args* args, const da_grid* grid, void* stream);

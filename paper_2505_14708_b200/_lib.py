@@ -73,6 +73,7 @@ SIGNATURES = {
     "da_block_sparse_fwd": (ctypes.c_int, [ctypes.POINTER(DaAttnArgs), ctypes.POINTER(DaGrid), c_vp]),
     "da_pipeline_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(DaGrid), c_i32, c_i32]),
     "da_pipeline_launches": (c_i32, [c_i32, c_i32]),
+    "da_pipeline_fallback_offset": (ctypes.c_int64, [ctypes.POINTER(DaGrid), c_i32, c_i32]),
     "da_debug_trace": (ctypes.c_int, [c_vp]),
     "da_sparse_attention": (ctypes.c_int, [ctypes.POINTER(DaPipelineArgs), ctypes.POINTER(DaGrid), c_vp]),
 }

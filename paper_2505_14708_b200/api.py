@@ -354,7 +354,7 @@ def _validate_pipeline_args(sparsity, select_on, pool_mode):
 
 def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
               shared_head_mask, qkv_layout, force_portable=False, attn_events=None, want_bitmap=True,
-              out_dev=None):
+              out_dev=None, debug=None):
     """Run the fused C-ABI pipeline; returns (output, mask, squeeze). ``out_dev``
     (internal): a preallocated contiguous (heads, n, dv) bf16 device tensor the
     output is written into (``hnd`` layout only)."""
@@ -405,6 +405,9 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     with torch.cuda.device(dev):
         check(lib().da_sparse_attention(ctypes.byref(pa), ctypes.byref(grid), _stream_ptr(dev)),
               "sparse_attention")
+    if debug is not None:  # tests: did the fp32 guard-band selection hand over to the fp64 path?
+        off = lib().da_pipeline_fallback_offset(ctypes.byref(grid), heads, d)
+        debug["selection_fallback"] = int(ws[off:off + 4].view(torch.int32).item()) != 0
     out = o3[0] if squeeze else (o_base if qkv_layout == "nhd" else o3)
     if out_dtype != torch.bfloat16:
         out = out.to(out_dtype)

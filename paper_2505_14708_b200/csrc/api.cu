@@ -214,6 +214,16 @@ __global__ void head_mean_kernel(const double* __restrict__ scores, double* __re
   out[e] = s / (double)heads;
 }
 
+int64_t da_pipeline_fallback_offset(const da_grid* grid, int32_t heads, int32_t d) {
+  if (!grid_ok(grid) || heads < 1 || d < 1) return -1;
+  da::Geo g = da::make_geo(*grid);
+  // carve a notional workspace at a non-null base (a null base carves to null pointers)
+  char* const base = reinterpret_cast<char*>(uintptr_t(1) << 20);
+  const PipeWs w = carve(base, g, heads, d);
+  const char* flag = reinterpret_cast<const char*>(da::select32_fallback_flag(w.sel32, heads, g.g));
+  return (int64_t)(flag - base);
+}
+
 size_t da_pipeline_workspace_size(const da_grid* grid, int32_t heads, int32_t d) {
   if (!grid_ok(grid) || heads < 1 || d < 1) return 0;
   da::Geo g = da::make_geo(*grid);
@@ -228,12 +238,12 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // scan, collect, threshold, kept totals, packbits (bitmap requested);
   // attention: pair plan, tcgen05 kernel, fallback list (key norms come from pooling)
   // (per-head logits path: the fp32 guard-band selection — init, eps, operand pack, GEMM,
-  // 2 digit histograms + 3 scans, mark, band finish, force, row scan, collect,
+  // 1 digit histogram + 2 scans, mark, band finish, force, row scan, collect,
   // kept totals, packbits — followed by the gated fp64 launches, which exit
   // at once unless the fp32 path flagged a fallback)
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
   const int fp64_path = 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1;
-  return 1 + (fused ? 16 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
+  return 1 + (fused ? 14 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {

@@ -796,7 +796,10 @@ __global__ void __launch_bounds__(256, 2) draft32_gemm_kernel(const float* __res
     if (sh[b]) atomicAdd(&hist0[(long long)h * NB + b], sh[b]);
 }
 
-// digits: 0 = bits 21..31 (fused in the GEMM), 1 = bits 10..20, 2 = bits 0..9
+// digits: 0 = bits 21..31 (fused in the GEMM), 1 = bits 10..20, 2 = bits 0..9.
+// Only digits 0 and 1 are resolved: the 22-bit key bucket of the m-th score
+// spans 2^10 fp32 ulps (2^-13 relative), so the guard band simply covers it.
+constexpr int S32_PASSES = 2;
 DA_DEV int p32_hi(int pass) { return pass == 0 ? 32 : pass == 1 ? 21 : 10; }
 DA_DEV int p32_lo(int pass) { return pass == 0 ? 21 : pass == 1 ? 10 : 0; }
 
@@ -857,7 +860,7 @@ __global__ void s32_scan_kernel(Sel32State* st, unsigned int* hist, int pass, in
     Sel32State s = st[h];
     s.remaining = rem - above;
     s.prefix = (pass == 0 ? 0u : (s.prefix << (hi - lo))) | (unsigned int)chosen;
-    if (pass == 2) s32_set_eps(s, d, scale, fallback);
+    if (pass == S32_PASSES - 1) s32_set_eps(s, d, scale, fallback);
     st[h] = s;
   }
 }
@@ -874,9 +877,13 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
   const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (row >= g) return;
   const double eps = st[h].eps;
-  const double t32 = (double)key32_score(st[h].prefix);
-  const float hi_f = __double2float_ru(t32 + 2.0 * eps);
-  const float lo_f = __double2float_rd(t32 - 2.0 * eps);
+  // the m-th largest fp32 score lies in the 22-bit key bucket the two radix
+  // passes resolved (key bits 10..31); the band spans that bucket plus the
+  // 2 eps guard
+  const unsigned int kb = st[h].prefix << p32_lo(S32_PASSES - 1);
+  const double t_lo = (double)key32_score(kb), t_hi = (double)key32_score(kb | ((1u << p32_lo(S32_PASSES - 1)) - 1u));
+  const float hi_f = __double2float_ru(t_hi + 2.0 * eps);
+  const float lo_f = __double2float_rd(t_lo - 2.0 * eps);
   const float rmax = key32_score(rowmax[(long long)h * g + row]);
   const float rlo = __double2float_rd((double)rmax - 2.0 * eps);
   const float* S = scores + (long long)h * s32_plane(g) + (long long)row * g;
@@ -1127,7 +1134,7 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
   int chunks = (int)((n / 4 + 256 * 8 - 1) / (256 * 8));
   if (chunks > 512) chunks = 512;
   if (chunks < 1) chunks = 1;
-  for (int pass = 0; pass < 3; ++pass) {
+  for (int pass = 0; pass < S32_PASSES; ++pass) {
     if (pass > 0) s32_hist_kernel<<<dim3(chunks, heads), 256, 0, st>>>(scores32, n, w.state, w.hist, pass, w.fallback);
     s32_scan_kernel<<<heads, 32, 0, st>>>(w.state, w.hist, pass, w.fallback, d, scale);
   }

@@ -490,3 +490,18 @@ def test_zero_sparsity_long_lists_equal_dense():
     # dense reference: bf16 flash attention (fp32 math would need the full n x n matrix)
     ref = torch.nn.functional.scaled_dot_product_attention(q[None], k[None], v[None])[0].float()
     _close(out.cpu().numpy(), ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("kind,expect_fallback", [("gaussian", False), ("zeros", True)])
+def test_selection_fast_path_decides_the_mask(kind, expect_fallback):
+    # the fp32 guard-band selection must decide ordinary masks itself (the
+    # fp64 path it hands over to is correct but ~4x slower, so a too-wide band
+    # would pass every parity test): check the device flag
+    from paper_2505_14708_b200 import api
+    grid, (q, k, v), _ = _inputs((4, 45, 80, 8, 8, 128, 3, 4), head_ids=None)
+    if kind == "zeros":
+        q = torch.zeros_like(q)
+    plan = da.pad_plan(4, 45, 80, 8, 8)
+    dbg = {}
+    api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(128), "average", "logits", True, False, "hnd", debug=dbg)
+    assert dbg["selection_fallback"] == expect_fallback
