@@ -467,7 +467,14 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
     if shared_head_mask or heads == 1 or not contiguous:
         groups = [(0, heads)]  # the head-mean mask needs every head at once
     else:
-        groups = [(h0, min(heads, h0 + hg)) for h0 in range(0, heads, hg)]
+        # the first group's upload and the last group's compute + download are
+        # not overlapped with anything: make those two groups half as large
+        edge = max(1, hg // 2) if heads >= 2 * hg else hg
+        bounds = [0] + ([edge] if edge < hg else [])
+        while bounds[-1] < heads:
+            left = heads - bounds[-1]
+            bounds.append(bounds[-1] + (left if left <= edge or left <= hg else min(hg, left - edge)))
+        groups = list(zip(bounds[:-1], bounds[1:]))
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     if out is not None:
         o3, _ = _as_heads(out, qkv_layout, "out")
