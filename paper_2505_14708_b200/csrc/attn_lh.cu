@@ -40,6 +40,20 @@
 #include "common.cuh"
 #include "kernels.h"
 
+// LH_PROF: per-CTA cycle accounting of the waits (tools/probes/lh_prof.py),
+// written to the da_debug_trace buffer as [CTA][32] int64 at kernel end
+#ifdef LH_PROF
+#define LH_T0() const long long _t0 = clock64()
+#define LH_ACC(k) prof[k] += clock64() - _t0
+#else
+#define LH_T0() \
+  do {          \
+  } while (0)
+#define LH_ACC(k) \
+  do {            \
+  } while (0)
+#endif
+
 namespace da {
 namespace lhk {
 
@@ -89,6 +103,7 @@ struct Params {
   int* work;
   int fake_load;
   uint64_t pol_kv, pol_q, pol_o;
+  long long* trace;  // LH_PROF output ([CTA][32]) or null
 };
 
 struct __align__(8) Bars {
@@ -219,6 +234,11 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
   Bars& B = aux.bars;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long items = (long long)p.heads * p.geo.g;
+#ifdef LH_PROF
+  long long prof[20];
+  for (int k = 0; k < 20; ++k) prof[k] = 0;
+  const long long t_start = clock64();
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < KSL; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
@@ -307,7 +327,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
           }
         }
         const int slot = claimed % IR;
-        if (claimed >= IR) mbar_wait(&B.item_empty[slot], (uint32_t)(((claimed / IR) - 1) & 1));
+        if (claimed >= IR) { LH_T0(); mbar_wait(&B.item_empty[slot], (uint32_t)(((claimed / IR) - 1) & 1)); LH_ACC(0); }
         if (lane == 0) {
           aux.items[slot] = (int)it;
           mbar_arrive(&B.item_full[slot]);
@@ -343,11 +363,11 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
             aux.info[ii] = e;
             mbar_arrive(&B.info_full[ii]);
           } else {
-            mbar_wait(&B.info_full[ii], (uint32_t)((kq / INFO) & 1));
+            { LH_T0(); mbar_wait(&B.info_full[ii], (uint32_t)((kq / INFO) & 1)); LH_ACC(18); }
             e = aux.info[ii];
           }
           const int s = kq % NSL;
-          if (kq >= NSL) mbar_wait(&empty[s], ((kq / NSL) - 1) & 1);
+          if (kq >= NSL) { LH_T0(); mbar_wait(&empty[s], ((kq / NSL) - 1) & 1); LH_ACC(is_k ? 16 : 17); }
           ++kq;
           if (p.fake_load & (is_k ? 1 : 2)) {
             mbar_arrive(&full[s]);
@@ -371,16 +391,16 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
     for (;;) {
       Item itm;
       if (!fetch_item(p, next_item(), items, itm)) break;
-      mbar_wait(&B.q_full, qi & 1);
+      { LH_T0(); mbar_wait(&B.q_full, qi & 1); LH_ACC(1); }
       for (;;) {
-        mbar_wait_spin(&B.info_full[iidx], iph);
+        { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(2); }
         const int4 e = aux.info[iidx];
         const int last = e.w & 1;
         const int h = gs & 1;
         // this half's S buffer: the softmax has loaded step gs - 2
-        if (gs >= 2) mbar_wait_spin(&B.s_free[h], (uint32_t)(((gs >> 1) - 1) & 1));
+        if (gs >= 2) { LH_T0(); mbar_wait_spin(&B.s_free[h], (uint32_t)(((gs >> 1) - 1) & 1)); LH_ACC(3); }
         const int s = gs % KSL;
-        mbar_wait_spin(&B.k_full[s], (uint32_t)((gs / KSL) & 1));
+        { LH_T0(); mbar_wait_spin(&B.k_full[s], (uint32_t)((gs / KSL) & 1)); LH_ACC(4); }
         tc_fence_after();
         if (elect_one_sync()) {
           const uint32_t lo = h ? LANE_H : 0u;
@@ -414,14 +434,14 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
       const int ob = qi & 1;
       int t = 0;
       for (;;) {
-        mbar_wait_spin(&B.info_full[iidx], iph);
+        { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(5); }
         const int4 e = aux.info[iidx];
         const int last = e.w & 1;
         const int h = gs & 1;
         const int s = gs % VSL;
-        mbar_wait_spin(&B.v_full[s], (uint32_t)((gs / VSL) & 1));
-        mbar_wait_spin(&B.p_full[h], (uint32_t)((gs >> 1) & 1));
-        if (t == 0 && qi >= 2) mbar_wait(&B.o_empty[ob], (uint32_t)(((qi >> 1) - 1) & 1));
+        { LH_T0(); mbar_wait_spin(&B.v_full[s], (uint32_t)((gs / VSL) & 1)); LH_ACC(6); }
+        { LH_T0(); mbar_wait_spin(&B.p_full[h], (uint32_t)((gs >> 1) & 1)); LH_ACC(7); }
+        if (t == 0 && qi >= 2) { LH_T0(); mbar_wait(&B.o_empty[ob], (uint32_t)(((qi >> 1) - 1) & 1)); LH_ACC(8); }
         tc_fence_after();
         if (elect_one_sync()) {
           const uint32_t lo = h ? LANE_H : 0u;
@@ -486,7 +506,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
       }
       qn2_next = s2;
-      if (wait_parity >= 0) mbar_wait(&B.q_empty, (uint32_t)wait_parity);
+      if (wait_parity >= 0) { LH_T0(); mbar_wait(&B.q_empty, (uint32_t)wait_parity); LH_ACC(13); }
       tc_fence_after();
       tmem_st16u(tl + COL_Q + wg * 32, *reinterpret_cast<uint32_t(*)[16]>(&qv[0]));
       tmem_st16u(tl + COL_Q + wg * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&qv[16]));
@@ -514,7 +534,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         kmax = mx;
       }
       if (lane < 16) aux.xq[qi & 1][wg][r] = qn2_own;
-      bar_sync(1, 256);
+      { LH_T0(); bar_sync(1, 256); LH_ACC(14); }
       const float qn2 = aux.xq[qi & 1][0][r] + aux.xq[qi & 1][1][r];
       const int first_wg = G & 1;  // the warpgroup that runs the item's first step fixes the offsets
       float m = 0.f, l = 0.f;
@@ -524,9 +544,9 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
       for (int t = (wg - first_wg) & 1; t < nsteps; t += 2) {
         const int gs = G + t;
         const int ii = gs & (INFO - 1);
-        mbar_wait_spin(&B.info_full[ii], (uint32_t)((gs / INFO) & 1));
+        { LH_T0(); mbar_wait_spin(&B.info_full[ii], (uint32_t)((gs / INFO) & 1)); LH_ACC(9); }
         const int4 e = aux.info[ii];
-        mbar_wait_spin(&B.s_full[wg], (uint32_t)((gs >> 1) & 1));
+        { LH_T0(); mbar_wait_spin(&B.s_full[wg], (uint32_t)((gs >> 1) & 1)); LH_ACC(10); }
         tc_fence_after();
         const bool kp = ((e.z >> c) & 1) && !(p.fake_load & 4);
         if (!(p.fake_load & 4)) {
@@ -564,7 +584,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
             if (lane < 16) aux.xm[qi & 1][r] = m;
             bar_arrive(2, 256);
           } else {
-            bar_sync(2, 256);
+            { LH_T0(); bar_sync(2, 256); LH_ACC(15); }
             m = aux.xm[qi & 1][r];
           }
           got_m = true;
@@ -584,7 +604,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         }
         // this half's P buffer: GEMM2 of step gs - 2 has read it
         if (gs >= 2) {
-          mbar_wait_spin(&B.p_free[wg], (uint32_t)(((gs >> 1) - 1) & 1));
+          { LH_T0(); mbar_wait_spin(&B.p_free[wg], (uint32_t)(((gs >> 1) - 1) & 1)); LH_ACC(11); }
           tc_fence_after();
         }
         tmem_st16x2_16(th + COL_P, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
@@ -617,7 +637,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
       bar_sync(1, 256);
       const float lt = aux.lsum[0][r] + aux.lsum[1][r];
       const bool bad = (aux.had[0][r] || aux.had[1][r]) && !(lt >= 0x1p-80f);
-      mbar_wait(&B.o_full[ob], (uint32_t)((qi >> 1) & 1));
+      { LH_T0(); mbar_wait(&B.o_full[ob], (uint32_t)((qi >> 1) & 1)); LH_ACC(12); }
       tc_fence_after();
       // lane < 16 reads O of half 0, lane >= 16 O of half 1 (same row); a half
       // without any step of this item holds no O for it
@@ -658,6 +678,15 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
       ++qi;
     }
   }
+#ifdef LH_PROF
+  // lane 0 of warps 0 (K producer), 1 (GEMM1), 2 (V), 3 (GEMM2), 4 and 8 (softmax): sums per CTA
+  if (p.trace != nullptr && lane == 0 && (warp <= 4 || warp == 8)) {
+    long long* o = p.trace + (long long)blockIdx.x * 32;
+    for (int k = 0; k < 20; ++k)
+      if (prof[k]) atomicAdd(reinterpret_cast<unsigned long long*>(&o[k]), (unsigned long long)prof[k]);
+    if (warp == 1) o[31] = clock64() - t_start;
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -671,8 +700,8 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
 cudaError_t launch_lh_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why, long long* trace,
                            const float* kpart, int kblk, bool tiles_ready) {
   (void)why;
-  (void)trace;
   lhk::Params p;
+  p.trace = trace;
   p.q = static_cast<const __nv_bfloat16*>(a.q);
   p.qh = a.q_head_stride;
   p.qr = a.q_row_stride;
