@@ -74,7 +74,17 @@ constexpr int SMEM_V = SMEM_K + KSL * SLOT;
 constexpr int SMEM_END = SMEM_V + VSL * SLOT;
 
 constexpr uint32_t TMEM_COLS = 512;
+#ifndef LH_S2
+#define LH_S2 0  // 1: two S buffers per lane half (O single-buffered) instead of one (O double-buffered); measured equal
+#endif
+#if LH_S2
+constexpr uint32_t COL_Q = 0, COL_S = 64, COL_P = 320, COL_O = 384;
+constexpr int NSB = 2;  // S buffers per lane half
+#else
 constexpr uint32_t COL_Q = 0, COL_S = 64, COL_P = 192, COL_O = 256;
+constexpr int NSB = 1;
+#endif
+constexpr int NOB = 3 - NSB;  // O buffers (item parity when 2)
 constexpr uint32_t LANE_H = 16u << 16;  // TMEM address offset of lane half 1
 
 struct Params {
@@ -109,8 +119,9 @@ struct Params {
 struct __align__(8) Bars {
   uint64_t k_full[KSL], k_empty[KSL];
   uint64_t v_full[VSL], v_empty[VSL];
-  uint64_t s_full[2], s_free[2], p_full[2], p_free[2];  // per lane half
-  uint64_t o_full[2], o_empty[2];                        // per O buffer (item parity)
+  uint64_t s_full[2][NSB], s_free[2][NSB];  // per lane half and S buffer
+  uint64_t p_full[2], p_free[2];            // per lane half
+  uint64_t o_full[NOB], o_empty[NOB];       // per O buffer
   uint64_t q_full, q_empty;
   uint64_t info_full[INFO];
   uint64_t item_full[IR], item_empty[IR];
@@ -244,12 +255,16 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
     for (int s = 0; s < KSL; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < VSL; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
     for (int h = 0; h < 2; ++h) {
-      mbar_init(&B.s_full[h], 1);
-      mbar_init(&B.s_free[h], 128);
+      for (int b = 0; b < NSB; ++b) {
+        mbar_init(&B.s_full[h][b], 1);
+        mbar_init(&B.s_free[h][b], 128);
+      }
       mbar_init(&B.p_full[h], 128);
       mbar_init(&B.p_free[h], 1);
-      mbar_init(&B.o_full[h], 1);
-      mbar_init(&B.o_empty[h], 256);
+      if (h < NOB) {
+        mbar_init(&B.o_full[h], 1);
+        mbar_init(&B.o_empty[h], 256);
+      }
     }
     mbar_init(&B.q_full, 256);
     mbar_init(&B.q_empty, 1);
@@ -398,7 +413,13 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         const int last = e.w & 1;
         const int h = gs & 1;
         // this half's S buffer: the softmax has loaded step gs - 2
-        if (gs >= 2) { LH_T0(); mbar_wait_spin(&B.s_free[h], (uint32_t)(((gs >> 1) - 1) & 1)); LH_ACC(3); }
+        // step gs uses S buffer sb of half h; the softmax has loaded its previous use (step gs - 2 NSB)
+        const int sb = (gs >> 1) % NSB;
+        if (gs >= 2 * NSB) {
+          LH_T0();
+          mbar_wait_spin(&B.s_free[h][sb], (uint32_t)(((gs / (2 * NSB)) - 1) & 1));
+          LH_ACC(3);
+        }
         const int s = gs % KSL;
         { LH_T0(); mbar_wait_spin(&B.k_full[s], (uint32_t)((gs / KSL) & 1)); LH_ACC(4); }
         tc_fence_after();
@@ -408,10 +429,10 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
           const uint64_t bk = dK + (uint64_t)(s * (SLOT >> 4));
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            umma_bf16_ts(tmem + lo + COL_S, tmem + lo + COL_Q + kk * 8,
+            umma_bf16_ts(tmem + lo + COL_S + 128 * sb, tmem + lo + COL_Q + kk * 8,
                          bk + (uint64_t)((kk >> 2) * (1024 >> 4) + (kk & 3) * 2), idesc, kk > 0 ? 1u : 0u);
           umma_commit(&B.k_empty[s]);
-          umma_commit(&B.s_full[h]);
+          umma_commit(&B.s_full[h][sb]);
           if (last) umma_commit(&B.q_empty);
         }
         __syncwarp();
@@ -431,7 +452,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
     for (;;) {
       Item itm;
       if (!fetch_item(p, next_item(), items, itm)) break;
-      const int ob = qi & 1;
+      const int ob = qi % NOB;
       int t = 0;
       for (;;) {
         { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(5); }
@@ -441,7 +462,11 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         const int s = gs % VSL;
         { LH_T0(); mbar_wait_spin(&B.v_full[s], (uint32_t)((gs / VSL) & 1)); LH_ACC(6); }
         { LH_T0(); mbar_wait_spin(&B.p_full[h], (uint32_t)((gs >> 1) & 1)); LH_ACC(7); }
-        if (t == 0 && qi >= 2) { LH_T0(); mbar_wait(&B.o_empty[ob], (uint32_t)(((qi >> 1) - 1) & 1)); LH_ACC(8); }
+        if (t == 0 && qi >= NOB) {
+          LH_T0();
+          mbar_wait(&B.o_empty[ob], (uint32_t)(((qi / NOB) - 1) & 1));
+          LH_ACC(8);
+        }
         tc_fence_after();
         if (elect_one_sync()) {
           const uint32_t lo = h ? LANE_H : 0u;
@@ -522,7 +547,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
       if (!fetch_item(p, next_item(), items, itm)) break;
       const long long row = token_row(p, itm.i, r);
       const int nsteps = (itm.n + 1) / 2;
-      const int ob = qi & 1;
+      const int ob = qi % NOB;
       if (!have_q) load_q(itm, -1);
       const float qn2_own = qn2_next;
       if (itm.h != cur_head) {
@@ -546,16 +571,17 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         const int ii = gs & (INFO - 1);
         { LH_T0(); mbar_wait_spin(&B.info_full[ii], (uint32_t)((gs / INFO) & 1)); LH_ACC(9); }
         const int4 e = aux.info[ii];
-        { LH_T0(); mbar_wait_spin(&B.s_full[wg], (uint32_t)((gs >> 1) & 1)); LH_ACC(10); }
+        const int sb = (gs >> 1) % NSB;
+        { LH_T0(); mbar_wait_spin(&B.s_full[wg][sb], (uint32_t)((gs / (2 * NSB)) & 1)); LH_ACC(10); }
         tc_fence_after();
         const bool kp = ((e.z >> c) & 1) && !(p.fake_load & 4);
         if (!(p.fake_load & 4)) {
-          tmem_ld16x2_32(th + COL_S, x);
-          tmem_ld16x2_32hi(th + COL_S + 32, x);
+          tmem_ld16x2_32(th + COL_S + 128 * sb, x);
+          tmem_ld16x2_32hi(th + COL_S + 128 * sb + 32, x);
           tmem_ld_wait();
         }
         tc_fence_before();
-        mbar_arrive(&B.s_free[wg]);  // scores in registers: GEMM1 may refill this half
+        mbar_arrive(&B.s_free[wg][sb]);  // scores in registers: GEMM1 may refill this buffer
         if (!(p.fake_load & 4)) {
           const int j = c ? e.y : e.x;
           const bool rag = (e.z >> (2 + c)) & 1;
@@ -637,7 +663,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
       bar_sync(1, 256);
       const float lt = aux.lsum[0][r] + aux.lsum[1][r];
       const bool bad = (aux.had[0][r] || aux.had[1][r]) && !(lt >= 0x1p-80f);
-      { LH_T0(); mbar_wait(&B.o_full[ob], (uint32_t)((qi >> 1) & 1)); LH_ACC(12); }
+      { LH_T0(); mbar_wait(&B.o_full[ob], (uint32_t)((qi / NOB) & 1)); LH_ACC(12); }
       tc_fence_after();
       // lane < 16 reads O of half 0, lane >= 16 O of half 1 (same row); a half
       // without any step of this item holds no O for it
