@@ -443,6 +443,18 @@ def _cat_masks(masks) -> RegionMask:
                       cat("forced"), cat("kept_counts"), single=False)
 
 
+def _head_groups(heads: int, hg: int):
+    """Head ranges [h0, h1) of a pipelined host call: groups of ``hg`` heads,
+    except that the first group's upload and the last group's compute +
+    download overlap nothing, so those two are half as large."""
+    edge = max(1, hg // 2) if heads >= 2 * hg else hg
+    bounds = [0] + ([edge] if edge < hg else [])
+    while bounds[-1] < heads:
+        left = heads - bounds[-1]
+        bounds.append(bounds[-1] + (left if left <= edge or left <= hg else min(hg, left - edge)))
+    return list(zip(bounds[:-1], bounds[1:]))
+
+
 def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, force_row_keep,
                    shared_head_mask, qkv_layout, group_heads=None, out=None, details=True):
     """Host (CPU) inputs, the reference's calling convention: the call stages
@@ -467,14 +479,7 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
     if shared_head_mask or heads == 1 or not contiguous:
         groups = [(0, heads)]  # the head-mean mask needs every head at once
     else:
-        # the first group's upload and the last group's compute + download are
-        # not overlapped with anything: make those two groups half as large
-        edge = max(1, hg // 2) if heads >= 2 * hg else hg
-        bounds = [0] + ([edge] if edge < hg else [])
-        while bounds[-1] < heads:
-            left = heads - bounds[-1]
-            bounds.append(bounds[-1] + (left if left <= edge or left <= hg else min(hg, left - edge)))
-        groups = list(zip(bounds[:-1], bounds[1:]))
+        groups = _head_groups(heads, hg)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     if out is not None:
         o3, _ = _as_heads(out, qkv_layout, "out")

@@ -87,3 +87,15 @@ def test_selection_argument_errors():
         da.top_fraction_count(10, 0.0)
     with pytest.raises(ValueError, match="square"):
         da.select_top_fraction(torch.zeros(2, 3), 0.5)
+
+
+@pytest.mark.parametrize("heads,hg", [(24, 2), (40, 4), (2, 1), (3, 1), (5, 1), (24, 1), (7, 2), (13, 2), (1, 1),
+                                      (4, 4), (9, 4)])
+def test_head_groups_cover_every_head_once(heads, hg):
+    from paper_2505_14708_b200.api import _head_groups
+    g = _head_groups(heads, hg)
+    assert g[0][0] == 0 and g[-1][1] == heads
+    assert all(a[1] == b[0] for a, b in zip(g, g[1:]))
+    assert all(0 < h1 - h0 <= hg for h0, h1 in g)
+    if heads >= 2 * hg and hg > 1:
+        assert g[0][1] - g[0][0] == hg // 2  # half-size first group (pipeline fill)
