@@ -402,10 +402,21 @@ __global__ void __launch_bounds__(256) sel_collect_kernel(const unsigned int* __
   const unsigned int* B = bm + ((long long)h * g + row) * w32;
   int out = row_ptr[(long long)h * (g + 1) + row];
   int* C = col_idx + (long long)h * cap;
-  for (int c = 0; c < w32; ++c) {
-    const unsigned word = __ldg(B + c);
-    if ((word >> lane) & 1u) C[out + __popc(word & ((1u << lane) - 1))] = c * 32 + lane;
-    out += __popc(word);
+  // 32 words per round, one per lane (independent loads), warp prefix sum of
+  // their popcounts, then each lane expands its own word: ascending columns
+  for (int c0 = 0; c0 < w32; c0 += 32) {
+    const int c = c0 + lane;
+    const unsigned word = c < w32 ? __ldg(B + c) : 0u;
+    const int cnt = __popc(word);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = out + incl - cnt;
+    for (unsigned wv = word; wv; wv &= wv - 1) C[pos++] = c * 32 + __ffs(wv) - 1;
+    out += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 
