@@ -745,9 +745,12 @@ cudaError_t launch_lh_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   p.geo = g;
   p.dec = make_decoder(g);
   p.per_head = make_fastdiv((uint32_t)g.g);
-  p.pol_kv = L2_EVICT_NORMAL;
-  p.pol_q = L2_EVICT_NORMAL;
-  p.pol_o = L2_EVICT_NORMAL;
+#ifndef LH_L2POL
+#define LH_L2POL 0  // bit 0: K/V tiles evict_last, bit 1: Q rows evict_first, bit 2: output rows evict_first
+#endif
+  p.pol_kv = (LH_L2POL & 1) ? L2_EVICT_LAST : L2_EVICT_NORMAL;
+  p.pol_q = (LH_L2POL & 2) ? L2_EVICT_FIRST : L2_EVICT_NORMAL;
+  p.pol_o = (LH_L2POL & 4) ? L2_EVICT_FIRST : L2_EVICT_NORMAL;
   {
     static int fk = -1;
     if (fk < 0) {
