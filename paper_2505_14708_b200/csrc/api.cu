@@ -184,6 +184,7 @@ struct PipeWs {
   void* attn;
   void* sel32;
   float* kpart;
+  unsigned long long* pnorm;  // [heads][2] pooled row norm^2 maxima (pooling pass -> fp32 selection)
   size_t total;
 };
 
@@ -200,6 +201,7 @@ static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
   w.attn = take(da::pair_attn_workspace_size(heads, g));
   w.sel32 = take(da::select32_workspace_size(heads, g.g, d));
   w.kpart = reinterpret_cast<float*>(take(sizeof(float) * (size_t)heads * (da::pool_norm_blocks(d, g) + 1)));
+  w.pnorm = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 2 * (size_t)heads));
   w.total = off;
   return w;
 }
@@ -237,13 +239,13 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // and scans, candidate compaction + finish, tie counts + scan, mark, row
   // scan, collect, threshold, kept totals, packbits (bitmap requested);
   // attention: pair plan, tcgen05 kernel, fallback list (key norms come from pooling)
-  // (per-head logits path: the fp32 guard-band selection — init, eps, operand pack, GEMM,
+  // (per-head logits path, average pooling: the fp32 guard-band selection — init, operand pack, GEMM,
   // 1 digit histogram + 2 scans, mark, band finish, force, row scan, collect,
   // kept totals, packbits — followed by the gated fp64 launches, which exit
   // at once unless the fp32 path flagged a fallback)
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
   const int fp64_path = 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1;
-  return 1 + (fused ? 14 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
+  return 1 + (fused ? 13 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
@@ -268,11 +270,14 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   const int kblk = pa->pool_mode == 0 ? da::pool_norm_blocks(a.d, g) : 0;
   const bool tiles = kblk > 0 && a.d == 128 && a.dv == 128 && g.ph == 8 && g.pw == 8 && a.v_row_stride % 8 == 0 &&
                      (reinterpret_cast<uintptr_t>(a.v) & 15) == 0;
+  // (the averaging kernel also records the pooled rows' largest norms for the fp32 selection)
+  if (kblk > 0) cudaMemsetAsync(w.pnorm, 0, sizeof(unsigned long long) * 2 * a.heads, st);
   if ((rc = cuda_status(da::launch_pool2(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.k, a.k_head_stride,
                                          a.k_row_stride, w.kp, a.heads, a.d, pa->pool_mode, g, st,
                                          kblk > 0 ? w.kpart : nullptr, tiles ? a.v : nullptr, a.v_head_stride,
                                          a.v_row_stride, tiles ? da::pair_attn_tiles(w.attn, a.heads, g, 0) : nullptr,
-                                         tiles ? da::pair_attn_tiles(w.attn, a.heads, g, 1) : nullptr),
+                                         tiles ? da::pair_attn_tiles(w.attn, a.heads, g, 1) : nullptr,
+                                         kblk > 0 ? w.pnorm : nullptr),
                         "pool")))
     return rc;
   // K3: per-head selection on raw logits (the default) runs on fp32 draft
@@ -286,7 +291,7 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
     if ((rc = cuda_status(da::launch_select32(w.qp, w.kp, reinterpret_cast<float*>(w.scores), a.heads, g.g, a.d,
                                               a.scale, pa->m, pa->force_row_keep, w.sel32, pa->row_ptr, pa->col_idx,
                                               pa->bitmap, pa->threshold, pa->forced, pa->kept,
-                                              da_mask_capacity(g.g, pa->m), st),
+                                              da_mask_capacity(g.g, pa->m), st, kblk > 0 ? w.pnorm : nullptr),
                           "select32")))
       return rc;
     gate = da::select32_fallback_flag(w.sel32, a.heads, g.g);

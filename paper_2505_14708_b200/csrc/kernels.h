@@ -24,7 +24,7 @@ cudaError_t launch_pool(const void* x, long long hs, long long rs, double* poole
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
                          long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
                          float* kpart, const void* x2 = nullptr, long long hs2 = 0, long long rs2 = 0,
-                         uint8_t* ktile = nullptr, uint8_t* vtile = nullptr);
+                         uint8_t* ktile = nullptr, uint8_t* vtile = nullptr, unsigned long long* pnorm = nullptr);
 // K / V tile buffers inside the attention workspace ([heads][g][16 KB] each)
 // and their layout: grouped (kv_tile_offset_grouped) for the lane-half K4
 // (DA_K4=lh), half-major (kv_tile_offset_halves) for the pair kernel
@@ -48,10 +48,12 @@ cudaError_t launch_select(const double* scores, int heads, int g, long long m, i
 // sets the flag select32_fallback_flag() points to when the fp64 path must run
 size_t select32_workspace_size(int heads, int g, int d);
 const int* select32_fallback_flag(void* ws, int heads, int g);
+// pnorm (optional): [heads][2] largest pooled row norms^2 (double bits) from
+// the pooling pass; null = computed here
 cudaError_t launch_select32(const double* qp, const double* kp, float* scores32, int heads, int g, int d,
                             double scale, long long m, int force, void* ws, int* row_ptr, int* col_idx,
                             uint8_t* bitmap, double* threshold, int64_t* forced, int64_t* kept, long long cap,
-                            cudaStream_t st);
+                            cudaStream_t st, const unsigned long long* pnorm = nullptr);
 
 size_t portable_smem_bytes(int p, int d, int dv);
 cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st);

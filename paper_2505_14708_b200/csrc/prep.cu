@@ -79,6 +79,7 @@ struct PoolSrc {
   double* out[2];
   uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
   int grouped;                // tile layout: 1 grouped (lane-half kernel), 0 half-major (pair kernel)
+  unsigned long long* pnorm;  // optional [heads][2]: largest pooled row norm^2 of Q (0) and K (1), as double bits
 };
 
 __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode, Geo g) {
@@ -350,12 +351,28 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
       }
     }
   }
+  double pn2 = 0.0;  // this thread's share of the pooled row's squared norm
   if (live && z < 2) {
     const int cnt = rc.vy * rc.vx;
     const double div = (double)(cnt > 1 ? cnt : 1);
     double* o = src.out[z] + ((long long)h * g.g + i) * d + k * 8;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = acc[e] / div;
+    for (int e = 0; e < 8; ++e) {
+      o[e] = acc[e] / div;
+      pn2 = fma(o[e], o[e], pn2);
+    }
+  }
+  if (z < 2 && src.pnorm != nullptr) {
+    // the pooled row's squared norm (its TPR threads), then the warp's largest;
+    // NaN stays visible (its bits sort above every finite value)
+#pragma unroll
+    for (int o = TPR / 2; o; o >>= 1) pn2 += __shfl_xor_sync(0xffffffffu, pn2, o);
+#pragma unroll
+    for (int o = 16; o >= TPR; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, pn2, o);
+      pn2 = (y != y || pn2 != pn2) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(pn2, y);
+    }
+    if (lane == 0) atomicMax(&src.pnorm[(long long)h * 2 + z], (unsigned long long)__double_as_longlong(pn2));
   }
   if (norms) {
 #pragma unroll
@@ -378,7 +395,7 @@ int pool_norm_blocks(int d, const Geo& g) {
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
                          long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
                          float* kpart, const void* x2, long long hs2, long long rs2, uint8_t* ktile,
-                         uint8_t* vtile) {
+                         uint8_t* vtile, unsigned long long* pnorm) {
   if (mode == 0 && pool_norm_blocks(d, g) > 0 && rs0 % 8 == 0 && (!x1 || rs1 % 8 == 0)) {
     PoolSrc src;
     src.x[0] = static_cast<const __nv_bfloat16*>(x0);
@@ -391,6 +408,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
     src.tile[0] = tiles ? ktile : nullptr;
     src.tile[1] = tiles ? vtile : nullptr;
     src.grouped = attn_tiles_grouped() ? 1 : 0;
+    src.pnorm = pnorm;
     dim3 grid(pool_norm_blocks(d, g), heads, x1 ? (tiles ? 3 : 2) : 1);
     float* kp = x1 ? kpart : nullptr;
     switch (d / 8) {

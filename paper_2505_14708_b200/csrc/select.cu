@@ -595,11 +595,13 @@ DA_DEV double score64_warp(const double* __restrict__ q, const double* __restric
 }
 
 __global__ void s32_init_kernel(Sel32State* st, unsigned int* hist, unsigned int* rowmax, int g, long long m,
-                                int* fallback) {
+                                int* fallback, const unsigned long long* __restrict__ pnorm) {
   const int h = blockIdx.x;
   if (threadIdx.x == 0) {
     Sel32State s;
-    s.prefix = 0; s.remaining = m; s.nq2 = 0; s.nk2 = 0; s.eps = 0.0; s.count_hi = 0; s.cand_count = 0;
+    s.prefix = 0; s.remaining = m; s.eps = 0.0; s.count_hi = 0; s.cand_count = 0;
+    s.nq2 = pnorm ? pnorm[2 * h] : 0;  // norms from the pooling pass, else s32_norm_kernel
+    s.nk2 = pnorm ? pnorm[2 * h + 1] : 0;
     st[h] = s;
     if (h == 0) *fallback = 0;
   }
@@ -1131,12 +1133,12 @@ const int* select32_fallback_flag(void* ws, int heads, int g) { return carve_sel
 cudaError_t launch_select32(const double* qp, const double* kp, float* scores32, int heads, int g, int d,
                             double scale, long long m, int force, void* ws, int* row_ptr, int* col_idx,
                             uint8_t* bitmap, double* threshold, int64_t* forced, int64_t* kept, long long cap,
-                            cudaStream_t st) {
+                            cudaStream_t st, const unsigned long long* pnorm) {
   Sel32Ws w = carve_sel32(ws, heads, g, d);
   const long long n = (long long)g * g;
   const int w32 = (g + 31) / 32;
-  s32_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, w.rowmax, g, m, w.fallback);
-  s32_norm_kernel<<<dim3(heads, EPSB), 256, 0, st>>>(qp, kp, g, d, w.state);
+  s32_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, w.rowmax, g, m, w.fallback, pnorm);
+  if (pnorm == nullptr) s32_norm_kernel<<<dim3(heads, EPSB), 256, 0, st>>>(qp, kp, g, d, w.state);
   dim3 ggrid((g + DT32 - 1) / DT32, (g + DT32 - 1) / DT32, heads);
   cudaFuncSetAttribute(draft32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G32_SMEM);
   s32_pack_kernel<<<dim3((unsigned)(g32_pad(g, DT32) / 32), (unsigned)g32_pad(d, 32) / 32, 2 * heads), dim3(32, 8), 0,
