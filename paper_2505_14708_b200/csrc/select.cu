@@ -857,20 +857,60 @@ __global__ void __launch_bounds__(256) s32_hist_kernel(const float* __restrict__
     if (sh[b]) atomicAdd(&hist[(long long)h * NB + b], sh[b]);
 }
 
-__global__ void s32_scan_kernel(Sel32State* st, unsigned int* hist, int pass, int* fallback, int d, double scale) {
+// One block (1024 threads) per head: resolve digit `pass` from the global
+// histogram. Bins are walked from the top: thread t owns bins nb-1-2t and
+// nb-2-2t, a block-wide scan of the pair sums gives every bin's count above
+// it, and the bin where that count first reaches `remaining` is chosen (the
+// warp-serial pick_bucket walk took 15-22 us).
+__global__ void __launch_bounds__(1024) s32_scan_kernel(Sel32State* st, unsigned int* hist, int pass, int* fallback,
+                                                        int d, double scale) {
+  __shared__ long long wsum[32];
+  __shared__ int s_chosen;
+  __shared__ long long s_above;
   if (*fallback) return;
   const int h = blockIdx.x;
-  const int lane = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int hi = p32_hi(pass), lo = p32_lo(pass);
+  const int nb = 1 << (hi - lo);
   unsigned int* H = hist + (long long)h * NB;
   const long long rem = st[h].remaining;
-  int chosen;
-  long long above, cnt;
-  pick_bucket(H, 1 << (hi - lo), rem, lane, chosen, above, cnt);
-  __syncwarp();
-  for (int b = lane; b < NB; b += 32) H[b] = 0;
-  if (lane == 0) {
+  const int b0 = nb - 1 - 2 * t, b1 = b0 - 1;  // descending
+  const long long c0 = b0 >= 0 ? (long long)H[b0] : 0, c1 = b1 >= 0 ? (long long)H[b1] : 0;
+  const long long local = c0 + c1;
+  long long incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  if (t == 0) s_chosen = -1;
+  __syncthreads();
+  if (w == 0) {
+    long long v = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    wsum[lane] = v;  // inclusive over warps
+  }
+  __syncthreads();
+  const long long excl = incl - local + (w > 0 ? wsum[w - 1] : 0);  // count in bins above b0
+  // exactly one bin satisfies above < rem <= above + count
+  if (b0 >= 0 && excl < rem && excl + c0 >= rem) {
+    s_chosen = b0;
+    s_above = excl;
+  } else if (b1 >= 0 && excl + c0 < rem && excl + c0 + c1 >= rem) {
+    s_chosen = b1;
+    s_above = excl + c0;
+  }
+  __syncthreads();
+  for (int b = t; b < NB; b += blockDim.x) H[b] = 0;
+  if (t == 0) {
     Sel32State s = st[h];
+    const int chosen = s_chosen;
+    const long long above = chosen >= 0 ? s_above : 0;
     s.remaining = rem - above;
     s.prefix = (pass == 0 ? 0u : (s.prefix << (hi - lo))) | (unsigned int)chosen;
     if (pass == S32_PASSES - 1) s32_set_eps(s, d, scale, fallback);
@@ -1149,7 +1189,7 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
   if (chunks < 1) chunks = 1;
   for (int pass = 0; pass < S32_PASSES; ++pass) {
     if (pass > 0) s32_hist_kernel<<<dim3(chunks, heads), 256, 0, st>>>(scores32, n, w.state, w.hist, pass, w.fallback);
-    s32_scan_kernel<<<heads, 32, 0, st>>>(w.state, w.hist, pass, w.fallback, d, scale);
+    s32_scan_kernel<<<heads, 1024, 0, st>>>(w.state, w.hist, pass, w.fallback, d, scale);
   }
   dim3 rows_grid((g + 7) / 8, heads);
   s32_mark_kernel<<<rows_grid, 256, 0, st>>>(scores32, qp, kp, g, d, scale, w.state, w.bm, w32, w.rowmax, w.argmax,
