@@ -1045,9 +1045,32 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
 // fp64, keep the `need` best (descending score, ties to the smaller flat
 // index), set their bits, emit the threshold.
 constexpr int S32_FINISH_SPLIT = 8;
+// fp64 rescoring of the band, one warp per candidate (coalesced fp64 row
+// reads): keys into bkey[head][S32_CAP]; grid (S32_SCORE_CTAS, heads)
+constexpr int S32_SCORE_CTAS = 64;
+__global__ void __launch_bounds__(256) s32_band_score_kernel(const double* __restrict__ qp,
+                                                             const double* __restrict__ kp, int g, int d, double scale,
+                                                             const Sel32State* __restrict__ st,
+                                                             const int* __restrict__ cand,
+                                                             unsigned long long* __restrict__ bkey,
+                                                             const int* __restrict__ fallback) {
+  if (*fallback) return;
+  const int h = blockIdx.y;
+  const int cnt = min(st[h].cand_count, S32_CAP);
+  const int lane = threadIdx.x & 31;
+  const int* C = cand + (long long)h * S32_CAP;
+  for (int c = blockIdx.x * 8 + (threadIdx.x >> 5); c < cnt; c += gridDim.x * 8) {
+    const int f = C[c];
+    const int i = f / g, j = f - i * g;
+    const double sc = score64_warp(qp + ((long long)h * g + i) * d, kp + ((long long)h * g + j) * d, d, scale);
+    if (lane == 0) bkey[(long long)h * S32_CAP + c] = score_key(sc);
+  }
+}
+
 __global__ void __launch_bounds__(1024) s32_finish_kernel(const double* __restrict__ qp,
                                                           const double* __restrict__ kp, int g, int d, double scale,
                                                           long long m, Sel32State* st, const int* __restrict__ cand,
+                                                          const unsigned long long* __restrict__ bkey,
                                                           unsigned int* bm, int w32, double* threshold,
                                                           int* fallback) {
   extern __shared__ unsigned char smraw[];
@@ -1065,17 +1088,10 @@ __global__ void __launch_bounds__(1024) s32_finish_kernel(const double* __restri
     return;
   }
   const int* C = cand + (long long)h * S32_CAP;
-  {  // one warp per candidate: coalesced fp64 row reads (every CTA of the head rescores the whole band)
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int c = wp; c < cnt; c += nw) {
-      const int f = C[c];
-      const int i = f / g, j = f - i * g;
-      const double sc = score64_warp(qp + ((long long)h * g + i) * d, kp + ((long long)h * g + j) * d, d, scale);
-      if (lane == 0) {
-        key[c] = score_key(sc);
-        idx[c] = f;
-      }
-    }
+  const unsigned long long* K = bkey + (long long)h * S32_CAP;  // fp64 band scores (s32_band_score_kernel)
+  for (int c = threadIdx.x; c < cnt; c += blockDim.x) {
+    key[c] = K[c];
+    idx[c] = C[c];
   }
   __syncthreads();
   unsigned int* Bh = bm + (long long)h * g * w32;
@@ -1136,6 +1152,7 @@ struct Sel32Ws {
   unsigned int* rowmax;
   int* argmax;
   int* cand;
+  unsigned long long* bkey;  // fp64 keys of the band candidates, [heads][S32_CAP]
   int* row_counts;
   int* row_forced;
   unsigned int* bm;
@@ -1156,6 +1173,7 @@ static Sel32Ws carve_sel32(void* base, int heads, int g, int d) {
   w.rowmax = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (size_t)heads * g));
   w.argmax = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * g));
   w.cand = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * S32_CAP));
+  w.bkey = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (size_t)heads * S32_CAP));
   w.row_counts = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * g));
   w.row_forced = reinterpret_cast<int*>(take(sizeof(int) * (size_t)heads * g));
   w.bm = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (size_t)heads * g * w32));
@@ -1196,8 +1214,10 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
                                              w.cand, w.fallback);
   const size_t fsmem = (sizeof(unsigned long long) + sizeof(int)) * S32_CAP;
   cudaFuncSetAttribute(s32_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
-  s32_finish_kernel<<<dim3(heads, S32_FINISH_SPLIT), 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bm, w32, threshold,
-                                               w.fallback);
+  s32_band_score_kernel<<<dim3(S32_SCORE_CTAS, heads), 256, 0, st>>>(qp, kp, g, d, scale, w.state, w.cand, w.bkey,
+                                                                    w.fallback);
+  s32_finish_kernel<<<dim3(heads, S32_FINISH_SPLIT), 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bkey,
+                                                                      w.bm, w32, threshold, w.fallback);
   s32_force_kernel<<<rows_grid, 256, 0, st>>>(w.bm, g, w32, w.argmax, force, w.row_counts, w.row_forced, w.fallback);
   scan_rows_kernel<<<heads, 1024, 0, st>>>(w.row_counts, row_ptr, g, g + 1, nullptr, 0, w.row_forced,
                                            reinterpret_cast<long long*>(forced), w.fallback, 0);
