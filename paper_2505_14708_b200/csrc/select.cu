@@ -1041,10 +1041,10 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
   }
 }
 
-// Per head (S32_FINISH_SPLIT CTAs, each ranking a slice): rescore the band in
-// fp64, keep the `need` best (descending score, ties to the smaller flat
-// index), set their bits, emit the threshold.
-constexpr int S32_FINISH_SPLIT = 8;
+// One CTA per head: sort the band (fp64 keys from s32_band_score_kernel) into
+// the reference order - descending score, ties to the smaller flat index -
+// with a bitonic sort in shared memory, keep the first `need`, set their bits
+// and emit the threshold.
 // fp64 rescoring of the band, one warp per candidate (coalesced fp64 row
 // reads): keys into bkey[head][S32_CAP]; grid (S32_SCORE_CTAS, heads)
 constexpr int S32_SCORE_CTAS = 64;
@@ -1089,26 +1089,38 @@ __global__ void __launch_bounds__(1024) s32_finish_kernel(const double* __restri
   }
   const int* C = cand + (long long)h * S32_CAP;
   const unsigned long long* K = bkey + (long long)h * S32_CAP;  // fp64 band scores (s32_band_score_kernel)
-  for (int c = threadIdx.x; c < cnt; c += blockDim.x) {
-    key[c] = K[c];
-    idx[c] = C[c];
+  int np = 1;
+  while (np < cnt) np <<= 1;
+  for (int c = threadIdx.x; c < np; c += blockDim.x) {  // padding sorts last (key 0, index INT_MAX)
+    key[c] = c < cnt ? K[c] : 0ull;
+    idx[c] = c < cnt ? C[c] : 0x7fffffff;
   }
   __syncthreads();
-  unsigned int* Bh = bm + (long long)h * g * w32;
-  // the O(cnt^2) ranking is split over gridDim.y CTAs per head (each rescored the whole band)
-  const int per = (cnt + gridDim.y - 1) / gridDim.y;
-  const int c0 = blockIdx.y * per, c1 = min(cnt, c0 + per);
-  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-    const unsigned long long kc = key[c];
-    const int fc = idx[c];
-    int rank = 0;
-    for (int o = 0; o < cnt; ++o) rank += (key[o] > kc) || (key[o] == kc && idx[o] < fc);
-    if (rank < need) {
-      const int i = fc / g, j = fc - i * g;
-      atomicOr(&Bh[(long long)i * w32 + (j >> 5)], 1u << (j & 31));
+  // bitonic sort into reference order: descending score, ties by ascending flat index
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < np / 2; t += blockDim.x) {
+        const int a = 2 * t - (t & (j - 1));  // lower element of the pair (bit j clear)
+        const int b = a + j;
+        const bool desc = (a & k) == 0;       // this run's direction
+        const unsigned long long ka = key[a], kb = key[b];
+        const int ia = idx[a], ib = idx[b];
+        const bool a_first = ka > kb || (ka == kb && ia < ib);
+        if (a_first != desc) {
+          key[a] = kb; key[b] = ka;
+          idx[a] = ib; idx[b] = ia;
+        }
+      }
+      __syncthreads();
     }
-    if (rank == need - 1) threshold[h] = key_score(kc);
   }
+  unsigned int* Bh = bm + (long long)h * g * w32;
+  for (int c = threadIdx.x; c < need; c += blockDim.x) {
+    const int fc = idx[c];
+    const int i = fc / g, j = fc - i * g;
+    atomicOr(&Bh[(long long)i * w32 + (j >> 5)], 1u << (j & 31));
+  }
+  if (threadIdx.x == 0) threshold[h] = key_score(key[need - 1]);
 }
 
 // Per row: force the first argmax in (force_row_keep) and count the row.
@@ -1216,7 +1228,7 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
   cudaFuncSetAttribute(s32_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
   s32_band_score_kernel<<<dim3(S32_SCORE_CTAS, heads), 256, 0, st>>>(qp, kp, g, d, scale, w.state, w.cand, w.bkey,
                                                                     w.fallback);
-  s32_finish_kernel<<<dim3(heads, S32_FINISH_SPLIT), 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bkey,
+  s32_finish_kernel<<<heads, 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bkey,
                                                                       w.bm, w32, threshold, w.fallback);
   s32_force_kernel<<<rows_grid, 256, 0, st>>>(w.bm, g, w32, w.argmax, force, w.row_counts, w.row_forced, w.fallback);
   scan_rows_kernel<<<heads, 1024, 0, st>>>(w.row_counts, row_ptr, g, g + 1, nullptr, 0, w.row_forced,
