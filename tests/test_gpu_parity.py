@@ -269,6 +269,26 @@ def test_hv720_sparsity_sweep_masks(sparsity):
     assert res.flops.sparse_logits_flops == 2 * ref.kept_count * 64 * 64 * 128
 
 
+def test_wan720_masks_and_sampled_rows():
+    # the second SURVEY config: Wan 720p, 21 x 45 x 80 tokens at 75 % sparsity
+    # (two of its 40 heads, generated with the same per-head seed streams)
+    grid, (q, k, v), (q64, k64, v64) = _inputs((21, 45, 80, 8, 8, 128, 40, 0), head_ids=[0, 1])
+    plan = da.pad_plan(21, 45, 80, 8, 8)
+    res = da.multi_head_sparse_attention(q, k, v, plan, 0.75, return_details=True)
+    out = res.output.float().cpu().numpy()
+    rows = np.arange(0, grid.num_regions, 97)
+    for hh in range(2):
+        ref = O.padded_sparse_attention(q64[hh], k64[hh], v64[hh], 21, 45, 80, 8, 8, 0.75, return_details=True,
+                                        sample_rows=rows)
+        got = res.mask.head(hh)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept)
+        assert got.kept_count == ref.mask.kept_count and got.forced_row_keeps == ref.mask.forced_row_keeps
+        src = O.real_source_index(grid)
+        pos = (rows[:, None] * grid.region_size + np.arange(grid.region_size)[None, :]).reshape(-1)
+        live = src[pos] >= 0
+        _close(out[hh][src[pos][live]], ref.output[src[pos][live]])
+
+
 # ---------------------------------------------------------------- executor seams and edge cases
 
 def _seam_case(g, p, d, heads, density, seed, key_valid=False):
