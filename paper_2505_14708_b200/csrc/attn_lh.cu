@@ -61,11 +61,20 @@ constexpr int P = 64;
 constexpr int D = 128;
 constexpr int TILE = 16384;
 constexpr int SLOT = 2 * TILE;  // a step: key regions j0, j1
-constexpr int KSL = 3;
-constexpr int VSL = 3;
+#ifndef LH_KSL
+#define LH_KSL 3
+#endif
+#ifndef LH_VSL
+#define LH_VSL 3
+#endif
+constexpr int KSL = LH_KSL;
+constexpr int VSL = LH_VSL;
 constexpr int INFO = 16;
 constexpr int RAGW = 512;
-constexpr int LISTCAP = 4096;
+#ifndef LH_LISTCAP
+#define LH_LISTCAP 4096
+#endif
+constexpr int LISTCAP = LH_LISTCAP;
 constexpr int IR = 8;
 constexpr int KBLK = 32;
 
