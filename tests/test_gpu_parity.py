@@ -525,3 +525,19 @@ def test_selection_fast_path_decides_the_mask(kind, expect_fallback):
     dbg = {}
     api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(128), "average", "logits", True, False, "hnd", debug=dbg)
     assert dbg["selection_fallback"] == expect_fallback
+
+
+@pytest.mark.parametrize("dims", [(2, 16, 48, 4, 16, 128, 2, 12), (3, 24, 40, 8, 8, 64, 2, 13)])
+def test_pipeline_other_pools_and_head_dims(dims):
+    # 64-token regions that are not 8x8 (4x16), and d = 64 with 8x8 pools:
+    # shapes the tcgen05 kernels do not take (the portable executor runs)
+    grid, (q, k, v), (q64, k64, v64) = _inputs(dims)
+    f, h, w, ph, pw = dims[:5]
+    plan = da.pad_plan(f, h, w, ph, pw)
+    res = da.multi_head_sparse_attention(q, k, v, plan, 0.8, return_details=True)
+    out = res.output.float().cpu().numpy()
+    for hh in range(q.shape[0]):
+        ref = O.padded_sparse_attention(q64[hh], k64[hh], v64[hh], f, h, w, ph, pw, 0.8, return_details=True)
+        got = res.mask.head(hh)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept)
+        _close(out[hh], ref.output)
