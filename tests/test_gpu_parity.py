@@ -541,3 +541,15 @@ def test_pipeline_other_pools_and_head_dims(dims):
         got = res.mask.head(hh)
         assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept)
         _close(out[hh], ref.output)
+
+
+@pytest.mark.parametrize("shared,select_on", [(True, "logits"), (False, "softmax"), (True, "softmax")])
+def test_720p_slice_shared_mask_and_softmax_selection(shared, select_on):
+    # the fp64 selection paths (head-mean basis, row-softmax basis) feeding the
+    # lane-half K4 on the 8x8 / d = 128 shape
+    grid, (q, k, v), (q64, k64, v64) = _inputs((2, 45, 80, 8, 8, 128, 3, 14))
+    plan = da.pad_plan(2, 45, 80, 8, 8)
+    out = da.multi_head_sparse_attention(q, k, v, plan, 0.85, shared_head_mask=shared, select_on=select_on)
+    ref = O.multi_head_sparse_attention(q64, k64, v64, 2, 45, 80, 8, 8, 0.85, shared_head_mask=shared,
+                                        select_on=select_on)
+    _close(out.float().cpu().numpy(), ref)
