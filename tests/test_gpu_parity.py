@@ -411,6 +411,17 @@ def test_host_inputs_pipelined_by_head_group_match_device_call():
     assert host.mask.kept_count == dev.mask.kept_count
     single = da.padded_sparse_attention(qh[1], kh[1], vh[1], 2, 45, 80, 8, 8, 0.9)
     assert torch.equal(single, dev.output[1].cpu())
+    # float32 host inputs: the output keeps the inputs' dtype (result_type,
+    # sparse.py:129-131) and equals the device call on the same values
+    qf, kf, vf = (x.float() for x in (qh, kh, vh))
+    hf = da.multi_head_sparse_attention(qf, kf, vf, plan, 0.9)
+    assert hf.dtype == torch.float32 and hf.device.type == "cpu"
+    df = da.multi_head_sparse_attention(qf.cuda(), kf.cuda(), vf.cuda(), plan, 0.9)
+    assert torch.equal(hf, df.cpu())
+    # caller-provided host output buffer
+    buf = torch.empty_like(host.output).pin_memory()
+    o2 = da.multi_head_sparse_attention(qh, kh, vh, plan, 0.9, out=buf)
+    assert o2.data_ptr() == buf.data_ptr() and torch.equal(buf, dev.output.cpu())
 
 
 @pytest.mark.parametrize("kind", ["zeros", "constant_rows", "nan_row"])
