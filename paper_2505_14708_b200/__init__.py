@@ -17,7 +17,11 @@ from .api import (
     draft_sparse_attention,
     flops_count,
     head_dim_scale,
+    kept_from_bitmap,
     mask_density_stats,
+    mask_from_json_dict,
+    mask_to_bitmap,
+    mask_to_json_dict,
     multi_head_sparse_attention,
     pad_plan,
     padded_sparse_attention,
@@ -34,7 +38,8 @@ __version__ = "0.1.0"
 __all__ = [
     "FlopsReport", "LatentLayout", "PadPlan", "PipelineResult", "RegionMask",
     "block_sparse_attention", "draft_logits", "draft_sparse_attention", "flops_count",
-    "head_dim_scale", "mask_density_stats", "multi_head_sparse_attention", "pad_plan",
+    "head_dim_scale", "kept_from_bitmap", "mask_density_stats", "mask_from_json_dict", "mask_to_bitmap",
+    "mask_to_json_dict", "multi_head_sparse_attention", "pad_plan",
     "padded_sparse_attention", "pool_regions", "pool_tokens", "reorder_tokens",
     "restore_tokens", "select_top_fraction", "top_fraction_count", "__version__",
 ]

@@ -10,17 +10,22 @@ defaults and ValueError messages of /root/reference/pkg/src/draftattn):
     select_top_fraction       masking.py:59-91
     draft_logits / pool_regions / top_fraction_count / head_dim_scale / flops_count
 
-Tensors are torch CUDA tensors (bf16 compute; other float dtypes are cast to
-bf16 on entry and the output is cast back, matching the reference's
-``result_type(q, k, v)`` output dtype). Token matrices are ``(n, d)`` or
-``(heads, n, d)``; ``qkv_layout="nhd"`` accepts the DiT ``(n, heads, d)``
-layout without a copy. All work runs in hand-written sm_100a kernels behind the
-C ABI (include/draftattn_b200.h); there is no CPU path.
+Tensors are torch tensors (bf16 compute: float32 / float64 inputs are rounded
+to bf16 on entry, so masks and outputs are those of the bf16-rounded inputs,
+and the output is cast back to the reference's ``result_type(q, k, v)``).
+Token matrices are ``(n, d)`` or ``(heads, n, d)``; ``qkv_layout="nhd"``
+accepts the DiT ``(n, heads, d)`` layout and ``qkv_layout="bnhd"`` a batch of
+them, ``(batch, n, heads, d)``, without a copy. Any head dim works: dims that
+are not a multiple of 8 are zero-padded to one (exact: zero features add
+nothing to any dot product). Host (CPU) tensors are staged to the GPU. All
+work runs in hand-written sm_100a kernels behind the C ABI
+(include/draftattn_b200.h); there is no CPU compute path.
 """
 
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import math
 from dataclasses import dataclass, field
 
@@ -32,6 +37,7 @@ from ._lib import DaAttnArgs, DaPipelineArgs, check, lib, make_grid
 _CEIL_EPS = 1e-9
 POOL_MODES = ("average", "max")
 SELECT_MODES = ("logits", "softmax")
+QKV_LAYOUTS = ("hnd", "nhd", "bnhd")
 
 
 # --------------------------------------------------------------------------
@@ -219,6 +225,48 @@ class RegionMask:
                           self.col_idx[h:h + 1], self.thresholds[h:h + 1], self.forced[h:h + 1],
                           self.kept_counts[h:h + 1], single=True)
 
+    @classmethod
+    def from_kept(cls, kept, keep_ratio: float, threshold, forced_row_keeps=0, device=None) -> "RegionMask":
+        """A GPU mask (executor lists + packed bitmap) from a boolean (g, g) or
+        (heads, g, g) kept matrix (numpy or torch), e.g. a cached mask reused
+        across denoising steps. ``threshold`` / ``forced_row_keeps``: scalars or
+        one per head."""
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        k = torch.as_tensor(kept, device=dev)
+        if k.dtype != torch.bool:
+            raise ValueError(f"kept must be a boolean matrix, got {k.dtype}")
+        single = k.ndim == 2
+        if single:
+            k = k.unsqueeze(0)
+        if k.ndim != 3 or k.shape[1] != k.shape[2]:
+            raise ValueError(f"kept must be a square boolean matrix, got shape {tuple(kept.shape)}")
+        heads, g, _ = k.shape
+        counts = k.sum(dim=2, dtype=torch.int64)
+        row_ptr = torch.zeros((heads, g + 1), dtype=torch.int32, device=dev)
+        row_ptr[:, 1:] = torch.cumsum(counts, dim=1).to(torch.int32)
+        totals = counts.sum(dim=1)
+        cap = max(1, int(totals.max().item()) if heads else 1)
+        col_idx = torch.zeros((heads, cap), dtype=torch.int32, device=dev)
+        for h in range(heads):
+            cols = k[h].nonzero()[:, 1]  # row-major: rows ascending, columns ascending within a row
+            col_idx[h, :cols.numel()] = cols.to(torch.int32)
+        nbytes = (g * g + 7) // 8
+        bits = torch.zeros((heads, nbytes * 8), dtype=torch.int32, device=dev)
+        bits[:, :g * g] = k.reshape(heads, -1).to(torch.int32)
+        w = torch.tensor([128, 64, 32, 16, 8, 4, 2, 1], dtype=torch.int32, device=dev)
+        packed = (bits.view(heads, nbytes, 8) * w).sum(-1).to(torch.uint8)
+        thr = torch.as_tensor(threshold, dtype=torch.float64, device=dev).reshape(-1).expand(heads).contiguous()
+        forced = torch.as_tensor(forced_row_keeps, dtype=torch.int64, device=dev).reshape(-1).expand(heads)
+        return cls(g, float(keep_ratio), packed, row_ptr, col_idx, thr, forced.contiguous(), totals,
+                   single=single)
+
+    @classmethod
+    def from_bitmap(cls, raw: bytes, g: int, keep_ratio: float, threshold, forced_row_keeps=0,
+                    device=None) -> "RegionMask":
+        """Inverse of ``bitmap_bytes`` (masking.py:168-176): a GPU mask from the
+        reference's packed row-major bitmap of one head."""
+        return cls.from_kept(kept_from_bitmap(raw, g), keep_ratio, threshold, forced_row_keeps, device)
+
 
 def mask_density_stats(mask: RegionMask, head: int = 0) -> dict:
     """Occupancy summary of one head (masking.py:128-141)."""
@@ -236,6 +284,52 @@ def mask_density_stats(mask: RegionMask, head: int = 0) -> dict:
         "row_kept_max": int(rows.max().item()),
         "forced_row_keeps": m.forced_row_keeps,
     }
+
+
+def mask_to_bitmap(mask: RegionMask, head: int = 0) -> bytes:
+    """Row-major packed bits of one head's kept matrix (masking.py:168-170)."""
+    return mask.bitmap_bytes(head)
+
+
+def kept_from_bitmap(raw: bytes, g: int) -> torch.Tensor:
+    """Unpack a row-major bitmap into a (g, g) bool tensor on the CPU (masking.py:173-176)."""
+    if g < 1:
+        raise ValueError(f"g must be positive, got {g}")
+    data = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+    if data.numel() * 8 < g * g:
+        raise ValueError(f"bitmap of {data.numel()} bytes is too short for g = {g}")
+    bits = torch.tensor([128, 64, 32, 16, 8, 4, 2, 1], dtype=torch.uint8)
+    return ((data.unsqueeze(-1) & bits) != 0).reshape(-1)[: g * g].reshape(g, g)
+
+
+def mask_to_json_dict(mask: RegionMask, head: int = 0) -> dict:
+    """JSON-ready export of one head: metadata plus the kept coordinate list in
+    row-major order (masking.py:144-155)."""
+    m = mask.head(head) if not mask.single else mask
+    total = int(m.row_ptr[0, m.g].item())
+    rows = torch.repeat_interleave(torch.arange(m.g, device=m.row_ptr.device),
+                                   (m.row_ptr[0, 1:] - m.row_ptr[0, :-1]).to(torch.int64))
+    cols = m.col_idx[0, :total]
+    pairs = torch.stack([rows.to(torch.int64), cols.to(torch.int64)], dim=1).cpu().tolist()
+    return {
+        "g": m.g,
+        "keep_ratio": m.keep_ratio,
+        "threshold": m.threshold,
+        "kept_count": int(m.kept_count),
+        "forced_row_keeps": int(m.forced_row_keeps),
+        "kept": pairs,
+    }
+
+
+def mask_from_json_dict(data: dict, device=None) -> RegionMask:
+    """Inverse of ``mask_to_json_dict`` (masking.py:158-166), on the GPU."""
+    g = int(data["g"])
+    kept = torch.zeros((g, g), dtype=torch.bool)
+    if data["kept"]:
+        idx = torch.as_tensor(data["kept"], dtype=torch.int64)
+        kept[idx[:, 0], idx[:, 1]] = True
+    return RegionMask.from_kept(kept, float(data["keep_ratio"]), float(data["threshold"]),
+                                int(data.get("forced_row_keeps", 0)), device)
 
 
 @dataclass(frozen=True)
@@ -293,9 +387,11 @@ def _stream_ptr(device) -> int:
 
 
 def _as_heads(x: torch.Tensor, qkv_layout: str, name: str):
-    """Return (tensor_3d, head_stride, row_stride, squeeze) for (n,d)/(h,n,d)/(n,h,d)."""
+    """Return (heads-first 3-d view, squeeze) for (n,d) / (h,n,d) / (n,h,d)."""
     if not isinstance(x, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor on a CUDA device")
+    if qkv_layout not in ("hnd", "nhd"):
+        raise ValueError(f"qkv_layout must be one of {QKV_LAYOUTS}, got {qkv_layout!r}")
     if x.ndim == 2:
         x3 = x.unsqueeze(0)
         squeeze = True
@@ -320,6 +416,18 @@ def _prep(x3: torch.Tensor) -> torch.Tensor:
 
 def _out_dtype(q, k, v):
     return torch.promote_types(torch.promote_types(q.dtype, k.dtype), v.dtype)
+
+
+def _pad_features(x3: torch.Tensor) -> torch.Tensor:
+    """(heads, n, d) -> bf16 (heads, n, ceil8(d)) with zero features appended
+    (zeros change no dot product, pooled mean or weighted sum)."""
+    d = x3.shape[2]
+    d8 = -(-d // 8) * 8
+    if not x3.is_cuda:
+        raise ValueError("inputs must be CUDA tensors (the B200 path has no CPU fallback)")
+    out = torch.zeros((x3.shape[0], x3.shape[1], d8), dtype=torch.bfloat16, device=x3.device)
+    out[..., :d] = x3
+    return out
 
 
 def _alloc_like_layout(heads, n, dv, qkv_layout, device):
@@ -356,8 +464,8 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
               shared_head_mask, qkv_layout, force_portable=False, attn_events=None, want_bitmap=True,
               out_dev=None, debug=None):
     """Run the fused C-ABI pipeline; returns (output, mask, squeeze). ``out_dev``
-    (internal): a preallocated contiguous (heads, n, dv) bf16 device tensor the
-    output is written into (``hnd`` layout only)."""
+    (internal): a preallocated bf16 device tensor, in the inputs' layout, the
+    output is written into."""
     q3, squeeze = _as_heads(q, qkv_layout, "q")
     k3, _ = _as_heads(k, qkv_layout, "k")
     v3, _ = _as_heads(v, qkv_layout, "v")
@@ -367,6 +475,19 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     if v3.shape[:2] != q3.shape[:2]:
         raise ValueError(f"v rows {v3.shape[1]} != key rows {n}")
     out_dtype = _out_dtype(q, k, v)
+    if d % 8 or v3.shape[2] % 8:
+        # zero-pad the features to a multiple of 8 (exact) and drop the padded
+        # output features; the caller's scale is kept
+        dv0 = v3.shape[2]
+        o, mask, _ = _pipeline(_pad_features(q3), _pad_features(k3), _pad_features(v3), plan, sparsity, scale,
+                               pool_mode, select_on, force_row_keep, shared_head_mask, "hnd", force_portable,
+                               attn_events, want_bitmap, None, debug)
+        o = o[..., :dv0]
+        if out_dev is not None:
+            _as_heads(out_dev, qkv_layout, "out")[0].copy_(o)
+            return out_dev, mask, squeeze
+        out = o[0] if squeeze else (o.transpose(0, 1) if qkv_layout == "nhd" else o)
+        return (out.to(out_dtype) if out_dtype != out.dtype else out), mask, squeeze
     q3, k3, v3 = _prep(q3), _prep(k3), _prep(v3)
     dv = v3.shape[2]
     layout = plan.layout
@@ -384,7 +505,12 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     ws_bytes = lib().da_pipeline_workspace_size(ctypes.byref(grid), heads, d)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     if out_dev is not None:
-        o_base = o3 = out_dev
+        # the caller's bf16 output buffer, in the inputs' layout
+        o3, _ = _as_heads(out_dev, qkv_layout, "out")
+        if o3.dtype != torch.bfloat16 or tuple(o3.shape) != (heads, n, dv) or o3.device != dev or \
+                o3.stride(2) != 1 or o3.stride(0) % 8 or o3.stride(1) % 8 or o3.data_ptr() % 16:
+            raise ValueError("internal output buffer has the wrong shape, dtype or strides")
+        o_base = out_dev
     else:
         o_base, o3 = _alloc_like_layout(heads, n, dv, qkv_layout if not squeeze else "hnd", dev)
     pa = DaPipelineArgs()
@@ -429,6 +555,53 @@ def _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, s
     else:
         o, mask, _ = _pipeline_host(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep,
                                     shared_head_mask, qkv_layout, out=out, details=details)
+    return o, mask
+
+
+def _run_layout(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask, qkv_layout,
+                out, details=True):
+    """``_run`` plus the batched DiT layout ``qkv_layout="bnhd"``: (batch, n,
+    heads, d) inputs, one pipeline call per batch element on its (n, heads, d)
+    slice (no copies), written straight into a (batch, n, heads, dv) output.
+    The mask stacks the batch elements' heads, batch-major (per element: one
+    mask per head, or one shared mask with ``shared_head_mask``)."""
+    if qkv_layout != "bnhd":
+        return _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask,
+                    qkv_layout, out, details)
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(x, torch.Tensor) or x.ndim != 4:
+            raise ValueError(f"qkv_layout='bnhd' expects (batch, n, heads, d) tensors; {name} has shape "
+                             f"{tuple(getattr(x, 'shape', ()))}")
+    if k.shape != q.shape:
+        raise ValueError(f"k shape {tuple(k.shape)} does not match q shape {tuple(q.shape)}")
+    if v.shape[:3] != q.shape[:3]:
+        raise ValueError(f"v shape {tuple(v.shape)} does not match q's (batch, n, heads) {tuple(q.shape[:3])}")
+    batch, n, heads, _ = q.shape
+    dv = v.shape[3]
+    out_dtype = _out_dtype(q, k, v)
+    masks = []
+    if q.is_cuda:
+        if out is not None:
+            raise ValueError("out= is for host inputs; device calls return a fresh tensor")
+        res = torch.empty((batch, n, heads, dv), dtype=torch.bfloat16, device=q.device)
+        for b in range(batch):
+            _, m_b, _ = _pipeline(q[b], k[b], v[b], plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                                  shared_head_mask, "nhd", want_bitmap=details, out_dev=res[b])
+            masks.append(m_b)
+        o = res if out_dtype == torch.bfloat16 else res.to(out_dtype)
+    else:
+        if out is None:
+            out = torch.empty((batch, n, heads, dv), dtype=out_dtype, pin_memory=torch.cuda.is_available())
+        elif out.shape != (batch, n, heads, dv) or out.dtype != out_dtype or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous CPU tensor of shape {(batch, n, heads, dv)} and dtype {out_dtype}")
+        for b in range(batch):
+            _, m_b, _ = _pipeline_host(q[b], k[b], v[b], plan, sparsity, scale, pool_mode, select_on, force_row_keep,
+                                       shared_head_mask, "nhd", out=out[b], details=details)
+            masks.append(m_b)
+        o = out
+    mask = _cat_masks(masks)
+    if mask.single:  # a one-element batch with a shared mask: still indexed per batch element
+        mask = dataclasses.replace(mask, single=False)
     return o, mask
 
 
@@ -482,11 +655,13 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
         groups = _head_groups(heads, hg)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     if out is not None:
-        o3, _ = _as_heads(out, qkv_layout, "out")
-        if o3.device.type != "cpu" or tuple(o3.shape) != (heads, n, dv) or o3.dtype != out_dtype or \
-                not o3.is_contiguous():
-            raise ValueError(f"out must be a contiguous CPU tensor of shape {(heads, n, dv)} and dtype {out_dtype}")
-        out_host = o3
+        # validated in the caller's own layout: (n, dv), (heads, n, dv) or, for
+        # qkv_layout="nhd", (n, heads, dv)
+        want = (n, dv) if squeeze else ((n, heads, dv) if qkv_layout == "nhd" else (heads, n, dv))
+        if not isinstance(out, torch.Tensor) or out.device.type != "cpu" or tuple(out.shape) != want or \
+                out.dtype != out_dtype or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous CPU tensor of shape {want} and dtype {out_dtype}")
+        out_host, _ = _as_heads(out, qkv_layout, "out")
     else:
         # pinned so the per-group downloads are asynchronous (pass out= to reuse a buffer)
         out_host = torch.empty((heads, n, dv), dtype=out_dtype, pin_memory=True)
@@ -526,6 +701,17 @@ def _pipeline_host(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on
     return res, _cat_masks(masks), squeeze
 
 
+def _rows_and_dim(q, qkv_layout: str):
+    """(token rows, head dim) of q in the caller's layout."""
+    if qkv_layout == "bnhd":
+        if not isinstance(q, torch.Tensor) or q.ndim != 4:
+            raise ValueError(f"qkv_layout='bnhd' expects (batch, n, heads, d) tensors, got shape "
+                             f"{tuple(getattr(q, 'shape', ()))}")
+        return q.shape[1], q.shape[3]
+    q3, _ = _as_heads(q, qkv_layout, "q")
+    return q3.shape[1], q3.shape[2]
+
+
 def _details(out, mask: RegionMask, layout: LatentLayout, d: int):
     if mask.single:
         return PipelineResult(out, mask, flops_count(layout, d, kept_count=int(mask.kept_count)),
@@ -555,14 +741,13 @@ def padded_sparse_attention(q, k, v, frames, height, width, patch_h, patch_w, sp
     _validate_pipeline_args(sparsity, select_on, pool_mode)
     if not plan.is_identity and pool_mode != "average":
         raise ValueError("padded grids support average pooling only")
-    q3, _ = _as_heads(q, qkv_layout, "q")
-    if q3.shape[1] != plan.num_valid:
+    rows, d = _rows_and_dim(q, qkv_layout)
+    if rows != plan.num_valid:
         raise ValueError(f"expected ({plan.num_valid}, d) real-token rows, got {tuple(q.shape)}")
-    d = q3.shape[2]
     if scale is None:
         scale = head_dim_scale(d)
-    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out,
-                     return_details)
+    out, mask = _run_layout(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout,
+                            out, return_details)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)
@@ -574,15 +759,14 @@ def draft_sparse_attention(q, k, v, layout: LatentLayout, sparsity, scale=None, 
     """Full pipeline on a divisible grid (sparse.py:193-246)."""
     del two_pass
     _validate_pipeline_args(sparsity, select_on, pool_mode)
-    q3, _ = _as_heads(q, qkv_layout, "q")
-    if q3.shape[1] != layout.num_tokens:
-        raise ValueError(f"q rows {q3.shape[1]} != layout token count {layout.num_tokens}")
-    d = q3.shape[2]
+    rows, d = _rows_and_dim(q, qkv_layout)
+    if rows != layout.num_tokens:
+        raise ValueError(f"q rows {rows} != layout token count {layout.num_tokens}")
     if scale is None:
         scale = head_dim_scale(d)
     plan = PadPlan(layout.frames, layout.height, layout.width, layout)
-    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout, out,
-                     return_details)
+    out, mask = _run_layout(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, False, qkv_layout,
+                            out, return_details)
     if not return_details:
         return out
     return _details(out, mask, layout, d)
@@ -596,21 +780,20 @@ def multi_head_sparse_attention(q, k, v, layout: LatentLayout, sparsity, shared_
     ``layout`` may also be a PadPlan for ragged grids (the reference has no
     padded multi-head entry; this is the batched form of its per-head loop).
     """
-    if q.ndim != 3:
+    if q.ndim != (4 if qkv_layout == "bnhd" else 3):
         raise ValueError(f"expected (heads, n, d) inputs, got shape {tuple(q.shape)}")
     _validate_pipeline_args(sparsity, select_on, pool_mode)
     plan = layout if isinstance(layout, PadPlan) else PadPlan(layout.frames, layout.height,
                                                                 layout.width, layout)
     if not plan.is_identity and pool_mode != "average":
         raise ValueError("padded grids support average pooling only")
-    q3, _ = _as_heads(q, qkv_layout, "q")
-    if q3.shape[1] != plan.num_valid:
-        raise ValueError(f"q rows {q3.shape[1]} != layout token count {plan.num_valid}")
-    d = q3.shape[2]
+    rows, d = _rows_and_dim(q, qkv_layout)
+    if rows != plan.num_valid:
+        raise ValueError(f"q rows {rows} != layout token count {plan.num_valid}")
     if scale is None:
         scale = head_dim_scale(d)
-    out, mask = _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask,
-                     qkv_layout, out, return_details)
+    out, mask = _run_layout(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask,
+                            qkv_layout, out, return_details)
     if not return_details:
         return out
     return _details(out, mask, plan.layout, d)
@@ -626,7 +809,8 @@ def reorder_tokens(x, plan: PadPlan, *, qkv_layout="hnd") -> torch.Tensor:
     Returns dense (heads, n_pad, d) (or (n_pad, d) for 2-d input) in patch-contiguous order.
     """
     x3, squeeze = _as_heads(x, qkv_layout, "x")
-    x3 = _prep(x3)
+    d0 = x3.shape[2]
+    x3 = _prep(x3) if d0 % 8 == 0 else _pad_features(x3)
     heads, n, d = x3.shape
     if n != plan.num_valid:
         raise ValueError(f"expected ({plan.num_valid}, d) real-token rows, got {tuple(x.shape)}")
@@ -636,13 +820,15 @@ def reorder_tokens(x, plan: PadPlan, *, qkv_layout="hnd") -> torch.Tensor:
     with torch.cuda.device(x3.device):
         check(lib().da_permute_in(x3.data_ptr(), x3.stride(0), x3.stride(1), out.data_ptr(), heads, d,
                                   ctypes.byref(grid), _stream_ptr(x3.device)), "permute_in")
+    out = out[..., :d0] if d0 != d else out
     return out[0] if squeeze else out
 
 
 def restore_tokens(x_r, plan: PadPlan) -> torch.Tensor:
     """extract_rows(permute_rows(x_r, perm.inverse), plan) (padding.py:157): K5, bit-exact."""
     x3, squeeze = _as_heads(x_r, "hnd", "x_r")
-    x3 = _prep(x3).contiguous()
+    d0 = x3.shape[2]
+    x3 = _prep(x3).contiguous() if d0 % 8 == 0 else _pad_features(x3)
     heads, n_pad, d = x3.shape
     lay = plan.layout
     if n_pad != lay.num_tokens:
@@ -652,6 +838,7 @@ def restore_tokens(x_r, plan: PadPlan) -> torch.Tensor:
     with torch.cuda.device(x3.device):
         check(lib().da_permute_out(x3.data_ptr(), out.data_ptr(), out.stride(0), out.stride(1), heads, d,
                                    ctypes.byref(grid), _stream_ptr(x3.device)), "permute_out")
+    out = out[..., :d0] if d0 != d else out
     return out[0] if squeeze else out
 
 
@@ -667,7 +854,8 @@ def pool_tokens(x, plan: PadPlan, mode="average", *, qkv_layout="hnd") -> torch.
     if mode != "average" and not plan.is_identity:
         raise ValueError("padded grids support average pooling only")
     x3, squeeze = _as_heads(x, qkv_layout, "x")
-    x3 = _prep(x3)
+    d0 = x3.shape[2]
+    x3 = _prep(x3) if d0 % 8 == 0 else _pad_features(x3)
     heads, n, d = x3.shape
     lay = plan.layout
     out = torch.empty((heads, lay.num_regions, d), dtype=torch.float64, device=x3.device)
@@ -675,6 +863,7 @@ def pool_tokens(x, plan: PadPlan, mode="average", *, qkv_layout="hnd") -> torch.
     with torch.cuda.device(x3.device):
         check(lib().da_pool(x3.data_ptr(), x3.stride(0), x3.stride(1), out.data_ptr(), heads, d, ctypes.byref(grid),
                             POOL_MODES.index(mode), _stream_ptr(x3.device)), "pool")
+    out = out[..., :d0] if d0 != d else out
     return out[0] if squeeze else out
 
 
@@ -779,7 +968,12 @@ def block_sparse_attention(q_r, k_r, v_r, mask: RegionMask, scale=None, key_vali
     if scale is None:
         scale = head_dim_scale(d)
     out_dtype = _out_dtype(q_r, k_r, v_r)
-    q3, k3, v3 = _prep(q3).contiguous(), _prep(k3).contiguous(), _prep(v3).contiguous()
+    dv0 = v3.shape[2]
+    if d % 8 or dv0 % 8:  # zero features: exact (see _pad_features)
+        q3, k3, v3 = _pad_features(q3), _pad_features(k3), _pad_features(v3)
+    else:
+        q3, k3, v3 = _prep(q3), _prep(k3), _prep(v3)
+    d = q3.shape[2]
     dv = v3.shape[2]
     kv_ptr = None
     if key_valid is not None:
@@ -804,5 +998,6 @@ def block_sparse_attention(q_r, k_r, v_r, mask: RegionMask, scale=None, key_vali
     with torch.cuda.device(q3.device):
         check(lib().da_block_sparse_fwd(ctypes.byref(a), ctypes.byref(grid), _stream_ptr(q3.device)),
               "block_sparse_fwd")
+    out = out[..., :dv0] if dv0 != dv else out
     out = out[0] if squeeze else out
     return out.to(out_dtype) if out_dtype != torch.bfloat16 else out

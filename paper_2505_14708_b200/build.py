@@ -13,7 +13,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libdraftattn_b200.so"
-SOURCES = ["api.cu", "prep.cu", "select.cu", "attn_portable.cu", "attn_tc.cu", "attn_pair.cu", "attn_lh.cu"]
+SOURCES = ["api.cu", "prep.cu", "select.cu", "attn_portable.cu", "attn_lh.cu"]
 HEADERS = ["common.cuh", "kernels.h"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 

@@ -2,10 +2,13 @@
 // reporting, workspace carving and the whole-pipeline driver. Validation
 // mirrors the reference's ValueError conditions where they apply to raw
 // buffers; the Python host layer raises the reference's own messages first.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -37,6 +40,56 @@ bool grid_ok(const da_grid* g) {
 size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
 
 }  // namespace
+
+namespace da {
+
+// Per-device facts, filled once per device and never changed afterwards.
+namespace {
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sms[kMaxDevices];
+std::mutex g_optin_mu;
+struct OptIn {
+  const void* kernel;
+  int dev;
+  int bytes;
+};
+std::vector<OptIn> g_optin;
+}  // namespace
+
+int device_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 1;
+  }
+  int n = g_sms[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 1;
+    g_sms[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+cudaError_t ensure_smem_optin(const void* kernel, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_optin_mu);
+  for (OptIn& o : g_optin)
+    if (o.kernel == kernel && o.dev == dev) {
+      if (o.bytes >= bytes) return cudaSuccess;
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) o.bytes = bytes;
+      return e;
+    }
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) g_optin.push_back({kernel, dev, bytes});
+  return e;
+}
+
+}  // namespace da
 
 extern "C" {
 
@@ -143,7 +196,7 @@ static int check_attn(const da_attn_args* a, const da_grid* grid) {
 
 size_t da_attn_workspace_size(int32_t heads, const da_grid* grid) {
   if (!grid_ok(grid) || heads < 1) return 0;
-  return da::pair_attn_workspace_size(heads, da::make_geo(*grid));
+  return da::attn_workspace_size(heads, da::make_geo(*grid));
 }
 
 static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, void* stream, const float* kpart,
@@ -162,10 +215,7 @@ static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, 
   if (!args->force_portable && da::tc_supported(*args, g)) {
     if (!args->workspace)
       return fail(DA_EINVAL, "block_sparse_fwd: the tcgen05 path needs a workspace (da_attn_workspace_size)");
-    const char* why = "";
-    cudaError_t e = da::launch_tc_attn(*args, g, st, &why, kpart, kblk, tiles_ready);
-    if (e == cudaErrorInvalidValue && why[0]) return fail(DA_ECUDA, "block_sparse_fwd (tcgen05): %s", why);
-    return cuda_status(e, "block_sparse_fwd (tcgen05)");
+    return cuda_status(da::launch_tc_attn(*args, g, st, kpart, kblk, tiles_ready), "block_sparse_fwd (tcgen05)");
   }
   if (da::portable_smem_bytes(g.p, args->d, args->dv) > 227 * 1024)
     return fail(DA_EINVAL, "block_sparse_fwd: region size %d with d=%d, dv=%d exceeds the portable kernel's "
@@ -198,7 +248,7 @@ static PipeWs carve(void* base, const da::Geo& g, int heads, int d) {
   // fp64 scores, or the fp32 planes of the guard-band path (per-head stride g * g rounded up to 4)
   w.scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)heads * ((size_t)g.g * g.g + 2)));
   w.sel = take(da::select_workspace_size(heads, g.g));
-  w.attn = take(da::pair_attn_workspace_size(heads, g));
+  w.attn = take(da::attn_workspace_size(heads, g));
   w.sel32 = take(da::select32_workspace_size(heads, g.g, d));
   w.kpart = reinterpret_cast<float*>(take(sizeof(float) * (size_t)heads * (da::pool_norm_blocks(d, g) + 1)));
   w.pnorm = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 2 * (size_t)heads));
@@ -275,8 +325,8 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   if ((rc = cuda_status(da::launch_pool2(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.k, a.k_head_stride,
                                          a.k_row_stride, w.kp, a.heads, a.d, pa->pool_mode, g, st,
                                          kblk > 0 ? w.kpart : nullptr, tiles ? a.v : nullptr, a.v_head_stride,
-                                         a.v_row_stride, tiles ? da::pair_attn_tiles(w.attn, a.heads, g, 0) : nullptr,
-                                         tiles ? da::pair_attn_tiles(w.attn, a.heads, g, 1) : nullptr,
+                                         a.v_row_stride, tiles ? da::attn_tiles(w.attn, a.heads, g, 0) : nullptr,
+                                         tiles ? da::attn_tiles(w.attn, a.heads, g, 1) : nullptr,
                                          kblk > 0 ? w.pnorm : nullptr),
                         "pool")))
     return rc;

@@ -35,10 +35,15 @@
 // warp 2 V copies; warp 3 GEMM2 issuer; warps 4-7 / 8-11 softmax warpgroups
 // for lane half 0 / 1 (each also loads half of Q's features into both halves
 // and writes half of the output features).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.h"
+
+// LH_FAKELOAD (probe builds only, tools/probes): bit 0 skips the K copies,
+// bit 1 the V copies, bit 2 the softmax work. Results are then wrong; the
+// shipped library is built with 0.
+#ifndef LH_FAKELOAD
+#define LH_FAKELOAD 0
+#endif
 
 // LH_PROF: per-CTA cycle accounting of the waits (tools/probes/lh_prof.py),
 // written to the da_debug_trace buffer as [CTA][32] int64 at kernel end
@@ -120,7 +125,6 @@ struct Params {
   int* fb_count;
   int* fb_items;
   int* work;
-  int fake_load;
   uint64_t pol_kv, pol_q, pol_o;
   long long* trace;  // LH_PROF output ([CTA][32]) or null
 };
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
     }
     fence_barrier_init();
   }
-  if (p.fake_load) {
+  if (LH_FAKELOAD) {
     for (int i = threadIdx.x; i < SMEM_END / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
   }
@@ -393,7 +397,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
           const int s = kq % NSL;
           if (kq >= NSL) { LH_T0(); mbar_wait(&empty[s], ((kq / NSL) - 1) & 1); LH_ACC(is_k ? 16 : 17); }
           ++kq;
-          if (p.fake_load & (is_k ? 1 : 2)) {
+          if (LH_FAKELOAD & (is_k ? 1 : 2)) {
             mbar_arrive(&full[s]);
             continue;
           }
@@ -583,15 +587,15 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         const int sb = (gs >> 1) % NSB;
         { LH_T0(); mbar_wait_spin(&B.s_full[wg][sb], (uint32_t)((gs / (2 * NSB)) & 1)); LH_ACC(10); }
         tc_fence_after();
-        const bool kp = ((e.z >> c) & 1) && !(p.fake_load & 4);
-        if (!(p.fake_load & 4)) {
+        const bool kp = ((e.z >> c) & 1) && !(LH_FAKELOAD & 4);
+        if (!(LH_FAKELOAD & 4)) {
           tmem_ld16x2_32(th + COL_S + 128 * sb, x);
           tmem_ld16x2_32hi(th + COL_S + 128 * sb + 32, x);
           tmem_ld_wait();
         }
         tc_fence_before();
         mbar_arrive(&B.s_free[wg][sb]);  // scores in registers: GEMM1 may refill this buffer
-        if (!(p.fake_load & 4)) {
+        if (!(LH_FAKELOAD & 4)) {
           const int j = c ? e.y : e.x;
           const bool rag = (e.z >> (2 + c)) & 1;
           const unsigned long long vm = kp ? (rag ? key_mask(p, j) : ~0ull) : 0ull;
@@ -730,13 +734,123 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
   }
 }
 
+// K and V re-laid out as per-region tiles that are byte-for-byte the
+// shared-memory image the MMAs read (GROUPED layout, kv_tile_offset_grouped;
+// padding rows zero): the attention kernel fetches each tile with one
+// contiguous bulk copy. The pipeline's pooling pass writes these itself; this
+// kernel serves the block-sparse seam. grid (g, heads, 2 tensors), 256 threads.
+struct KvTileArgs {
+  const __nv_bfloat16* x[2];
+  long long hs[2], rs[2];
+  uint8_t* out[2];
+  int layout;
+};
+__global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, RegionDecoder dec) {
+  const int j = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
+  const RegionXY rc = dec(j);
+  const uint4* src = reinterpret_cast<const uint4*>(a.x[z] + h * a.hs[z]);
+  const long long rs8 = a.rs[z] / 8;
+  uint8_t* dst = a.out[z] + ((long long)h * g.g + j) * TILE;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = threadIdx.x + 256 * i;
+    const int r = idx >> 4, c = idx & 15;
+    long long row;
+    if (a.layout == DA_LAYOUT_REORDERED) {
+      row = (long long)j * P + r;
+    } else {
+      const int u = r >> 3, v = r & 7;
+      row = (rc.y0 + u < g.H && rc.x0 + v < g.W) ? ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v : -1;
+    }
+    const uint4 val = row >= 0 ? __ldg(src + row * rs8 + c) : make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
+  }
+}
+
+// Per-head maximum key row norm as KBLK per-block partial maxima (the bound
+// behind the fixed softmax offset), for callers without the pooling pass.
+// grid (KBLK, heads), 256 threads: each warp reads two 256-byte rows per load.
+__global__ void __launch_bounds__(256) key_norm_kernel(const __nv_bfloat16* __restrict__ k, long long kh, long long kr,
+                                                       long long rows, float* __restrict__ kpart) {
+  __shared__ float red[8];
+  const int h = blockIdx.y;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int sub = lane >> 4, c = lane & 15;
+  const uint4* base = reinterpret_cast<const uint4*>(k + h * kh);
+  const long long kr8 = kr / 8;
+  const long long step = (long long)KBLK * 8 * 2;
+  float mx = 0.f;
+  for (long long r0 = ((long long)blockIdx.x * 8 + w) * 2 + sub; r0 < rows; r0 += 4 * step) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long rr = r0 + u * step;
+      v[u] = rr < rows ? __ldg(base + rr * kr8 + c) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+      float s2 = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+        s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+      }
+#pragma unroll
+      for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      mx = fmaxf(mx, s2);
+    }
+  }
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  if (lane == 0) red[w] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = red[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) b = fmaxf(b, red[i]);
+    kpart[(long long)h * KBLK + blockIdx.x] = sqrtf(b);
+  }
+}
+
 }  // namespace lhk
 
-cudaError_t launch_lh_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why, long long* trace,
-                           const float* kpart, int kblk, bool tiles_ready) {
-  (void)why;
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static long long* g_trace = nullptr;  // LH_PROF builds only (da_debug_trace)
+void set_tc_trace(void* buf) { g_trace = static_cast<long long*>(buf); }
+
+static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// Attention workspace: [counters 256 B | key norm maxima (heads x KBLK floats)
+// | fallback items (4 per item) | region order (heads x g) | K tiles | V tiles]
+static size_t ws_norms() { return 256; }
+static size_t ws_items(int heads) { return ws_norms() + align256(sizeof(float) * heads * lhk::KBLK); }
+static size_t ws_order(int heads, const Geo& g) { return ws_items(heads) + align256(sizeof(int) * 4 * (size_t)heads * g.g); }
+static size_t ws_tiles(int heads, const Geo& g) { return ws_order(heads, g) + align256(sizeof(int) * (size_t)heads * g.g); }
+
+uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which) {
+  return static_cast<uint8_t*>(ws) + ws_tiles(heads, g) + (size_t)which * heads * g.g * lhk::TILE;
+}
+
+size_t attn_workspace_size(int heads, const Geo& g) { return ws_tiles(heads, g) + 2 * (size_t)heads * g.g * lhk::TILE; }
+
+bool tc_supported(const da_attn_args& a, const Geo& g) {
+  if (a.d != 128 || a.dv != 128 || g.p != 64) return false;
+  if (!(a.scale > 0.0)) return false;  // the fixed softmax offset bounds scale * |q| |k| from above
+  if (a.layout == DA_LAYOUT_ORIGINAL && (g.ph != 8 || g.pw != 8)) return false;
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  if (!al16(a.q) || !al16(a.k) || !al16(a.v) || !al16(a.out)) return false;
+  if (a.q_row_stride % 8 || a.k_row_stride % 8 || a.v_row_stride % 8) return false;
+  if (a.q_head_stride % 8 || a.k_head_stride % 8 || a.v_head_stride % 8) return false;
+  if (a.o_row_stride % 8 || a.o_head_stride % 8) return false;
+  return (long long)a.heads * g.g < (1ll << 31);
+}
+
+cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const float* kpart, int kblk,
+                           bool tiles_ready) {
   lhk::Params p;
-  p.trace = trace;
+  p.trace = g_trace;
   p.q = static_cast<const __nv_bfloat16*>(a.q);
   p.qh = a.q_head_stride;
   p.qr = a.q_row_stride;
@@ -760,58 +874,55 @@ cudaError_t launch_lh_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   p.pol_kv = (LH_L2POL & 1) ? L2_EVICT_LAST : L2_EVICT_NORMAL;
   p.pol_q = (LH_L2POL & 2) ? L2_EVICT_FIRST : L2_EVICT_NORMAL;
   p.pol_o = (LH_L2POL & 4) ? L2_EVICT_FIRST : L2_EVICT_NORMAL;
-  {
-    static int fk = -1;
-    if (fk < 0) {
-      const char* env = getenv("DA_FAKELOAD");
-      fk = env ? atoi(env) : 0;
-    }
-    p.fake_load = fk;
-  }
-  // workspace: the pair kernel's layout (counters | key norm maxima | fallback
-  // items | plan | tiles); the region order fits in the pair plan's space
   char* ws = static_cast<char*>(a.workspace);
   p.fb_count = reinterpret_cast<int*>(ws);
   p.work = reinterpret_cast<int*>(ws + 4);
-  const size_t kb = (sizeof(float) * a.heads * lhk::KBLK + 255) & ~(size_t)255;
-  p.fb_items = reinterpret_cast<int*>(ws + 256 + kb);
-  int* order = reinterpret_cast<int*>(reinterpret_cast<char*>(p.fb_items) +
-                                      ((sizeof(int) * 4 * (size_t)a.heads * g.g + 255) & ~(size_t)255));
-  // the block-sparse seam (no pooling pass, so no key norms / tiles): pair kernel
-  if (kpart == nullptr) return launch_pair_attn(a, g, st, why, trace, kpart, kblk, tiles_ready);
-  p.kpart = kpart;
-  p.kblk = kblk;
+  p.fb_items = reinterpret_cast<int*>(ws + ws_items(a.heads));
+  int* order = reinterpret_cast<int*>(ws + ws_order(a.heads, g));
+  cudaMemsetAsync(ws, 0, 2 * sizeof(int), st);  // fallback counter, item counter
+  if (kpart != nullptr) {  // norms from the pooling pass
+    p.kpart = kpart;
+    p.kblk = kblk;
+  } else {
+    float* kp = reinterpret_cast<float*>(ws + ws_norms());
+    const long long key_rows = a.layout == DA_LAYOUT_REORDERED ? g.n_pad : g.n_real;
+    lhk::key_norm_kernel<<<dim3(lhk::KBLK, a.heads), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a.k),
+                                                                  a.k_head_stride, a.k_row_stride, key_rows, kp);
+    p.kpart = kp;
+    p.kblk = lhk::KBLK;
+  }
+  cudaError_t e;
   {
     const size_t smem = sizeof(int) * ((size_t)g.g + 1);
-    if (smem <= 200 * 1024) {
-      cudaFuncSetAttribute(lhk::region_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem <= 200 * 1024 && ensure_smem_optin((const void*)lhk::region_order_kernel, (int)smem) == cudaSuccess) {
       lhk::region_order_kernel<<<a.heads, 1024, smem, st>>>(a.row_ptr, g.g, a.shared_mask ? 0 : 1, order);
       p.order = order;
     } else {
-      p.order = nullptr;
+      cudaGetLastError();
+      p.order = nullptr;  // natural region order
     }
   }
   if (!tiles_ready) {
-    cudaError_t e = launch_kv_tiles(a, g, st, 1);
-    if (e != cudaSuccess) return e;
+    lhk::KvTileArgs ta;
+    ta.x[0] = static_cast<const __nv_bfloat16*>(a.k);
+    ta.x[1] = static_cast<const __nv_bfloat16*>(a.v);
+    ta.hs[0] = a.k_head_stride; ta.hs[1] = a.v_head_stride;
+    ta.rs[0] = a.k_row_stride; ta.rs[1] = a.v_row_stride;
+    ta.out[0] = attn_tiles(a.workspace, a.heads, g, 0);
+    ta.out[1] = attn_tiles(a.workspace, a.heads, g, 1);
+    ta.layout = a.layout;
+    lhk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
   }
-  p.kt = pair_attn_tiles(a.workspace, a.heads, g, 0);
-  p.vt = pair_attn_tiles(a.workspace, a.heads, g, 1);
-  cudaMemsetAsync(ws, 0, 2 * sizeof(int), st);
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  cudaError_t e = cudaFuncSetAttribute(lhk::sparse_attn_lh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       lhk::SMEM_ALLOC);
-  if (e != cudaSuccess) return e;
+  p.kt = attn_tiles(a.workspace, a.heads, g, 0);
+  p.vt = attn_tiles(a.workspace, a.heads, g, 1);
+  if ((e = ensure_smem_optin((const void*)lhk::sparse_attn_lh_kernel, lhk::SMEM_ALLOC)) != cudaSuccess) return e;
+  const int sms = device_sms();
   const long long items = (long long)a.heads * g.g;
-  const int grid = (int)(items < num_sms ? items : num_sms);
+  const int grid = (int)(items < sms ? items : sms);
   lhk::sparse_attn_lh_kernel<<<grid, 384, lhk::SMEM_ALLOC, st>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * num_sms);
+  // rows whose fixed softmax offset underflowed: redo their regions exactly
+  return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * sms);
 }
 
 }  // namespace da

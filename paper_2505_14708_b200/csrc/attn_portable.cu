@@ -4,8 +4,9 @@
 // (sparse.py:88-166): per query region, kept key regions in ascending order,
 // streaming softmax over valid keys, fully dropped rows -> 0.
 //
-// grid: (g, heads); block 256. Shared memory: Q, K, V tiles (fp32), the p x p
-// score tile, the fp32 output accumulator and per-row m / l.
+// grid: (g, heads); block 256. Shared memory: the Q tile and the output
+// accumulator (fp32, p rows), per-row m / l, and one key chunk: K and V rows
+// (fp32) and the p x kc score tile.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -24,6 +25,7 @@ struct PortableArgs {
   long long cap;
   const uint8_t* key_valid;
   int mask_h;  // 1 = per-head masks, 0 = head 0's mask for all heads
+  int kc;      // key rows per chunk (portable_key_chunk)
   Geo geo;
 };
 
@@ -39,17 +41,19 @@ DA_DEV bool key_ok(const PortableArgs& a, int region, int r) {
 }
 
 // One query region i of head h (the whole block; block-uniform control flow).
+// Each kept key region is consumed in chunks of kc key rows so that large
+// regions (8x16 pools: p = 128) fit in shared memory with d = 128.
 __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) {
-  const int p = a.geo.p, d = a.d, dv = a.dv;
+  const int p = a.geo.p, d = a.d, dv = a.dv, kc = a.kc;
   float* Qs = sm;                 // p*d
-  float* Ks = Qs + p * d;         // p*d
-  float* Vs = Ks + p * d;         // p*dv
-  float* S = Vs + p * dv;         // p*p
-  float* O = S + p * p;           // p*dv
+  float* O = Qs + p * d;          // p*dv
   float* M = O + p * dv;          // p
   float* L = M + p;               // p
   float* alpha = L + p;           // p
-  int* kval = reinterpret_cast<int*>(alpha + p);  // p
+  float* Ks = alpha + p;          // kc*d
+  float* Vs = Ks + kc * d;        // kc*dv
+  float* S = Vs + kc * dv;        // p*kc
+  int* kval = reinterpret_cast<int*>(S + p * kc);  // kc
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int g = a.geo.g;
@@ -68,67 +72,70 @@ __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) 
 
   for (int t = beg; t < end; ++t) {
     const int j = cols[t];
-    for (int e = tid; e < p * d; e += nt) {
-      int r = e / d, c = e - r * d;
-      long long row = token_row(a, j, r);
-      Ks[e] = row >= 0 ? __bfloat162float(a.k[h * a.kh + row * a.kr + c]) : 0.f;
-    }
-    for (int e = tid; e < p * dv; e += nt) {
-      int r = e / dv, c = e - r * dv;
-      long long row = token_row(a, j, r);
-      Vs[e] = row >= 0 ? __bfloat162float(a.v[h * a.vh + row * a.vr + c]) : 0.f;
-    }
-    for (int r = tid; r < p; r += nt) kval[r] = key_ok(a, j, r);
-    __syncthreads();
-    for (int e = tid; e < p * p; e += nt) {
-      int r = e / p, c = e - r * p;
-      float s = -INFINITY;
-      if (kval[c]) {
-        float acc = 0.f;
-        for (int kk = 0; kk < d; ++kk) acc = fmaf(Qs[r * d + kk], Ks[c * d + kk], acc);
-        s = acc * a.scale;
+    for (int c0 = 0; c0 < p; c0 += kc) {
+      const int nc = min(kc, p - c0);
+      for (int e = tid; e < nc * d; e += nt) {
+        int r = e / d, c = e - r * d;
+        long long row = token_row(a, j, c0 + r);
+        Ks[e] = row >= 0 ? __bfloat162float(a.k[h * a.kh + row * a.kr + c]) : 0.f;
       }
-      S[e] = s;
-    }
-    __syncthreads();
-    // per-row online softmax update, one warp per row
-    const int lane = tid % 32, w = tid / 32, nw = nt / 32;
-    for (int r = w; r < p; r += nw) {
-      float mx = -INFINITY;
-      for (int c = lane; c < p; c += 32) mx = fmaxf(mx, S[r * p + c]);
+      for (int e = tid; e < nc * dv; e += nt) {
+        int r = e / dv, c = e - r * dv;
+        long long row = token_row(a, j, c0 + r);
+        Vs[e] = row >= 0 ? __bfloat162float(a.v[h * a.vh + row * a.vr + c]) : 0.f;
+      }
+      for (int r = tid; r < nc; r += nt) kval[r] = key_ok(a, j, c0 + r);
+      __syncthreads();
+      for (int e = tid; e < p * nc; e += nt) {
+        int r = e / nc, c = e - r * nc;
+        float s = -INFINITY;
+        if (kval[c]) {
+          float acc = 0.f;
+          for (int kk = 0; kk < d; ++kk) acc = fmaf(Qs[r * d + kk], Ks[c * d + kk], acc);
+          s = acc * a.scale;
+        }
+        S[r * kc + c] = s;
+      }
+      __syncthreads();
+      // per-row online softmax update, one warp per row
+      const int lane = tid % 32, w = tid / 32, nw = nt / 32;
+      for (int r = w; r < p; r += nw) {
+        float mx = -INFINITY;
+        for (int c = lane; c < nc; c += 32) mx = fmaxf(mx, S[r * kc + c]);
 #pragma unroll
-      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      float mold = M[r];
-      float mnew = fmaxf(mold, mx);
-      float sum = 0.f;
-      if (mnew == -INFINITY) {  // block entirely invalid for this row: skip
-        for (int c = lane; c < p; c += 32) S[r * p + c] = 0.f;
-      } else {
-        for (int c = lane; c < p; c += 32) {
-          float s = S[r * p + c];
-          float pr = s == -INFINITY ? 0.f : expf(s - mnew);
-          S[r * p + c] = pr;
-          sum += pr;
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float mold = M[r];
+        float mnew = fmaxf(mold, mx);
+        float sum = 0.f;
+        if (mnew == -INFINITY) {  // chunk entirely invalid for this row: skip
+          for (int c = lane; c < nc; c += 32) S[r * kc + c] = 0.f;
+        } else {
+          for (int c = lane; c < nc; c += 32) {
+            float s = S[r * kc + c];
+            float pr = s == -INFINITY ? 0.f : expf(s - mnew);
+            S[r * kc + c] = pr;
+            sum += pr;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) {
+          float al = (mold == -INFINITY) ? 0.f : expf(mold - mnew);
+          if (mnew == -INFINITY) al = 1.f;
+          alpha[r] = al;
+          L[r] = L[r] * al + sum;
+          M[r] = mnew;
         }
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (lane == 0) {
-        float al = (mold == -INFINITY) ? 0.f : expf(mold - mnew);
-        if (mnew == -INFINITY) al = 1.f;
-        alpha[r] = al;
-        L[r] = L[r] * al + sum;
-        M[r] = mnew;
+      __syncthreads();
+      for (int e = tid; e < p * dv; e += nt) {
+        int r = e / dv, c = e - r * dv;
+        float acc = O[e] * alpha[r];
+        for (int kk = 0; kk < nc; ++kk) acc = fmaf(S[r * kc + kk], Vs[kk * dv + c], acc);
+        O[e] = acc;
       }
+      __syncthreads();
     }
-    __syncthreads();
-    for (int e = tid; e < p * dv; e += nt) {
-      int r = e / dv, c = e - r * dv;
-      float acc = O[e] * alpha[r];
-      for (int kk = 0; kk < p; ++kk) acc = fmaf(S[r * p + kk], Vs[kk * dv + c], acc);
-      O[e] = acc;
-    }
-    __syncthreads();
   }
   for (int e = tid; e < p * dv; e += nt) {
     int r = e / dv, c = e - r * dv;
@@ -157,8 +164,24 @@ __global__ void __launch_bounds__(256) portable_list_kernel(PortableArgs a, cons
   }
 }
 
+static size_t portable_smem_for(int p, int d, int dv, int kc) {
+  return sizeof(float) * ((size_t)p * d + (size_t)p * dv + 3 * (size_t)p + (size_t)kc * (d + dv + p)) +
+         sizeof(int) * kc;
+}
+
+// Largest key chunk (the whole region, else a power of two) whose tiles fit
+// in the 227 KB of shared memory a CTA may opt into; 0 if none does.
+static int portable_key_chunk(int p, int d, int dv) {
+  constexpr size_t kMax = 227 * 1024;
+  if (portable_smem_for(p, d, dv, p) <= kMax) return p;
+  for (int kc = 256; kc >= 1; kc >>= 1)
+    if (kc < p && portable_smem_for(p, d, dv, kc) <= kMax) return kc;
+  return 0;
+}
+
 size_t portable_smem_bytes(int p, int d, int dv) {
-  return sizeof(float) * ((size_t)p * d * 2 + (size_t)p * dv * 2 + (size_t)p * p + 3 * (size_t)p) + sizeof(int) * p;
+  const int kc = portable_key_chunk(p, d, dv);
+  return portable_smem_for(p, d, dv, kc ? kc : 1);
 }
 
 static PortableArgs portable_args(const da_attn_args& args, const Geo& geo) {
@@ -176,6 +199,7 @@ static PortableArgs portable_args(const da_attn_args& args, const Geo& geo) {
   a.row_ptr = args.row_ptr; a.col_idx = args.col_idx; a.cap = args.mask_cap;
   a.key_valid = args.key_valid;
   a.mask_h = args.shared_mask ? 0 : 1;
+  a.kc = portable_key_chunk(geo.p, args.d, args.dv);
   a.geo = geo;
   return a;
 }
@@ -183,7 +207,7 @@ static PortableArgs portable_args(const da_attn_args& args, const Geo& geo) {
 cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaStream_t st) {
   const PortableArgs a = portable_args(args, geo);
   size_t smem = portable_smem_bytes(geo.p, args.d, args.dv);
-  cudaError_t e = cudaFuncSetAttribute(portable_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_optin((const void*)portable_attn_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(geo.g, args.heads);
   portable_attn_kernel<<<grid, 256, smem, st>>>(a);
@@ -194,7 +218,7 @@ cudaError_t launch_portable_list(const da_attn_args& args, const Geo& geo, cudaS
                                  const int* count, int blocks) {
   const PortableArgs a = portable_args(args, geo);
   size_t smem = portable_smem_bytes(geo.p, args.d, args.dv);
-  cudaError_t e = cudaFuncSetAttribute(portable_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_optin((const void*)portable_list_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   portable_list_kernel<<<blocks, 256, smem, st>>>(a, items, count);
   return cudaGetLastError();

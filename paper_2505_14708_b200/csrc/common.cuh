@@ -265,10 +265,6 @@ DA_DEV void sts128(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t 
 DA_DEV uint32_t kv_tile_offset_grouped(int r, int h, int c) {
   return (uint32_t)((((r >> 3) * 2 + h) << 10) + ((r & 7) << 7) + (((c ^ r) & 7) << 4));
 }
-// The same in the HALF-MAJOR layout of the pair kernel: [half][64 rows x 128 B].
-DA_DEV uint32_t kv_tile_offset_halves(int r, int h, int c) {
-  return (uint32_t)((h << 13) + (r << 7) + (((c ^ r) & 7) << 4));
-}
 // Shared-memory matrix descriptor (SM100 "version 1"), SWIZZLE_128B.
 //   start address >> 4 in [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46),
 //   version 1 at bit 46, layout type SWIZZLE_128B (2) in [61,64).

@@ -20,16 +20,14 @@ cudaError_t launch_pool(const void* x, long long hs, long long rs, double* poole
 // pool_norm_blocks(d, g) > 0) receives per-block maxima of K's row norms,
 // [heads][pool_norm_blocks(d, g)]
 // x2/ktile/vtile (optional, d = 128 and 8x8 pools): the same pass also writes
-// K and V as the attention kernel's region tiles (pair_attn_tiles)
+// K and V as the attention kernel's region tiles (attn_tiles)
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
                          long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
                          float* kpart, const void* x2 = nullptr, long long hs2 = 0, long long rs2 = 0,
                          uint8_t* ktile = nullptr, uint8_t* vtile = nullptr, unsigned long long* pnorm = nullptr);
-// K / V tile buffers inside the attention workspace ([heads][g][16 KB] each)
-// and their layout: grouped (kv_tile_offset_grouped) for the lane-half K4
-// (DA_K4=lh), half-major (kv_tile_offset_halves) for the pair kernel
-bool attn_tiles_grouped();
-uint8_t* pair_attn_tiles(void* ws, int heads, const Geo& g, int which);
+// K / V tile buffers inside the attention workspace ([heads][g][16 KB] each),
+// in the GROUPED layout of kv_tile_offset_grouped (the K4 shared-memory image)
+uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which);
 int pool_norm_blocks(int d, const Geo& g);
 // hist0 (optional): per-head 2048-bin histogram of the top 11 key bits, filled in the epilogue
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
@@ -60,18 +58,19 @@ cudaError_t launch_portable_attn(const da_attn_args& args, const Geo& geo, cudaS
 // regions listed in items[0 .. *count) (entries h * g + i; count read on the device)
 cudaError_t launch_portable_list(const da_attn_args& args, const Geo& geo, cudaStream_t st, const int* items,
                                  const int* count, int blocks);
-size_t pair_attn_workspace_size(int heads, const Geo& g);
-cudaError_t launch_pair_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                             long long* trace, const float* kpart, int kblk, bool tiles_ready);
-cudaError_t launch_kv_tiles(const da_attn_args& a, const Geo& g, cudaStream_t st, int grouped);
-cudaError_t launch_lh_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                           long long* trace, const float* kpart, int kblk, bool tiles_ready);
+size_t attn_workspace_size(int heads, const Geo& g);
 
 void set_tc_trace(void* buf);
 bool tc_supported(const da_attn_args& a, const Geo& g);
 // kpart/kblk: per-head key row norm maxima already computed by the pooling
-// pass ([heads][kblk]); null = the attention launch computes them itself
-cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const char** why,
-                           const float* kpart = nullptr, int kblk = 0, bool tiles_ready = false);
+// pass ([heads][kblk]); null = the attention launch computes them itself.
+// tiles_ready: the pooling pass already wrote the K/V region tiles.
+cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const float* kpart = nullptr,
+                           int kblk = 0, bool tiles_ready = false);
+
+// Per-device facts cached once per device (the library keeps no other state):
+// the SM count, and the dynamic shared-memory opt-in of a kernel.
+int device_sms();  // of the current device
+cudaError_t ensure_smem_optin(const void* kernel, int bytes);
 
 }  // namespace da

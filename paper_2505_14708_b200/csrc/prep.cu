@@ -78,7 +78,6 @@ struct PoolSrc {
   long long hs[3], rs[3];
   double* out[2];
   uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
-  int grouped;                // tile layout: 1 grouped (lane-half kernel), 0 half-major (pair kernel)
   unsigned long long* pnorm;  // optional [heads][2]: largest pooled row norm^2 of Q (0) and K (1), as double bits
 };
 
@@ -322,7 +321,7 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
       for (int t = 0; t < RB; ++t) {
         const int r = r0 + t;
         if (r < g.p) {
-          const uint32_t off = src.grouped ? kv_tile_offset_grouped(r, k >> 3, k & 7) : kv_tile_offset_halves(r, k >> 3, k & 7);
+          const uint32_t off = kv_tile_offset_grouped(r, k >> 3, k & 7);
           *reinterpret_cast<uint4*>(tdst + off) = q[t];
         }
       }
@@ -407,7 +406,6 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
     src.hs[2] = tiles ? hs2 : hs0; src.rs[2] = tiles ? rs2 : rs0;
     src.tile[0] = tiles ? ktile : nullptr;
     src.tile[1] = tiles ? vtile : nullptr;
-    src.grouped = attn_tiles_grouped() ? 1 : 0;
     src.pnorm = pnorm;
     dim3 grid(pool_norm_blocks(d, g), heads, x1 ? (tiles ? 3 : 2) : 1);
     float* kp = x1 ? kpart : nullptr;
@@ -434,7 +432,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
   const int threads = rg * d8;
   const size_t smem = sizeof(double) * rg * d;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem_optin((const void*)pool_kernel, (int)smem);
     if (e != cudaSuccess) return e;
   }
   dim3 grid(g.g, heads, x1 ? 2 : 1);

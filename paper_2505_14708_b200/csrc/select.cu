@@ -581,17 +581,26 @@ DA_DEV float key32_score(unsigned int k) {
   return __uint_as_float(b);
 }
 
-// fp64 score exactly as the fp64 GEMM forms it: sequential FMA over features, then * scale
-// fp64 score of one (query region, key region) pair computed by a whole warp
-// (lanes split the features, coalesced row reads, fixed shuffle tree; the
-// mark kernel's argmax rescoring uses the same order): every lane returns it.
-DA_DEV double score64_warp(const double* __restrict__ q, const double* __restrict__ k, int d, double scale) {
+// fp64 dot product of two feature rows in the fp64 GEMM's order
+// (draft_gemm_kernel, prep.cu: one sequential FMA chain over the features,
+// starting from 0.0), computed by a whole warp: the lanes load the rows
+// coalesced and every lane runs the same chain on shuffled operands, so every
+// lane returns the identical value. Band rescoring and the argmax rescoring
+// therefore rank exactly as the fp64 fallback path does.
+DA_DEV double dot64_seq_warp(const double* __restrict__ q, const double* __restrict__ k, int d) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
-  for (int c = lane; c < d; c += 32) acc = fma(__ldg(q + c), __ldg(k + c), acc);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  return acc * scale;
+  for (int c0 = 0; c0 < d; c0 += 32) {
+    const int c = c0 + lane;
+    const double qv = c < d ? __ldg(q + c) : 0.0;
+    const double kv = c < d ? __ldg(k + c) : 0.0;
+    const int n = min(32, d - c0);
+    for (int s = 0; s < n; ++s) acc = fma(__shfl_sync(0xffffffffu, qv, s), __shfl_sync(0xffffffffu, kv, s), acc);
+  }
+  return acc;
+}
+DA_DEV double score64_warp(const double* __restrict__ q, const double* __restrict__ k, int d, double scale) {
+  return dot64_seq_warp(q, k, d) * scale;
 }
 
 __global__ void s32_init_kernel(Sel32State* st, unsigned int* hist, unsigned int* rowmax, int g, long long m,
@@ -946,16 +955,12 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
   int best = -1, nbest = 0;
   double bv = 0.0;
   const double* qrow = qp + ((long long)h * g + row) * d;
-  // fp64 score of candidate column jj (lane-split over features); keeps the
-  // first maximum in ascending column order
+  // fp64 score of candidate column jj (the fp64 GEMM's summation order); keeps
+  // the first maximum in ascending column order
   auto argmax_candidate = [&](int jj) {
     ++nbest;
     const double* krow = kp + ((long long)h * g + jj) * d;
-    double sv = 0.0;
-    for (int c = lane; c < d; c += 32) sv = fma(__ldg(qrow + c), __ldg(krow + c), sv);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
-    sv *= scale;
+    const double sv = dot64_seq_warp(qrow, krow, d) * scale;
     if (best < 0 || sv > bv) { best = jj; bv = sv; }
   };
   if ((g & 3) == 0) {
@@ -1210,7 +1215,10 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
   s32_init_kernel<<<heads, 256, 0, st>>>(w.state, w.hist, w.rowmax, g, m, w.fallback, pnorm);
   if (pnorm == nullptr) s32_norm_kernel<<<dim3(heads, EPSB), 256, 0, st>>>(qp, kp, g, d, w.state);
   dim3 ggrid((g + DT32 - 1) / DT32, (g + DT32 - 1) / DT32, heads);
-  cudaFuncSetAttribute(draft32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G32_SMEM);
+  {
+    cudaError_t e = ensure_smem_optin((const void*)draft32_gemm_kernel, G32_SMEM);
+    if (e != cudaSuccess) return e;
+  }
   s32_pack_kernel<<<dim3((unsigned)(g32_pad(g, DT32) / 32), (unsigned)g32_pad(d, 32) / 32, 2 * heads), dim3(32, 8), 0,
                     st>>>(qp, kp, g, d, w.qt, w.kt);
   draft32_gemm_kernel<<<ggrid, 256, G32_SMEM, st>>>(w.qt, w.kt, scores32, g, d, (float)scale, w.hist, w.rowmax);
@@ -1225,7 +1233,10 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
   s32_mark_kernel<<<rows_grid, 256, 0, st>>>(scores32, qp, kp, g, d, scale, w.state, w.bm, w32, w.rowmax, w.argmax,
                                              w.cand, w.fallback);
   const size_t fsmem = (sizeof(unsigned long long) + sizeof(int)) * S32_CAP;
-  cudaFuncSetAttribute(s32_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+  {
+    cudaError_t e = ensure_smem_optin((const void*)s32_finish_kernel, (int)fsmem);
+    if (e != cudaSuccess) return e;
+  }
   s32_band_score_kernel<<<dim3(S32_SCORE_CTAS, heads), 256, 0, st>>>(qp, kp, g, d, scale, w.state, w.cand, w.bkey,
                                                                     w.fallback);
   s32_finish_kernel<<<heads, 1024, fsmem, st>>>(qp, kp, g, d, scale, m, w.state, w.cand, w.bkey,

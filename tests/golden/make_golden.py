@@ -112,6 +112,27 @@ def gen_selection(da):
     np.savez_compressed(OUT / "selection.npz", **out)
 
 
+def gen_wire(da):
+    """Mask wire formats (masking.py:128-176): the reference's JSON export and
+    density stats of a few selections, as JSON next to their score matrices."""
+    import json  # noqa: PLC0415
+
+    from draftattn.masking import mask_density_stats, mask_to_json_dict  # noqa: PLC0415
+
+    rng = np.random.default_rng(13)
+    cases = []
+    for g, r, force, tied in ((3, 0.5, True, False), (8, 0.25, False, True), (17, 0.1, True, False),
+                              (40, 0.3, True, True)):
+        s = rng.standard_normal((g, g))
+        if tied:
+            s = np.round(s * 2) / 2
+        m = da.select_top_fraction(s, r, force_row_keep=force)
+        cases.append({"scores": s.tolist(), "keep_ratio": r, "force_row_keep": force,
+                      "json": mask_to_json_dict(m), "stats": mask_density_stats(m),
+                      "bitmap_hex": da.masking.mask_to_bitmap(m).hex()})
+    (OUT / "wire.json").write_text(json.dumps(cases))
+
+
 def _pipeline_case(da, name, frames, height, width, ph, pw, d, heads, sparsity, seed,
                    sample_rows=None, full_output=True, head_ids=None):
     q, k, v = real_inputs(da, frames, height, width, ph, pw, d, seed, heads, head_ids)
@@ -176,6 +197,11 @@ def main():
     gen_permutations(da)
     gen_pooling(da)
     gen_selection(da)
+    gen_wire(da)
+    # the paper's 8x16 pool (p = 128) with d = 128 on a ragged grid, and a head
+    # dim that is not a multiple of 8 (the reference's own tests use d = 4)
+    _pipeline_case(da, "pool816", 2, 12, 20, 8, 16, 128, 2, 0.75, 5)
+    _pipeline_case(da, "d4", 2, 8, 12, 4, 4, 4, 2, 0.5, 6)
     # tiny config (BASELINE configs[0]): divisible grid, draft_sparse_attention path
     _pipeline_case(da, "tiny", 4, 16, 16, 4, 4, 64, 2, 0.5, 0)
     # small ragged grids through the padded path

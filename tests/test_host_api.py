@@ -99,3 +99,72 @@ def test_head_groups_cover_every_head_once(heads, hg):
     assert all(0 < h1 - h0 <= hg for h0, h1 in g)
     if heads >= 2 * hg and hg > 1:
         assert g[0][1] - g[0][0] == hg // 2  # half-size first group (pipeline fill)
+
+
+# ---------------------------------------------------------------- mask wire formats (masking.py:128-176)
+
+def _wire_cases():
+    import json
+    from pathlib import Path
+    return json.loads((Path(__file__).resolve().parent / "golden" / "wire.json").read_text())
+
+
+def test_mask_json_round_trip_matches_reference_export():
+    for case in _wire_cases():
+        ref = case["json"]
+        m = da.mask_from_json_dict(ref, device="cpu")
+        assert m.bitmap_bytes().hex() == case["bitmap_hex"]
+        assert da.mask_to_json_dict(m) == ref
+        assert da.mask_density_stats(m) == case["stats"]
+
+
+def test_mask_bitmap_round_trip():
+    for case in _wire_cases():
+        g = case["json"]["g"]
+        raw = bytes.fromhex(case["bitmap_hex"])
+        kept = da.kept_from_bitmap(raw, g)
+        assert kept.dtype == torch.bool and tuple(kept.shape) == (g, g)
+        m = da.RegionMask.from_bitmap(raw, g, case["keep_ratio"], case["json"]["threshold"],
+                                      case["json"]["forced_row_keeps"], device="cpu")
+        assert da.mask_to_bitmap(m) == raw
+        assert m.kept_count == case["json"]["kept_count"]
+        # executor lists: ascending kept columns per row
+        rp, ci = m.row_ptr[0].tolist(), m.col_idx[0].tolist()
+        for i in range(g):
+            assert ci[rp[i]:rp[i + 1]] == torch.nonzero(kept[i]).flatten().tolist()
+    with pytest.raises(ValueError, match="too short"):
+        da.kept_from_bitmap(b"\x00", 4)
+
+
+def test_multi_head_mask_from_kept():
+    rng = np.random.default_rng(0)
+    kept = rng.random((3, 9, 9)) < 0.3
+    m = da.RegionMask.from_kept(kept, 0.3, [0.1, 0.2, 0.3], [0, 1, 2], device="cpu")
+    assert m.heads == 3 and not m.single
+    assert m.kept_count == kept.reshape(3, -1).sum(1).tolist()
+    assert m.threshold == [0.1, 0.2, 0.3] and m.forced_row_keeps == [0, 1, 2]
+    for h in range(3):
+        assert m.bitmap_bytes(h) == O.mask_bitmap(kept[h])
+    with pytest.raises(ValueError, match="boolean"):
+        da.RegionMask.from_kept(kept.astype(np.int8), 0.3, 0.0, device="cpu")
+
+
+# ---------------------------------------------------------------- layouts
+
+def test_bnhd_layout_validation():
+    lay = da.LatentLayout(1, 4, 8, 2, 4)
+    q = torch.zeros(2, 32, 3, 8, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="qkv_layout must be one of"):
+        da.multi_head_sparse_attention(q[0], q[0], q[0], lay, 0.5, qkv_layout="nchw")
+    with pytest.raises(ValueError, match="does not match"):
+        da.multi_head_sparse_attention(q, q[:, :, :2], q, lay, 0.5, qkv_layout="bnhd")
+    with pytest.raises(ValueError, match="layout token count"):
+        da.draft_sparse_attention(q[:, :30], q[:, :30], q[:, :30], lay, 0.5, qkv_layout="bnhd")
+    with pytest.raises(ValueError, match="bnhd"):
+        da.padded_sparse_attention(q[0], q[0], q[0], 1, 4, 8, 2, 4, 0.5, qkv_layout="bnhd")
+
+
+def test_feature_padding_is_exact():
+    from paper_2505_14708_b200.api import _pad_features
+    with pytest.raises(ValueError, match="CUDA"):
+        _pad_features(torch.zeros(1, 4, 5))

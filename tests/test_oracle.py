@@ -116,7 +116,7 @@ def test_selection_fixtures_bit_exact():
 
 # ---------------------------------------------------------------- pipelines
 
-@pytest.mark.parametrize("name", ["tiny", "ragged_small", "ragged_w"])
+@pytest.mark.parametrize("name", ["tiny", "ragged_small", "ragged_w", "pool816", "d4"])
 def test_pipeline_fixtures_full(name):
     z = _npz(name)
     grid, q, k, v = _bf16_inputs(z["dims"])
@@ -157,3 +157,17 @@ def test_pipeline_hv720_full_shape_masks():
         assert O.mask_bitmap(mask.kept) == z[f"h{h}_bitmap"].tobytes()
         thr, forced, kept = z[f"h{h}_meta"]
         assert mask.threshold == thr and mask.forced_row_keeps == forced and mask.kept_count == kept
+
+
+def test_mask_wire_fixtures():
+    # masking.py:128-176: the reference's JSON export, density stats and bitmap
+    import json
+
+    for case in json.loads((GOLD / "wire.json").read_text()):
+        s = np.asarray(case["scores"])
+        m = O.select_top_fraction(s, case["keep_ratio"], case["force_row_keep"])
+        assert O.mask_bitmap(m.kept).hex() == case["bitmap_hex"]
+        assert [list(x) for x in zip(*np.nonzero(m.kept))] == case["json"]["kept"]
+        stats = O.mask_stats(m)
+        for key, val in case["stats"].items():
+            assert stats[key] == val, key
