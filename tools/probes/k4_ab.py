@@ -1,7 +1,7 @@
-"""Probe: K4 variants (DA_K4 env) on gaussian and smooth synthetic data at HV720.
+"""Probe: K4 on gaussian and smooth synthetic data at HV720 (pair-union statistics of the masks).
 
     python tools/probes/k4_ab.py --data gaussian,smooth --sparsity 0.9
-(run once per DA_K4 value; the variant is fixed per process)
+(build variants with DA_NVCC_FLAGS, e.g. -DLH_KSL=4)
 """
 import argparse
 import os
