@@ -12,10 +12,16 @@ head-sharded, each rank runs its heads, all-to-all back (strong scaling: the
 call's total work is fixed). Inputs (2.2 GB for HV720) are larger than L2, so
 no L2 flush is needed between steps.
 
+The line also carries dense attention at the same shape (cuDNN / flash SDPA,
+bf16, the north-star comparator) as ``dense_sdpa_ms`` and
+``speedup_vs_dense_sdpa`` (skip with --no-dense).
+
 --impl reference times the CPU oracle port of the reference algorithm
-(oracle/, the reference itself is numpy) on the host cores, on a bounded
-sample of the same call (one head's selection stages in full plus a fixed
-subset of its query regions), extrapolated to ms per call.
+(oracle/: the reference itself is Python/numpy and cannot travel to the GPU
+box) on the host cores: whole heads of the same call, float32 inputs (the
+reference's default precision) holding the bf16-rounded values the GPU gets,
+heads one after another as the reference runs them; ms per call = the mean
+per-head time x heads (labelled extrapolated).
 """
 
 from __future__ import annotations
@@ -113,33 +119,40 @@ class ClockSampler:
 # CPU reference arm / baseline (oracle port of the reference algorithm)
 # --------------------------------------------------------------------------
 
-def cpu_reference_sample(cfg, seed=0, n_rows=48):
-    """Time the reference algorithm (oracle port) on one head: selection stages
-    in full, the executor on ``n_rows`` evenly spaced query regions.
-    Returns (ms_per_call_extrapolated, sample description, threads)."""
+def cpu_reference_sample(cfg, seed=0, head_ids=(0, 1)):
+    """Time the reference algorithm (oracle port, float32 numpy) on whole heads
+    of the call: padded_sparse_attention per head (padding.py:95-165), heads
+    sequential. Returns (ms per call extrapolated to every head, sample
+    description, BLAS threads)."""
     import numpy as np
+    import torch
     from oracle import draftattn_oracle as O
 
     f, h, w, ph, pw, heads, d, sp = cfg
     grid = O.Grid(f, h, w, ph, pw)
-    q, k, v = O.gen_real_inputs(grid, d, seed, heads, head_ids=[0])
-    q, k, v = (x[0].astype(np.float64) for x in (q, k, v))
-    t0 = time.perf_counter()
-    mask, _ = O.draft_mask(q, k, grid, sp)
-    t1 = time.perf_counter()
-    rows = np.linspace(0, grid.num_regions - 1, min(n_rows, grid.num_regions)).astype(np.int64)
-    qr, kr, vr = O.permute_in(q, grid), O.permute_in(k, grid), O.permute_in(v, grid)
-    kv = None if grid.divisible else O.valid_reordered(grid)
-    t2 = time.perf_counter()
-    O.block_sparse_attention(qr, kr, vr, mask.kept, O.head_dim_scale(d), key_valid=kv, rows=rows)
-    t3 = time.perf_counter()
-    exec_full = (t3 - t2) * grid.num_regions / len(rows)
-    per_head = (t1 - t0) + (t2 - t1) + exec_full
-    threads = os.cpu_count() or 1
-    sample = (f"1 of {heads} heads: pool+draft+select in full ({t1 - t0:.2f}s), executor on "
-              f"{len(rows)}/{grid.num_regions} query regions ({t3 - t2:.2f}s); x{grid.num_regions // len(rows)} "
-              f"regions, x{heads} heads extrapolated; float64 numpy, BLAS threads={threads}")
+    q, k, v = O.gen_real_inputs(grid, d, seed, heads, head_ids=list(head_ids))
+    rnd = lambda x: torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()  # noqa: E731
+    q, k, v = rnd(q), rnd(k), rnd(v)
+    times = []
+    for slot in range(len(head_ids)):
+        t0 = time.perf_counter()
+        O.padded_sparse_attention(q[slot], k[slot], v[slot], f, h, w, ph, pw, sp)
+        times.append(time.perf_counter() - t0)
+    per_head = statistics.mean(times)
+    threads = _blas_threads()
+    sample = (f"{len(head_ids)} of {heads} heads in full ({', '.join(f'{t:.2f}' for t in times)} s), float32 numpy "
+              f"(oracle port), BLAS threads={threads}, {os.cpu_count()} host cores; ms/call = mean per head x "
+              f"{heads} heads (extrapolated)")
     return per_head * heads * 1e3, sample, threads
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(n[0]) if n else (os.cpu_count() or 1)
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
 
 
 def run_reference(args, cfg, name):
@@ -148,18 +161,25 @@ def run_reference(args, cfg, name):
         return
     vals, sample, threads = [], "", 1
     for _ in range(args.warmup_ref):
-        cpu_reference_sample(cfg, n_rows=8)
-    for _ in range(args.steps):
-        ms, sample, threads = cpu_reference_sample(cfg)
+        cpu_reference_sample(CONFIGS["tiny"], head_ids=(0,))
+    heads = cfg[5]
+    for s in range(args.steps):  # one whole head per step, a different head each step
+        ms, sample, threads = cpu_reference_sample(cfg, head_ids=(s % heads,))
         vals.append(ms)
     ms = statistics.median(vals)
+    sample = (f"one whole head per step (heads 0..{args.steps - 1}), float32 numpy (oracle port), "
+              f"BLAS threads={threads}, {os.cpu_count()} host cores; ms/call = per-head median x {heads} heads "
+              f"(extrapolated)")
     line = {
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth.py gaussian, seeded)",
         "config": _config_dict(name, cfg, args.gpus),
         "cpu_baseline": {"value": ms, "unit": "ms/call", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": ms, "unit": "ms/call", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # each step times ONE head of the call; value = that x heads
+        "extrapolated": {"timed_s_per_step": [v / heads / 1e3 for v in vals], "factor": heads,
+                         "what": "whole heads timed, call = per-head time x heads"},
     }
     print(json.dumps(line), flush=True)
 
@@ -276,10 +296,11 @@ def run_ours(args, cfg, name):
         e2e = _e2e_sharded(hp, q.shape, dev, args, world)
     if world == 1:
         e2e = _e2e(da, plan, cfg, dev, args)
-        dense_ms = _dense_sdpa_ms(heads, n, d, dev) if args.dense else None
+        dense_ms = None if args.no_dense else _dense_sdpa_ms(heads, n, d, dev)
         if not args.no_cpu:
             cms, sample, threads = cpu_reference_sample(cfg)
-            cpu_base = {"value": cms, "unit": "ms/call", "cores": threads, "kind": "port", "sample": sample}
+            cpu_base = {"value": cms, "unit": "ms/call", "cores": threads, "kind": "port", "sample": sample,
+                        "extrapolated": True}
     if rank == 0:
         launches = _lib.lib().da_pipeline_launches(0, 0) * args.steps
         line = {
@@ -404,7 +425,7 @@ def main():
     ap.add_argument("--sparsity", type=float, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--dense", action="store_true", help="also time dense cuDNN SDPA at the same shape")
+    ap.add_argument("--no-dense", action="store_true", help="skip timing dense SDPA at the same shape")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.sparsity is not None:

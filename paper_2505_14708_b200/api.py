@@ -605,6 +605,45 @@ def _run_layout(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_
     return o, mask
 
 
+def _attend(q, k, v, plan: PadPlan, mask: RegionMask, scale, qkv_layout="hnd", out_dev=None):
+    """K4 alone on ORIGINAL-order token tensors with a given mask (one mask
+    per head, or one shared by all heads): the executor stage of
+    padded_sparse_attention (padding.py:155-157) with the permutation fused.
+    Used by the head-parallel path once a cross-rank shared mask is known.
+    ``out_dev``: optional bf16 output buffer in the inputs' layout."""
+    q3, squeeze = _as_heads(q, qkv_layout, "q")
+    k3, _ = _as_heads(k, qkv_layout, "k")
+    v3, _ = _as_heads(v, qkv_layout, "v")
+    heads, n, d = q3.shape
+    if n != plan.num_valid:
+        raise ValueError(f"expected {plan.num_valid} real-token rows, got {n}")
+    if mask.heads not in (1, heads) or mask.g != plan.layout.num_regions:
+        raise ValueError(f"mask of {mask.heads} heads over {mask.g} regions does not fit {heads} heads / "
+                         f"{plan.layout.num_regions} regions")
+    if d % 8 or v3.shape[2] % 8:
+        raise ValueError("_attend needs head dims that are multiples of 8")
+    q3, k3, v3 = _prep(q3), _prep(k3), _prep(v3)
+    dv = v3.shape[2]
+    dev = q3.device
+    if out_dev is not None:
+        o3, _ = _as_heads(out_dev, qkv_layout, "out")
+        if o3.dtype != torch.bfloat16 or tuple(o3.shape) != (heads, n, dv) or o3.stride(2) != 1:
+            raise ValueError("output buffer has the wrong shape, dtype or strides")
+        o_base = out_dev
+    else:
+        o_base, o3 = _alloc_like_layout(heads, n, dv, qkv_layout if not squeeze else "hnd", dev)
+    lay = plan.layout
+    grid = make_grid(plan.frames, plan.height, plan.width, lay.patch_h, lay.patch_w)
+    a = _attn_struct(q3, k3, v3, o3, d, dv, _lib.LAYOUT_ORIGINAL, scale)
+    a.row_ptr, a.col_idx, a.mask_cap = mask.row_ptr.data_ptr(), mask.col_idx.data_ptr(), mask.col_idx.shape[1]
+    a.shared_mask = 1 if mask.heads == 1 else 0
+    ws = torch.empty(max(1, lib().da_attn_workspace_size(heads, ctypes.byref(grid))), dtype=torch.uint8, device=dev)
+    a.workspace = ws.data_ptr()
+    with torch.cuda.device(dev):
+        check(lib().da_block_sparse_fwd(ctypes.byref(a), ctypes.byref(grid), _stream_ptr(dev)), "block_sparse_fwd")
+    return o3[0] if squeeze else (o_base if qkv_layout == "nhd" else o3)
+
+
 def _cat_masks(masks) -> RegionMask:
     """Stack per-head-group masks of one call (same g, keep ratio, capacity)."""
     if len(masks) == 1:

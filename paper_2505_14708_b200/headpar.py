@@ -2,9 +2,32 @@
 
 The reference runs heads one after another (sparse.py:273-279); heads are
 independent (per-head masks by default), so P ranks each own heads/P heads.
-A sequence-parallel caller holds n/P tokens of every head; one NCCL
-all-to-all reshards Q/K/V to "all tokens of my heads" before the call and one
-reshards the output back (Ulysses-style). No other collective is needed.
+A sequence-parallel caller holds n/P tokens of every head; all-to-alls
+reshard Q/K/V to "all tokens of my heads" before the pipeline and reshard the
+output back (Ulysses-style).
+
+The local heads are processed in head GROUPS so the collectives overlap the
+compute: the input all-to-alls of group g+1 are in flight while group g runs
+its pipeline, and group g's output all-to-all runs while group g+1 computes.
+The collectives are asynchronous NCCL calls (their stream waits for the
+packing copies; the compute stream waits for their completion only where it
+needs the data).
+
+Layouts (no copies beyond the one pack per input tensor and the one unpack of
+the output):
+  * send buffer of a group: [dest rank][my rows][its heads of the group][d]
+    (one strided copy of the caller's (n/P, H, d) shard);
+  * receive buffer: [src rank][its rows][my heads of the group][d], which IS
+    the (n, heads_of_group, d) "nhd" layout the pipeline reads in place;
+  * the pipeline writes (n, heads_of_group, dv), whose per-destination row
+    blocks are contiguous: it is the output all-to-all's send buffer as is.
+
+``shared_head_mask`` (sparse.py:281-297) needs the mean of every head's
+selection basis before any head can attend. The ranks fold the per-head fp64
+bases in global head order, as the reference's ``basis_sum + basis`` loop does
+(rank r continues the running sum it receives from rank r-1 with its own heads
+and passes it on), so the mean, and therefore the mask, is bit-identical to
+the single-process result; the last rank broadcasts the mean.
 """
 
 from __future__ import annotations
@@ -16,7 +39,7 @@ from . import api
 
 
 def seq_to_head(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """(n/P, H, d) sequence shard -> (n, H/P, d) head shard (all-to-all)."""
+    """(n/P, H, d) sequence shard -> (n, H/P, d) head shard (one blocking all-to-all)."""
     nl, heads, d = x.shape
     hl = heads // world
     send = x.reshape(nl, world, hl, d).permute(1, 0, 2, 3).contiguous()  # [dest rank][rows][my heads]
@@ -26,7 +49,7 @@ def seq_to_head(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
 
 
 def head_to_seq(o: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """(n, H/P, d) head shard -> (n/P, H, d) sequence shard (all-to-all)."""
+    """(n, H/P, d) head shard -> (n/P, H, d) sequence shard (one blocking all-to-all)."""
     n, hl, d = o.shape
     nl = n // world
     send = o.reshape(world, nl, hl, d).contiguous()                        # [dest rank][its rows][my heads]
@@ -35,28 +58,174 @@ def head_to_seq(o: torch.Tensor, world: int, group=None) -> torch.Tensor:
     return recv.permute(1, 0, 2, 3).reshape(nl, world * hl, d)
 
 
+def head_groups(local_heads: int, groups: int):
+    """Contiguous [h0, h1) ranges splitting a rank's heads into ``groups`` groups."""
+    groups = max(1, min(groups, local_heads))
+    base, extra = divmod(local_heads, groups)
+    out, h0 = [], 0
+    for gi in range(groups):
+        h1 = h0 + base + (1 if gi < extra else 0)
+        out.append((h0, h1))
+        h0 = h1
+    return out
+
+
+def ordered_head_sum(bases: torch.Tensor, rank: int, world: int, group=None) -> torch.Tensor | None:
+    """Sum of every rank's per-head bases in global head order, left fold
+    ((b_0 + b_1) + b_2) + ... (sparse.py:296), across ranks: rank r receives
+    the running sum of ranks < r, adds its own heads in order and sends it on.
+    Returns the total on the LAST rank, None elsewhere. ``bases``: this rank's
+    (heads, ...) float64 bases, its heads being the next ones in global order."""
+    acc = None
+    if rank > 0:
+        acc = torch.empty_like(bases[0])
+        dist.recv(acc, src=_global(rank - 1, group), group=group)
+    for h in range(bases.shape[0]):
+        acc = bases[h].clone() if acc is None else acc + bases[h]
+    if rank < world - 1:
+        dist.send(acc, dst=_global(rank + 1, group), group=group)
+        return None
+    return acc
+
+
+def _record(events):
+    """Start a (begin, end) CUDA event pair on the current stream, or None."""
+    if events is None:
+        return None
+    pair = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    pair[0].record()
+    events.append(pair)
+    return pair
+
+
+def _close(pair):
+    if pair is not None:
+        pair[1].record()
+
+
+def _global(rank: int, group) -> int:
+    return rank if group is None else dist.get_global_rank(group, rank)
+
+
 class HeadParallelAttention:
-    """padded_sparse_attention over a sequence-sharded (n/P, H, d) input."""
+    """padded_sparse_attention over a sequence-sharded (n/P, H, d) input.
+
+    ``head_groups``: how many groups the rank's heads are split into for the
+    communication / compute overlap (1 = no overlap). ``compute`` (tests):
+    replaces the pipeline, called as compute(q, k, v, out) on (n, hg, d) "nhd"
+    views and a (n, hg, dv) output buffer; returns a mask or None.
+    """
 
     def __init__(self, plan: api.PadPlan, sparsity: float, world: int, rank: int, group=None,
-                 scale=None, pool_mode="average", select_on="logits", force_row_keep=True):
+                 scale=None, pool_mode="average", select_on="logits", force_row_keep=True,
+                 shared_head_mask=False, head_groups=2, compute=None):
         self.plan, self.sparsity, self.world, self.rank, self.group = plan, sparsity, world, rank, group
         self.scale, self.pool_mode, self.select_on, self.force = scale, pool_mode, select_on, force_row_keep
+        self.shared = shared_head_mask
+        self.groups = head_groups
+        self.compute = compute
 
-    def __call__(self, q, k, v, attn_events=None, a2a_events=None):
-        """``a2a_events`` (optional): two (begin, end) CUDA event pairs recorded
-        around the input and output all-to-alls, for timing the collectives."""
-        if a2a_events is not None:
-            a2a_events[0][0].record()
-        qh, kh, vh = (seq_to_head(x, self.world, self.group) for x in (q, k, v))
-        if a2a_events is not None:
-            a2a_events[0][1].record()
-        scale = self.scale if self.scale is not None else api.head_dim_scale(q.shape[-1])
-        out, mask, _ = api._pipeline(qh, kh, vh, self.plan, self.sparsity, scale, self.pool_mode, self.select_on,
-                                     self.force, False, "nhd", attn_events=attn_events, want_bitmap=False)
-        if a2a_events is not None:
-            a2a_events[1][0].record()
-        res = head_to_seq(out, self.world, self.group)
-        if a2a_events is not None:
-            a2a_events[1][1].record()
-        return res, mask
+    # ------------------------------------------------------------ collectives
+    def _pack(self, x, h0, h1):
+        nl, heads, d = x.shape
+        hl = heads // self.world
+        return x.reshape(nl, self.world, hl, d)[:, :, h0:h1, :].permute(1, 0, 2, 3).contiguous()
+
+    def _a2a(self, recv, send):
+        return dist.all_to_all_single(recv, send, group=self.group, async_op=True)
+
+    def _issue_inputs(self, q, k, v, h0, h1):
+        bufs, works = [], []
+        for x in (q, k, v):
+            send = self._pack(x, h0, h1)                      # [dest][nl][hg][d]
+            recv = torch.empty_like(send)                     # [src][nl][hg][d] == (n, hg, d)
+            works.append(self._a2a(recv, send))
+            bufs.append(recv)
+        return bufs, works
+
+    # ------------------------------------------------------------ call
+    def __call__(self, q, k, v, compute_events=None):
+        """q, k, v: this rank's (n/P, H, d) sequence shards. Returns the
+        (n/P, H, dv) output shard and this rank's mask(s). ``compute_events``
+        (timing): a list that receives one (begin, end) CUDA event pair per
+        compute phase on the current stream; the collectives run on NCCL's
+        stream, so call time minus compute time is the exposed communication."""
+        nl, heads, d = q.shape
+        dv = v.shape[2]
+        if heads % self.world or k.shape != q.shape or v.shape[:2] != q.shape[:2]:
+            raise ValueError("q, k, v must be (n/P, H, d) shards with H divisible by the world size")
+        hl = heads // self.world
+        n = nl * self.world
+        scale = self.scale if self.scale is not None else api.head_dim_scale(d)
+        groups = head_groups(hl, self.groups)
+        out = torch.empty((nl, heads, dv), dtype=torch.bfloat16, device=q.device)
+        if self.shared:
+            return self._call_shared(q, k, v, out, groups, scale, compute_events)
+
+        inflight = {0: self._issue_inputs(q, k, v, *groups[0])}
+        outs, masks = [], []
+        for gi, (h0, h1) in enumerate(groups):
+            if gi + 1 < len(groups):  # next group's inputs travel while this group computes
+                inflight[gi + 1] = self._issue_inputs(q, k, v, *groups[gi + 1])
+            (qh, kh, vh), works = inflight.pop(gi)
+            for w in works:
+                w.wait()
+            hg = h1 - h0
+            res = torch.empty((n, hg, dv), dtype=torch.bfloat16, device=q.device)
+            ev = _record(compute_events)
+            masks.append(self._compute(qh.view(n, hg, d), kh.view(n, hg, d), vh.view(n, hg, dv), res, scale))
+            _close(ev)
+            recv = torch.empty((self.world, nl, hg, dv), dtype=torch.bfloat16, device=q.device)
+            outs.append((h0, h1, recv, self._a2a(recv, res.view(self.world, nl, hg, dv))))
+        for h0, h1, recv, work in outs:
+            work.wait()
+            out.view(nl, self.world, hl, dv)[:, :, h0:h1, :].copy_(recv.permute(1, 0, 2, 3))
+        masks = [m for m in masks if m is not None]
+        return out, (api._cat_masks(masks) if masks else None)
+
+    def _compute(self, qh, kh, vh, res, scale):
+        if self.compute is not None:
+            return self.compute(qh, kh, vh, res)
+        _, mask, _ = api._pipeline(qh, kh, vh, self.plan, self.sparsity, scale, self.pool_mode, self.select_on,
+                                   self.force, False, "nhd", want_bitmap=False, out_dev=res)
+        return mask
+
+    def _call_shared(self, q, k, v, out, groups, scale, compute_events):
+        """One mask for all heads of all ranks: inputs first, then the ordered
+        cross-rank fold of the bases, the selection, and the attention."""
+        nl, heads, d = q.shape
+        dv = v.shape[2]
+        hl = heads // self.world
+        n = nl * self.world
+        inputs = []
+        for h0, h1 in groups:
+            bufs, works = self._issue_inputs(q, k, v, h0, h1)
+            for w in works:
+                w.wait()
+            hg = h1 - h0
+            inputs.append((h0, h1, bufs[0].view(n, hg, d), bufs[1].view(n, hg, d), bufs[2].view(n, hg, dv)))
+        ev = _record(compute_events)
+        bases = []
+        for _, _, qh, kh, _ in inputs:
+            qp = api.pool_tokens(qh, self.plan, self.pool_mode, qkv_layout="nhd")
+            kp = api.pool_tokens(kh, self.plan, self.pool_mode, qkv_layout="nhd")
+            bases.append(api.draft_logits(qp, kp, scale, softmax=self.select_on == "softmax"))
+        _close(ev)
+        total = ordered_head_sum(torch.cat(bases, 0), self.rank, self.world, self.group)
+        g = self.plan.layout.num_regions
+        mean = total / heads if total is not None else torch.empty((g, g), dtype=torch.float64, device=q.device)
+        dist.broadcast(mean, src=_global(self.world - 1, self.group), group=self.group)
+        ev = _record(compute_events)
+        mask = api.select_top_fraction(mean, 1.0 - self.sparsity, self.force)
+        outs = []
+        for h0, h1, qh, kh, vh in inputs:
+            hg = h1 - h0
+            res = torch.empty((n, hg, dv), dtype=torch.bfloat16, device=q.device)
+            api._attend(qh, kh, vh, self.plan, mask, scale, qkv_layout="nhd", out_dev=res)
+            recv = torch.empty((self.world, nl, hg, dv), dtype=torch.bfloat16, device=q.device)
+            outs.append((h0, h1, recv, self._a2a(recv, res.view(self.world, nl, hg, dv))))
+        _close(ev)
+        for h0, h1, recv, work in outs:
+            work.wait()
+            out.view(nl, self.world, hl, dv)[:, :, h0:h1, :].copy_(recv.permute(1, 0, 2, 3))
+        return out, mask

@@ -1,4 +1,7 @@
-"""Sequence <-> head resharding of the multi-GPU path, world_size 2 over gloo (CPU)."""
+"""Host-side logic of the multi-GPU path, world_size 2 and 3 over gloo (CPU):
+the sequence <-> head resharding, the pipelined head-group schedule with
+asynchronous all-to-alls, and the head-ordered cross-rank fold behind the
+shared-head mask."""
 
 import os
 import socket
@@ -17,10 +20,14 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, results):
+def _init(rank, world, port):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _reshard_worker(rank, world, port, results):
+    _init(rank, world, port)
     try:
         from paper_2505_14708_b200.headpar import head_to_seq, seq_to_head
 
@@ -41,5 +48,88 @@ def test_seq_head_resharding_world2():
     world = 2
     mgr = mp.Manager()
     results = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    mp.spawn(_reshard_worker, args=(world, _free_port(), results), nprocs=world, join=True)
     assert dict(results) == {0: True, 1: True}
+
+
+def _pipelined_worker(rank, world, port, groups, results):
+    # HeadParallelAttention's schedule with a stand-in per-head compute
+    # (out = 2 v + row-sum of q, per head: any function of all of a head's rows
+    # would show a resharding error); the pipeline itself needs a GPU
+    _init(rank, world, port)
+    try:
+        from paper_2505_14708_b200 import api
+        from paper_2505_14708_b200.headpar import HeadParallelAttention
+
+        n, heads, d = 24, 6 * world, 8
+        g = torch.Generator().manual_seed(0)
+        full = [torch.randn(n, heads, d, generator=g).to(torch.bfloat16) for _ in range(3)]
+        nl = n // world
+
+        def compute(qh, kh, vh, out):  # (n, hg, d) views
+            out.copy_((2 * vh.float() + qh.float().sum(0, keepdim=True) + kh.float().mean(0, keepdim=True)).to(torch.bfloat16))
+            return None
+
+        plan = api.pad_plan(1, 1, n, 1, 1)
+        hp = HeadParallelAttention(plan, 0.5, world, rank, head_groups=groups, compute=compute)
+        out, _ = hp(*(x[rank * nl:(rank + 1) * nl].contiguous() for x in full))
+        want = torch.empty(n, heads, d, dtype=torch.bfloat16)
+        for h in range(heads):
+            compute(full[0][:, h:h + 1], full[1][:, h:h + 1], full[2][:, h:h + 1], want[:, h:h + 1])
+        results[rank] = bool(torch.equal(out, want[rank * nl:(rank + 1) * nl]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,groups", [(2, 1), (2, 3), (3, 2), (2, 6)])
+def test_pipelined_head_groups_world(world, groups):
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_pipelined_worker, args=(world, _free_port(), groups, results), nprocs=world, join=True)
+    assert dict(results) == {r: True for r in range(world)}
+
+
+def _fold_worker(rank, world, port, results):
+    _init(rank, world, port)
+    try:
+        from paper_2505_14708_b200.headpar import ordered_head_sum
+
+        heads = 4 * world
+        g = torch.Generator().manual_seed(1)
+        # wide dynamic range so that the summation order changes the rounding
+        bases = torch.randn(heads, 16, 16, generator=g, dtype=torch.float64) * \
+            torch.logspace(-12, 12, heads, dtype=torch.float64)[torch.randperm(heads, generator=g)][:, None, None]
+        hl = heads // world
+        total = ordered_head_sum(bases[rank * hl:(rank + 1) * hl].clone(), rank, world)
+        if rank == world - 1:
+            ref = bases[0].clone()
+            for h in range(1, heads):
+                ref = ref + bases[h]  # sparse.py:296 left fold
+            rev = bases[-1].clone()
+            for h in range(heads - 2, -1, -1):
+                rev = rev + bases[h]  # another order rounds differently on these inputs
+            results[rank] = bool(torch.equal(total, ref)) and not bool(torch.equal(ref, rev))
+        else:
+            results[rank] = total is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ordered_head_sum_is_the_reference_left_fold(world):
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_fold_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    assert dict(results) == {r: True for r in range(world)}
+
+
+def test_head_groups_split():
+    from paper_2505_14708_b200.headpar import head_groups
+
+    assert head_groups(3, 2) == [(0, 2), (2, 3)]
+    assert head_groups(12, 1) == [(0, 12)]
+    assert head_groups(2, 8) == [(0, 1), (1, 2)]
+    for hl in range(1, 20):
+        for G in range(1, 6):
+            gs = head_groups(hl, G)
+            assert gs[0][0] == 0 and gs[-1][1] == hl and all(a[1] == b[0] for a, b in zip(gs, gs[1:]))
