@@ -144,12 +144,13 @@ class HeadParallelAttention:
         return bufs, works
 
     # ------------------------------------------------------------ call
-    def __call__(self, q, k, v, compute_events=None):
+    def __call__(self, q, k, v, compute_events=None, k4_events=None):
         """q, k, v: this rank's (n/P, H, d) sequence shards. Returns the
         (n/P, H, dv) output shard and this rank's mask(s). ``compute_events``
         (timing): a list that receives one (begin, end) CUDA event pair per
         compute phase on the current stream; the collectives run on NCCL's
-        stream, so call time minus compute time is the exposed communication."""
+        stream, so call time minus compute time is the exposed communication.
+        ``k4_events``: likewise, one pair around each group's attention kernel."""
         nl, heads, d = q.shape
         dv = v.shape[2]
         if heads % self.world or k.shape != q.shape or v.shape[:2] != q.shape[:2]:
@@ -173,7 +174,8 @@ class HeadParallelAttention:
             hg = h1 - h0
             res = torch.empty((n, hg, dv), dtype=torch.bfloat16, device=q.device)
             ev = _record(compute_events)
-            masks.append(self._compute(qh.view(n, hg, d), kh.view(n, hg, d), vh.view(n, hg, dv), res, scale))
+            masks.append(self._compute(qh.view(n, hg, d), kh.view(n, hg, d), vh.view(n, hg, dv), res, scale,
+                                       k4_events))
             _close(ev)
             recv = torch.empty((self.world, nl, hg, dv), dtype=torch.bfloat16, device=q.device)
             outs.append((h0, h1, recv, self._a2a(recv, res.view(self.world, nl, hg, dv))))
@@ -183,11 +185,15 @@ class HeadParallelAttention:
         masks = [m for m in masks if m is not None]
         return out, (api._cat_masks(masks) if masks else None)
 
-    def _compute(self, qh, kh, vh, res, scale):
+    def _compute(self, qh, kh, vh, res, scale, k4_events=None):
         if self.compute is not None:
             return self.compute(qh, kh, vh, res)
+        ev = None
+        if k4_events is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            k4_events.append(ev)
         _, mask, _ = api._pipeline(qh, kh, vh, self.plan, self.sparsity, scale, self.pool_mode, self.select_on,
-                                   self.force, False, "nhd", want_bitmap=False, out_dev=res)
+                                   self.force, False, "nhd", want_bitmap=False, out_dev=res, attn_events=ev)
         return mask
 
     def _call_shared(self, q, k, v, out, groups, scale, compute_events):
