@@ -33,20 +33,23 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Build libdraftattn_b200.so for sm_100a unless it is up to date."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, flags=()) -> Path:
+    """Build libdraftattn_b200.so for sm_100a unless it is up to date.
+    ``out`` / ``flags``: experiment builds (tools/probes) into another path
+    with extra -D options; the shipped library takes neither."""
+    target = Path(out) if out is not None else OUT
+    if out is None and not force and not _stale():
         return OUT
-    extra = os.environ.get("DA_NVCC_FLAGS", "").split()  # experiments only (e.g. -DDA_MBAR_NOHINT)
+    extra = os.environ.get("DA_NVCC_FLAGS", "").split() + list(flags)  # experiments only
     cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-o", str(OUT)] + extra + [str(CSRC / s) for s in SOURCES]
+           "-o", str(target)] + extra + [str(CSRC / s) for s in SOURCES]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed ({res.returncode})")
-    return OUT
+    return target
 
 
 if __name__ == "__main__":

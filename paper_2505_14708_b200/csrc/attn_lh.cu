@@ -74,6 +74,15 @@ constexpr int SLOT = 2 * TILE;  // a step: key regions j0, j1
 #endif
 constexpr int KSL = LH_KSL;
 constexpr int VSL = LH_VSL;
+// LH_VCP: V tiles move by cp.async (LDGSTS) issued from LH_VCP extra warps
+// (warps 12 ..) instead of bulk copies from warp 2, so K (bulk copy engine)
+// and V (load/store units) travel L2 -> SM on two paths at once. 0 = both by
+// bulk copies.
+#ifndef LH_VCP
+#define LH_VCP 0
+#endif
+constexpr int VCP = LH_VCP;
+constexpr int THREADS = 384 + 32 * VCP;
 constexpr int INFO = 16;
 constexpr int RAGW = 512;
 #ifndef LH_LISTCAP
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restric
   }
 }
 
-__global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) {
+__global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
   SmemAux& aux = *reinterpret_cast<SmemAux*>(smem + SMEM_END);
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < KSL; ++s) { mbar_init(&B.k_full[s], 1); mbar_init(&B.k_empty[s], 1); }
-    for (int s = 0; s < VSL; ++s) { mbar_init(&B.v_full[s], 1); mbar_init(&B.v_empty[s], 1); }
+    for (int s = 0; s < VSL; ++s) { mbar_init(&B.v_full[s], VCP ? 32 * VCP : 1); mbar_init(&B.v_empty[s], 1); }
     for (int h = 0; h < 2; ++h) {
       for (int b = 0; b < NSB; ++b) {
         mbar_init(&B.s_full[h][b], 1);
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
     for (int s = 0; s < INFO; ++s) mbar_init(&B.info_full[s], 1);
     for (int s = 0; s < IR; ++s) {
       mbar_init(&B.item_full[s], 1);
-      mbar_init(&B.item_empty[s], 11);  // warps 1, 2, 3 and the 8 softmax warps
+      mbar_init(&B.item_empty[s], VCP ? 10 + VCP : 11);  // warps 1, 3, the 8 softmax warps and the V warp(s)
     }
     fence_barrier_init();
   }
@@ -324,7 +333,7 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
     return it;
   };
 
-  if (warp == 0 || warp == 2) {
+  if (warp == 0 || (warp == 2 && VCP == 0)) {
     // ===================== producers (warp 0: items, step info, K; warp 2: V) =====================
     const bool is_k = warp == 0;
     const int NSL = is_k ? KSL : VSL;
@@ -504,6 +513,35 @@ __global__ void __launch_bounds__(384, 1) sparse_attn_lh_kernel(const Params p) 
         if (last) break;
       }
       ++qi;
+    }
+  } else if (warp >= 12) {
+    // ============ V copiers (LH_VCP > 0): cp.async of the step's V tiles ============
+    const int t = threadIdx.x - 384;
+    constexpr int NT = 32 * VCP;
+    int kq = 0;
+    for (;;) {
+      Item itm;
+      if (!fetch_item(p, next_item(), items, itm)) break;
+      const uint8_t* hb = p.vt + (long long)itm.h * p.geo.g * TILE;
+      const int n = (itm.n + 1) / 2;
+      for (int st = 0; st < n; ++st) {
+        const int ii = kq % INFO;
+        mbar_wait_warp(&B.info_full[ii], (uint32_t)((kq / INFO) & 1));
+        const int4 e = aux.info[ii];
+        const int s = kq % VSL;
+        if (kq >= VSL) mbar_wait_warp(&B.v_empty[s], ((kq / VSL) - 1) & 1);
+        ++kq;
+        const uint32_t dst = smem_u32(sV + s * SLOT);
+        const uint8_t* src0 = hb + (long long)e.x * TILE;
+#pragma unroll
+        for (int c = t; c < TILE / 16; c += NT) cp_async16(dst + 16 * c, src0 + 16 * c, 16);
+        if (e.z & 2) {
+          const uint8_t* src1 = hb + (long long)e.y * TILE;
+#pragma unroll
+          for (int c = t; c < TILE / 16; c += NT) cp_async16(dst + TILE + 16 * c, src1 + 16 * c, 16);
+        }
+        cp_async_arrive_noinc(&B.v_full[s]);
+      }
     }
   } else if (warp >= 4) {
     // ============ softmax warpgroup wg = lane half wg; Q loader; epilogue ============
@@ -919,7 +957,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   const int sms = device_sms();
   const long long items = (long long)a.heads * g.g;
   const int grid = (int)(items < sms ? items : sms);
-  lhk::sparse_attn_lh_kernel<<<grid, 384, lhk::SMEM_ALLOC, st>>>(p);
+  lhk::sparse_attn_lh_kernel<<<grid, lhk::THREADS, lhk::SMEM_ALLOC, st>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // rows whose fixed softmax offset underflowed: redo their regions exactly
   return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * sms);
