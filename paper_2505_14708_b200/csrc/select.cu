@@ -583,24 +583,22 @@ DA_DEV float key32_score(unsigned int k) {
 
 // fp64 dot product of two feature rows in the fp64 GEMM's order
 // (draft_gemm_kernel, prep.cu: one sequential FMA chain over the features,
-// starting from 0.0), computed by a whole warp: the lanes load the rows
-// coalesced and every lane runs the same chain on shuffled operands, so every
-// lane returns the identical value. Band rescoring and the argmax rescoring
-// therefore rank exactly as the fp64 fallback path does.
-DA_DEV double dot64_seq_warp(const double* __restrict__ q, const double* __restrict__ k, int d) {
-  const int lane = threadIdx.x & 31;
+// starting from 0.0), by ONE thread: band rescoring and the argmax rescoring
+// therefore rank exactly as the fp64 fallback path does. Callers give each
+// lane its own candidate so a warp runs 32 chains at once.
+DA_DEV double dot64_seq(const double* __restrict__ q, const double* __restrict__ k, int d) {
   double acc = 0.0;
-  for (int c0 = 0; c0 < d; c0 += 32) {
-    const int c = c0 + lane;
-    const double qv = c < d ? __ldg(q + c) : 0.0;
-    const double kv = c < d ? __ldg(k + c) : 0.0;
-    const int n = min(32, d - c0);
-    for (int s = 0; s < n; ++s) acc = fma(__shfl_sync(0xffffffffu, qv, s), __shfl_sync(0xffffffffu, kv, s), acc);
+  int c = 0;
+  for (; c + 4 <= d; c += 4) {
+    const double q0 = __ldg(q + c), q1 = __ldg(q + c + 1), q2 = __ldg(q + c + 2), q3 = __ldg(q + c + 3);
+    const double k0 = __ldg(k + c), k1 = __ldg(k + c + 1), k2 = __ldg(k + c + 2), k3 = __ldg(k + c + 3);
+    acc = fma(q0, k0, acc);
+    acc = fma(q1, k1, acc);
+    acc = fma(q2, k2, acc);
+    acc = fma(q3, k3, acc);
   }
+  for (; c < d; ++c) acc = fma(__ldg(q + c), __ldg(k + c), acc);
   return acc;
-}
-DA_DEV double score64_warp(const double* __restrict__ q, const double* __restrict__ k, int d, double scale) {
-  return dot64_seq_warp(q, k, d) * scale;
 }
 
 __global__ void s32_init_kernel(Sel32State* st, unsigned int* hist, unsigned int* rowmax, int g, long long m,
@@ -952,16 +950,37 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
   unsigned int* B = bm + ((long long)h * g + row) * w32;
   int* C = cand + (long long)h * S32_CAP;
   long long hi_cnt = 0;
-  int best = -1, nbest = 0;
+  int best = -1;
   double bv = 0.0;
   const double* qrow = qp + ((long long)h * g + row) * d;
-  // fp64 score of candidate column jj (the fp64 GEMM's summation order); keeps
-  // the first maximum in ascending column order
+  // Row argmax candidates (within 2 eps of the fp32 row max) are collected in
+  // ascending column order, 32 at a time, and rescored in fp64 (the fp64
+  // GEMM's summation order) one candidate per lane; the first maximum in
+  // ascending column order wins, as np.argmax's does.
+  __shared__ int acand[8][32];
+  int* ac = acand[threadIdx.x / 32];
+  int na = 0;  // warp-uniform
+  auto flush_candidates = [&]() {
+    __syncwarp();
+    double sv = 0.0;
+    int col = 0x7fffffff;
+    if (lane < na) {
+      col = ac[lane];
+      sv = dot64_seq(qrow, kp + ((long long)h * g + col) * d, d) * scale;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double s2 = __shfl_xor_sync(0xffffffffu, sv, o);
+      const int c2 = __shfl_xor_sync(0xffffffffu, col, o);
+      if (c2 != 0x7fffffff && (col == 0x7fffffff || s2 > sv || (s2 == sv && c2 < col))) { sv = s2; col = c2; }
+    }
+    if (best < 0 || sv > bv) { best = col; bv = sv; }  // later batches hold larger columns
+    na = 0;
+    __syncwarp();
+  };
   auto argmax_candidate = [&](int jj) {
-    ++nbest;
-    const double* krow = kp + ((long long)h * g + jj) * d;
-    const double sv = dot64_seq_warp(qrow, krow, d) * scale;
-    if (best < 0 || sv > bv) { best = jj; bv = sv; }
+    if (lane == 0) ac[na] = jj;
+    if (++na == 32) flush_candidates();
   };
   if ((g & 3) == 0) {
     // 16-byte path: lane holds columns j0 + 4 lane .. + 3 (128 per step, the
@@ -1040,6 +1059,7 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
       }
     }
   }
+  if (na > 0) flush_candidates();
   if (lane == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&st[h].count_hi), (unsigned long long)hi_cnt);
     argmax[(long long)h * g + row] = best;
@@ -1050,8 +1070,8 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
 // the reference order - descending score, ties to the smaller flat index -
 // with a bitonic sort in shared memory, keep the first `need`, set their bits
 // and emit the threshold.
-// fp64 rescoring of the band, one warp per candidate (coalesced fp64 row
-// reads): keys into bkey[head][S32_CAP]; grid (S32_SCORE_CTAS, heads)
+// fp64 rescoring of the band, one thread per candidate (the fp64 GEMM's
+// summation order): keys into bkey[head][S32_CAP]; grid (S32_SCORE_CTAS, heads)
 constexpr int S32_SCORE_CTAS = 64;
 __global__ void __launch_bounds__(256) s32_band_score_kernel(const double* __restrict__ qp,
                                                              const double* __restrict__ kp, int g, int d, double scale,
@@ -1062,13 +1082,12 @@ __global__ void __launch_bounds__(256) s32_band_score_kernel(const double* __res
   if (*fallback) return;
   const int h = blockIdx.y;
   const int cnt = min(st[h].cand_count, S32_CAP);
-  const int lane = threadIdx.x & 31;
   const int* C = cand + (long long)h * S32_CAP;
-  for (int c = blockIdx.x * 8 + (threadIdx.x >> 5); c < cnt; c += gridDim.x * 8) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cnt; c += gridDim.x * blockDim.x) {
     const int f = C[c];
     const int i = f / g, j = f - i * g;
-    const double sc = score64_warp(qp + ((long long)h * g + i) * d, kp + ((long long)h * g + j) * d, d, scale);
-    if (lane == 0) bkey[(long long)h * S32_CAP + c] = score_key(sc);
+    const double sc = dot64_seq(qp + ((long long)h * g + i) * d, kp + ((long long)h * g + j) * d, d) * scale;
+    bkey[(long long)h * S32_CAP + c] = score_key(sc);
   }
 }
 
