@@ -13,8 +13,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libdraftattn_b200.so"
-SOURCES = ["api.cu", "prep.cu", "select.cu", "attn_portable.cu", "attn_lh.cu"]
-HEADERS = ["common.cuh", "kernels.h"]
+SOURCES = ["api.cu", "prep.cu", "select.cu", "attn_portable.cu", "attn_lh.cu", "attn_tk.cu"]
+HEADERS = ["common.cuh", "kernels.h", "attn_k4.cuh"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 

@@ -1,0 +1,101 @@
+// Shared pieces of the K4 kernels (attn_lh.cu, attn_tk.cu): launch
+// parameters, the work item (one query region of one head with its kept key
+// list) and token / key geometry in either tensor layout.
+#pragma once
+
+#include "common.cuh"
+
+namespace da {
+namespace k4 {
+
+constexpr int P = 64;         // region rows (8x8 pool)
+constexpr int D = 128;        // head dim
+constexpr int TILE = 16384;   // one region of K or V, bf16
+constexpr int KBLK = 32;      // key_norm_kernel blocks per head
+constexpr int RAGW = 512;     // ragged-region bitmap words (g <= 16384)
+constexpr int LISTCAP = 4096; // staged kept-list entries per item (else read from global)
+
+struct Params {
+  const __nv_bfloat16* q;
+  long long qh, qr;
+  __nv_bfloat16* out;
+  long long oh, orow;
+  int heads;
+  int layout;
+  float scale_log2;
+  const int* row_ptr;
+  const int* col_idx;
+  long long cap;
+  const uint8_t* key_valid;
+  int mask_h;
+  Geo geo;
+  RegionDecoder dec;
+  FastDiv per_head;  // g
+  const uint8_t* kt;
+  const uint8_t* vt;
+  const int* order;  // [heads][g] query regions by kept count (descending), or null
+  const float* kpart;
+  int kblk;
+  int* fb_count;
+  int* fb_items;
+  int* work;
+  uint64_t pol_kv, pol_q, pol_o;
+  long long* trace;  // LH_PROF output ([CTA][32]) or null
+};
+
+struct Item {
+  int h, i;
+  const int* list;
+  int n;
+};
+
+DA_DEV bool fetch_item(const Params& p, long long it, long long items, Item& o) {
+  if (it < 0 || it >= items) return false;
+  const int g = p.geo.g;
+  const int h = (int)fdiv((uint32_t)it, p.per_head);
+  const int k = (int)(it - (long long)h * g);
+  o.h = h;
+  o.i = p.order != nullptr ? __ldg(p.order + it) : k;
+  const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
+  const int b = rp[o.i];
+  o.list = p.col_idx + (long long)(h * p.mask_h) * p.cap + b;
+  o.n = rp[o.i + 1] - b;
+  return true;
+}
+
+DA_DEV long long token_row(const Params& p, int region, int r) {
+  if (p.layout == DA_LAYOUT_REORDERED) return (long long)region * P + r;
+  const RegionXY rc = p.dec(region);
+  const int u = r / p.geo.pw, v = r - u * p.geo.pw;
+  const int y = rc.y0 + u, x = rc.x0 + v;
+  if (y >= p.geo.H || x >= p.geo.W) return -1;
+  return ((long long)rc.f * p.geo.H + y) * p.geo.W + x;
+}
+
+DA_DEV unsigned long long key_mask(const Params& p, int j) {
+  if (p.key_valid != nullptr) {
+    const uint8_t* kv = p.key_valid + (long long)j * P;
+    unsigned long long m = 0;
+#pragma unroll 8
+    for (int r = 0; r < P; ++r) m |= (unsigned long long)(kv[r] != 0) << r;
+    return m;
+  }
+  const RegionXY rc = p.dec(j);
+  const int vy = min(p.geo.ph, p.geo.H - rc.y0), vx = min(p.geo.pw, p.geo.W - rc.x0);
+  if (vy == p.geo.ph && vx == p.geo.pw) return ~0ull;
+  const unsigned long long rowm = (1ull << vx) - 1ull;
+  unsigned long long m = 0;
+  for (int u = 0; u < vy; ++u) m |= rowm << (u * p.geo.pw);
+  return m;
+}
+
+// Is key row r of key region j a real (unmasked) key?
+DA_DEV bool key_row_valid(const Params& p, int j, int r) {
+  if (p.key_valid != nullptr) return p.key_valid[(long long)j * P + r] != 0;
+  const RegionXY rc = p.dec(j);
+  const int u = r / p.geo.pw, v = r - u * p.geo.pw;
+  return rc.y0 + u < p.geo.H && rc.x0 + v < p.geo.W;
+}
+
+}  // namespace k4
+}  // namespace da

@@ -35,6 +35,7 @@
 // warp 2 V copies; warp 3 GEMM2 issuer; warps 4-7 / 8-11 softmax warpgroups
 // for lane half 0 / 1 (each also loads half of Q's features into both halves
 // and writes half of the output features).
+#include "attn_k4.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -110,33 +111,11 @@ constexpr int NSB = 1;
 constexpr int NOB = 3 - NSB;  // O buffers (item parity when 2)
 constexpr uint32_t LANE_H = 16u << 16;  // TMEM address offset of lane half 1
 
-struct Params {
-  const __nv_bfloat16* q;
-  long long qh, qr;
-  __nv_bfloat16* out;
-  long long oh, orow;
-  int heads;
-  int layout;
-  float scale_log2;
-  const int* row_ptr;
-  const int* col_idx;
-  long long cap;
-  const uint8_t* key_valid;
-  int mask_h;
-  Geo geo;
-  RegionDecoder dec;
-  FastDiv per_head;  // g
-  const uint8_t* kt;
-  const uint8_t* vt;
-  const int* order;  // [heads][g] query regions by kept count (descending), or null
-  const float* kpart;
-  int kblk;
-  int* fb_count;
-  int* fb_items;
-  int* work;
-  uint64_t pol_kv, pol_q, pol_o;
-  long long* trace;  // LH_PROF output ([CTA][32]) or null
-};
+using k4::Params;
+using k4::Item;
+using k4::fetch_item;
+using k4::token_row;
+using k4::key_mask;
 
 struct __align__(8) Bars {
   uint64_t k_full[KSL], k_empty[KSL];
@@ -162,52 +141,6 @@ struct SmemAux {
 };
 constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
 static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
-
-struct Item {
-  int h, i;
-  const int* list;
-  int n;
-};
-
-DA_DEV bool fetch_item(const Params& p, long long it, long long items, Item& o) {
-  if (it < 0 || it >= items) return false;
-  const int g = p.geo.g;
-  const int h = (int)fdiv((uint32_t)it, p.per_head);
-  const int k = (int)(it - (long long)h * g);
-  o.h = h;
-  o.i = p.order != nullptr ? __ldg(p.order + it) : k;
-  const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
-  const int b = rp[o.i];
-  o.list = p.col_idx + (long long)(h * p.mask_h) * p.cap + b;
-  o.n = rp[o.i + 1] - b;
-  return true;
-}
-
-DA_DEV long long token_row(const Params& p, int region, int r) {
-  if (p.layout == DA_LAYOUT_REORDERED) return (long long)region * P + r;
-  const RegionXY rc = p.dec(region);
-  const int u = r / p.geo.pw, v = r - u * p.geo.pw;
-  const int y = rc.y0 + u, x = rc.x0 + v;
-  if (y >= p.geo.H || x >= p.geo.W) return -1;
-  return ((long long)rc.f * p.geo.H + y) * p.geo.W + x;
-}
-
-DA_DEV unsigned long long key_mask(const Params& p, int j) {
-  if (p.key_valid != nullptr) {
-    const uint8_t* kv = p.key_valid + (long long)j * P;
-    unsigned long long m = 0;
-#pragma unroll 8
-    for (int r = 0; r < P; ++r) m |= (unsigned long long)(kv[r] != 0) << r;
-    return m;
-  }
-  const RegionXY rc = p.dec(j);
-  const int vy = min(p.geo.ph, p.geo.H - rc.y0), vx = min(p.geo.pw, p.geo.W - rc.x0);
-  if (vy == p.geo.ph && vx == p.geo.pw) return ~0ull;
-  const unsigned long long rowm = (1ull << vx) - 1ull;
-  unsigned long long m = 0;
-  for (int u = 0; u < vy; ++u) m |= rowm << (u * p.geo.pw);
-  return m;
-}
 
 // Per head: query regions by kept count, descending: the dynamic item order
 // puts the heaviest items first (the order within a count does not matter:
@@ -782,8 +715,10 @@ struct KvTileArgs {
   long long hs[2], rs[2];
   uint8_t* out[2];
   int layout;
+  int tk;  // 1: the TMEM-fed K4's layouts (K row chunks, V^T), 0: GROUPED smem images
 };
 __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, RegionDecoder dec) {
+  __shared__ __align__(16) uint16_t vs[P * D];  // V^T: the region's V rows, transposed on the way out
   const int j = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
   const RegionXY rc = dec(j);
   const uint4* src = reinterpret_cast<const uint4*>(a.x[z] + h * a.hs[z]);
@@ -801,7 +736,21 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
       row = (rc.y0 + u < g.H && rc.x0 + v < g.W) ? ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v : -1;
     }
     const uint4 val = row >= 0 ? __ldg(src + row * rs8 + c) : make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
+    if (!a.tk) *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
+    else if (z == 0) *reinterpret_cast<uint4*>(dst + c * 1024 + r * 16) = val;
+    else *reinterpret_cast<uint4*>(vs + r * D + 8 * c) = val;
+  }
+  if (a.tk && z == 1) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int o = threadIdx.x + 256 * i;
+      const int kc = o >> 7, d = o & 127;  // keys 8 kc .. 8 kc + 7 of feature d
+      uint32_t w[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) w[m] = (uint32_t)vs[(8 * kc + 2 * m) * D + d] | ((uint32_t)vs[(8 * kc + 2 * m + 1) * D + d] << 16);
+      *reinterpret_cast<uint4*>(dst + kc * 2048 + d * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 
@@ -872,6 +821,15 @@ uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which) {
 }
 
 size_t attn_workspace_size(int heads, const Geo& g) { return ws_tiles(heads, g) + 2 * (size_t)heads * g.g * lhk::TILE; }
+
+// DA_K4_LH builds the lane-half kernel instead (A/B experiments)
+bool attn_uses_tk() {
+#ifdef DA_K4_LH
+  return false;
+#else
+  return true;
+#endif
+}
 
 bool tc_supported(const da_attn_args& a, const Geo& g) {
   if (a.d != 128 || a.dv != 128 || g.p != 64) return false;
@@ -949,16 +907,21 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
     ta.out[0] = attn_tiles(a.workspace, a.heads, g, 0);
     ta.out[1] = attn_tiles(a.workspace, a.heads, g, 1);
     ta.layout = a.layout;
+    ta.tk = attn_uses_tk() ? 1 : 0;
     lhk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
   }
   p.kt = attn_tiles(a.workspace, a.heads, g, 0);
   p.vt = attn_tiles(a.workspace, a.heads, g, 1);
-  if ((e = ensure_smem_optin((const void*)lhk::sparse_attn_lh_kernel, lhk::SMEM_ALLOC)) != cudaSuccess) return e;
   const int sms = device_sms();
   const long long items = (long long)a.heads * g.g;
   const int grid = (int)(items < sms ? items : sms);
-  lhk::sparse_attn_lh_kernel<<<grid, lhk::THREADS, lhk::SMEM_ALLOC, st>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (attn_uses_tk()) {
+    if ((e = launch_tk_kernel(p, grid, st)) != cudaSuccess) return e;
+  } else {
+    if ((e = ensure_smem_optin((const void*)lhk::sparse_attn_lh_kernel, lhk::SMEM_ALLOC)) != cudaSuccess) return e;
+    lhk::sparse_attn_lh_kernel<<<grid, lhk::THREADS, lhk::SMEM_ALLOC, st>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   // rows whose fixed softmax offset underflowed: redo their regions exactly
   return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * sms);
 }

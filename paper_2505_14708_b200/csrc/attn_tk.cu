@@ -1,0 +1,550 @@
+// K4 "tk": block-sparse FlashAttention forward, TRANSPOSED and TMEM-fed.
+//
+// Same semantics as the reference executor (sparse.py:88-166): per query
+// region, its kept key regions in ascending order, padding keys masked out,
+// softmax over the valid kept keys, rows with no valid kept key -> 0.
+//
+// Why this shape. A kept block is 64 query x 64 key rows. With the query
+// region on M, every tcgen05.mma is an M = 64 tile, which costs the cycles of
+// an M = 128 one (attn_lh.cu: 512 tensor cycles per block), and both K and V
+// pass through shared memory twice (the bulk-copy write and the MMA's operand
+// read: 64 KB of shared-memory traffic per block, ~all of the SM's 128 B/clk
+// at that rate). Here a step takes TWO kept key regions of one query region and
+// puts the 128 keys on M, with K and V^T as the MMA's A operand in TMEM:
+//
+//     GEMM1  S^T[128 keys x 64 q]  = K_pair . Q^T      A = K pair (TMEM), B = Q tile (smem, K-major)
+//     GEMM2  O^T[128 d   x 64 q]  += V_pair^T . P^T    A = V^T pair (TMEM), B = P^T (smem, MN-major)
+//
+// K and V^T go L2 -> registers (LDG.128) -> TMEM (tcgen05.st), so shared
+// memory carries only Q^T reads and the 16 KB P^T tile per step
+// (tools/probes/step_tmem.cu: 468 vs ~615 cycles per block for the lane-half
+// kernel's pipeline). The pooling pass writes K and V^T in the register-friendly
+// tile layouts (kt_off / vt_off below); Q rows are read in original order and
+// output rows are written back to it (padding.py:139-157 fused).
+//
+// Softmax per query COLUMN with a fixed offset per (query, item): m[q] =
+// |q| max|k| scale log2(e) - 64 (Cauchy-Schwarz bounds every score, so no
+// exponent exceeds 2^64 and O^T is never rescaled). A thread owns one key (TMEM
+// lane) and 32 query columns; padding keys are a per-thread predicate. Row sums
+// l[q] are reduced across each warp's 32 keys every step (butterfly) and across
+// warps at the item end. A query whose sum ends below 2^-80 while it had valid
+// keys (its true max more than ~80 binades under the bound) is redone by the
+// portable kernel, so results never depend on the bound being tight.
+//
+// Roles (28 warps, 896 threads):
+//   warp 0      scheduler: claims items (heaviest first), stages kept lists,
+//               emits the step ring (j0, j1, head, flags, region); zero-fills
+//               items without kept regions
+//   warp 1      GEMM1 issuer (and TMEM owner)      warp 2   GEMM2 issuer
+//   warp 3      Q loader: the item's Q tile into smem + the offsets m[q]
+//   warps 4-11  K loaders, two groups of 4 (group = step parity); lane = key row
+//   warps 12-19 V^T loaders, likewise; lane = feature row
+//   warps 20-27 softmax, two warpgroups: query columns [0,32) / [32,64);
+//               each also writes its half of the item's output rows
+// TMEM: K pair [0,128) and V^T pair [128,256) (two buffers of 64 columns each),
+// S^T [256,384) (two), O^T [384,512) (two: item parity).
+#include "attn_k4.cuh"
+#include "common.cuh"
+#include "kernels.h"
+
+// registers per thread of the control / loader / softmax warpgroups after
+// setmaxnreg (4 x CTL + 16 x LD + 8 x SM warps must fit the launch's 64512)
+#ifndef TK_REG_CTL
+#define TK_REG_CTL 56
+#endif
+#ifndef TK_REG_LD
+#define TK_REG_LD 80
+#endif
+#ifndef TK_REG_SM
+#define TK_REG_SM 56
+#endif
+static_assert(32 * (4 * TK_REG_CTL + 16 * TK_REG_LD + 8 * TK_REG_SM) <= 64512, "register budget");
+
+#ifndef TK_POLY
+#define TK_POLY 1  // every fourth exponential pair on the FMA pipe (exp2_poly2) instead of MUFU
+#endif
+
+namespace da {
+namespace tkk {
+
+using k4::D;
+using k4::fetch_item;
+using k4::Item;
+using k4::key_mask;
+using k4::key_row_valid;
+using k4::LISTCAP;
+using k4::P;
+using k4::Params;
+using k4::RAGW;
+using k4::TILE;
+using k4::token_row;
+
+constexpr int INFO = 16;  // step ring
+constexpr int W_SCHED = 0, W_G1 = 1, W_G2 = 2, W_Q = 3, W_KLD = 4, W_VLD = 12, W_SM = 20;
+constexpr int NWARPS = 28;
+constexpr int THREADS = 32 * NWARPS;
+constexpr int INFO_CONSUMERS = 27;  // every warp but the scheduler reads (and releases) every step entry
+
+constexpr uint32_t COL_K = 0, COL_V = 128, COL_S = 256, COL_O = 384;
+
+constexpr int SMEM_Q = 0;        // 2 x 16 KB Q tiles: [feature half][64 rows x 128 B], 128-byte swizzle
+constexpr int SMEM_P = 32768;    // 2 x 16 KB P^T tiles: [8-key group][8 keys x 128 B], 128-byte swizzle
+constexpr int SMEM_O = 65536;    // 16 KB output staging [64 q][128 d] bf16
+constexpr int SMEM_END = 81920;
+
+// step entry flags (int4.z low byte; head in the bits above)
+constexpr int F_J1 = 1, F_RAG0 = 2, F_RAG1 = 4;
+// int4.w: bit 0 last step of the item, bit 1 first step, bit 2 end of stream; region << 3
+constexpr int W_LAST = 1, W_FIRST = 2, W_END = 4;
+
+struct __align__(8) Bars {
+  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
+  uint64_t q_full[2], q_empty[2], o_full[2], o_empty[2];
+  uint64_t info_full[INFO], info_empty[INFO];
+};
+struct SmemAux {
+  Bars bars;
+  int4 info[INFO];
+  uint32_t tmem_base;
+  alignas(16) float m[2][64];  // [item parity][query] fixed offsets (log2 units), read as float4
+  float lsum[2][4][32];   // [softmax warpgroup][warp slice][column] per-warp row sums
+  float linv[2][32];      // [softmax warpgroup][column] 1 / l, or 0
+  uint32_t ragged[RAGW];
+  int list[LISTCAP];
+};
+constexpr int SMEM_ALLOC = SMEM_END + (int)sizeof(SmemAux);
+static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
+
+// byte offsets inside the register-friendly global tiles (pooling pass):
+// K: chunk c (features 8c..8c+7) of key row r; a warp's 32 rows of one chunk
+// are 512 contiguous bytes. V^T: key chunk c (keys 8c..8c+7) of feature row d.
+DA_DEV uint32_t kt_off(int r, int c) { return (uint32_t)(c * 1024 + r * 16); }
+DA_DEV uint32_t vt_off(int d, int c) { return (uint32_t)(c * 2048 + d * 16); }
+
+template <int N>
+DA_DEV void set_maxnreg() {
+  if constexpr (N > 72) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N) : "memory");
+  else if constexpr (N < 72) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N) : "memory");
+}
+
+DA_DEV void ldg16x4(const uint8_t* src, uint32_t* r) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
+  r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+}
+
+__global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  SmemAux& aux = *reinterpret_cast<SmemAux*>(smem + SMEM_END);
+  Bars& B = aux.bars;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long items = (long long)p.heads * p.geo.g;
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&B.k_full[b], 128);
+      mbar_init(&B.k_empty[b], 1);
+      mbar_init(&B.v_full[b], 128);
+      mbar_init(&B.v_empty[b], 1);
+      mbar_init(&B.s_full[b], 1);
+      mbar_init(&B.s_free[b], 256);
+      mbar_init(&B.p_full[b], 256);
+      mbar_init(&B.p_free[b], 1);
+      mbar_init(&B.q_full[b], 32);
+      mbar_init(&B.q_empty[b], 1 + 256);  // GEMM1's last MMA of the item + the softmax's last read of m
+      mbar_init(&B.o_full[b], 1);
+      mbar_init(&B.o_empty[b], 256);
+    }
+    for (int s = 0; s < INFO; ++s) {
+      mbar_init(&B.info_full[s], 1);
+      mbar_init(&B.info_empty[s], INFO_CONSUMERS);
+    }
+    fence_barrier_init();
+  }
+  if (p.key_valid == nullptr && p.geo.g <= 32 * RAGW) {
+    for (int wd = threadIdx.x; wd < (p.geo.g + 31) / 32; wd += blockDim.x) {
+      uint32_t bits = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int j = wd * 32 + b;
+        if (j < p.geo.g && key_mask(p, j) != ~0ull) bits |= 1u << b;
+      }
+      aux.ragged[wd] = bits;
+    }
+  }
+  if (warp == W_G1) tmem_alloc<512>(&aux.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = aux.tmem_base;
+  // registers are split across the roles (launch: 72 per thread, 64512 in all):
+  // each role branch below starts with its set_maxnreg
+
+  // every consumer walks the step ring in order and releases each entry
+  int ri = 0;
+  uint32_t rph = 0;
+  auto next_step = [&]() {
+    mbar_wait_warp(&B.info_full[ri], rph);
+    const int4 e = aux.info[ri];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&B.info_empty[ri]);
+    if (++ri == INFO) { ri = 0; rph ^= 1u; }
+    return e;
+  };
+
+  if (warp == W_SCHED) {
+    // ================================ scheduler ================================
+    set_maxnreg<TK_REG_CTL>();
+    const bool bitmap = p.key_valid == nullptr && p.geo.g <= 32 * RAGW;
+    int kq = 0;
+    long long next_claim = 0;
+    if (lane == 0) next_claim = atomicAdd(p.work, 1);
+    auto publish = [&](int4 e) {  // lane 0
+      const int ii = kq % INFO;
+      if (kq >= INFO) mbar_wait(&B.info_empty[ii], (uint32_t)(((kq / INFO) - 1) & 1));
+      aux.info[ii] = e;
+      mbar_arrive(&B.info_full[ii]);
+      ++kq;
+    };
+    auto ragged = [&](int j) {
+      return bitmap ? ((aux.ragged[j >> 5] >> (j & 31)) & 1u) != 0 : key_mask(p, j) != ~0ull;
+    };
+    for (;;) {
+      Item itm;
+      bool live = false;
+      for (;;) {
+        long long c = 0;
+        if (lane == 0) {
+          c = next_claim;
+          next_claim = atomicAdd(p.work, 1);
+        }
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (!fetch_item(p, c, items, itm)) break;
+        if (itm.n > 0) { live = true; break; }
+        // no kept key region: the region's output rows are zero (sparse.py:137-138)
+        for (int e = lane; e < P * (D / 8); e += 32) {
+          const long long row = token_row(p, itm.i, e / (D / 8));
+          if (row >= 0) reinterpret_cast<uint4*>(p.out + itm.h * p.oh + row * p.orow)[e % (D / 8)] = make_uint4(0, 0, 0, 0);
+        }
+      }
+      if (!live) break;
+      const bool staged = itm.n <= LISTCAP;
+      __syncwarp();
+      if (staged)
+        for (int e = lane; e < itm.n; e += 32) aux.list[e] = __ldg(itm.list + e);
+      __syncwarp();
+      if (lane == 0) {
+        const int n = (itm.n + 1) / 2;
+        for (int t = 0; t < n; ++t) {
+          const int j0 = staged ? aux.list[2 * t] : __ldg(itm.list + 2 * t);
+          const int j1 = 2 * t + 1 < itm.n ? (staged ? aux.list[2 * t + 1] : __ldg(itm.list + 2 * t + 1)) : -1;
+          int fl = ragged(j0) ? F_RAG0 : 0;
+          if (j1 >= 0) fl |= F_J1 | (ragged(j1) ? F_RAG1 : 0);
+          publish(make_int4(j0, j1, fl | (itm.h << 8),
+                            (itm.i << 3) | (t == n - 1 ? W_LAST : 0) | (t == 0 ? W_FIRST : 0)));
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) publish(make_int4(-1, -1, 0, W_END));
+  } else if (warp == W_G1 || warp == W_G2) {
+    // ============================== MMA issuers ===============================
+    set_maxnreg<TK_REG_CTL>();
+    const bool g1 = warp == W_G1;
+    constexpr uint32_t I1 = umma_idesc_bf16(128, 64, 0, 0);  // A = K (TMEM), B = Q tile, K-major
+    constexpr uint32_t I2 = umma_idesc_bf16(128, 64, 0, 1);  // A = V^T (TMEM), B = P^T, MN-major
+    const uint64_t dQ = umma_desc_sw128(0, 16, 1024) + (smem_u32(smem + SMEM_Q) >> 4);
+    const uint64_t dP = umma_desc_sw128(0, 16, 1024) + (smem_u32(smem + SMEM_P) >> 4);
+    int gs = 0, seq = 0;
+    for (;;) {
+      const int4 e = next_step();
+      if (e.w & W_END) break;
+      const int b = gs & 1;
+      const uint32_t par = (uint32_t)((gs >> 1) & 1);
+      const int xb = seq & 1;  // Q tile (GEMM1) / O^T buffer (GEMM2) of the item
+      const bool first = e.w & W_FIRST, last = e.w & W_LAST;
+      if (g1) {
+        if (first) mbar_wait_spin(&B.q_full[xb], (uint32_t)((seq >> 1) & 1));
+        mbar_wait_spin(&B.k_full[b], par);
+        if (gs >= 2) mbar_wait_spin(&B.s_free[b], par ^ 1u);
+        tc_fence_after();
+        if (elect_one_sync()) {
+          const uint64_t bq = dQ + (uint64_t)(xb * (16384 >> 4));
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ts(tmem + COL_S + 64 * b, tmem + COL_K + 64 * b + 8 * kk,
+                         bq + (uint64_t)((kk >> 2) * (8192 >> 4) + (kk & 3) * 2), I1, kk > 0 ? 1u : 0u);
+          umma_commit(&B.k_empty[b]);
+          umma_commit(&B.s_full[b]);
+          if (last) umma_commit(&B.q_empty[xb]);
+        }
+        __syncwarp();
+      } else {
+        if (first && seq >= 2) mbar_wait(&B.o_empty[xb], (uint32_t)(((seq >> 1) - 1) & 1));
+        mbar_wait_spin(&B.v_full[b], par);
+        mbar_wait_spin(&B.p_full[b], par);
+        tc_fence_after();
+        if (elect_one_sync()) {
+          const int nk = (e.z & F_J1) ? 8 : 4;  // an odd last region: keys 64..127 absent
+          for (int kk = 0; kk < nk; ++kk)
+            umma_bf16_ts(tmem + COL_O + 64 * xb, tmem + COL_V + 64 * b + 8 * kk,
+                         dP + (uint64_t)(b * (16384 >> 4) + kk * (2048 >> 4)), I2, (first && kk == 0) ? 0u : 1u);
+          umma_commit(&B.v_empty[b]);
+          umma_commit(&B.p_free[b]);
+          if (last) umma_commit(&B.o_full[xb]);
+        }
+        __syncwarp();
+      }
+      if (last) ++seq;
+      ++gs;
+    }
+  } else if (warp == W_Q) {
+    // ====================== Q tiles and fixed offsets ======================
+    set_maxnreg<TK_REG_CTL>();
+    // lane handles query rows lane and lane + 32 of the item
+    int seq = 0, cur_head = -1;
+    float kmax = 0.f;
+    const float sl2 = p.scale_log2;
+    for (;;) {
+      const int4 e = next_step();
+      if (e.w & W_END) break;
+      if (!(e.w & W_FIRST)) continue;
+      const int h = e.z >> 8, region = e.w >> 3;
+      const int qb = seq & 1;
+      if (h != cur_head) {
+        cur_head = h;
+        const float* kp = p.kpart + (long long)h * p.kblk;
+        float mx = 0.f;
+        for (int k = 0; k < p.kblk; ++k) mx = fmaxf(mx, __ldg(kp + k));
+        kmax = mx;
+      }
+      if (seq >= 2) mbar_wait(&B.q_empty[qb], (uint32_t)(((seq >> 1) - 1) & 1));
+      uint8_t* qt = smem + SMEM_Q + qb * 16384;
+#pragma unroll 1
+      for (int rr = 0; rr < 2; ++rr) {
+        const int r = lane + 32 * rr;
+        const long long row = token_row(p, region, r);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.q + h * p.qh + (row >= 0 ? row : 0) * p.qr);
+        float s2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          uint32_t w[4] = {0u, 0u, 0u, 0u};
+          if (row >= 0) ldg16x4(src + 16 * c, w);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+            s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+          }
+          // [half c >> 3][row r][chunk c & 7 swizzled]
+          sts128(smem_u32(qt + (c >> 3) * 8192 + r * 128 + ((((c & 7) ^ r) & 7) << 4)), w[0], w[1], w[2], w[3]);
+        }
+        aux.m[qb][r] = sqrtf(s2) * kmax * sl2 * 1.0001f - 64.f;
+      }
+      fence_proxy_async_smem();  // Q tile: generic-proxy stores -> the MMA's async-proxy reads
+      mbar_arrive(&B.q_full[qb]);
+      ++seq;
+    }
+  } else if (warp >= W_KLD && warp < W_SM) {
+    // ============================ K / V^T loaders ============================
+    set_maxnreg<TK_REG_LD>();
+    const bool is_v = warp >= W_VLD;
+    const int lw = warp - (is_v ? W_VLD : W_KLD);
+    const int grp = lw >> 2, slice = lw & 3;
+    const int L = 32 * slice + lane;  // TMEM lane: key of the pair (K) or feature (V^T)
+    const uint32_t tl = tmem + ((uint32_t)(32 * slice) << 16) + (is_v ? COL_V : COL_K);
+    uint64_t* full = is_v ? B.v_full : B.k_full;
+    uint64_t* empty = is_v ? B.v_empty : B.k_empty;
+    const uint8_t* tiles = is_v ? p.vt : p.kt;
+    const long long hstride = (long long)p.geo.g * TILE;
+    int gs = 0;
+    for (;;) {
+      const int4 e = next_step();
+      if (e.w & W_END) break;
+      if ((gs & 1) != grp) { ++gs; continue; }
+      const uint8_t* hb = tiles + (long long)(e.z >> 8) * hstride;
+      uint32_t r[64];
+      if (!is_v) {
+        const int j = (L >> 6) ? e.y : e.x;
+        if (j >= 0) {
+          const uint8_t* src = hb + (long long)j * TILE + kt_off(L & 63, 0);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) ldg16x4(src + c * 1024, r + 4 * c);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) r[c] = 0u;
+        }
+      } else {
+        const uint8_t* s0 = hb + (long long)e.x * TILE + vt_off(L, 0);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) ldg16x4(s0 + c * 2048, r + 4 * c);
+        if (e.y >= 0) {
+          const uint8_t* s1 = hb + (long long)e.y * TILE + vt_off(L, 0);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) ldg16x4(s1 + c * 2048, r + 32 + 4 * c);
+        } else {
+#pragma unroll
+          for (int c = 32; c < 64; ++c) r[c] = 0u;
+        }
+      }
+      const int b = gs & 1;
+      if (gs >= 2) mbar_wait_spin(&empty[b], (uint32_t)(((gs >> 1) - 1) & 1));
+      tc_fence_after();
+      tmem_st32(tl + 64 * b, *reinterpret_cast<float(*)[32]>(&r[0]));
+      tmem_st32(tl + 64 * b + 32, *reinterpret_cast<float(*)[32]>(&r[32]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&full[b]);
+      ++gs;
+    }
+  } else {
+    // ========================= softmax + epilogue =========================
+    set_maxnreg<TK_REG_SM>();
+    const int wg = (warp - W_SM) >> 2, slice = (warp - W_SM) & 3;
+    const int L = 32 * slice + lane;  // TMEM lane: key of the pair (softmax) / feature (epilogue)
+    const uint32_t tl = tmem + ((uint32_t)(32 * slice) << 16);
+    const float sl2 = p.scale_log2;
+    const int bar_id = 1 + wg;  // named barrier of this warpgroup
+    int gs = 0, seq = 0;
+    float lpart = 0.f;
+    bool anyv = false;
+    for (;;) {
+      const int4 e = next_step();
+      if (e.w & W_END) break;
+      const int b = gs & 1;
+      const uint32_t par = (uint32_t)((gs >> 1) & 1);
+      const int qb = seq & 1;
+      const bool first = e.w & W_FIRST, last = e.w & W_LAST;
+      if (first) {
+        mbar_wait_spin(&B.q_full[qb], (uint32_t)((seq >> 1) & 1));  // the item's offsets m[q]
+        lpart = 0.f;
+        anyv = false;
+      }
+      // this thread's key: row L & 63 of region j0 (L < 64) or j1
+      const int sel = L >> 6;
+      const int j = sel ? e.y : e.x;
+      bool kv = j >= 0;
+      if (kv && (e.z & (sel ? F_RAG1 : F_RAG0))) kv = key_row_valid(p, j, L & 63);
+      anyv |= kv;
+      mbar_wait_spin(&B.s_full[b], par);
+      tc_fence_after();
+      float x[32];
+      tmem_ld32(tl + COL_S + 64 * b + 32 * wg, x);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&B.s_free[b]);
+      uint32_t pk[16];
+      {
+        const float* mq = &aux.m[qb][32 * wg];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 m4 = *reinterpret_cast<const float4*>(mq + i);
+          float2 e0 = ffma2(make_float2(x[i], x[i + 1]), make_float2(sl2, sl2), make_float2(-m4.x, -m4.y));
+          float2 e1 = ffma2(make_float2(x[i + 2], x[i + 3]), make_float2(sl2, sl2), make_float2(-m4.z, -m4.w));
+          float2 p0, p1;
+          p0 = make_float2(fast_exp2(e0.x), fast_exp2(e0.y));
+          if (TK_POLY && (i & 4)) p1 = exp2_poly2(e1);
+          else p1 = make_float2(fast_exp2(e1.x), fast_exp2(e1.y));
+          if (!kv) p0 = p1 = make_float2(0.f, 0.f);
+          x[i] = p0.x; x[i + 1] = p0.y; x[i + 2] = p1.x; x[i + 3] = p1.y;
+          pk[i / 2] = pack_bf16(p0.x, p0.y);
+          pk[i / 2 + 1] = pack_bf16(p1.x, p1.y);
+        }
+      }
+      // row sums: butterfly over the warp's 32 keys; lane c ends with column c
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+          const float send = up ? x[i] : x[i + o];
+          const float keep = up ? x[i + o] : x[i];
+          x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      lpart += x[0];
+      if (gs >= 2) {
+        mbar_wait_spin(&B.p_free[b], par ^ 1u);
+        tc_fence_after();
+      }
+      {
+        const uint32_t base = smem_u32(smem + SMEM_P + b * 16384) + (uint32_t)((L >> 3) * 1024 + (L & 7) * 128);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c = 4 * wg + i;
+          sts128(base + (uint32_t)(((c ^ L) & 7) << 4), pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&B.p_full[b]);
+      if (last) {
+        mbar_arrive(&B.q_empty[qb]);  // done with m[qb]
+        // ---------------- item epilogue (this warpgroup's 32 query rows) ----------------
+        const int h = e.z >> 8, region = e.w >> 3;
+        aux.lsum[wg][slice][lane] = lpart;
+        const bool had = bar_red_or(bar_id, 128, anyv);
+        if (slice == 0) {
+          const float l = aux.lsum[wg][0][lane] + aux.lsum[wg][1][lane] + aux.lsum[wg][2][lane] + aux.lsum[wg][3][lane];
+          aux.linv[wg][lane] = l > 0.f ? 1.f / l : 0.f;
+          const long long row = token_row(p, region, 32 * wg + lane);
+          const bool bad = had && !(l >= 0x1p-80f) && row >= 0;
+          const unsigned bal = __ballot_sync(0xffffffffu, bad);
+          if (bal != 0u && lane == 0) {  // duplicates (both warpgroups) are harmless
+            const int slot = atomicAdd(p.fb_count, 1);
+            p.fb_items[slot] = h * p.geo.g + region;
+          }
+        }
+        mbar_wait(&B.o_full[qb], (uint32_t)((seq >> 1) & 1));
+        tc_fence_after();
+        float o[32];
+        tmem_ld32(tl + COL_O + 64 * qb + 32 * wg, o);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&B.o_empty[qb]);
+        bar_sync(bar_id, 128);  // linv written
+        {
+          // lane L = feature d: column i of O^T is query 32 wg + i
+          uint16_t* st = reinterpret_cast<uint16_t*>(smem + SMEM_O);
+          const float* li = aux.linv[wg];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const __nv_bfloat16 v = __float2bfloat16_rn(o[i] * li[i]);
+            st[(32 * wg + i) * D + L] = *reinterpret_cast<const uint16_t*>(&v);
+          }
+        }
+        bar_sync(bar_id, 128);  // staging complete
+        {
+          const int t = threadIdx.x - 32 * (W_SM + 4 * wg);  // 0..127
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int id = t + 128 * k;          // 512 chunks: 32 rows x 16 chunks of 16 B
+            const int q = 32 * wg + (id >> 4), c = id & 15;
+            const long long row = token_row(p, region, q);
+            if (row >= 0) {
+              const uint4 v = *reinterpret_cast<const uint4*>(smem + SMEM_O + q * 256 + c * 16);
+              reinterpret_cast<uint4*>(p.out + h * p.oh + row * p.orow)[c] = v;
+            }
+          }
+        }
+        ++seq;
+      }
+      ++gs;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == W_G1) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+}  // namespace tkk
+
+cudaError_t launch_tk_kernel(const k4::Params& p, int grid, cudaStream_t st) {
+  cudaError_t e = ensure_smem_optin((const void*)tkk::sparse_attn_tk_kernel, tkk::SMEM_ALLOC);
+  if (e != cudaSuccess) return e;
+  tkk::sparse_attn_tk_kernel<<<grid, tkk::THREADS, tkk::SMEM_ALLOC, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace da

@@ -28,6 +28,9 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
 // K / V tile buffers inside the attention workspace ([heads][g][16 KB] each),
 // in the GROUPED layout of kv_tile_offset_grouped (the K4 shared-memory image)
 uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which);
+// The library's K4 for d = 128, 8x8 pools: the transposed TMEM-fed kernel
+// (attn_tk.cu; its own tile layouts) or the lane-half kernel (attn_lh.cu).
+bool attn_uses_tk();
 int pool_norm_blocks(int d, const Geo& g);
 // hist0 (optional): per-head 2048-bin histogram of the top 11 key bits, filled in the epilogue
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,
@@ -67,6 +70,12 @@ bool tc_supported(const da_attn_args& a, const Geo& g);
 // tiles_ready: the pooling pass already wrote the K/V region tiles.
 cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const float* kpart = nullptr,
                            int kblk = 0, bool tiles_ready = false);
+
+namespace k4 {
+struct Params;
+}
+// K4 transposed TMEM-fed kernel (attn_tk.cu), launched by launch_tc_attn
+cudaError_t launch_tk_kernel(const k4::Params& p, int grid, cudaStream_t st);
 
 // Per-device facts cached once per device (the library keeps no other state):
 // the SM count, and the dynamic shared-memory opt-in of a kernel.

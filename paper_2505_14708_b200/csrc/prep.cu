@@ -78,6 +78,7 @@ struct PoolSrc {
   long long hs[3], rs[3];
   double* out[2];
   uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
+  int tile_tk;                // tile layouts: 1 = the TMEM-fed K4's (K row chunks, V^T), 0 = GROUPED smem images
   unsigned long long* pnorm;  // optional [heads][2]: largest pooled row norm^2 of Q (0) and K (1), as double bits
 };
 
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
   // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
   uint8_t* tdst = (z >= 1 && src.tile[z - 1] != nullptr && live)
                       ? src.tile[z - 1] + ((long long)h * g.g + i) * 16384 : nullptr;
+  uint4 vprev[4];  // V^T tiles: the previous 4-row batch
   // fp64 sums of bf16 values are exact, in any order
   double acc[8];
 #pragma unroll
@@ -317,12 +319,39 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
       q[t] = ok[t] ? __ldg(base + row * rs8) : make_uint4(0, 0, 0, 0);
     }
     if (tdst != nullptr) {
+      if (!src.tile_tk) {
 #pragma unroll
-      for (int t = 0; t < RB; ++t) {
-        const int r = r0 + t;
-        if (r < g.p) {
-          const uint32_t off = kv_tile_offset_grouped(r, k >> 3, k & 7);
-          *reinterpret_cast<uint4*>(tdst + off) = q[t];
+        for (int t = 0; t < RB; ++t) {
+          const int r = r0 + t;
+          if (r < g.p) *reinterpret_cast<uint4*>(tdst + kv_tile_offset_grouped(r, k >> 3, k & 7)) = q[t];
+        }
+      } else if (z == 1) {
+        // K: chunk k (features 8k..8k+7) of key row r at k * 1024 + r * 16
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+          const int r = r0 + t;
+          if (r < g.p) *reinterpret_cast<uint4*>(tdst + k * 1024 + r * 16) = q[t];
+        }
+      } else {
+        // V^T: this thread holds features 8k..8k+7 of rows r0 .. r0 + RB - 1;
+        // two batches make an 8 x 8 block, transposed in registers into key
+        // chunk r0 / 8 (keys r0 - 4 .. r0 + 3) of feature rows 8k .. 8k + 7
+        static_assert(RB == 4, "V^T tiles pair two 4-row batches");
+        if ((r0 & 4) == 0) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) vprev[t] = q[t];
+        } else {
+          const uint4 rows[8] = {vprev[0], vprev[1], vprev[2], vprev[3], q[0], q[1], q[2], q[3]};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t a = (&rows[2 * i].x)[e >> 1], b = (&rows[2 * i + 1].x)[e >> 1];
+              w[i] = __byte_perm(a, b, (e & 1) ? 0x7632 : 0x5410);
+            }
+            *reinterpret_cast<uint4*>(tdst + ((r0 - 4) >> 3) * 2048 + (8 * k + e) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
         }
       }
     }
@@ -406,6 +435,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
     src.hs[2] = tiles ? hs2 : hs0; src.rs[2] = tiles ? rs2 : rs0;
     src.tile[0] = tiles ? ktile : nullptr;
     src.tile[1] = tiles ? vtile : nullptr;
+    src.tile_tk = attn_uses_tk() ? 1 : 0;
     src.pnorm = pnorm;
     dim3 grid(pool_norm_blocks(d, g), heads, x1 ? (tiles ? 3 : 2) : 1);
     float* kp = x1 ? kpart : nullptr;
