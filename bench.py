@@ -16,12 +16,14 @@ The line also carries dense attention at the same shape (cuDNN / flash SDPA,
 bf16, the north-star comparator) as ``dense_sdpa_ms`` and
 ``speedup_vs_dense_sdpa`` (skip with --no-dense).
 
---impl reference times the CPU oracle port of the reference algorithm
-(oracle/: the reference itself is Python/numpy and cannot travel to the GPU
-box) on the host cores: whole heads of the same call, float32 inputs (the
-reference's default precision) holding the bf16-rounded values the GPU gets,
-heads one after another as the reference runs them; ms per call = the mean
-per-head time x heads (labelled extrapolated).
+--impl reference times the UNMODIFIED reference (``draftattn`` installed into
+baseline/_ref with ``pip install --no-index --no-deps --target baseline/_ref``,
+git-ignored, travels to the GPU box with the snapshot) through its public
+``padded_sparse_attention`` on the host cores: whole heads of the same call,
+float32 inputs (the reference's default precision) holding the bf16-rounded
+values the GPU gets, heads one after another as the reference runs them; ms per
+call = the per-head time x heads (labelled extrapolated). Without baseline/_ref
+it times the oracle port of the same algorithm (oracle/, kind "port").
 """
 
 from __future__ import annotations
@@ -119,16 +121,35 @@ class ClockSampler:
 # CPU reference arm / baseline (oracle port of the reference algorithm)
 # --------------------------------------------------------------------------
 
-def cpu_reference_sample(cfg, seed=0, head_ids=(0, 1)):
-    """Time the reference algorithm (oracle port, float32 numpy) on whole heads
-    of the call: padded_sparse_attention per head (padding.py:95-165), heads
-    sequential. Returns (ms per call extrapolated to every head, sample
-    description, BLAS threads)."""
-    import numpy as np
+def _reference_impl():
+    """padded_sparse_attention of the unmodified reference from baseline/_ref,
+    or None (then the oracle port stands in)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "draftattn" / "padding.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from draftattn.padding import padded_sparse_attention
+    except Exception:  # noqa: BLE001
+        return None
+    return padded_sparse_attention
+
+
+def cpu_reference_sample(cfg, seed=0, head_ids=(0, 1), use_reference=True):
+    """Time the reference path on whole heads of the call:
+    padded_sparse_attention per head (padding.py:95-165), heads sequential,
+    float32 inputs holding the bf16-rounded values. The unmodified reference
+    (baseline/_ref) when installed, else the oracle port. Returns (ms per call
+    extrapolated to every head, sample description, BLAS threads, kind)."""
     import torch
     from oracle import draftattn_oracle as O
 
     f, h, w, ph, pw, heads, d, sp = cfg
+    fn = _reference_impl() if use_reference else None
+    kind = "reference" if fn is not None else "port"
+    if fn is None:
+        fn = O.padded_sparse_attention
     grid = O.Grid(f, h, w, ph, pw)
     q, k, v = O.gen_real_inputs(grid, d, seed, heads, head_ids=list(head_ids))
     rnd = lambda x: torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()  # noqa: E731
@@ -136,14 +157,16 @@ def cpu_reference_sample(cfg, seed=0, head_ids=(0, 1)):
     times = []
     for slot in range(len(head_ids)):
         t0 = time.perf_counter()
-        O.padded_sparse_attention(q[slot], k[slot], v[slot], f, h, w, ph, pw, sp)
+        fn(q[slot], k[slot], v[slot], f, h, w, ph, pw, sp)
         times.append(time.perf_counter() - t0)
     per_head = statistics.mean(times)
     threads = _blas_threads()
-    sample = (f"{len(head_ids)} of {heads} heads in full ({', '.join(f'{t:.2f}' for t in times)} s), float32 numpy "
-              f"(oracle port), BLAS threads={threads}, {os.cpu_count()} host cores; ms/call = mean per head x "
+    what = ("unmodified reference draftattn.padded_sparse_attention (baseline/_ref)" if kind == "reference"
+            else "oracle port of the reference algorithm")
+    sample = (f"{len(head_ids)} of {heads} heads in full ({', '.join(f'{t:.2f}' for t in times)} s), float32 numpy, "
+              f"{what}, BLAS threads={threads}, {os.cpu_count()} host cores; ms/call = mean per head x "
               f"{heads} heads (extrapolated)")
-    return per_head * heads * 1e3, sample, threads
+    return per_head * heads * 1e3, sample, threads, kind
 
 
 def _blas_threads():
@@ -159,15 +182,17 @@ def run_reference(args, cfg, name):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals, sample, threads = [], "", 1
+    vals, threads, kind = [], 1, "port"
     for _ in range(args.warmup_ref):
         cpu_reference_sample(CONFIGS["tiny"], head_ids=(0,))
     heads = cfg[5]
     for s in range(args.steps):  # one whole head per step, a different head each step
-        ms, sample, threads = cpu_reference_sample(cfg, head_ids=(s % heads,))
+        ms, _, threads, kind = cpu_reference_sample(cfg, head_ids=(s % heads,))
         vals.append(ms)
     ms = statistics.median(vals)
-    sample = (f"one whole head per step (heads 0..{args.steps - 1}), float32 numpy (oracle port), "
+    what = ("unmodified reference draftattn.padded_sparse_attention (baseline/_ref)" if kind == "reference"
+            else "oracle port of the reference algorithm")
+    sample = (f"one whole head per step (heads 0..{args.steps - 1}), float32 numpy, {what}, "
               f"BLAS threads={threads}, {os.cpu_count()} host cores; ms/call = per-head median x {heads} heads "
               f"(extrapolated)")
     line = {
@@ -175,7 +200,7 @@ def run_reference(args, cfg, name):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (synth.py gaussian, seeded)",
         "config": _config_dict(name, cfg, args.gpus),
-        "cpu_baseline": {"value": ms, "unit": "ms/call", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": ms, "unit": "ms/call", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": ms, "unit": "ms/call", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         # each step times ONE head of the call; value = that x heads
         "extrapolated": {"timed_s_per_step": [v / heads / 1e3 for v in vals], "factor": heads,
@@ -303,8 +328,10 @@ def run_ours(args, cfg, name):
         e2e = _e2e(da, plan, cfg, dev, args)
         dense_ms = None if args.no_dense else _dense_sdpa_ms(heads, n, d, dev)
         if not args.no_cpu:
-            cms, sample, threads = cpu_reference_sample(cfg)
-            cpu_base = {"value": cms, "unit": "ms/call", "cores": threads, "kind": "port", "sample": sample,
+            # one whole head through the unmodified reference (~45 s), else two through the port
+            ids = (0,) if _reference_impl() is not None else (0, 1)
+            cms, sample, threads, kind = cpu_reference_sample(cfg, head_ids=ids)
+            cpu_base = {"value": cms, "unit": "ms/call", "cores": threads, "kind": kind, "sample": sample,
                         "extrapolated": True}
     if rank == 0:
         launches = _lib.lib().da_pipeline_launches(0, 0) * args.steps

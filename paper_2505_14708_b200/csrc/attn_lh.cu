@@ -822,12 +822,13 @@ uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which) {
 
 size_t attn_workspace_size(int heads, const Geo& g) { return ws_tiles(heads, g) + 2 * (size_t)heads * g.g * lhk::TILE; }
 
-// DA_K4_LH builds the lane-half kernel instead (A/B experiments)
+// The lane-half kernel is the shipped K4; DA_K4_TK builds the transposed
+// TMEM-fed kernel instead (A/B experiments, tools/probes/k4_variants.py)
 bool attn_uses_tk() {
-#ifdef DA_K4_LH
-  return false;
-#else
+#ifdef DA_K4_TK
   return true;
+#else
+  return false;
 #endif
 }
 
