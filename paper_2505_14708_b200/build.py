@@ -13,7 +13,10 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libdraftattn_b200.so"
-SOURCES = ["api.cu", "prep.cu", "select.cu", "attn_portable.cu", "attn_lh.cu", "attn_tk.cu"]
+SOURCES = ["api.cu", "prep.cu", "select.cu", "attn_portable.cu", "attn_lh.cu"]
+# the transposed TMEM-fed K4 (attn_tk.cu) is an experiment: only builds with
+# -DDA_K4_TK link it (tools/probes/k4_variants.py); the shipped library does not
+EXPERIMENT_SOURCES = {"-DDA_K4_TK": ["attn_tk.cu"]}
 HEADERS = ["common.cuh", "kernels.h", "attn_k4.cuh"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
@@ -41,8 +44,12 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, f
     if out is None and not force and not _stale():
         return OUT
     extra = os.environ.get("DA_NVCC_FLAGS", "").split() + list(flags)  # experiments only
+    sources = list(SOURCES)
+    for flag, more in EXPERIMENT_SOURCES.items():
+        if flag in extra:
+            sources += more
     cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-o", str(target)] + extra + [str(CSRC / s) for s in SOURCES]
+           "-o", str(target)] + extra + [str(CSRC / s) for s in sources]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -916,9 +916,12 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   const int sms = device_sms();
   const long long items = (long long)a.heads * g.g;
   const int grid = (int)(items < sms ? items : sms);
+#ifdef DA_K4_TK
   if (attn_uses_tk()) {
     if ((e = launch_tk_kernel(p, grid, st)) != cudaSuccess) return e;
-  } else {
+  } else
+#endif
+  {
     if ((e = ensure_smem_optin((const void*)lhk::sparse_attn_lh_kernel, lhk::SMEM_ALLOC)) != cudaSuccess) return e;
     lhk::sparse_attn_lh_kernel<<<grid, lhk::THREADS, lhk::SMEM_ALLOC, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

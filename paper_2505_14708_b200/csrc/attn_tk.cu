@@ -31,34 +31,108 @@
 // keys (its true max more than ~80 binades under the bound) is redone by the
 // portable kernel, so results never depend on the bound being tight.
 //
-// Roles (28 warps, 896 threads):
+// Roles (4 + 4 TK_LDG + 8 warps):
 //   warp 0      scheduler: claims items (heaviest first), stages kept lists,
 //               emits the step ring (j0, j1, head, flags, region); zero-fills
 //               items without kept regions
 //   warp 1      GEMM1 issuer (and TMEM owner)      warp 2   GEMM2 issuer
 //   warp 3      Q loader: the item's Q tile into smem + the offsets m[q]
-//   warps 4-11  K loaders, two groups of 4 (group = step parity); lane = key row
-//   warps 12-19 V^T loaders, likewise; lane = feature row
-//   warps 20-27 softmax, two warpgroups: query columns [0,32) / [32,64);
+//   warps 4..    loaders: TK_LDG groups of 4 warps (one per TMEM lane quadrant)
+//               taking the jobs K(step 0), V^T(step 0), K(step 1), ... in
+//               turn; lane = key row (K) or feature row (V^T)
+//   last 8      softmax, two warpgroups: query columns [0,32) / [32,64);
 //               each also writes its half of the item's output rows
 // TMEM: K pair [0,128) and V^T pair [128,256) (two buffers of 64 columns each),
 // S^T [256,384) (two), O^T [384,512) (two: item parity).
+#include <type_traits>
+
 #include "attn_k4.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
 // registers per thread of the control / loader / softmax warpgroups after
 // setmaxnreg (4 x CTL + 16 x LD + 8 x SM warps must fit the launch's 64512)
+// loader groups: TK_LDG x 32 KB of K / V^T in flight
+#ifndef TK_LDG
+#define TK_LDG 2
+#endif
 #ifndef TK_REG_CTL
 #define TK_REG_CTL 56
 #endif
 #ifndef TK_REG_LD
-#define TK_REG_LD 80
+#define TK_REG_LD 88
 #endif
 #ifndef TK_REG_SM
-#define TK_REG_SM 56
+#define TK_REG_SM 120
 #endif
-static_assert(32 * (4 * TK_REG_CTL + 16 * TK_REG_LD + 8 * TK_REG_SM) <= 64512, "register budget");
+#ifndef TK_NOASSERT
+// the launch gives every thread floor(65536 / threads) registers, rounded down to 8
+static_assert(4 * TK_REG_CTL + 4 * TK_LDG * TK_REG_LD + 8 * TK_REG_SM <=
+                  (12 + 4 * TK_LDG) * ((65536 / (32 * (12 + 4 * TK_LDG))) & ~7),
+              "register budget");
+#endif
+
+#ifndef TK_SPIN
+#define TK_SPIN 0  // waits on the MMA <-> softmax critical path: 0 sleep (try_wait), 1 every lane spins (test_wait), 2 lane 0 spins
+#endif
+
+#if TK_SPIN == 1
+#define TK_WAIT mbar_wait_spin
+#elif TK_SPIN == 2
+#define TK_WAIT mbar_wait_warp
+#else
+#define TK_WAIT mbar_wait
+#endif
+
+// TK_PROF (probe builds, tools/probes/tk_prof.py): per-role cycle accounting of
+// the waits, lane 0 of one warp per role, summed per CTA into the
+// da_debug_trace buffer as [CTA][64] int64 (role r: slots 8 r .. 8 r + 7;
+// slot 63: CTA cycles)
+#ifdef TK_PROF
+#define TK_T0() const long long _t0 = clock64()
+#define TK_ACC(k) prof[k] += clock64() - _t0
+#define TK_TIME(k, stmt) \
+  {                      \
+    TK_T0();             \
+    stmt;                \
+    TK_ACC(k);           \
+  }
+#else
+#define TK_T0() \
+  do {          \
+  } while (0)
+#define TK_ACC(k) \
+  do {            \
+  } while (0)
+#define TK_TIME(k, stmt) \
+  { stmt; }
+#endif
+
+#ifndef TK_MQ_SMEM
+#define TK_MQ_SMEM 0  // 1: the item's offsets m[q] are read from shared memory every step (16 fewer registers)
+#endif
+
+// TK_FAKE (probe builds only; results are then wrong): bit 0 skips the
+// exponentials, bit 1 the P^T stores and their proxy fence, bit 2 the K / V^T
+// loads (zeros), bit 3 the K / V^T stores into TMEM, bit 4 the GEMM2 MMAs,
+// bit 5 the GEMM1 MMAs
+#ifndef TK_FAKE
+#define TK_FAKE 0
+#endif
+
+// TK_TRACE (probe builds, tools/probes/tk_trace.py): CTA 0 records clock64()
+// of per-step events into the da_debug_trace buffer as [event][TK_NT] int64
+#ifdef TK_TRACE
+constexpr int TK_NT = 4096;
+#define TK_EV(ev, step)                                                                                   \
+  do {                                                                                                    \
+    if (blockIdx.x == 0 && lane == 0 && p.trace != nullptr && (step) < TK_NT) p.trace[(ev) * TK_NT + (step)] = clock64(); \
+  } while (0)
+#else
+#define TK_EV(ev, step) \
+  do {                  \
+  } while (0)
+#endif
 
 #ifndef TK_POLY
 #define TK_POLY 1  // every fourth exponential pair on the FMA pipe (exp2_poly2) instead of MUFU
@@ -80,10 +154,12 @@ using k4::TILE;
 using k4::token_row;
 
 constexpr int INFO = 16;  // step ring
-constexpr int W_SCHED = 0, W_G1 = 1, W_G2 = 2, W_Q = 3, W_KLD = 4, W_VLD = 12, W_SM = 20;
-constexpr int NWARPS = 28;
+constexpr int LDG = TK_LDG;
+constexpr int W_SCHED = 0, W_G1 = 1, W_G2 = 2, W_Q = 3, W_LD = 4, W_SM = 4 + 4 * LDG;
+constexpr int NWARPS = W_SM + 8;
 constexpr int THREADS = 32 * NWARPS;
-constexpr int INFO_CONSUMERS = 27;  // every warp but the scheduler reads (and releases) every step entry
+constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;  // registers per thread at launch (__launch_bounds__(THREADS, 1))
+constexpr int INFO_CONSUMERS = NWARPS - 1;  // every warp but the scheduler reads (and releases) every step entry
 
 constexpr uint32_t COL_K = 0, COL_V = 128, COL_S = 256, COL_O = 384;
 
@@ -108,8 +184,9 @@ struct SmemAux {
   int4 info[INFO];
   uint32_t tmem_base;
   alignas(16) float m[2][64];  // [item parity][query] fixed offsets (log2 units), read as float4
-  float lsum[2][4][32];   // [softmax warpgroup][warp slice][column] per-warp row sums
+  float lsum[2][2][4][64];  // [item parity][softmax warpgroup][warp slice][query] per-warp partial row sums
   float linv[2][32];      // [softmax warpgroup][column] 1 / l, or 0
+  int kv_done[2][2][4];    // [tensor][buffer][lane quadrant] last step stored (loader hand-over, TK_LDG odd)
   uint32_t ragged[RAGW];
   int list[LISTCAP];
 };
@@ -124,9 +201,35 @@ DA_DEV uint32_t vt_off(int d, int c) { return (uint32_t)(c * 2048 + d * 16); }
 
 template <int N>
 DA_DEV void set_maxnreg() {
-  if constexpr (N > 72) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N) : "memory");
-  else if constexpr (N < 72) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N) : "memory");
+  if constexpr (N > LAUNCH_REGS) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N) : "memory");
+  else if constexpr (N < LAUNCH_REGS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N) : "memory");
 }
+
+// .16x256b.x4 load into v[OFF .. OFF + 15] (mapping: tools/probes/tmem16x256.cu)
+DA_DEV void tmem_ld16x256_x4(uint32_t taddr, float (&v)[32], int off) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[off + i] = __uint_as_float(r[i]);
+}
+// .16x256b.x8 load into v[OFF .. OFF + 31]
+DA_DEV void tmem_ld16x256_x8(uint32_t taddr, float (&v)[64], int off) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v) + off;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x8.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+DA_DEV void sts32(uint32_t saddr, uint32_t v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory"); }
 
 DA_DEV void ldg16x4(const uint8_t* src, uint32_t* r) {
   const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
@@ -140,6 +243,11 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
   Bars& B = aux.bars;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long items = (long long)p.heads * p.geo.g;
+#ifdef TK_PROF
+  long long prof[8];
+  for (int k = 0; k < 8; ++k) prof[k] = 0;
+  const long long t_start = clock64();
+#endif
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -148,8 +256,8 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       mbar_init(&B.v_full[b], 128);
       mbar_init(&B.v_empty[b], 1);
       mbar_init(&B.s_full[b], 1);
-      mbar_init(&B.s_free[b], 256);
-      mbar_init(&B.p_full[b], 256);
+      mbar_init(&B.s_free[b], 128);  // buffer b: the warpgroup of step parity b
+      mbar_init(&B.p_full[b], 128);
       mbar_init(&B.p_free[b], 1);
       mbar_init(&B.q_full[b], 32);
       mbar_init(&B.q_empty[b], 1 + 256);  // GEMM1's last MMA of the item + the softmax's last read of m
@@ -162,6 +270,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
     }
     fence_barrier_init();
   }
+  if (threadIdx.x < 16) (&aux.kv_done[0][0][0])[threadIdx.x] = -2 + ((threadIdx.x >> 2) & 1);
   if (p.key_valid == nullptr && p.geo.g <= 32 * RAGW) {
     for (int wd = threadIdx.x; wd < (p.geo.g + 31) / 32; wd += blockDim.x) {
       uint32_t bits = 0;
@@ -184,7 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
   int ri = 0;
   uint32_t rph = 0;
   auto next_step = [&]() {
-    mbar_wait_warp(&B.info_full[ri], rph);
+    TK_TIME(0, mbar_wait_warp_sleep(&B.info_full[ri], rph));
     const int4 e = aux.info[ri];
     __syncwarp();
     if (lane == 0) mbar_arrive(&B.info_empty[ri]);
@@ -201,7 +310,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
     if (lane == 0) next_claim = atomicAdd(p.work, 1);
     auto publish = [&](int4 e) {  // lane 0
       const int ii = kq % INFO;
-      if (kq >= INFO) mbar_wait(&B.info_empty[ii], (uint32_t)(((kq / INFO) - 1) & 1));
+      if (kq >= INFO) TK_TIME(1, mbar_wait(&B.info_empty[ii], (uint32_t)(((kq / INFO) - 1) & 1)));
       aux.info[ii] = e;
       mbar_arrive(&B.info_full[ii]);
       ++kq;
@@ -264,14 +373,15 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       const int xb = seq & 1;  // Q tile (GEMM1) / O^T buffer (GEMM2) of the item
       const bool first = e.w & W_FIRST, last = e.w & W_LAST;
       if (g1) {
-        if (first) mbar_wait_spin(&B.q_full[xb], (uint32_t)((seq >> 1) & 1));
-        mbar_wait_spin(&B.k_full[b], par);
-        if (gs >= 2) mbar_wait_spin(&B.s_free[b], par ^ 1u);
+        if (first) TK_TIME(1, TK_WAIT(&B.q_full[xb], (uint32_t)((seq >> 1) & 1)));
+        TK_TIME(2, TK_WAIT(&B.k_full[b], par));
+        if (gs >= 2) TK_TIME(3, TK_WAIT(&B.s_free[b], par ^ 1u));
         tc_fence_after();
+        TK_EV(0, gs);
         if (elect_one_sync()) {
           const uint64_t bq = dQ + (uint64_t)(xb * (16384 >> 4));
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
+          for (int kk = 0; kk < ((TK_FAKE & 32) ? 0 : 8); ++kk)
             umma_bf16_ts(tmem + COL_S + 64 * b, tmem + COL_K + 64 * b + 8 * kk,
                          bq + (uint64_t)((kk >> 2) * (8192 >> 4) + (kk & 3) * 2), I1, kk > 0 ? 1u : 0u);
           umma_commit(&B.k_empty[b]);
@@ -280,12 +390,13 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
         }
         __syncwarp();
       } else {
-        if (first && seq >= 2) mbar_wait(&B.o_empty[xb], (uint32_t)(((seq >> 1) - 1) & 1));
-        mbar_wait_spin(&B.v_full[b], par);
-        mbar_wait_spin(&B.p_full[b], par);
+        if (first && seq >= 2) TK_TIME(1, mbar_wait(&B.o_empty[xb], (uint32_t)(((seq >> 1) - 1) & 1)));
+        TK_TIME(2, TK_WAIT(&B.v_full[b], par));
+        TK_TIME(3, TK_WAIT(&B.p_full[b], par));
         tc_fence_after();
+        TK_EV(1, gs);
         if (elect_one_sync()) {
-          const int nk = (e.z & F_J1) ? 8 : 4;  // an odd last region: keys 64..127 absent
+          const int nk = (TK_FAKE & 16) ? 0 : (e.z & F_J1) ? 8 : 4;  // an odd last region: keys 64..127 absent
           for (int kk = 0; kk < nk; ++kk)
             umma_bf16_ts(tmem + COL_O + 64 * xb, tmem + COL_V + 64 * b + 8 * kk,
                          dP + (uint64_t)(b * (16384 >> 4) + kk * (2048 >> 4)), I2, (first && kk == 0) ? 0u : 1u);
@@ -318,7 +429,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
         for (int k = 0; k < p.kblk; ++k) mx = fmaxf(mx, __ldg(kp + k));
         kmax = mx;
       }
-      if (seq >= 2) mbar_wait(&B.q_empty[qb], (uint32_t)(((seq >> 1) - 1) & 1));
+      if (seq >= 2) TK_TIME(1, mbar_wait(&B.q_empty[qb], (uint32_t)(((seq >> 1) - 1) & 1)));
       uint8_t* qt = smem + SMEM_Q + qb * 16384;
 #pragma unroll 1
       for (int rr = 0; rr < 2; ++rr) {
@@ -344,26 +455,21 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       mbar_arrive(&B.q_full[qb]);
       ++seq;
     }
-  } else if (warp >= W_KLD && warp < W_SM) {
+  } else if (warp >= W_LD && warp < W_SM) {
     // ============================ K / V^T loaders ============================
     set_maxnreg<TK_REG_LD>();
-    const bool is_v = warp >= W_VLD;
-    const int lw = warp - (is_v ? W_VLD : W_KLD);
-    const int grp = lw >> 2, slice = lw & 3;
+    const int grp = (warp - W_LD) >> 2, slice = (warp - W_LD) & 3;
     const int L = 32 * slice + lane;  // TMEM lane: key of the pair (K) or feature (V^T)
-    const uint32_t tl = tmem + ((uint32_t)(32 * slice) << 16) + (is_v ? COL_V : COL_K);
-    uint64_t* full = is_v ? B.v_full : B.k_full;
-    uint64_t* empty = is_v ? B.v_empty : B.k_empty;
-    const uint8_t* tiles = is_v ? p.vt : p.kt;
     const long long hstride = (long long)p.geo.g * TILE;
     int gs = 0;
-    for (;;) {
-      const int4 e = next_step();
-      if (e.w & W_END) break;
-      if ((gs & 1) != grp) { ++gs; continue; }
-      const uint8_t* hb = tiles + (long long)(e.z >> 8) * hstride;
+    auto job = [&](const int4& e, auto is_v_t) {
+      constexpr bool is_v = decltype(is_v_t)::value;
+      const uint8_t* hb = (is_v ? p.vt : p.kt) + (long long)(e.z >> 8) * hstride;
       uint32_t r[64];
-      if (!is_v) {
+      if (TK_FAKE & 4) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) r[c] = 0u;
+      } else if (!is_v) {
         const int j = (L >> 6) ? e.y : e.x;
         if (j >= 0) {
           const uint8_t* src = hb + (long long)j * TILE + kt_off(L & 63, 0);
@@ -387,105 +493,176 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
         }
       }
       const int b = gs & 1;
-      if (gs >= 2) mbar_wait_spin(&empty[b], (uint32_t)(((gs >> 1) - 1) & 1));
+      if (LDG % 2 == 1) {
+        // this buffer's previous job (step gs - 2) belongs to another group: let
+        // it store first, so the empty-barrier phase below cannot alias
+        volatile int* done = &aux.kv_done[is_v][b][slice];
+        if (lane == 0)
+          while (*done != gs - 2) __nanosleep(32);
+        __syncwarp();
+      }
+      if (gs >= 2) TK_TIME(2, TK_WAIT(is_v ? &B.v_empty[b] : &B.k_empty[b], (uint32_t)(((gs >> 1) - 1) & 1)));
       tc_fence_after();
-      tmem_st32(tl + 64 * b, *reinterpret_cast<float(*)[32]>(&r[0]));
-      tmem_st32(tl + 64 * b + 32, *reinterpret_cast<float(*)[32]>(&r[32]));
-      tmem_st_wait();
+      const uint32_t tl = tmem + ((uint32_t)(32 * slice) << 16) + (is_v ? COL_V : COL_K) + 64 * b;
+      if (!(TK_FAKE & 8))
+        TK_TIME(3, tmem_st32(tl, *reinterpret_cast<float(*)[32]>(&r[0]));
+                tmem_st32(tl + 32, *reinterpret_cast<float(*)[32]>(&r[32])); tmem_st_wait());
       tc_fence_before();
-      mbar_arrive(&full[b]);
+      mbar_arrive(is_v ? &B.v_full[b] : &B.k_full[b]);
+#ifndef TK_TRACE2
+      if (slice == 0) TK_EV(5 + is_v, gs);
+#endif
+      if (LDG % 2 == 1) {
+        __syncwarp();
+        if (lane == 0) *(volatile int*)&aux.kv_done[is_v][b][slice] = gs;
+      }
+    };
+    for (;;) {
+      const int4 e = next_step();
+      if (e.w & W_END) break;
+      // jobs 2 gs (K) and 2 gs + 1 (V^T) go to groups in turn
+      if ((2 * gs) % LDG == grp) job(e, std::false_type{});
+      if ((2 * gs + 1) % LDG == grp) job(e, std::true_type{});
       ++gs;
     }
   } else {
     // ========================= softmax + epilogue =========================
+    // Warpgroup wg takes the steps of parity wg (S^T / P^T buffer wg), all 64
+    // query columns; warp sp of it owns S^T lanes 32 sp .. 32 sp + 31 (keys).
+    // Two .16x256b.x8 loads (lane bases 0 and 16; tools/probes/tmem16x256.cu):
+    // register i of load h holds key 32 sp + 16 h + t/4 + 8 ((i >> 1) & 1) and
+    // query 8 (i >> 2) + 2 (t % 4) + (i & 1). So each thread owns 4 keys x 16
+    // queries: the queries' row sums accumulate in 16 registers across the
+    // item (no cross-lane reduction per step) and their 16 offsets m[q] stay
+    // in registers for the whole item.
     set_maxnreg<TK_REG_SM>();
-    const int wg = (warp - W_SM) >> 2, slice = (warp - W_SM) & 3;
-    const int L = 32 * slice + lane;  // TMEM lane: key of the pair (softmax) / feature (epilogue)
-    const uint32_t tl = tmem + ((uint32_t)(32 * slice) << 16);
+    const int wg = (warp - W_SM) >> 2, sp = (warp - W_SM) & 3;
+    const int c4 = lane & 3, r8 = lane >> 2;
+    const uint32_t tl = tmem + ((uint32_t)(32 * sp) << 16);
     const float sl2 = p.scale_log2;
-    const int bar_id = 1 + wg;  // named barrier of this warpgroup
+    // P^T tile: [8-key group][8 keys x 128 B], 128-byte swizzle; this thread's
+    // words: key 32 sp + 8 kk + r8, 16-byte chunk jj ^ r8, word c4
+    const uint32_t pbase = smem_u32(smem + SMEM_P + wg * 16384) + (uint32_t)(4 * sp * 1024 + r8 * 128 + 4 * c4);
     int gs = 0, seq = 0;
-    float lpart = 0.f;
+    float2 lsum[8], mq[8];
     bool anyv = false;
     for (;;) {
+#ifdef TK_TRACE2
+      if (wg == 0 && sp == 0) TK_EV(5, gs);
+#endif
       const int4 e = next_step();
       if (e.w & W_END) break;
-      const int b = gs & 1;
+#ifdef TK_TRACE2
+      if (wg == 0 && sp == 0) TK_EV(6, gs);
+#endif
       const uint32_t par = (uint32_t)((gs >> 1) & 1);
       const int qb = seq & 1;
       const bool first = e.w & W_FIRST, last = e.w & W_LAST;
       if (first) {
-        mbar_wait_spin(&B.q_full[qb], (uint32_t)((seq >> 1) & 1));  // the item's offsets m[q]
-        lpart = 0.f;
+        TK_TIME(1, TK_WAIT(&B.q_full[qb], (uint32_t)((seq >> 1) & 1)));  // the item's offsets m[q]
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          mq[jj] = *reinterpret_cast<const float2*>(&aux.m[qb][8 * jj + 2 * c4]);
+          lsum[jj] = make_float2(0.f, 0.f);
+        }
         anyv = false;
       }
-      // this thread's key: row L & 63 of region j0 (L < 64) or j1
-      const int sel = L >> 6;
-      const int j = sel ? e.y : e.x;
-      bool kv = j >= 0;
-      if (kv && (e.z & (sel ? F_RAG1 : F_RAG0))) kv = key_row_valid(p, j, L & 63);
-      anyv |= kv;
-      mbar_wait_spin(&B.s_full[b], par);
-      tc_fence_after();
-      float x[32];
-      tmem_ld32(tl + COL_S + 64 * b + 32 * wg, x);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&B.s_free[b]);
-      uint32_t pk[16];
-      {
-        const float* mq = &aux.m[qb][32 * wg];
+      if ((gs & 1) == wg) {
+        if (sp == 0) TK_EV(7, gs);
+        // this warp's keys are rows 32 (sp & 1) + [0, 32) of region j0 (sp < 2) or j1
+        const int sel = sp >> 1;
+        const int j = sel ? e.y : e.x;
+        if (j < 0) {
+          // odd last step: keys 64..127 absent; GEMM2 reads only P^T rows 0..63
+          TK_TIME(2, TK_WAIT(&B.s_full[wg], par));
+          tc_fence_before();
+          mbar_arrive(&B.s_free[wg]);
+          if (gs >= 2) TK_TIME(4, TK_WAIT(&B.p_free[wg], par ^ 1u));
+          mbar_arrive(&B.p_full[wg]);
+        } else {
+          uint32_t kvm = 0xfu;  // validity of keys kk = 0..3 (row 32 (sp & 1) + 8 kk + r8)
+          if (e.z & (sel ? F_RAG1 : F_RAG0)) {
+            const unsigned long long km = key_mask(p, j) >> (32 * (sp & 1) + r8);
+            kvm = (uint32_t)((km & 1ull) | ((km >> 7) & 2ull) | ((km >> 14) & 4ull) | ((km >> 21) & 8ull));
+          }
+          anyv |= kvm != 0u;
+          TK_TIME(2, TK_WAIT(&B.s_full[wg], par));
+          if (sp == 0) TK_EV(2, gs);
+          TK_T0();
+          tc_fence_after();
+          float x[64];
+          tmem_ld16x256_x8(tl + COL_S + 64 * wg, x, 0);
+          tmem_ld16x256_x8(tl + (16u << 16) + COL_S + 64 * wg, x, 32);
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(&B.s_free[wg]);
+          if (sp == 0) TK_EV(3, gs);
+          TK_ACC(3);
+          if (gs >= 2) {
+            TK_TIME(4, TK_WAIT(&B.p_free[wg], par ^ 1u));
+            tc_fence_after();
+          }
+          {
+          TK_T0();
+          // x[32 h + 4 jj + 2 kb + e]: key 8 kk + r8 (kk = 2 h + kb), query 8 jj + 2 c4 + e
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 m4 = *reinterpret_cast<const float4*>(mq + i);
-          float2 e0 = ffma2(make_float2(x[i], x[i + 1]), make_float2(sl2, sl2), make_float2(-m4.x, -m4.y));
-          float2 e1 = ffma2(make_float2(x[i + 2], x[i + 3]), make_float2(sl2, sl2), make_float2(-m4.z, -m4.w));
-          float2 p0, p1;
-          p0 = make_float2(fast_exp2(e0.x), fast_exp2(e0.y));
-          if (TK_POLY && (i & 4)) p1 = exp2_poly2(e1);
-          else p1 = make_float2(fast_exp2(e1.x), fast_exp2(e1.y));
-          if (!kv) p0 = p1 = make_float2(0.f, 0.f);
-          x[i] = p0.x; x[i + 1] = p0.y; x[i + 2] = p1.x; x[i + 3] = p1.y;
-          pk[i / 2] = pack_bf16(p0.x, p0.y);
-          pk[i / 2 + 1] = pack_bf16(p1.x, p1.y);
+          for (int i = 0; i < 64; i += 2) {
+            const int jj = (i >> 2) & 7;
+            const int kk = 2 * (i >> 5) + ((i >> 1) & 1);
+#if TK_MQ_SMEM
+            const float2 m2 = *reinterpret_cast<const float2*>(&aux.m[qb][8 * jj + 2 * c4]);
+#else
+            const float2 m2 = mq[jj];
+#endif
+            float2 v = ffma2(make_float2(x[i], x[i + 1]), make_float2(sl2, sl2), make_float2(-m2.x, -m2.y));
+            if (TK_FAKE & 1) {
+            } else if (TK_POLY && (i & 6) == 6) {
+              v = exp2_poly2(v);
+            } else {
+              v = make_float2(fast_exp2(v.x), fast_exp2(v.y));
+            }
+            if (kvm != 0xfu && !((kvm >> kk) & 1u)) v = make_float2(0.f, 0.f);  // ragged region / padding keys
+            lsum[jj] = fadd2(lsum[jj], v);
+            if (!(TK_FAKE & 2)) sts32(pbase + (uint32_t)(kk * 1024) + (uint32_t)(((jj ^ r8) & 7) << 4), pack_bf16(v.x, v.y));
+          }
+          TK_ACC(6);
+          }
+          {
+          TK_T0();
+          if (!(TK_FAKE & 2)) fence_proxy_async_smem();
+          mbar_arrive(&B.p_full[wg]);
+          if (sp == 0) TK_EV(4, gs);
+          TK_ACC(7);
+          }
         }
       }
-      // row sums: butterfly over the warp's 32 keys; lane c ends with column c
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-          const float send = up ? x[i] : x[i + o];
-          const float keep = up ? x[i + o] : x[i];
-          x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      lpart += x[0];
-      if (gs >= 2) {
-        mbar_wait_spin(&B.p_free[b], par ^ 1u);
-        tc_fence_after();
-      }
-      {
-        const uint32_t base = smem_u32(smem + SMEM_P + b * 16384) + (uint32_t)((L >> 3) * 1024 + (L & 7) * 128);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int c = 4 * wg + i;
-          sts128(base + (uint32_t)(((c ^ L) & 7) << 4), pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-        }
-      }
-      fence_proxy_async_smem();
-      mbar_arrive(&B.p_full[b]);
       if (last) {
         mbar_arrive(&B.q_empty[qb]);  // done with m[qb]
-        // ---------------- item epilogue (this warpgroup's 32 query rows) ----------------
+        // ---------------- item epilogue (warpgroup wg: query rows 32 wg .. 32 wg + 31) ----------------
         const int h = e.z >> 8, region = e.w >> 3;
-        aux.lsum[wg][slice][lane] = lpart;
-        const bool had = bar_red_or(bar_id, 128, anyv);
-        if (slice == 0) {
-          const float l = aux.lsum[wg][0][lane] + aux.lsum[wg][1][lane] + aux.lsum[wg][2][lane] + aux.lsum[wg][3][lane];
+        // row sums: reduce the 8 key groups (lane bits 2..4) of each warp; the
+        // 8 warps' partials (both warpgroups) meet in shared memory
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            lsum[jj].x += __shfl_xor_sync(0xffffffffu, lsum[jj].x, o);
+            lsum[jj].y += __shfl_xor_sync(0xffffffffu, lsum[jj].y, o);
+          }
+        if (r8 == 0)
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            *reinterpret_cast<float2*>(&aux.lsum[qb][wg][sp][8 * jj + 2 * c4]) = lsum[jj];
+        const bool had = bar_red_or(1, 256, anyv);  // both warpgroups: partial sums written
+        if (sp == 0) {
+          const int q = 32 * wg + lane;
+          float l = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < 2; ++w2)
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) l += aux.lsum[qb][w2][s2][q];
           aux.linv[wg][lane] = l > 0.f ? 1.f / l : 0.f;
-          const long long row = token_row(p, region, 32 * wg + lane);
+          const long long row = token_row(p, region, q);
           const bool bad = had && !(l >= 0x1p-80f) && row >= 0;
           const unsigned bal = __ballot_sync(0xffffffffu, bad);
           if (bal != 0u && lane == 0) {  // duplicates (both warpgroups) are harmless
@@ -493,14 +670,15 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
             p.fb_items[slot] = h * p.geo.g + region;
           }
         }
-        mbar_wait(&B.o_full[qb], (uint32_t)((seq >> 1) & 1));
+        TK_TIME(5, mbar_wait(&B.o_full[qb], (uint32_t)((seq >> 1) & 1)));
         tc_fence_after();
+        const int L = 32 * sp + lane;  // TMEM lane of O^T: feature d
         float o[32];
         tmem_ld32(tl + COL_O + 64 * qb + 32 * wg, o);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&B.o_empty[qb]);
-        bar_sync(bar_id, 128);  // linv written
+        bar_sync(2 + wg, 128);  // linv written
         {
           // lane L = feature d: column i of O^T is query 32 wg + i
           uint16_t* st = reinterpret_cast<uint16_t*>(smem + SMEM_O);
@@ -511,7 +689,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
             st[(32 * wg + i) * D + L] = *reinterpret_cast<const uint16_t*>(&v);
           }
         }
-        bar_sync(bar_id, 128);  // staging complete
+        bar_sync(2 + wg, 128);  // staging complete
         {
           const int t = threadIdx.x - 32 * (W_SM + 4 * wg);  // 0..127
 #pragma unroll
@@ -530,6 +708,17 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       ++gs;
     }
   }
+#ifdef TK_PROF
+  {
+    const int role = warp == W_G1 ? 0 : warp == W_G2 ? 1 : warp == W_LD ? 2 : warp == W_LD + 4 ? 3 : warp == W_SM ? 4
+                     : warp == W_Q ? 5 : warp == W_SCHED ? 6 : -1;
+    if (p.trace != nullptr && lane == 0 && role >= 0) {
+      long long* o = p.trace + (long long)blockIdx.x * 64 + 8 * role;
+      for (int k = 0; k < 8; ++k) o[k] = prof[k];
+      if (role == 0) p.trace[(long long)blockIdx.x * 64 + 63] = clock64() - t_start;
+    }
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == W_G1) {

@@ -191,6 +191,13 @@ DA_DEV void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   if ((threadIdx.x & 31) == 0) mbar_wait_spin(bar, parity);
   __syncwarp();
 }
+// Same, but the polling lane sleeps in try_wait (suspend-time hint) instead of
+// spinning: for waits off the critical path, so that waiting warps leave the
+// issue slots to the warps that compute.
+DA_DEV void mbar_wait_warp_sleep(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
+}
 
 // ---------------------------------------------------------------------------
 // TMA
