@@ -84,7 +84,8 @@ constexpr int VSL = LH_VSL;
 #endif
 constexpr int VCP = LH_VCP;
 constexpr int THREADS = 384 + 32 * VCP;
-constexpr int INFO = 16;
+constexpr int INFO = 16;  // step-info ring; even, so a slot always holds steps of one lane half
+static_assert(INFO % 2 == 0, "info ring parity");
 constexpr int RAGW = 512;
 #ifndef LH_LISTCAP
 #define LH_LISTCAP 4096
@@ -124,7 +125,7 @@ struct __align__(8) Bars {
   uint64_t p_full[2], p_free[2];            // per lane half
   uint64_t o_full[NOB], o_empty[NOB];       // per O buffer
   uint64_t q_full, q_empty;
-  uint64_t info_full[INFO];
+  uint64_t info_full[INFO], info_empty[INFO];
   uint64_t item_full[IR], item_empty[IR];
 };
 struct SmemAux {
@@ -193,6 +194,21 @@ __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restric
   }
 }
 
+// A warp takes a step-info entry: lane 0 reads it, releases the slot and
+// broadcasts it (the slot's release then orders the only read of it).
+DA_DEV int4 take_info(const int4* info, uint64_t* empty, int i, int lane) {
+  int4 e = make_int4(0, 0, 0, 0);
+  if (lane == 0) {
+    e = info[i];
+    mbar_arrive(empty);
+  }
+  e.x = __shfl_sync(0xffffffffu, e.x, 0);
+  e.y = __shfl_sync(0xffffffffu, e.y, 0);
+  e.z = __shfl_sync(0xffffffffu, e.z, 0);
+  e.w = __shfl_sync(0xffffffffu, e.w, 0);
+  return e;
+}
+
 __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
@@ -223,7 +239,13 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     }
     mbar_init(&B.q_full, 256);
     mbar_init(&B.q_empty, 1);
-    for (int s = 0; s < INFO; ++s) mbar_init(&B.info_full[s], 1);
+    for (int s = 0; s < INFO; ++s) {
+      mbar_init(&B.info_full[s], 1);
+      // readers of a step entry: the V producer, GEMM1, GEMM2 and the 4 warps of
+      // the softmax warpgroup of the step's lane half (INFO is even: a slot
+      // always holds steps of one parity)
+      mbar_init(&B.info_empty[s], (VCP ? VCP : 1) + 2 + 4);
+    }
     for (int s = 0; s < IR; ++s) {
       mbar_init(&B.item_full[s], 1);
       mbar_init(&B.item_empty[s], VCP ? 10 + VCP : 11);  // warps 1, 3, the 8 softmax warps and the V warp(s)
@@ -330,11 +352,13 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
               if (bitmap ? (aux.ragged[j1 >> 5] >> (j1 & 31)) & 1 : key_mask(p, j1) != ~0ull) fl |= 8;
             }
             e = make_int4(j0, j1, fl, (t == n - 1 ? 1 : 0) | (t == 0 ? 2 : 0));
+            if (kq >= INFO) mbar_wait(&B.info_empty[ii], (uint32_t)(((kq / INFO) - 1) & 1));
             aux.info[ii] = e;
             mbar_arrive(&B.info_full[ii]);
           } else {
             { LH_T0(); mbar_wait(&B.info_full[ii], (uint32_t)((kq / INFO) & 1)); LH_ACC(18); }
             e = aux.info[ii];
+            mbar_arrive(&B.info_empty[ii]);
           }
           const int s = kq % NSL;
           if (kq >= NSL) { LH_T0(); mbar_wait(&empty[s], ((kq / NSL) - 1) & 1); LH_ACC(is_k ? 16 : 17); }
@@ -364,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
       { LH_T0(); mbar_wait(&B.q_full, qi & 1); LH_ACC(1); }
       for (;;) {
         { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(2); }
-        const int4 e = aux.info[iidx];
+        const int4 e = take_info(aux.info, &B.info_empty[iidx], iidx, lane);
         const int last = e.w & 1;
         const int h = gs & 1;
         // this half's S buffer: the softmax has loaded step gs - 2
@@ -411,7 +435,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
       int t = 0;
       for (;;) {
         { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(5); }
-        const int4 e = aux.info[iidx];
+        const int4 e = take_info(aux.info, &B.info_empty[iidx], iidx, lane);
         const int last = e.w & 1;
         const int h = gs & 1;
         const int s = gs % VSL;
@@ -460,7 +484,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
       for (int st = 0; st < n; ++st) {
         const int ii = kq % INFO;
         mbar_wait_warp(&B.info_full[ii], (uint32_t)((kq / INFO) & 1));
-        const int4 e = aux.info[ii];
+        const int4 e = take_info(aux.info, &B.info_empty[ii], ii, lane);
         const int s = kq % VSL;
         if (kq >= VSL) mbar_wait_warp(&B.v_empty[s], ((kq / VSL) - 1) & 1);
         ++kq;
@@ -554,7 +578,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
         const int gs = G + t;
         const int ii = gs & (INFO - 1);
         { LH_T0(); mbar_wait_spin(&B.info_full[ii], (uint32_t)((gs / INFO) & 1)); LH_ACC(9); }
-        const int4 e = aux.info[ii];
+        const int4 e = take_info(aux.info, &B.info_empty[ii], ii, lane);
         const int sb = (gs >> 1) % NSB;
         { LH_T0(); mbar_wait_spin(&B.s_full[wg][sb], (uint32_t)((gs / (2 * NSB)) & 1)); LH_ACC(10); }
         tc_fence_after();

@@ -119,6 +119,7 @@ __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) 
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __syncwarp();  // every lane has read M[r] before lane 0 rewrites it
         if (lane == 0) {
           float al = (mold == -INFINITY) ? 0.f : expf(mold - mnew);
           if (mnew == -INFINITY) al = 1.f;

@@ -563,11 +563,13 @@ constexpr int S32_CAP = 8192;    // band candidates per head resolved in one CTA
 
 struct Sel32State {
   unsigned int prefix;           // resolved high bits of T32's key
+  int pad0;                      // explicit padding: the state is copied whole (initcheck-clean)
   long long remaining;           // entries still to take from the current bucket
   unsigned long long nq2, nk2;   // largest pooled row norms^2 (double bits; non-negative so uint order)
   double eps;
   long long count_hi;            // sure-kept entries
   int cand_count;
+  int pad1;
 };
 
 DA_DEV unsigned int key32(float s) {
@@ -606,7 +608,7 @@ __global__ void s32_init_kernel(Sel32State* st, unsigned int* hist, unsigned int
   const int h = blockIdx.x;
   if (threadIdx.x == 0) {
     Sel32State s;
-    s.prefix = 0; s.remaining = m; s.eps = 0.0; s.count_hi = 0; s.cand_count = 0;
+    s.prefix = 0; s.pad0 = 0; s.remaining = m; s.eps = 0.0; s.count_hi = 0; s.cand_count = 0; s.pad1 = 0;
     s.nq2 = pnorm ? pnorm[2 * h] : 0;  // norms from the pooling pass, else s32_norm_kernel
     s.nk2 = pnorm ? pnorm[2 * h + 1] : 0;
     st[h] = s;

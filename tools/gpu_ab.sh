@@ -1,1 +1,3 @@
-DRAFTATTN_B200_LIB=$PWD/tools/probes/libs/lib_tkT2.so timeout 300 python tools/probes/tk_trace2.py > gpurun_out/tk_trace2.log 2>&1; echo "rc=$?"; cat gpurun_out/tk_trace2.log | tail -20
+timeout 600 python tools/probes/k4_variants.py run lhold lhnew3 --rounds 3 > gpurun_out/k4_lh_ring3.log 2>&1; echo "ab rc=$?"; tail -2 gpurun_out/k4_lh_ring3.log
+bash tools/gpu_sanitize.sh
+STAGES="test" bash tools/gpu_round.sh

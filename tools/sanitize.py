@@ -41,21 +41,20 @@ def main():
     n = f * h * w
     q, k, v = rnd(heads, n, d, seed=1), rnd(heads, n, d, seed=2), rnd(heads, n, d, seed=3)
     plan = da.pad_plan(f, h, w, 8, 8)
-    layout = plan.layout
-    check("pipeline hv slice", da.multi_head_sparse_attention(q, k, v, layout, 0.9))
+    check("pipeline hv slice", da.multi_head_sparse_attention(q, k, v, plan, 0.9))
     check("pipeline padded, details",
           da.padded_sparse_attention(q[0], k[0], v[0], f, h, w, 8, 8, 0.9, return_details=True))
-    check("pipeline softmax basis", da.multi_head_sparse_attention(q, k, v, layout, 0.75, select_on="softmax"))
-    check("pipeline shared mask", da.multi_head_sparse_attention(q, k, v, layout, 0.5, shared_head_mask=True))
-    check("pipeline fp64 fallback (ties)", da.multi_head_sparse_attention(torch.zeros_like(q), k, v, layout, 0.9))
+    check("pipeline softmax basis", da.multi_head_sparse_attention(q, k, v, plan, 0.75, select_on="softmax"))
+    check("pipeline shared mask", da.multi_head_sparse_attention(q, k, v, plan, 0.5, shared_head_mask=True))
+    check("pipeline fp64 fallback (ties)", da.multi_head_sparse_attention(torch.zeros_like(q), k, v, plan, 0.9))
     # portable executor: d = 64, 4x4 pool; and d % 8 != 0
     f2, h2, w2 = 2, 16, 20
     n2 = f2 * h2 * w2
     q2, k2, v2 = rnd(2, n2, 64, seed=4), rnd(2, n2, 64, seed=5), rnd(2, n2, 64, seed=6)
-    check("portable d=64", da.multi_head_sparse_attention(q2, k2, v2, da.pad_plan(f2, h2, w2, 4, 4).layout, 0.5))
+    check("portable d=64", da.multi_head_sparse_attention(q2, k2, v2, da.pad_plan(f2, h2, w2, 4, 4), 0.5))
     check("portable d=36", da.multi_head_sparse_attention(q2[..., :36].contiguous(), k2[..., :36].contiguous(),
                                                           v2[..., :36].contiguous(),
-                                                          da.pad_plan(f2, h2, w2, 4, 4).layout, 0.5))
+                                                          da.pad_plan(f2, h2, w2, 4, 4), 0.5))
     # seams
     qr = da.reorder_tokens(q, plan)
     check("reorder", qr)
