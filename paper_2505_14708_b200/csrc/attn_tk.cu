@@ -159,7 +159,13 @@ constexpr int W_SCHED = 0, W_G1 = 1, W_G2 = 2, W_Q = 3, W_LD = 4, W_SM = 4 + 4 *
 constexpr int NWARPS = W_SM + 8;
 constexpr int THREADS = 32 * NWARPS;
 constexpr int LAUNCH_REGS = (65536 / THREADS) & ~7;  // registers per thread at launch (__launch_bounds__(THREADS, 1))
-constexpr int INFO_CONSUMERS = NWARPS - 1;  // every warp but the scheduler reads (and releases) every step entry
+// step entries are read by GEMM1, GEMM2, every loader warp and the 4 warps of
+// the softmax warpgroup of the step's parity (INFO is even: a slot always holds
+// steps of one parity); item records by the Q warp and the 8 softmax warps
+constexpr int INFO_CONSUMERS = 2 + 4 * LDG + 4;
+constexpr int IR = 8;  // item ring
+constexpr int ITEM_CONSUMERS = 1 + 8;
+static_assert(INFO % 2 == 0, "step ring parity");
 
 constexpr uint32_t COL_K = 0, COL_V = 128, COL_S = 256, COL_O = 384;
 
@@ -178,10 +184,12 @@ struct __align__(8) Bars {
   uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
   uint64_t q_full[2], q_empty[2], o_full[2], o_empty[2];
   uint64_t info_full[INFO], info_empty[INFO];
+  uint64_t item_full[IR], item_empty[IR];
 };
 struct SmemAux {
   Bars bars;
   int4 info[INFO];
+  int4 items[IR];  // (first global step, steps, head, region); steps < 0: end of work
   uint32_t tmem_base;
   alignas(16) float m[2][64];  // [item parity][query] fixed offsets (log2 units), read as float4
   float lsum[2][2][4][64];  // [item parity][softmax warpgroup][warp slice][query] per-warp partial row sums
@@ -268,9 +276,13 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       mbar_init(&B.info_full[s], 1);
       mbar_init(&B.info_empty[s], INFO_CONSUMERS);
     }
+    for (int s = 0; s < IR; ++s) {
+      mbar_init(&B.item_full[s], 1);
+      mbar_init(&B.item_empty[s], ITEM_CONSUMERS);
+    }
     fence_barrier_init();
   }
-  if (threadIdx.x < 16) (&aux.kv_done[0][0][0])[threadIdx.x] = -2 + ((threadIdx.x >> 2) & 1);
+  if (threadIdx.x < 16) (&aux.kv_done[0][0][0])[threadIdx.x] = -2 + (int)((threadIdx.x >> 2) & 1);
   if (p.key_valid == nullptr && p.geo.g <= 32 * RAGW) {
     for (int wd = threadIdx.x; wd < (p.geo.g + 31) / 32; wd += blockDim.x) {
       uint32_t bits = 0;
@@ -289,7 +301,28 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
   // registers are split across the roles (launch: 72 per thread, 64512 in all):
   // each role branch below starts with its set_maxnreg
 
-  // every consumer walks the step ring in order and releases each entry
+  // a warp takes ring entry i (lane 0 reads it, releases the slot, broadcasts)
+  auto take = [&](const int4* ring, uint64_t* full, uint64_t* empty, uint32_t parity) {
+    int4 v = make_int4(0, 0, 0, 0);
+    if (lane == 0) {
+      mbar_wait(full, parity);
+      v = *ring;
+      mbar_arrive(empty);
+    }
+    v.x = __shfl_sync(0xffffffffu, v.x, 0);
+    v.y = __shfl_sync(0xffffffffu, v.y, 0);
+    v.z = __shfl_sync(0xffffffffu, v.z, 0);
+    v.w = __shfl_sync(0xffffffffu, v.w, 0);
+    return v;
+  };
+  int ii_item = 0;
+  uint32_t iph_item = 0;
+  auto next_item = [&]() {
+    const int4 v = take(&aux.items[ii_item], &B.item_full[ii_item], &B.item_empty[ii_item], iph_item);
+    if (++ii_item == IR) { ii_item = 0; iph_item ^= 1u; }
+    return v;
+  };
+  // every step consumer but the softmax walks the step ring in order and releases each entry
   int ri = 0;
   uint32_t rph = 0;
   auto next_step = [&]() {
@@ -314,6 +347,14 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       aux.info[ii] = e;
       mbar_arrive(&B.info_full[ii]);
       ++kq;
+    };
+    int kit = 0;
+    auto publish_item = [&](int4 v) {  // lane 0
+      const int si = kit % IR;
+      if (kit >= IR) mbar_wait(&B.item_empty[si], (uint32_t)(((kit / IR) - 1) & 1));
+      aux.items[si] = v;
+      mbar_arrive(&B.item_full[si]);
+      ++kit;
     };
     auto ragged = [&](int j) {
       return bitmap ? ((aux.ragged[j >> 5] >> (j & 31)) & 1u) != 0 : key_mask(p, j) != ~0ull;
@@ -344,6 +385,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       __syncwarp();
       if (lane == 0) {
         const int n = (itm.n + 1) / 2;
+        publish_item(make_int4(kq, n, itm.h, itm.i));
         for (int t = 0; t < n; ++t) {
           const int j0 = staged ? aux.list[2 * t] : __ldg(itm.list + 2 * t);
           const int j1 = 2 * t + 1 < itm.n ? (staged ? aux.list[2 * t + 1] : __ldg(itm.list + 2 * t + 1)) : -1;
@@ -355,7 +397,10 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
       }
       __syncwarp();
     }
-    if (lane == 0) publish(make_int4(-1, -1, 0, W_END));
+    if (lane == 0) {
+      publish(make_int4(-1, -1, 0, W_END));
+      publish_item(make_int4(0, -1, 0, 0));
+    }
   } else if (warp == W_G1 || warp == W_G2) {
     // ============================== MMA issuers ===============================
     set_maxnreg<TK_REG_CTL>();
@@ -417,10 +462,9 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
     float kmax = 0.f;
     const float sl2 = p.scale_log2;
     for (;;) {
-      const int4 e = next_step();
-      if (e.w & W_END) break;
-      if (!(e.w & W_FIRST)) continue;
-      const int h = e.z >> 8, region = e.w >> 3;
+      const int4 it = next_item();
+      if (it.y < 0) break;
+      const int h = it.z, region = it.w;
       const int qb = seq & 1;
       if (h != cur_head) {
         cur_head = h;
@@ -543,32 +587,31 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
     // P^T tile: [8-key group][8 keys x 128 B], 128-byte swizzle; this thread's
     // words: key 32 sp + 8 kk + r8, 16-byte chunk jj ^ r8, word c4
     const uint32_t pbase = smem_u32(smem + SMEM_P + wg * 16384) + (uint32_t)(4 * sp * 1024 + r8 * 128 + 4 * c4);
-    int gs = 0, seq = 0;
+    int seq = 0;
     float2 lsum[8], mq[8];
     bool anyv = false;
     for (;;) {
-#ifdef TK_TRACE2
-      if (wg == 0 && sp == 0) TK_EV(5, gs);
-#endif
-      const int4 e = next_step();
-      if (e.w & W_END) break;
-#ifdef TK_TRACE2
-      if (wg == 0 && sp == 0) TK_EV(6, gs);
-#endif
-      const uint32_t par = (uint32_t)((gs >> 1) & 1);
+      const int4 it = next_item();
+      if (it.y < 0) break;
+      const int G = it.x, nst = it.y;
       const int qb = seq & 1;
-      const bool first = e.w & W_FIRST, last = e.w & W_LAST;
-      if (first) {
-        TK_TIME(1, TK_WAIT(&B.q_full[qb], (uint32_t)((seq >> 1) & 1)));  // the item's offsets m[q]
+      TK_TIME(1, TK_WAIT(&B.q_full[qb], (uint32_t)((seq >> 1) & 1)));  // the item's offsets m[q]
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          mq[jj] = *reinterpret_cast<const float2*>(&aux.m[qb][8 * jj + 2 * c4]);
-          lsum[jj] = make_float2(0.f, 0.f);
-        }
-        anyv = false;
+      for (int jj = 0; jj < 8; ++jj) {
+        mq[jj] = *reinterpret_cast<const float2*>(&aux.m[qb][8 * jj + 2 * c4]);
+        lsum[jj] = make_float2(0.f, 0.f);
       }
-      if ((gs & 1) == wg) {
-        if (sp == 0) TK_EV(7, gs);
+      anyv = false;
+      // this warpgroup's steps of the item: global steps G + t of parity wg
+      for (int t = (wg - G) & 1; t < nst; t += 2) {
+        const int gs = G + t;
+        const int ii = gs & (INFO - 1);
+        TK_T0();
+        const int4 e = take(&aux.info[ii], &B.info_full[ii], &B.info_empty[ii], (uint32_t)((gs / INFO) & 1));
+        TK_ACC(0);
+        const uint32_t par = (uint32_t)((gs >> 1) & 1);
+        {
+          if (sp == 0) TK_EV(7, gs);
         // this warp's keys are rows 32 (sp & 1) + [0, 32) of region j0 (sp < 2) or j1
         const int sel = sp >> 1;
         const int j = sel ? e.y : e.x;
@@ -622,8 +665,16 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
               v = make_float2(fast_exp2(v.x), fast_exp2(v.y));
             }
             if (kvm != 0xfu && !((kvm >> kk) & 1u)) v = make_float2(0.f, 0.f);  // ragged region / padding keys
-            lsum[jj] = fadd2(lsum[jj], v);
+            x[i] = v.x;
+            x[i + 1] = v.y;
             if (!(TK_FAKE & 2)) sts32(pbase + (uint32_t)(kk * 1024) + (uint32_t)(((jj ^ r8) & 7) << 4), pack_bf16(v.x, v.y));
+          }
+          // row sums after the stores: they drain while the adds run, so the
+          // proxy fence below waits on fewer stores in flight
+#pragma unroll
+          for (int i = 0; i < 64; i += 2) {
+            const int jj = (i >> 2) & 7;
+            lsum[jj] = fadd2(lsum[jj], make_float2(x[i], x[i + 1]));
           }
           TK_ACC(6);
           }
@@ -636,10 +687,11 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
           }
         }
       }
-      if (last) {
+      }
+      {
         mbar_arrive(&B.q_empty[qb]);  // done with m[qb]
         // ---------------- item epilogue (warpgroup wg: query rows 32 wg .. 32 wg + 31) ----------------
-        const int h = e.z >> 8, region = e.w >> 3;
+        const int h = it.z, region = it.w;
         // row sums: reduce the 8 key groups (lane bits 2..4) of each warp; the
         // 8 warps' partials (both warpgroups) meet in shared memory
 #pragma unroll
@@ -705,7 +757,6 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_tk_kernel(const Params
         }
         ++seq;
       }
-      ++gs;
     }
   }
 #ifdef TK_PROF
