@@ -248,8 +248,11 @@ def run_ours(args, cfg, name):
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     if world == 1:
-        q, k, v = (torch.randn(heads, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
-                   for _ in range(3))
+        if args.data == "smooth":
+            q, k, v = (_smooth_inputs(plan, heads, d, dev, gen) for _ in range(3))
+        else:
+            q, k, v = (torch.randn(heads, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+                       for _ in range(3))
 
         def step(events=None):
             return da.api._pipeline(q, k, v, plan, sp, da.head_dim_scale(d), "average", "logits", True, False,
@@ -321,12 +324,12 @@ def run_ours(args, cfg, name):
     k4_tflops = eff_flops / (k4_ms * 1e-3) / 1e12 / world
     e2e = None
     cpu_base = None
-    dense_ms = None
+    dense_ms = dense_err = None
     if world > 1:
         e2e = _e2e_sharded(hp, q.shape, dev, args, world)
     if world == 1:
         e2e = _e2e(da, plan, cfg, dev, args)
-        dense_ms = None if args.no_dense else _dense_sdpa_ms(heads, n, d, dev)
+        dense_ms, dense_err = (None, None) if args.no_dense else _dense_sdpa(q, k, v, res[0])
         if not args.no_cpu:
             # one whole head through the unmodified reference (~45 s), else two through the port
             ids = (0,) if _reference_impl() is not None else (0, 1)
@@ -338,7 +341,9 @@ def run_ours(args, cfg, name):
         line = {
             "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn gaussian, seeded)",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": ("synthetic (torch.randn gaussian, seeded)" if args.data == "gaussian" else
+                     "synthetic (smooth per-frame bilinear fields + 0.1 noise, synth.py mode, torch RNG, seeded)"),
             "config": _config_dict(name, cfg, world),
             "effective_tflops_per_gpu": eff_flops / (ms * 1e-3) / 1e12 / world,
             "kept_blocks": kept_total,
@@ -351,6 +356,16 @@ def run_ours(args, cfg, name):
             "gpu_launches": launches,
             "clocks": clocks.result,
         }
+        if clocks.result and kept_total and world == 1:
+            # K4's structural floor: a kept block is a 64-row tcgen05 tile pair
+            # (GEMM1 + GEMM2 at M = 64) = 512 tensor cycles whatever the peak
+            # says; at the SM clock measured during the timed steps
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            f_hz = clocks.result["sm_mhz"] * 1e6
+            floor_ms = kept_total * 512 / (sms * f_hz) * 1e3
+            line["roofline"]["tile_floor"] = {
+                "what": "512 tensor cycles per kept 64x64x128 block (M = 64 tcgen05 tiles), all SMs, measured SM clock",
+                "ms": floor_ms, "frac": floor_ms / k4_ms, "sm_mhz": clocks.result["sm_mhz"]}
         if a2a_ms is not None:  # all-to-all time NOT hidden under compute, per call, max over ranks
             line["collective_exposed_ms"] = a2a_ms
             line["head_groups"] = args.head_groups
@@ -359,11 +374,39 @@ def run_ours(args, cfg, name):
         if dense_ms is not None:
             line["dense_sdpa_ms"] = dense_ms
             line["speedup_vs_dense_sdpa"] = dense_ms / ms
+        if dense_err is not None:
+            line["sparse_vs_dense_output"] = dense_err
         if cpu_base is not None:
             line["cpu_baseline"] = cpu_base
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _smooth_inputs(plan, heads, d, dev, gen, field_scale=0.5, noise_scale=0.1):
+    """The reference's secondary data mode (synth.py:44-86) on the GPU: per
+    frame, a Gaussian field at patch corners, bilinearly upsampled to the token
+    grid, plus 0.1-scaled i.i.d. noise; drawn on the padded grid, real rows
+    kept (cli.py:77-98). torch RNG, so the values differ from numpy's."""
+    import torch
+
+    lay = plan.layout
+    ch, cw, hp, wp = lay.patches_h, lay.patches_w, lay.height, lay.width
+    ys = torch.linspace(0.0, ch, hp, device=dev, dtype=torch.float64)
+    xs = torch.linspace(0.0, cw, wp, device=dev, dtype=torch.float64)
+    y0 = ys.long().clamp(0, ch - 1)
+    x0 = xs.long().clamp(0, cw - 1)
+    fy = (ys - y0)[:, None, None].float()
+    fx = (xs - x0)[None, :, None].float()
+    knots = torch.randn(heads, lay.frames, ch + 1, cw + 1, d, device=dev, generator=gen) * field_scale
+    k00 = knots[:, :, y0][:, :, :, x0]
+    k01 = knots[:, :, y0][:, :, :, x0 + 1]
+    k10 = knots[:, :, y0 + 1][:, :, :, x0]
+    k11 = knots[:, :, y0 + 1][:, :, :, x0 + 1]
+    field = k00 * (1 - fy) * (1 - fx) + k01 * (1 - fy) * fx + k10 * fy * (1 - fx) + k11 * fy * fx
+    field += noise_scale * torch.randn(field.shape, device=dev, generator=gen)
+    real = field[:, :, :plan.height, :plan.width]  # (heads, F, H, W, d): real rows, original order
+    return real.reshape(heads, -1, d).to(torch.bfloat16).contiguous()
 
 
 def _e2e_sharded(hp, shape, dev, args, world):
@@ -428,25 +471,35 @@ def _e2e(da, plan, cfg, dev, args):
             "d2h_bytes_per_step": nb}
 
 
-def _dense_sdpa_ms(heads, n, d, dev):
+def _dense_sdpa(q, k, v, sparse_out):
+    """Dense attention (cuDNN / flash SDPA, bf16) on the call's own inputs: its
+    time per call, and how far the sparse output is from it (the sweep's
+    sparse-vs-dense output error)."""
     import torch
     import torch.nn.functional as F
     from torch.nn.attention import SDPBackend, sdpa_kernel
 
-    q, k, v = (torch.randn(1, heads, n, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
+    qd, kd, vd = (x.unsqueeze(0) for x in (q, k, v))  # (1, heads, n, d) views
     try:
         with sdpa_kernel([SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION]):
-            F.scaled_dot_product_attention(q, k, v)
+            dense = F.scaled_dot_product_attention(qd, kd, vd)
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
             for _ in range(3):
-                F.scaled_dot_product_attention(q, k, v)
+                F.scaled_dot_product_attention(qd, kd, vd)
             e.record()
             torch.cuda.synchronize()
-        return s.elapsed_time(e) / 3
+        ms = s.elapsed_time(e) / 3
     except Exception:  # noqa: BLE001
-        return None
+        return None, None
+    a = sparse_out.float().reshape(-1)
+    b = dense[0].float().reshape(-1)
+    err = {"rel_l2": float((a - b).norm() / b.norm()), "max_abs": float((a - b).abs().max()),
+           "cosine": float(torch.nn.functional.cosine_similarity(a, b, dim=0)),
+           "what": "sparse call output vs dense SDPA on the same bf16 inputs (all heads)"}
+    del dense, a, b
+    return ms, err
 
 
 def main():
@@ -459,6 +512,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-dense", action="store_true", help="skip timing dense SDPA at the same shape")
+    ap.add_argument("--data", default="gaussian", choices=["gaussian", "smooth"],
+                    help="synthetic input mode (synth.py): i.i.d. gaussian (primary) or smooth fields")
     ap.add_argument("--head-groups", type=int, default=3,
                     help="N > 1: head groups per rank (all-to-all / compute overlap)")
     args = ap.parse_args()

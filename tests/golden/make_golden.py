@@ -192,8 +192,21 @@ def _sampled_reference(da, q, k, v, frames, height, width, ph, pw, sparsity, reg
     return mask, out_r[rows]
 
 
+def gen_smooth(da):
+    """synth.gen_inputs(mode="smooth") on a small padded grid (the reference's
+    secondary data mode), to pin the oracle's restatement of the generator."""
+    from draftattn import synth
+    plan = da.pad_plan(2, 13, 20, 4, 4)
+    q, k, v = synth.gen_inputs(plan.layout, 8, 7, mode="smooth", dtype=np.float32, heads=2)
+    np.savez_compressed(OUT / "smooth.npz", q=q, k=k, v=v)
+
+
 def main():
     da = _ref()
+    if sys.argv[1:] == ["smooth"]:
+        gen_smooth(da)
+        return
+    gen_smooth(da)
     gen_permutations(da)
     gen_pooling(da)
     gen_selection(da)

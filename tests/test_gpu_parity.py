@@ -720,3 +720,24 @@ def test_cached_mask_through_json_reproduces_the_call():
                                         da.reorder_tokens(v[h], plan), m, key_valid=kv)
         got = da.restore_tokens(o_r, plan)
         assert (got.float() - res.output[h].float()).abs().max().item() <= 4e-3
+
+
+@pytest.mark.gpu
+def test_smooth_inputs_720p_slice_masks_and_outputs():
+    # the reference's secondary data mode (smooth per-frame fields: patches
+    # nearly uniform, neighbouring regions alike, so many near-equal draft
+    # scores) through the full pipeline: masks identical, outputs within bars
+    grid = O.Grid(2, 45, 80, 8, 8)
+    q, k, v = O.gen_real_inputs(grid, 128, 11, 2, mode="smooth")
+    tq, tk, tv = (torch.from_numpy(x).to("cuda").to(torch.bfloat16) for x in (q, k, v))
+    plan = da.pad_plan(2, 45, 80, 8, 8)
+    res = da.multi_head_sparse_attention(tq, tk, tv, plan, 0.9, return_details=True)
+    out = res.output.float().cpu().numpy()
+    for h in range(2):
+        ref = O.padded_sparse_attention(tq[h].double().cpu().numpy(), tk[h].double().cpu().numpy(),
+                                        tv[h].double().cpu().numpy(), 2, 45, 80, 8, 8, 0.9, return_details=True)
+        got = res.mask.head(h)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept)
+        assert int(got.kept_count) == int(ref.mask.kept.sum())
+        assert int(got.forced_row_keeps) == int(ref.mask.forced_row_keeps)
+        _close(out[h], ref.output)

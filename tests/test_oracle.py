@@ -171,3 +171,11 @@ def test_mask_wire_fixtures():
         stats = O.mask_stats(m)
         for key, val in case["stats"].items():
             assert stats[key] == val, key
+
+
+def test_smooth_generator_matches_reference_fixture():
+    # synth.gen_inputs(mode="smooth") (synth.py:44-114), the reference's
+    # secondary data mode, restated in the oracle: identical float32 values
+    z = np.load(GOLD / "smooth.npz")
+    q, k, v = O.gen_smooth_heads(O.Grid(2, 13, 20, 4, 4), 8, 7, 2)
+    assert np.array_equal(q, z["q"]) and np.array_equal(k, z["k"]) and np.array_equal(v, z["v"])
