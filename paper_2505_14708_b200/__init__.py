@@ -24,6 +24,7 @@ from .api import (
     mask_to_json_dict,
     multi_head_sparse_attention,
     pad_plan,
+    padded_block_sparse_attention,
     padded_sparse_attention,
     pool_regions,
     pool_tokens,
@@ -39,7 +40,7 @@ __all__ = [
     "FlopsReport", "LatentLayout", "PadPlan", "PipelineResult", "RegionMask",
     "block_sparse_attention", "draft_logits", "draft_sparse_attention", "flops_count",
     "head_dim_scale", "kept_from_bitmap", "mask_density_stats", "mask_from_json_dict", "mask_to_bitmap",
-    "mask_to_json_dict", "multi_head_sparse_attention", "pad_plan",
+    "mask_to_json_dict", "multi_head_sparse_attention", "pad_plan", "padded_block_sparse_attention",
     "padded_sparse_attention", "pool_regions", "pool_tokens", "reorder_tokens",
     "restore_tokens", "select_top_fraction", "top_fraction_count", "__version__",
 ]

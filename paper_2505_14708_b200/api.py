@@ -644,6 +644,41 @@ def _attend(q, k, v, plan: PadPlan, mask: RegionMask, scale, qkv_layout="hnd", o
     return o3[0] if squeeze else (o_base if qkv_layout == "nhd" else o3)
 
 
+def padded_block_sparse_attention(q, k, v, plan: PadPlan, mask: RegionMask, scale=None, *, qkv_layout="hnd",
+                                  out=None) -> torch.Tensor:
+    """The executor stage of padded_sparse_attention (padding.py:155-157:
+    embed, permute, block_sparse_attention with key_valid, permute back,
+    extract) on ORIGINAL-order tensors with a given mask, the permutation fused
+    into the kernel: the way to reuse a cached mask (mask_from_json_dict /
+    a previous call's ``res.mask``) across denoising steps without pooling and
+    selection. ``mask``: one per head or one shared by all heads, over
+    ``plan``'s regions. Inputs as for multi_head_sparse_attention
+    ((n, d), (heads, n, d), or (n, heads, d) with qkv_layout="nhd")."""
+    if qkv_layout not in ("hnd", "nhd"):
+        raise ValueError(f"qkv_layout must be 'hnd' or 'nhd', got {qkv_layout!r}")
+    q3, squeeze = _as_heads(q, qkv_layout, "q")
+    k3, _ = _as_heads(k, qkv_layout, "k")
+    v3, _ = _as_heads(v, qkv_layout, "v")
+    if k3.shape != q3.shape or v3.shape[:2] != q3.shape[:2]:
+        raise ValueError(f"q {tuple(q3.shape)}, k {tuple(k3.shape)} and v {tuple(v3.shape)} do not match")
+    if scale is None:
+        scale = head_dim_scale(q3.shape[2])
+    out_dtype = _out_dtype(q, k, v)
+    dv0 = v3.shape[2]
+    if q3.shape[2] % 8 or dv0 % 8:  # exact zero features, as the pipeline does
+        o = _attend(_pad_features(q3), _pad_features(k3), _pad_features(v3), plan, mask, scale)[..., :dv0]
+        o = o[0] if squeeze else (o.transpose(0, 1) if qkv_layout == "nhd" else o)
+    else:
+        o = _attend(q, k, v, plan, mask, scale, qkv_layout)
+    o = o.to(out_dtype) if o.dtype != out_dtype else o
+    if out is not None:
+        if tuple(out.shape) != tuple(o.shape) or out.dtype != o.dtype:
+            raise ValueError(f"out must have shape {tuple(o.shape)} and dtype {o.dtype}")
+        out.copy_(o)
+        return out
+    return o
+
+
 def _cat_masks(masks) -> RegionMask:
     """Stack per-head-group masks of one call (same g, keep ratio, capacity)."""
     if len(masks) == 1:

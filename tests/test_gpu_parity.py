@@ -741,3 +741,26 @@ def test_smooth_inputs_720p_slice_masks_and_outputs():
         assert int(got.kept_count) == int(ref.mask.kept.sum())
         assert int(got.forced_row_keeps) == int(ref.mask.forced_row_keeps)
         _close(out[h], ref.output)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shared", [False, True])
+def test_cached_mask_on_original_order_equals_the_call(shared):
+    # mask reuse across denoising steps: the executor alone on original-order
+    # tensors with a cached (JSON round-tripped) mask reproduces the full call
+    grid, (q, k, v), _ = _inputs((2, 45, 80, 8, 8, 128, 3, 27))
+    plan = da.pad_plan(2, 45, 80, 8, 8)
+    res = da.multi_head_sparse_attention(q, k, v, plan, 0.9, shared_head_mask=shared, return_details=True)
+    if shared:
+        mask = da.mask_from_json_dict(da.mask_to_json_dict(res.mask, 0))
+    else:
+        mask = res.mask
+    got = da.padded_block_sparse_attention(q, k, v, plan, mask)
+    assert got.shape == res.output.shape and got.dtype == res.output.dtype
+    assert (got.float() - res.output.float()).abs().max().item() <= 4e-3
+    # (n, heads, d) DiT layout, and one head as (n, d)
+    got_nhd = da.padded_block_sparse_attention(q.transpose(0, 1), k.transpose(0, 1), v.transpose(0, 1), plan,
+                                               mask, qkv_layout="nhd")
+    assert torch.equal(got_nhd.transpose(0, 1), got)
+    one = da.padded_block_sparse_attention(q[1], k[1], v[1], plan, mask if shared else res.mask.head(1))
+    assert torch.equal(one, got[1])

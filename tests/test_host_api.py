@@ -168,3 +168,12 @@ def test_feature_padding_is_exact():
     from paper_2505_14708_b200.api import _pad_features
     with pytest.raises(ValueError, match="CUDA"):
         _pad_features(torch.zeros(1, 4, 5))
+
+
+def test_padded_block_sparse_attention_argument_errors():
+    plan = da.pad_plan(2, 13, 20, 4, 4)
+    q = torch.zeros(2, plan.num_valid, 16, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="qkv_layout"):
+        da.padded_block_sparse_attention(q, q, q, plan, None, qkv_layout="bhnd")
+    with pytest.raises(ValueError, match="do not match"):
+        da.padded_block_sparse_attention(q, q[:1], q, plan, None)
