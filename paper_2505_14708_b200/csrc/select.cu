@@ -591,6 +591,22 @@ DA_DEV float key32_score(unsigned int k) {
 DA_DEV double dot64_seq(const double* __restrict__ q, const double* __restrict__ k, int d) {
   double acc = 0.0;
   int c = 0;
+  if (((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15) == 0) {
+    // 16 features per batch: all 16 loads in flight, then the FMAs in order
+    for (; c + 16 <= d; c += 16) {
+      double2 qa[8], ka[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        qa[u] = __ldg(reinterpret_cast<const double2*>(q + c) + u);
+        ka[u] = __ldg(reinterpret_cast<const double2*>(k + c) + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc = fma(qa[u].x, ka[u].x, acc);
+        acc = fma(qa[u].y, ka[u].y, acc);
+      }
+    }
+  }
   for (; c + 4 <= d; c += 4) {
     const double q0 = __ldg(q + c), q1 = __ldg(q + c + 1), q2 = __ldg(q + c + 2), q3 = __ldg(q + c + 3);
     const double k0 = __ldg(k + c), k1 = __ldg(k + c + 1), k2 = __ldg(k + c + 2), k3 = __ldg(k + c + 3);
@@ -1061,7 +1077,11 @@ __global__ void __launch_bounds__(256) s32_mark_kernel(const float* __restrict__
       }
     }
   }
-  if (na > 0) flush_candidates();
+  if (na > 0) {
+    __syncwarp();
+    if (best < 0 && na == 1) best = ac[0];  // the row's only candidate is its argmax: nothing to rescore
+    else flush_candidates();
+  }
   if (lane == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&st[h].count_hi), (unsigned long long)hi_cnt);
     argmax[(long long)h * g + row] = best;
@@ -1243,7 +1263,10 @@ cudaError_t launch_select32(const double* qp, const double* kp, float* scores32,
   s32_pack_kernel<<<dim3((unsigned)(g32_pad(g, DT32) / 32), (unsigned)g32_pad(d, 32) / 32, 2 * heads), dim3(32, 8), 0,
                     st>>>(qp, kp, g, d, w.qt, w.kt);
   draft32_gemm_kernel<<<ggrid, 256, G32_SMEM, st>>>(w.qt, w.kt, scores32, g, d, (float)scale, w.hist, w.rowmax);
-  int chunks = (int)((n / 4 + 256 * 8 - 1) / (256 * 8));
+#ifndef S32_HIST_EPT
+#define S32_HIST_EPT 32  // 16-byte groups per thread per CTA of the digit-histogram pass
+#endif
+  int chunks = (int)((n / 4 + 256 * S32_HIST_EPT - 1) / (256 * S32_HIST_EPT));
   if (chunks > 512) chunks = 512;
   if (chunks < 1) chunks = 1;
   for (int pass = 0; pass < S32_PASSES; ++pass) {
