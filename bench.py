@@ -209,12 +209,15 @@ def run_reference(args, cfg, name):
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(name, cfg, n):
+def _config_dict(name, cfg, n, head_sharded=False):
     f, h, w, ph, pw, heads, d, sp = cfg
     return {"workload": f"{name}: {f}x{h}x{w} tokens ({f * h * w}), {heads} heads, d={d}, "
                         f"{ph}x{pw} pool, {int(sp * 100)}% sparsity",
             "frames": f, "height": h, "width": w, "patch": [ph, pw], "heads": heads, "head_dim": d,
-            "sparsity": sp, "parallelism": f"head-parallel x{n}" if n > 1 else "single GPU",
+            "sparsity": sp,
+            "parallelism": ((f"head-sharded replicas x{n} (no collective)" if head_sharded else
+                             f"head-parallel x{n} (sequence-sharded inputs, NCCL all-to-all)") if n > 1
+                            else "single GPU"),
             "l2": "inputs (3 x heads x n x d bf16) exceed the 126 MB L2; no flush needed"}
 
 
@@ -246,12 +249,18 @@ def run_ours(args, cfg, name):
     g = plan.layout.num_regions
     p = plan.layout.region_size
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # N > 1: sequence-sharded inputs through the head-parallel all-to-alls, or
+    # (--head-sharded) every rank already holds its heads: replicas, no collective
+    collective = world > 1 and not args.head_sharded
+    if world > 1 and args.head_sharded:
+        assert heads % world == 0, "heads must divide the world size"
+    hl = heads // world if world > 1 else heads
 
-    if world == 1:
+    if not collective:
         if args.data == "smooth":
-            q, k, v = (_smooth_inputs(plan, heads, d, dev, gen) for _ in range(3))
+            q, k, v = (_smooth_inputs(plan, hl, d, dev, gen) for _ in range(3))
         else:
-            q, k, v = (torch.randn(heads, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
+            q, k, v = (torch.randn(hl, n, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
                        for _ in range(3))
 
         def step(events=None):
@@ -301,7 +310,7 @@ def run_ours(args, cfg, name):
     mask = res[1]
     kept_total = int(mask.kept_counts.sum().item())
     a2a_ms = None
-    if world > 1:
+    if collective:
         # compute phases and K4 launches of every head group (current stream);
         # the all-to-alls run on NCCL's stream: call - compute = exposed comm
         k4_ms = statistics.mean(sum(b.elapsed_time(e) for b, e in evs) for evs in k4_ev)
@@ -315,6 +324,13 @@ def run_ours(args, cfg, name):
         kept_total = int(kt.item())
     else:
         k4_ms = statistics.mean(b.elapsed_time(e) for b, e in ev)
+        if world > 1:  # replicas: max over ranks
+            t = torch.tensor([elapsed, k4_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            elapsed, k4_ms = float(t[0]), float(t[1])
+            kt = torch.tensor([kept_total], device=dev, dtype=torch.int64)
+            dist.all_reduce(kt)
+            kept_total = int(kt.item())
     ms = elapsed / args.steps
 
     # effective work: 4 p^2 d per kept block pair (sparse.py:74-84 on the padded layout)
@@ -325,8 +341,10 @@ def run_ours(args, cfg, name):
     e2e = None
     cpu_base = None
     dense_ms = dense_err = None
-    if world > 1:
+    if collective:
         e2e = _e2e_sharded(hp, q.shape, dev, args, world)
+    elif world > 1:
+        e2e = _e2e(da, plan, cfg[:5] + (hl,) + cfg[6:], dev, args, world)
     if world == 1:
         e2e = _e2e(da, plan, cfg, dev, args)
         dense_ms, dense_err = (None, None) if args.no_dense else _dense_sdpa(q, k, v, res[0])
@@ -344,7 +362,7 @@ def run_ours(args, cfg, name):
             "vs_baseline": None, "dtype": "bf16",
             "data": ("synthetic (torch.randn gaussian, seeded)" if args.data == "gaussian" else
                      "synthetic (smooth per-frame bilinear fields + 0.1 noise, synth.py mode, torch RNG, seeded)"),
-            "config": _config_dict(name, cfg, world),
+            "config": _config_dict(name, cfg, world, head_sharded=world > 1 and args.head_sharded),
             "effective_tflops_per_gpu": eff_flops / (ms * 1e-3) / 1e12 / world,
             "kept_blocks": kept_total,
             "roofline": {"bound": "tensor", "kernel": "sparse_attn_lh_kernel (K4)", "achieved": k4_tflops,
@@ -442,8 +460,9 @@ def _e2e_sharded(hp, shape, dev, args, world):
             "d2h_bytes_per_step": nb * world}
 
 
-def _e2e(da, plan, cfg, dev, args):
-    """Public API with pinned host inputs and a host copy of the output."""
+def _e2e(da, plan, cfg, dev, args, world=1):
+    """Public API with pinned host inputs and a host copy of the output (max
+    over ranks when replicas run on N > 1 GPUs)."""
     import torch
 
     f, h, w, ph, pw, heads, d, sp = cfg
@@ -467,8 +486,13 @@ def _e2e(da, plan, cfg, dev, args):
     e.record()
     torch.cuda.synchronize()
     nb = heads * n * d * 2
-    return {"value": s.elapsed_time(e) / steps, "unit": "ms/call", "h2d_bytes_per_step": 3 * nb,
-            "d2h_bytes_per_step": nb}
+    val = s.elapsed_time(e) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([val], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        val = float(t[0])
+    return {"value": val, "unit": "ms/call", "h2d_bytes_per_step": 3 * nb * world, "d2h_bytes_per_step": nb * world}
 
 
 def _dense_sdpa(q, k, v, sparse_out):
@@ -514,6 +538,8 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip timing dense SDPA at the same shape")
     ap.add_argument("--data", default="gaussian", choices=["gaussian", "smooth"],
                     help="synthetic input mode (synth.py): i.i.d. gaussian (primary) or smooth fields")
+    ap.add_argument("--head-sharded", action="store_true",
+                    help="N > 1: inputs arrive head-sharded (heads/N per rank): replicas, no collective")
     ap.add_argument("--head-groups", type=int, default=3,
                     help="N > 1: head groups per rank (all-to-all / compute overlap)")
     args = ap.parse_args()
