@@ -764,3 +764,40 @@ def test_cached_mask_on_original_order_equals_the_call(shared):
     assert torch.equal(got_nhd.transpose(0, 1), got)
     one = da.padded_block_sparse_attention(q[1], k[1], v[1], plan, mask if shared else res.mask.head(1))
     assert torch.equal(one, got[1])
+
+
+def _random_configs(count, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        ph, pw = [(4, 4), (8, 8), (4, 8), (8, 4), (2, 8)][rng.integers(5)]
+        f = int(rng.integers(1, 4))
+        h = int(rng.integers(ph, 6 * ph))
+        w = int(rng.integers(pw, 6 * pw))
+        d = int([8, 16, 36, 64, 128][rng.integers(5)])
+        heads = int(rng.integers(1, 4))
+        sp = float(rng.choice([0.0, 0.3, 0.5, 0.75, 0.9, 0.97]))
+        out.append((f, h, w, ph, pw, d, heads, sp, int(rng.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", _random_configs(48))
+def test_random_shapes_vs_oracle(cfg):
+    # random grids (ragged and divisible), pools, head dims (incl. d % 8 != 0),
+    # head counts and sparsities through the full pipeline: masks identical,
+    # outputs within the bars
+    f, h, w, ph, pw, d, heads, sp, seed = cfg
+    grid = O.Grid(f, h, w, ph, pw)
+    q, k, v = O.gen_real_inputs(grid, d, seed % 100000, heads)
+    tq, tk, tv = (torch.from_numpy(x).to("cuda").to(torch.bfloat16) for x in (q, k, v))
+    plan = da.pad_plan(f, h, w, ph, pw)
+    res = da.multi_head_sparse_attention(tq, tk, tv, plan, sp, return_details=True)
+    out = res.output.float().cpu().numpy()
+    for hh in range(heads):
+        ref = O.padded_sparse_attention(tq[hh].double().cpu().numpy(), tk[hh].double().cpu().numpy(),
+                                        tv[hh].double().cpu().numpy(), f, h, w, ph, pw, sp, return_details=True)
+        got = res.mask.head(hh)
+        assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept), cfg
+        assert int(got.forced_row_keeps) == int(ref.mask.forced_row_keeps), cfg
+        _close(out[hh], ref.output)
