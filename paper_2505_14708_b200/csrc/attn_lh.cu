@@ -739,10 +739,11 @@ struct KvTileArgs {
   long long hs[2], rs[2];
   uint8_t* out[2];
   int layout;
-  int tk;  // 1: the TMEM-fed K4's layouts (K row chunks, V^T), 0: GROUPED smem images
 };
 __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, RegionDecoder dec) {
-  __shared__ __align__(16) uint16_t vs[P * D];  // V^T: the region's V rows, transposed on the way out
+#ifdef DA_K4_TK
+  __shared__ __align__(16) uint16_t vs[P * D];  // V^T (experimental transposed K4): V rows, transposed on the way out
+#endif
   const int j = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
   const RegionXY rc = dec(j);
   const uint4* src = reinterpret_cast<const uint4*>(a.x[z] + h * a.hs[z]);
@@ -760,11 +761,15 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
       row = (rc.y0 + u < g.H && rc.x0 + v < g.W) ? ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v : -1;
     }
     const uint4 val = row >= 0 ? __ldg(src + row * rs8 + c) : make_uint4(0, 0, 0, 0);
-    if (!a.tk) *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
-    else if (z == 0) *reinterpret_cast<uint4*>(dst + c * 1024 + r * 16) = val;
+#ifndef DA_K4_TK
+    *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
+#else
+    if (z == 0) *reinterpret_cast<uint4*>(dst + c * 1024 + r * 16) = val;
     else *reinterpret_cast<uint4*>(vs + r * D + 8 * c) = val;
+#endif
   }
-  if (a.tk && z == 1) {
+#ifdef DA_K4_TK
+  if (z == 1) {
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -776,6 +781,7 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
       *reinterpret_cast<uint4*>(dst + kc * 2048 + d * 16) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+#endif
 }
 
 // Per-head maximum key row norm as KBLK per-block partial maxima (the bound
@@ -932,7 +938,6 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
     ta.out[0] = attn_tiles(a.workspace, a.heads, g, 0);
     ta.out[1] = attn_tiles(a.workspace, a.heads, g, 1);
     ta.layout = a.layout;
-    ta.tk = attn_uses_tk() ? 1 : 0;
     lhk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
   }
   p.kt = attn_tiles(a.workspace, a.heads, g, 0);

@@ -78,7 +78,6 @@ struct PoolSrc {
   long long hs[3], rs[3];
   double* out[2];
   uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
-  int tile_tk;                // tile layouts: 1 = the TMEM-fed K4's (K row chunks, V^T), 0 = GROUPED smem images
   unsigned long long* pnorm;  // optional [heads][2]: largest pooled row norm^2 of Q (0) and K (1), as double bits
 };
 
@@ -297,7 +296,9 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
   // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
   uint8_t* tdst = (z >= 1 && src.tile[z - 1] != nullptr && live)
                       ? src.tile[z - 1] + ((long long)h * g.g + i) * 16384 : nullptr;
-  uint4 vprev[4];  // V^T tiles: the previous 4-row batch
+#ifdef DA_K4_TK
+  uint4 vprev[4];  // V^T tiles (the experimental transposed K4's layout): the previous 4-row batch
+#endif
   // fp64 sums of bf16 values are exact, in any order
   double acc[8];
 #pragma unroll
@@ -319,13 +320,15 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
       q[t] = ok[t] ? __ldg(base + row * rs8) : make_uint4(0, 0, 0, 0);
     }
     if (tdst != nullptr) {
-      if (!src.tile_tk) {
+#ifndef DA_K4_TK
 #pragma unroll
-        for (int t = 0; t < RB; ++t) {
-          const int r = r0 + t;
-          if (r < g.p) *reinterpret_cast<uint4*>(tdst + kv_tile_offset_grouped(r, k >> 3, k & 7)) = q[t];
-        }
-      } else if (z == 1) {
+      for (int t = 0; t < RB; ++t) {
+        const int r = r0 + t;
+        if (r < g.p) *reinterpret_cast<uint4*>(tdst + kv_tile_offset_grouped(r, k >> 3, k & 7)) = q[t];
+      }
+#else
+      // the experimental transposed K4's layouts (attn_tk.cu; probe builds only)
+      if (z == 1) {
         // K: chunk k (features 8k..8k+7) of key row r at k * 1024 + r * 16
 #pragma unroll
         for (int t = 0; t < RB; ++t) {
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
           }
         }
       }
+#endif
     }
     if (z == 2) continue;  // V: tiles only
 #pragma unroll
@@ -435,7 +439,6 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
     src.hs[2] = tiles ? hs2 : hs0; src.rs[2] = tiles ? rs2 : rs0;
     src.tile[0] = tiles ? ktile : nullptr;
     src.tile[1] = tiles ? vtile : nullptr;
-    src.tile_tk = attn_uses_tk() ? 1 : 0;
     src.pnorm = pnorm;
     dim3 grid(pool_norm_blocks(d, g), heads, x1 ? (tiles ? 3 : 2) : 1);
     float* kp = x1 ? kpart : nullptr;
