@@ -746,9 +746,10 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
 #endif
   const int j = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
   const RegionXY rc = dec(j);
-  const uint4* src = reinterpret_cast<const uint4*>(a.x[z] + h * a.hs[z]);
-  const long long rs8 = a.rs[z] / 8;
-  uint8_t* dst = a.out[z] + ((long long)h * g.g + j) * TILE;
+  // z selects K (0) or V (1) without dynamic parameter indexing (no local-memory copy)
+  const uint4* src = reinterpret_cast<const uint4*>(z ? a.x[1] + h * a.hs[1] : a.x[0] + h * a.hs[0]);
+  const long long rs8 = (z ? a.rs[1] : a.rs[0]) / 8;
+  uint8_t* dst = (z ? a.out[1] : a.out[0]) + ((long long)h * g.g + j) * TILE;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int idx = threadIdx.x + 256 * i;

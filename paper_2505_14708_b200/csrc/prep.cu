@@ -80,6 +80,12 @@ struct PoolSrc {
   uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
   unsigned long long* pnorm;  // optional [heads][2]: largest pooled row norm^2 of Q (0) and K (1), as double bits
 };
+// element z of a 2- or 3-entry parameter array, selected without dynamic
+// indexing (which would copy the kernel parameters to local memory)
+template <class T>
+DA_DEV T pick3(const T (&a)[3], int z) { return z == 0 ? a[0] : (z == 1 ? a[1] : a[2]); }
+template <class T>
+DA_DEV T pick2(const T (&a)[2], int z) { return z == 0 ? a[0] : a[1]; }
 
 __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode, Geo g) {
   extern __shared__ double red[];  // [RG][d]
@@ -89,8 +95,8 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode,
   const int tid = threadIdx.x;
   const int k = tid % d8, rg = tid / d8;
   const RegionCoord rc = region_coord(g, i);
-  const __nv_bfloat16* base = src.x[z] + h * src.hs[z];
-  const long long rs = src.rs[z];
+  const __nv_bfloat16* base = pick3(src.x, z) + h * pick3(src.hs, z);
+  const long long rs = pick3(src.rs, z);
   double acc[8];
   const double init = mode == 0 ? 0.0 : -INFINITY;
 #pragma unroll
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode,
     double outv;
     if (mode == 0) outv = s / (double)(cnt > 1 ? cnt : 1);
     else outv = cnt > 0 ? s : 0.0;
-    src.out[z][((long long)h * g.g + i) * d + c] = outv;
+    pick2(src.out, z)[((long long)h * g.g + i) * d + c] = outv;
   }
 }
 
@@ -289,13 +295,13 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
   const int k = threadIdx.x % TPR;
   const bool live = i < g.g;
   const RegionCoord rc = region_coord(g, live ? i : 0);
-  const uint4* base = reinterpret_cast<const uint4*>(src.x[z] + h * src.hs[z]) + k;
-  const long long rs8 = src.rs[z] / 8;
+  const uint4* base = reinterpret_cast<const uint4*>(pick3(src.x, z) + h * pick3(src.hs, z)) + k;
+  const long long rs8 = pick3(src.rs, z) / 8;
   const bool norms = z == 1 && kpart != nullptr;
   // K / V tiles ([half][64 rows x 128 B], 128-byte swizzle, zero padding rows):
   // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
-  uint8_t* tdst = (z >= 1 && src.tile[z - 1] != nullptr && live)
-                      ? src.tile[z - 1] + ((long long)h * g.g + i) * 16384 : nullptr;
+  uint8_t* const tz = z >= 1 ? pick2(src.tile, z - 1) : nullptr;
+  uint8_t* tdst = (tz != nullptr && live) ? tz + ((long long)h * g.g + i) * 16384 : nullptr;
 #ifdef DA_K4_TK
   uint4 vprev[4];  // V^T tiles (the experimental transposed K4's layout): the previous 4-row batch
 #endif
@@ -387,7 +393,7 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
   if (live && z < 2) {
     const int cnt = rc.vy * rc.vx;
     const double div = (double)(cnt > 1 ? cnt : 1);
-    double* o = src.out[z] + ((long long)h * g.g + i) * d + k * 8;
+    double* o = pick2(src.out, z) + ((long long)h * g.g + i) * d + k * 8;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       o[e] = acc[e] / div;
