@@ -33,7 +33,10 @@ struct Params {
   FastDiv per_head;  // g
   const uint8_t* kt;
   const uint8_t* vt;
-  const int* order;  // [heads][g] query regions by kept count (descending), or null
+  // [heads][g] item records in claim order (query regions by kept count,
+  // descending): {region i, list offset rp[i], kept count, head}, or null
+  // (natural region order, records computed from row_ptr)
+  const int4* meta;
   const float* kpart;
   int kblk;
   int* fb_count;
@@ -49,18 +52,31 @@ struct Item {
   int n;
 };
 
-DA_DEV bool fetch_item(const Params& p, long long it, long long items, Item& o) {
-  if (it < 0 || it >= items) return false;
+// The record of claimed item ``it``: {region, list offset, kept count, head};
+// kept count -1 past the last item. One 16-byte load with the region-order
+// pass's records, else two dependent row_ptr loads.
+DA_DEV int4 item_record(const Params& p, long long it, long long items) {
+  if (it < 0 || it >= items) return make_int4(0, 0, -1, 0);
+  if (p.meta != nullptr) return __ldg(p.meta + it);
   const int g = p.geo.g;
   const int h = (int)fdiv((uint32_t)it, p.per_head);
-  const int k = (int)(it - (long long)h * g);
-  o.h = h;
-  o.i = p.order != nullptr ? __ldg(p.order + it) : k;
+  const int i = (int)(it - (long long)h * g);
   const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
-  const int b = rp[o.i];
-  o.list = p.col_idx + (long long)(h * p.mask_h) * p.cap + b;
-  o.n = rp[o.i + 1] - b;
+  const int b = rp[i];
+  return make_int4(i, b, rp[i + 1] - b, h);
+}
+
+DA_DEV bool item_from_record(const Params& p, const int4 r, Item& o) {
+  if (r.z < 0) return false;
+  o.h = r.w;
+  o.i = r.x;
+  o.list = p.col_idx + (long long)(r.w * p.mask_h) * p.cap + r.y;
+  o.n = r.z;
   return true;
+}
+
+DA_DEV bool fetch_item(const Params& p, long long it, long long items, Item& o) {
+  return item_from_record(p, item_record(p, it, items), o);
 }
 
 DA_DEV long long token_row(const Params& p, int region, int r) {

@@ -115,6 +115,8 @@ constexpr uint32_t LANE_H = 16u << 16;  // TMEM address offset of lane half 1
 using k4::Params;
 using k4::Item;
 using k4::fetch_item;
+using k4::item_from_record;
+using k4::item_record;
 using k4::token_row;
 using k4::key_mask;
 
@@ -131,7 +133,7 @@ struct __align__(8) Bars {
 struct SmemAux {
   Bars bars;
   int4 info[INFO];      // per step: j0, j1, flags (1 j0, 2 j1, 4 j0 ragged, 8 j1 ragged), w (1 last, 2 first)
-  int items[IR];
+  int4 items[IR];  // item records (attn_k4.cuh item_record), kept count -1: end
   uint32_t tmem_base;
   float xm[2][64];      // [item parity][row] fixed softmax offset
   float xq[2][2][64];   // [item parity][warpgroup][row] partial |q|^2
@@ -148,7 +150,7 @@ static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
 // every region's output is computed independently). One block per head:
 // count histogram, block-wide exclusive scan, atomic placement.
 __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restrict__ row_ptr, int g, int mask_h,
-                                                            int* __restrict__ order) {
+                                                            int4* __restrict__ meta) {
   extern __shared__ int bins[];  // [g + 1], key = g - count
   __shared__ int wsum[32];
   const int h = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -190,7 +192,8 @@ __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restric
   __syncthreads();
   for (int i = t; i < g; i += blockDim.x) {
     const int pos = atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1);
-    order[(long long)h * g + pos] = i;
+    const int b = rp[i];
+    meta[(long long)h * g + pos] = make_int4(i, b, rp[i + 1] - b, h);  // the item record (attn_k4.cuh)
   }
 }
 
@@ -278,14 +281,14 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
   uint32_t ring_ph = 0;
   auto peek_item = [&]() {
     mbar_wait_spin(&B.item_full[ring_i], ring_ph);
-    return (long long)aux.items[ring_i];
+    return aux.items[ring_i];
   };
   auto next_item = [&]() {
-    const long long it = peek_item();
+    const int4 r = peek_item();
     __syncwarp();
     if (lane == 0) mbar_arrive(&B.item_empty[ring_i]);
     if (++ring_i == IR) { ring_i = 0; ring_ph ^= 1u; }
-    return it;
+    return r;
   };
 
   if (warp == 0 || (warp == 2 && VCP == 0)) {
@@ -297,38 +300,48 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     uint64_t* empty = is_k ? B.k_empty : B.v_empty;
     const bool bitmap = p.key_valid == nullptr && p.geo.g <= 32 * RAGW;
     int kq = 0, claimed = 0;
-    long long next_claim = 0;
-    if (is_k && lane == 0) next_claim = atomicAdd(p.work, 1);
+    // K producer: claims run two items ahead and item records one ahead, so
+    // a new item's first steps follow the previous item's without waiting on
+    // global memory; consumers get the record through the item ring
+    long long claim = 0;
+    int4 rec_next = make_int4(0, 0, -1, 0);
+    if (is_k) {
+      long long c0 = 0;
+      if (lane == 0) {
+        c0 = atomicAdd(p.work, 1);
+        claim = atomicAdd(p.work, 1);
+      }
+      rec_next = item_record(p, __shfl_sync(0xffffffffu, c0, 0), items);
+    }
     for (;;) {
       Item itm;
-      long long it;
       if (is_k) {
+        int4 rec;
         for (;;) {
+          rec = rec_next;
           long long c = 0;
           if (lane == 0) {
-            c = next_claim;
-            next_claim = atomicAdd(p.work, 1);
+            c = claim;
+            claim = atomicAdd(p.work, 1);
           }
-          c = __shfl_sync(0xffffffffu, c, 0);
-          if (!fetch_item(p, c, items, itm)) { it = items; break; }
-          if (itm.n > 0) { it = c; break; }
+          rec_next = item_record(p, __shfl_sync(0xffffffffu, c, 0), items);  // lands while this item streams
+          if (rec.z != 0) break;  // kept key regions, or past the last item
           // no kept key region: the region's output rows are zero
           for (int e = lane; e < P * (D / 8); e += 32) {
-            const long long row = token_row(p, itm.i, e / (D / 8));
-            if (row >= 0) reinterpret_cast<uint4*>(p.out + itm.h * p.oh + row * p.orow)[e % (D / 8)] = make_uint4(0, 0, 0, 0);
+            const long long row = token_row(p, rec.x, e / (D / 8));
+            if (row >= 0) reinterpret_cast<uint4*>(p.out + rec.w * p.oh + row * p.orow)[e % (D / 8)] = make_uint4(0, 0, 0, 0);
           }
         }
         const int slot = claimed % IR;
         if (claimed >= IR) { LH_T0(); mbar_wait(&B.item_empty[slot], (uint32_t)(((claimed / IR) - 1) & 1)); LH_ACC(0); }
         if (lane == 0) {
-          aux.items[slot] = (int)it;
+          aux.items[slot] = rec;
           mbar_arrive(&B.item_full[slot]);
         }
         ++claimed;
-        if (it >= items) break;
+        if (!item_from_record(p, rec, itm)) break;
       } else {
-        it = next_item();
-        if (!fetch_item(p, it, items, itm)) break;
+        if (!item_from_record(p, next_item(), itm)) break;
       }
       const bool staged = is_k && itm.n <= LISTCAP;
       if (staged) {
@@ -384,7 +397,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     int qi = 0;
     for (;;) {
       Item itm;
-      if (!fetch_item(p, next_item(), items, itm)) break;
+      if (!item_from_record(p, next_item(), itm)) break;
       { LH_T0(); mbar_wait(&B.q_full, qi & 1); LH_ACC(1); }
       for (;;) {
         { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(2); }
@@ -430,7 +443,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     int qi = 0;
     for (;;) {
       Item itm;
-      if (!fetch_item(p, next_item(), items, itm)) break;
+      if (!item_from_record(p, next_item(), itm)) break;
       const int ob = qi % NOB;
       int t = 0;
       for (;;) {
@@ -478,7 +491,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     int kq = 0;
     for (;;) {
       Item itm;
-      if (!fetch_item(p, next_item(), items, itm)) break;
+      if (!item_from_record(p, next_item(), itm)) break;
       const uint8_t* hb = p.vt + (long long)itm.h * p.geo.g * TILE;
       const int n = (itm.n + 1) / 2;
       for (int st = 0; st < n; ++st) {
@@ -552,7 +565,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     float kmax = 0.f;
     for (;;) {
       Item itm;
-      if (!fetch_item(p, next_item(), items, itm)) break;
+      if (!item_from_record(p, next_item(), itm)) break;
       const long long row = token_row(p, itm.i, r);
       const int nsteps = (itm.n + 1) / 2;
       const int ob = qi % NOB;
@@ -656,7 +669,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
       have_q = false;
       {
         Item nx;
-        if (fetch_item(p, peek_item(), items, nx)) {
+        if (item_from_record(p, peek_item(), nx)) {
           load_q(nx, qi & 1);
           have_q = true;
         }
@@ -845,7 +858,7 @@ static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 static size_t ws_norms() { return 256; }
 static size_t ws_items(int heads) { return ws_norms() + align256(sizeof(float) * heads * lhk::KBLK); }
 static size_t ws_order(int heads, const Geo& g) { return ws_items(heads) + align256(sizeof(int) * 4 * (size_t)heads * g.g); }
-static size_t ws_tiles(int heads, const Geo& g) { return ws_order(heads, g) + align256(sizeof(int) * (size_t)heads * g.g); }
+static size_t ws_tiles(int heads, const Geo& g) { return ws_order(heads, g) + align256(sizeof(int4) * (size_t)heads * g.g); }
 
 uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which) {
   return static_cast<uint8_t*>(ws) + ws_tiles(heads, g) + (size_t)which * heads * g.g * lhk::TILE;
@@ -906,7 +919,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   p.fb_count = reinterpret_cast<int*>(ws);
   p.work = reinterpret_cast<int*>(ws + 4);
   p.fb_items = reinterpret_cast<int*>(ws + ws_items(a.heads));
-  int* order = reinterpret_cast<int*>(ws + ws_order(a.heads, g));
+  int4* meta = reinterpret_cast<int4*>(ws + ws_order(a.heads, g));
   cudaMemsetAsync(ws, 0, 2 * sizeof(int), st);  // fallback counter, item counter
   if (kpart != nullptr) {  // norms from the pooling pass
     p.kpart = kpart;
@@ -923,11 +936,11 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   {
     const size_t smem = sizeof(int) * ((size_t)g.g + 1);
     if (smem <= 200 * 1024 && ensure_smem_optin((const void*)lhk::region_order_kernel, (int)smem) == cudaSuccess) {
-      lhk::region_order_kernel<<<a.heads, 1024, smem, st>>>(a.row_ptr, g.g, a.shared_mask ? 0 : 1, order);
-      p.order = order;
+      lhk::region_order_kernel<<<a.heads, 1024, smem, st>>>(a.row_ptr, g.g, a.shared_mask ? 0 : 1, meta);
+      p.meta = meta;
     } else {
       cudaGetLastError();
-      p.order = nullptr;  // natural region order
+      p.meta = nullptr;  // natural region order
     }
   }
   if (!tiles_ready) {
