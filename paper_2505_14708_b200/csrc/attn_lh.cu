@@ -42,6 +42,12 @@
 // LH_FAKELOAD (probe builds only, tools/probes): bit 0 skips the K copies,
 // bit 1 the V copies, bit 2 the softmax work. Results are then wrong; the
 // shipped library is built with 0.
+// LH_QPRE: the next item's Q rows are loaded during each warpgroup's last
+// step of the current item instead of after it
+#ifndef LH_QPRE
+#define LH_QPRE 0  // measured slower (24.05 vs 23.79 ms interleaved: 161 vs 120 registers)
+#endif
+
 #ifndef LH_FAKELOAD
 #define LH_FAKELOAD 0
 #endif
@@ -531,9 +537,12 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     float qn2_next = 0.f;
     // Q row r, feature half wg, into BOTH lane halves of columns [32 wg, 32 wg + 32)
     // (lane < 16 writes half 0, lane >= 16 half 1: the same row)
-    auto load_q = [&](const Item& itm, int wait_parity) {
+    // the next item's Q rows can be fetched early, during this warpgroup's
+    // last step of the current item (LH_QPRE), and stored once GEMM1 is done
+    // with the current Q
+    uint32_t qv[32];
+    auto issue_q = [&](const Item& itm) {
       const long long qrow = token_row(p, itm.i, r);
-      uint32_t qv[32];
       if (qrow >= 0) {
         const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + qrow * p.qr) + wg * 8;
 #pragma unroll
@@ -545,6 +554,8 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
 #pragma unroll
         for (int k = 0; k < 32; ++k) qv[k] = 0u;
       }
+    };
+    auto finish_q = [&](int wait_parity) {
       float s2 = 0.f;
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
@@ -560,6 +571,11 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
       tc_fence_before();
       mbar_arrive(&B.q_full);
     };
+    auto load_q = [&](const Item& itm, int wait_parity) {
+      issue_q(itm);
+      finish_q(wait_parity);
+    };
+    bool q_issued = false;  // the next item's Q rows are in flight in qv
     bool have_q = false;
     int cur_head = -1;
     float kmax = 0.f;
@@ -589,6 +605,18 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
       float x[64];
       for (int t = (wg - first_wg) & 1; t < nsteps; t += 2) {
         const int gs = G + t;
+#if LH_QPRE
+        if (t + 2 >= nsteps && !q_issued &&
+            mbar_test_wait(smem_u32(&B.item_full[ring_i]), ring_ph)) {
+          // this warpgroup's last step of the item: the next record is out,
+          // fetch its Q rows while this step's softmax runs
+          Item nx;
+          if (item_from_record(p, aux.items[ring_i], nx)) {
+            issue_q(nx);
+            q_issued = true;
+          }
+        }
+#endif
         const int ii = gs & (INFO - 1);
         { LH_T0(); mbar_wait_spin(&B.info_full[ii], (uint32_t)((gs / INFO) & 1)); LH_ACC(9); }
         const int4 e = take_info(aux.info, &B.info_empty[ii], ii, lane);
@@ -667,7 +695,11 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
       G += nsteps;
       // ---- next item's Q
       have_q = false;
-      {
+      if (q_issued) {
+        finish_q(qi & 1);
+        have_q = true;
+        q_issued = false;
+      } else {
         Item nx;
         if (item_from_record(p, peek_item(), nx)) {
           load_q(nx, qi & 1);
