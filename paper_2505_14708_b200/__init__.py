@@ -13,6 +13,7 @@ from .api import (
     PipelineResult,
     RegionMask,
     block_sparse_attention,
+    draft_attention_map,
     draft_logits,
     draft_sparse_attention,
     flops_count,
@@ -38,7 +39,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "FlopsReport", "LatentLayout", "PadPlan", "PipelineResult", "RegionMask",
-    "block_sparse_attention", "draft_logits", "draft_sparse_attention", "flops_count",
+    "block_sparse_attention", "draft_attention_map", "draft_logits", "draft_sparse_attention", "flops_count",
     "head_dim_scale", "kept_from_bitmap", "mask_density_stats", "mask_from_json_dict", "mask_to_bitmap",
     "mask_to_json_dict", "multi_head_sparse_attention", "pad_plan", "padded_block_sparse_attention",
     "padded_sparse_attention", "pool_regions", "pool_tokens", "reorder_tokens",

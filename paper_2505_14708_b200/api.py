@@ -981,6 +981,12 @@ def draft_logits(q_pooled, k_pooled, scale=None, head_dim=None, *, softmax=False
     return out[0] if squeeze else out
 
 
+def draft_attention_map(q_pooled, k_pooled, scale=None) -> torch.Tensor:
+    """Row-softmaxed draft map of the pooled sequences (pooling.py:59-65):
+    softmax_rows(draft_logits(q_pooled, k_pooled, scale)), float64."""
+    return draft_logits(q_pooled, k_pooled, scale, softmax=True)
+
+
 def select_top_fraction(scores, keep_ratio: float, force_row_keep: bool = False,
                         dead_columns=None) -> RegionMask:
     """Global top-ceil(r*g^2) with flat-index ties (+ row argmax keep) (masking.py:59-91): K3b.

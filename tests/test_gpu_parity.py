@@ -141,6 +141,9 @@ def test_draft_logits_float64():
     sm = da.draft_logits(torch.from_numpy(qp).cuda(), torch.from_numpy(kp).cuda(), softmax=True).cpu().numpy()
     np.testing.assert_allclose(sm[0], O.softmax_rows(O.draft_logits(qp[0], kp[0], O.head_dim_scale(128))),
                                rtol=1e-12, atol=1e-15)
+    # draft_attention_map (pooling.py:59-65) is the same row-softmaxed map
+    dm = da.draft_attention_map(torch.from_numpy(qp[0]).cuda(), torch.from_numpy(kp[0]).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(dm, sm[0])
 
 
 def test_selection_matches_reference_fixtures_bit_exact():
