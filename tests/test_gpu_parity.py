@@ -804,3 +804,23 @@ def test_random_shapes_vs_oracle(cfg):
         assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept), cfg
         assert int(got.forced_row_keeps) == int(ref.mask.forced_row_keeps), cfg
         _close(out[hh], ref.output)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("frames,sparsity", [(129, 0.9), (65, 0.97)])
+def test_long_video_masks_vs_oracle(frames, sparsity):
+    # longer clips than the paper's 720p shapes (129 frames: 464,400 tokens,
+    # g = 7,740 regions, 60 M draft scores per head): the fp32 selection, its
+    # guard band and the lane-half executor at that size; masks bit-identical
+    grid = O.Grid(frames, 45, 80, 8, 8)
+    q, k, v = O.gen_real_inputs(grid, 128, 31, 1)
+    tq, tk, tv = (torch.from_numpy(x).to("cuda").to(torch.bfloat16) for x in (q, k, v))
+    plan = da.pad_plan(frames, 45, 80, 8, 8)
+    res = da.multi_head_sparse_attention(tq, tk, tv, plan, sparsity, return_details=True)
+    ref, _ = O.draft_mask(tq[0].double().cpu().numpy(), tk[0].double().cpu().numpy(), grid, sparsity)
+    got = res.mask.head(0)
+    assert got.bitmap_bytes() == O.mask_bitmap(ref.kept)
+    assert int(got.kept_count) == int(ref.kept.sum())
+    assert float(got.threshold) == pytest.approx(ref.threshold, rel=1e-12)
+    out = res.output.float()
+    assert torch.isfinite(out).all() and out.abs().max().item() < 10.0
