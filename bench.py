@@ -238,11 +238,11 @@ def run_ours(args, cfg, name):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if rank == 0:
         build()
-    if world > 1:
-        dist.init_process_group("nccl")
-        dist.barrier()
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local)  # before NCCL: its communicator binds the current device
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
     f, h, w, ph, pw, heads, d, sp = cfg
     plan = da.pad_plan(f, h, w, ph, pw)
     n = plan.num_valid
