@@ -824,3 +824,27 @@ def test_long_video_masks_vs_oracle(frames, sparsity):
     assert float(got.threshold) == pytest.approx(ref.threshold, rel=1e-12)
     out = res.output.float()
     assert torch.isfinite(out).all() and out.abs().max().item() < 10.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["wan720", "hv720_smooth"])
+def test_full_head_outputs_other_headline_data(config):
+    # complete output of one whole head of the Wan 720p config (75 %) and of
+    # HV720 on the reference's smooth data mode (90 %) against the fp64 oracle
+    if config == "wan720":
+        dims, sp, mode = (21, 45, 80, 8, 8), 0.75, "gaussian"
+    else:
+        dims, sp, mode = (33, 45, 80, 8, 8), 0.9, "smooth"
+    grid = O.Grid(*dims)
+    q, k, v = O.gen_real_inputs(grid, 128, 5, 40 if config == "wan720" else 24, head_ids=[7], mode=mode)
+    tq, tk, tv = (torch.from_numpy(x).to("cuda").to(torch.bfloat16) for x in (q, k, v))
+    plan = da.pad_plan(*dims)
+    res = da.multi_head_sparse_attention(tq, tk, tv, plan, sp, return_details=True)
+    ref = O.padded_sparse_attention(tq[0].double().cpu().numpy(), tk[0].double().cpu().numpy(),
+                                    tv[0].double().cpu().numpy(), *dims, sp, return_details=True)
+    got = res.mask.head(0)
+    assert got.bitmap_bytes() == O.mask_bitmap(ref.mask.kept)
+    rep = _full_output_report(res.output[0].float().cpu().numpy(), ref.output, grid)
+    print(f"{config} head 7 sparsity {sp}: {rep}")
+    assert rep["max_abs"] <= MAX_ABS and rep["cosine"] >= MIN_COS, rep
+    assert rep["min_row_cosine"] >= 0.999, rep
