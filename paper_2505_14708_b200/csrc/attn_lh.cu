@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
 #ifndef DA_K4_TK
     *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
 #else
-    if (z == 0) *reinterpret_cast<uint4*>(dst + c * 1024 + r * 16) = val;
+    if (z == 0) *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
     else *reinterpret_cast<uint4*>(vs + r * D + 8 * c) = val;
 #endif
   }

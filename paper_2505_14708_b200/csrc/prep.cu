@@ -333,13 +333,13 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
         if (r < g.p) *reinterpret_cast<uint4*>(tdst + kv_tile_offset_grouped(r, k >> 3, k & 7)) = q[t];
       }
 #else
-      // the experimental transposed K4's layouts (attn_tk.cu; probe builds only)
+      // the experimental transposed K4 (attn_tk.cu; probe builds only): K as
+      // the GROUPED smem image, V as V^T
       if (z == 1) {
-        // K: chunk k (features 8k..8k+7) of key row r at k * 1024 + r * 16
 #pragma unroll
         for (int t = 0; t < RB; ++t) {
           const int r = r0 + t;
-          if (r < g.p) *reinterpret_cast<uint4*>(tdst + k * 1024 + r * 16) = q[t];
+          if (r < g.p) *reinterpret_cast<uint4*>(tdst + kv_tile_offset_grouped(r, k >> 3, k & 7)) = q[t];
         }
       } else {
         // V^T: this thread holds features 8k..8k+7 of rows r0 .. r0 + RB - 1;

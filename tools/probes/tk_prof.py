@@ -28,16 +28,15 @@ torch.cuda.synchronize()
 _lib.lib().da_debug_trace(None)
 t = tr.reshape(148, 64).cpu().numpy().astype(np.float64)
 tot = t[:, 63].mean()
-roles = ["GEMM1", "GEMM2", "K loader", "V loader", "softmax", "Q loader", "scheduler"]
+roles = ["GEMM1", "GEMM2", "V loader 0", "V loader 1", "softmax", "Q loader", "scheduler"]
 slots = {
-    0: {0: "step info", 1: "q_full", 2: "k_full", 3: "s_free"},
-    1: {0: "step info", 1: "o_empty", 2: "v_full", 3: "p_full"},
+    0: {0: "step info", 1: "q_full", 2: "k_full", 3: "s_free", 4: "MMA issue + commits"},
+    1: {0: "step info", 1: "o_empty", 2: "v_full", 3: "p_full", 4: "MMA issue + commits"},
     2: {0: "step info", 2: "buffer empty", 3: "tmem st (incl. LDG latency)"},
     3: {0: "step info", 2: "buffer empty", 3: "tmem st (incl. LDG latency)"},
-    4: {0: "step info", 1: "q_full", 2: "s_full", 3: "S ld (issue to data)", 4: "p_free", 5: "o_full",
-        6: "exp + row sums + P^T stores", 7: "proxy fence + arrive"},
-    5: {0: "step info", 1: "q_empty"},
-    6: {1: "ring full (info_empty)"},
+    4: {0: "step info", 1: "q_full", 2: "s_full", 3: "S ld + exp + P^T stores + sums", 4: "p_free", 5: "o_full"},
+    5: {0: "item", 1: "q_empty"},
+    6: {1: "ring full (info_empty)", 2: "K slot (k_empty)"},
 }
 print(f"CTA cycles (mean) {tot:.3e}")
 for r, name in enumerate(roles):

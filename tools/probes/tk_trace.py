@@ -29,7 +29,7 @@ api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(d), "average", "logits", Tru
 torch.cuda.synchronize()
 _lib.lib().da_debug_trace(None)
 t = tr.reshape(8, NT).cpu().numpy().astype(np.int64)
-names = ["G1 issue", "G2 issue", "S ready", "S read", "P written", "K stored", "V stored", "SM step start"]
+names = ["G1 issue", "G2 issue", "S ready", "S read", "P written", "K copy / K stored", "V stored", "SM step start"]
 lo, hi = 200, 3000
 t0 = t[:, lo:hi]
 print("median per-step gap (cycles):", {names[e]: float(np.median(np.diff(t0[e]))) for e in range(8)})
@@ -47,5 +47,8 @@ print("S read(s) -> G1 issue(s+2)", lat(3, 0, 2))
 print("G2 issue(s) -> P written(s+2)", lat(1, 4, 2))
 print("G1 issue(s) -> K stored(s+2)", lat(0, 5, 2))
 print("G2 issue(s) -> V stored(s+2)", lat(1, 6, 2))
+print("P written(s) -> SM step start(s+3)", lat(4, 7, 3))
+print("S read(s) -> G1 issue(s+3)", lat(3, 0, 3))
+print("G2 issue(s) -> P written(s+3)", lat(1, 4, 3))
 for s in range(lo, lo + 12):
     print(s, [int(t[e, s] - t[0, lo]) for e in range(8)])
