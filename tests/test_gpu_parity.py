@@ -848,3 +848,22 @@ def test_full_head_outputs_other_headline_data(config):
     print(f"{config} head 7 sparsity {sp}: {rep}")
     assert rep["max_abs"] <= MAX_ABS and rep["cosine"] >= MIN_COS, rep
     assert rep["min_row_cosine"] >= 0.999, rep
+
+
+@pytest.mark.gpu
+def test_repeated_calls_bit_identical():
+    # the persistent K4 claims items dynamically and its roles hand work over
+    # through mbarrier rings: any ordering race would show up as run-to-run
+    # differences. Full HV720 calls (24 heads) and many small calls, all
+    # bit-identical.
+    torch.manual_seed(3)
+    plan = da.pad_plan(33, 45, 80, 8, 8)
+    q, k, v = (torch.randn(24, plan.num_valid, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
+    ref = da.multi_head_sparse_attention(q, k, v, plan, 0.9)
+    for _ in range(6):
+        assert torch.equal(da.multi_head_sparse_attention(q, k, v, plan, 0.9), ref)
+    small = da.pad_plan(2, 45, 80, 8, 8)
+    qs, ks, vs = (x[:3, :small.num_valid].contiguous() for x in (q, k, v))
+    ref_s = da.multi_head_sparse_attention(qs, ks, vs, small, 0.75)
+    for _ in range(40):
+        assert torch.equal(da.multi_head_sparse_attention(qs, ks, vs, small, 0.75), ref_s)
