@@ -123,6 +123,7 @@ int da_select(const double* scores, int32_t heads, int32_t g, int64_t m, int32_t
  * the portable CUDA-core kernel (same semantics). */
 #define DA_LAYOUT_REORDERED 0
 #define DA_LAYOUT_ORIGINAL 1
+#define DA_MAX_SHARDS 8
 typedef struct da_attn_args {
   const void* q;
   const void* k;
@@ -146,6 +147,22 @@ typedef struct da_attn_args {
   int32_t force_portable; /* nonzero: use the CUDA-core kernel even when tcgen05 applies */
   void* workspace;        /* da_attn_workspace_size(heads, grid) bytes of device memory (caller-owned;
                              required by the tcgen05 path, ignored by the portable one) */
+  /* Sequence shards (layout ORIGINAL only; no reference counterpart: the
+     reference is single-process). shard_count >= 2: the tokens are split into
+     row blocks held in separate buffers, typically the sequence shards of a
+     group of ranks in peer GPUs' memory (mapped with da_ipc_open), which the
+     kernels then read and write over NVLink directly, with no all-to-all.
+     Token row r (original order) is row r - s*shard_rows of shard
+     s = r / shard_rows, at q_shards[s] + h*q_head_stride + (r - s*shard_rows)*q_row_stride
+     (likewise k, v, out; all shards share the strides); every shard but the
+     last holds shard_rows rows, and q/k/v/out are unused.
+     shard_count 0 or 1: plain tensors at q/k/v/out. */
+  int32_t shard_count;
+  int64_t shard_rows;
+  const void* q_shards[DA_MAX_SHARDS];
+  const void* k_shards[DA_MAX_SHARDS];
+  const void* v_shards[DA_MAX_SHARDS];
+  void* out_shards[DA_MAX_SHARDS];
 } da_attn_args;
 size_t da_attn_workspace_size(int32_t heads, const da_grid* grid);
 int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* stream);
@@ -184,6 +201,20 @@ int64_t da_pipeline_fallback_offset(const da_grid* grid, int32_t heads, int32_t 
 /* Kernel launches one da_sparse_attention call issues (for launch accounting). */
 int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask);
 int da_sparse_attention(const da_pipeline_args* args, const da_grid* grid, void* stream);
+
+/* ---- Peer memory (sequence shards over NVLink) ------------------------------
+ * CUDA IPC for da_attn_args' shard tables. da_ipc_export: the 64-byte handle
+ * of the device allocation holding dev_ptr and dev_ptr's byte offset in it
+ * (any pointer into a cudaMalloc allocation, e.g. a caching allocator's).
+ * da_ipc_open (in another process): maps that allocation into the current
+ * device, enabling peer access when it lives on another GPU, and returns the
+ * exported pointer's address here. da_ipc_close unmaps (the pointer
+ * da_ipc_open returned and the same offset). A process cannot open its own
+ * exports (use the pointer itself). */
+#define DA_IPC_HANDLE_BYTES 64
+int da_ipc_export(const void* dev_ptr, void* handle, int64_t* offset);
+int da_ipc_open(const void* handle, int64_t offset, void** dev_ptr);
+int da_ipc_close(void* dev_ptr, int64_t offset);
 
 /* ---- Diagnostics -------------------------------------------------------------
  * While set, the tcgen05 kernel of CTA 0 records clock64() stamps of its

@@ -32,6 +32,7 @@ from .api import (
     reorder_tokens,
     restore_tokens,
     select_top_fraction,
+    sharded_sparse_attention,
     top_fraction_count,
 )
 
@@ -43,5 +44,5 @@ __all__ = [
     "head_dim_scale", "kept_from_bitmap", "mask_density_stats", "mask_from_json_dict", "mask_to_bitmap",
     "mask_to_json_dict", "multi_head_sparse_attention", "pad_plan", "padded_block_sparse_attention",
     "padded_sparse_attention", "pool_regions", "pool_tokens", "reorder_tokens",
-    "restore_tokens", "select_top_fraction", "top_fraction_count", "__version__",
+    "restore_tokens", "select_top_fraction", "sharded_sparse_attention", "top_fraction_count", "__version__",
 ]

@@ -17,6 +17,8 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 DA_OK, DA_EINVAL, DA_ECUDA = 0, 1, 2
 LAYOUT_REORDERED, LAYOUT_ORIGINAL = 0, 1
+MAX_SHARDS = 8
+IPC_HANDLE_BYTES = 64
 
 c_i32, c_i64, c_f64, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 
@@ -39,6 +41,9 @@ class DaAttnArgs(ctypes.Structure):
         ("key_valid", c_vp),
         ("shared_mask", c_i32), ("force_portable", c_i32),
         ("workspace", c_vp),
+        ("shard_count", c_i32), ("shard_rows", c_i64),
+        ("q_shards", c_vp * MAX_SHARDS), ("k_shards", c_vp * MAX_SHARDS),
+        ("v_shards", c_vp * MAX_SHARDS), ("out_shards", c_vp * MAX_SHARDS),
     ]
 
 
@@ -75,6 +80,9 @@ SIGNATURES = {
     "da_pipeline_launches": (c_i32, [c_i32, c_i32]),
     "da_pipeline_fallback_offset": (ctypes.c_int64, [ctypes.POINTER(DaGrid), c_i32, c_i32]),
     "da_debug_trace": (ctypes.c_int, [c_vp]),
+    "da_ipc_export": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(c_i64)]),
+    "da_ipc_open": (ctypes.c_int, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    "da_ipc_close": (ctypes.c_int, [c_vp, c_i64]),
     "da_sparse_attention": (ctypes.c_int, [ctypes.POINTER(DaPipelineArgs), ctypes.POINTER(DaGrid), c_vp]),
 }
 

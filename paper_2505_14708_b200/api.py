@@ -490,8 +490,34 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
         return (out.to(out_dtype) if out_dtype != out.dtype else out), mask, squeeze
     q3, k3, v3 = _prep(q3), _prep(k3), _prep(v3)
     dv = v3.shape[2]
+    dev = q3.device
+    if out_dev is not None:
+        # the caller's bf16 output buffer, in the inputs' layout
+        o3, _ = _as_heads(out_dev, qkv_layout, "out")
+        if o3.dtype != torch.bfloat16 or tuple(o3.shape) != (heads, n, dv) or o3.device != dev or \
+                o3.stride(2) != 1 or o3.stride(0) % 8 or o3.stride(1) % 8 or o3.data_ptr() % 16:
+            raise ValueError("internal output buffer has the wrong shape, dtype or strides")
+        o_base = out_dev
+    else:
+        o_base, o3 = _alloc_like_layout(heads, n, dv, qkv_layout if not squeeze else "hnd", dev)
+    a = _attn_struct(q3, k3, v3, o3, d, dv, _lib.LAYOUT_ORIGINAL, scale)
+    a.force_portable = 1 if force_portable else 0
+    mask = _launch_pipeline(a, plan, sparsity, pool_mode, select_on, force_row_keep, shared_head_mask, dev,
+                            want_bitmap, attn_events, debug, single=squeeze or shared_head_mask)
+    out = o3[0] if squeeze else (o_base if qkv_layout == "nhd" else o3)
+    if out_dtype != torch.bfloat16:
+        out = out.to(out_dtype)
+    return out, mask, squeeze
+
+
+def _launch_pipeline(a: DaAttnArgs, plan: PadPlan, sparsity, pool_mode, select_on, force_row_keep,
+                     shared_head_mask, dev, want_bitmap=True, attn_events=None, debug=None,
+                     single=False) -> RegionMask:
+    """Allocate the mask outputs and the workspace, run da_sparse_attention
+    with the tensor fields of ``a`` (plain or sharded) and return the mask."""
+    heads, d = a.heads, a.d
     layout = plan.layout
-    g, dev = layout.num_regions, q3.device
+    g = layout.num_regions
     grid = make_grid(plan.frames, plan.height, plan.width, layout.patch_h, layout.patch_w)
     m = top_fraction_count(g * g, 1.0 - sparsity)
     mheads = 1 if shared_head_mask else heads
@@ -504,18 +530,8 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     kept = torch.empty(mheads, dtype=torch.int64, device=dev)
     ws_bytes = lib().da_pipeline_workspace_size(ctypes.byref(grid), heads, d)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    if out_dev is not None:
-        # the caller's bf16 output buffer, in the inputs' layout
-        o3, _ = _as_heads(out_dev, qkv_layout, "out")
-        if o3.dtype != torch.bfloat16 or tuple(o3.shape) != (heads, n, dv) or o3.device != dev or \
-                o3.stride(2) != 1 or o3.stride(0) % 8 or o3.stride(1) % 8 or o3.data_ptr() % 16:
-            raise ValueError("internal output buffer has the wrong shape, dtype or strides")
-        o_base = out_dev
-    else:
-        o_base, o3 = _alloc_like_layout(heads, n, dv, qkv_layout if not squeeze else "hnd", dev)
     pa = DaPipelineArgs()
-    pa.attn = _attn_struct(q3, k3, v3, o3, d, dv, _lib.LAYOUT_ORIGINAL, scale)
-    pa.attn.force_portable = 1 if force_portable else 0
+    pa.attn = a
     pa.m = m
     pa.force_row_keep = 1 if force_row_keep else 0
     pa.pool_mode = POOL_MODES.index(pool_mode)
@@ -534,12 +550,7 @@ def _pipeline(q, k, v, plan: PadPlan, sparsity, scale, pool_mode, select_on, for
     if debug is not None:  # tests: did the fp32 guard-band selection hand over to the fp64 path?
         off = lib().da_pipeline_fallback_offset(ctypes.byref(grid), heads, d)
         debug["selection_fallback"] = int(ws[off:off + 4].view(torch.int32).item()) != 0
-    out = o3[0] if squeeze else (o_base if qkv_layout == "nhd" else o3)
-    if out_dtype != torch.bfloat16:
-        out = out.to(out_dtype)
-    mask = RegionMask(g, float(1.0 - sparsity), bitmap, row_ptr, col_idx, thr, forced, kept,
-                      single=(squeeze or shared_head_mask))
-    return out, mask, squeeze
+    return RegionMask(g, float(1.0 - sparsity), bitmap, row_ptr, col_idx, thr, forced, kept, single=single)
 
 
 def _run(q, k, v, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask, qkv_layout, out,
@@ -677,6 +688,129 @@ def padded_block_sparse_attention(q, k, v, plan: PadPlan, mask: RegionMask, scal
         out.copy_(o)
         return out
     return o
+
+
+# --------------------------------------------------------------------------
+# sequence shards (no reference counterpart: the reference is single-process)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class ShardTable:
+    """Token tensors split into row blocks: q/k/v/out[s] are the device
+    addresses of element (head 0, local row 0) of shard s, which holds tokens
+    [s * rows, s * rows + rows_s) in original order (every shard but the last
+    has ``rows`` rows). The addresses may be other GPUs' memory mapped into
+    this process (``headpar.PeerShards``); the kernels then read and write the
+    peers' rows over NVLink. ``strides``: element strides (head, row) of q, k,
+    v and out, shared by all shards."""
+    q: tuple
+    k: tuple
+    v: tuple
+    out: tuple
+    rows: int
+    n: int
+    heads: int
+    d: int
+    dv: int
+    strides: tuple  # (qh, qr, kh, kr, vh, vr, oh, orow)
+
+    def struct(self, scale) -> DaAttnArgs:
+        a = DaAttnArgs()
+        (a.q_head_stride, a.q_row_stride, a.k_head_stride, a.k_row_stride,
+         a.v_head_stride, a.v_row_stride, a.o_head_stride, a.o_row_stride) = self.strides
+        a.heads, a.d, a.dv, a.layout = self.heads, self.d, self.dv, _lib.LAYOUT_ORIGINAL
+        a.scale = float(scale)
+        a.shard_count, a.shard_rows = len(self.q), self.rows
+        for i in range(len(self.q)):
+            a.q_shards[i], a.k_shards[i] = self.q[i], self.k[i]
+            a.v_shards[i], a.out_shards[i] = self.v[i], self.out[i]
+        return a
+
+
+def _shard_table(qs, ks, vs, outs) -> ShardTable:
+    """ShardTable of lists of (rows_s, heads, d) CUDA tensors (the "nhd" layout)."""
+    count = len(qs)
+    if not 2 <= count <= _lib.MAX_SHARDS or not len(ks) == len(vs) == len(outs) == count:
+        raise ValueError(f"need 2..{_lib.MAX_SHARDS} shards of q, k, v and out, got "
+                         f"{len(qs)}, {len(ks)}, {len(vs)}, {len(outs)}")
+    rows = qs[0].shape[0]
+    heads, d = qs[0].shape[1], qs[0].shape[2]
+    dv = vs[0].shape[2]
+    for s in range(count):
+        q, k, v, o = qs[s], ks[s], vs[s], outs[s]
+        for x, name, last in ((q, "q", d), (k, "k", d), (v, "v", dv), (o, "out", dv)):
+            if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.bfloat16 or x.ndim != 3:
+                raise ValueError(f"{name} shard {s} must be a 3-d bf16 CUDA tensor (rows, heads, d)")
+            if x.shape[1:] != (heads, last) or x.shape[0] != q.shape[0]:
+                raise ValueError(f"{name} shard {s} has shape {tuple(x.shape)}, expected "
+                                 f"({q.shape[0]}, {heads}, {last})")
+            ref = {"q": qs[0], "k": ks[0], "v": vs[0], "out": outs[0]}[name]
+            if x.stride() != ref.stride() or x.stride(2) != 1 or x.data_ptr() % 16:
+                raise ValueError(f"{name} shards need identical strides, unit feature stride and 16-byte alignment")
+        if (s < count - 1 and q.shape[0] != rows) or not 1 <= q.shape[0] <= rows:
+            raise ValueError(f"every shard but the last must hold {rows} rows (the last 1..{rows}), "
+                             f"shard {s} holds {q.shape[0]}")
+    if d % 8 or dv % 8:
+        raise ValueError("sharded calls need head dims that are multiples of 8")
+    n = rows * (count - 1) + qs[-1].shape[0]
+    q0, k0, v0, o0 = qs[0], ks[0], vs[0], outs[0]
+    return ShardTable(tuple(x.data_ptr() for x in qs), tuple(x.data_ptr() for x in ks),
+                      tuple(x.data_ptr() for x in vs), tuple(x.data_ptr() for x in outs), rows, n, heads, d, dv,
+                      (q0.stride(1), q0.stride(0), k0.stride(1), k0.stride(0), v0.stride(1), v0.stride(0),
+                       o0.stride(1), o0.stride(0)))
+
+
+def _run_sharded(table: ShardTable, plan: PadPlan, sparsity, scale, pool_mode="average", select_on="logits",
+                 force_row_keep=True, shared_head_mask=False, device=None, want_bitmap=False, attn_events=None,
+                 mask: RegionMask | None = None) -> RegionMask:
+    """The pipeline (or, with ``mask``, the executor alone) over a ShardTable,
+    on ``device``'s current stream. Returns the mask."""
+    if table.n != plan.num_valid:
+        raise ValueError(f"shards hold {table.n} rows, the layout has {plan.num_valid} tokens")
+    scale = head_dim_scale(table.d) if scale is None else scale
+    a = table.struct(scale)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if mask is None:
+        _validate_pipeline_args(sparsity, select_on, pool_mode)
+        return _launch_pipeline(a, plan, sparsity, pool_mode, select_on, force_row_keep, shared_head_mask, dev,
+                                want_bitmap, attn_events, single=shared_head_mask)
+    if mask.heads not in (1, table.heads) or mask.g != plan.layout.num_regions:
+        raise ValueError(f"mask of {mask.heads} heads over {mask.g} regions does not fit {table.heads} heads / "
+                         f"{plan.layout.num_regions} regions")
+    lay = plan.layout
+    grid = make_grid(plan.frames, plan.height, plan.width, lay.patch_h, lay.patch_w)
+    a.row_ptr, a.col_idx, a.mask_cap = mask.row_ptr.data_ptr(), mask.col_idx.data_ptr(), mask.col_idx.shape[1]
+    a.shared_mask = 1 if mask.heads == 1 else 0
+    ws = torch.empty(max(1, lib().da_attn_workspace_size(table.heads, ctypes.byref(grid))), dtype=torch.uint8,
+                     device=dev)
+    a.workspace = ws.data_ptr()
+    with torch.cuda.device(dev):
+        check(lib().da_block_sparse_fwd(ctypes.byref(a), ctypes.byref(grid), _stream_ptr(dev)), "block_sparse_fwd")
+    return mask
+
+
+def sharded_sparse_attention(q_shards, k_shards, v_shards, plan: PadPlan, sparsity, scale=None,
+                             pool_mode="average", select_on="logits", force_row_keep=True,
+                             shared_head_mask=False, *, out_shards=None, mask: RegionMask | None = None,
+                             return_mask=False):
+    """``multi_head_sparse_attention`` (per-head masks, or ``shared_head_mask``)
+    over a sequence held as row blocks: ``q_shards[s]`` etc. are (rows_s,
+    heads, d) bf16 CUDA tensors (the DiT "nhd" layout) holding tokens
+    [s * rows_0, s * rows_0 + rows_s) in original order, every shard but the
+    last with rows_0 rows (2 .. 8 shards). The kernels address the shards in
+    place (no gather). ``out_shards``: (rows_s, heads, dv) output buffers (new
+    ones if None). ``mask``: run the executor alone with this mask (cached
+    masks, ``padded_block_sparse_attention``). Returns the output shards
+    (and the mask with ``return_mask``). ``headpar.HeadParallelAttention``
+    with ``transport="peer"`` uses the same C-ABI path with other GPUs'
+    shards."""
+    if out_shards is None:
+        out_shards = [torch.empty(q.shape[:2] + (v.shape[2],), dtype=torch.bfloat16, device=q.device)
+                      for q, v in zip(q_shards, v_shards)]
+    table = _shard_table(list(q_shards), list(k_shards), list(v_shards), list(out_shards))
+    m = _run_sharded(table, plan, sparsity, scale, pool_mode, select_on, force_row_keep, shared_head_mask,
+                     q_shards[0].device, want_bitmap=return_mask, mask=mask)
+    return (list(out_shards), m) if return_mask else list(out_shards)
 
 
 def _cat_masks(masks) -> RegionMask:

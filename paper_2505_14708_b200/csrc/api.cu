@@ -93,7 +93,51 @@ cudaError_t ensure_smem_optin(const void* kernel, int bytes) {
 
 extern "C" {
 
-int32_t da_version(void) { return 100; }
+int32_t da_version(void) { return 101; }  // 1.01: sequence shards, IPC
+
+// ---------------------------------------------------------------------------
+// CUDA IPC for the sequence-shard tables (peer GPUs' shards over NVLink)
+// ---------------------------------------------------------------------------
+static_assert(sizeof(cudaIpcMemHandle_t) == DA_IPC_HANDLE_BYTES, "IPC handle size");
+
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int da_ipc_export(const void* dev_ptr, void* handle, int64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(DA_EINVAL, "ipc_export: null argument");
+  static AddrRangeFn range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return fail(DA_ECUDA, "ipc_export: cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<AddrRangeFn>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(DA_EINVAL, "ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  if (int rc = cuda_status(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "ipc_export")) return rc;
+  memcpy(handle, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return DA_OK;
+}
+
+int da_ipc_open(const void* handle, int64_t offset, void** dev_ptr) {
+  if (!handle || !dev_ptr || offset < 0) return fail(DA_EINVAL, "ipc_open: bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  if (int rc = cuda_status(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "ipc_open")) return rc;
+  *dev_ptr = static_cast<char*>(base) + offset;
+  return DA_OK;
+}
+
+int da_ipc_close(void* dev_ptr, int64_t offset) {
+  if (!dev_ptr || offset < 0) return fail(DA_EINVAL, "ipc_close: bad argument");
+  return cuda_status(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset), "ipc_close");
+}
 
 int da_debug_trace(void* device_buffer) {
   da::set_tc_trace(device_buffer);
@@ -182,8 +226,39 @@ int da_select(const double* scores, int32_t heads, int32_t g, int64_t m, int32_t
                      "select");
 }
 
+// Sequence shards: 2..DA_MAX_SHARDS non-null, 16-byte aligned buffers whose
+// row blocks cover exactly the grid's real tokens (every shard non-empty).
+static int check_shards(const da_attn_args& a, const da_grid* grid, const char* what) {
+  if (a.shard_count <= 1) return DA_OK;
+  if (a.layout != DA_LAYOUT_ORIGINAL) return fail(DA_EINVAL, "%s: sequence shards need the original layout", what);
+  if (a.shard_count > DA_MAX_SHARDS) return fail(DA_EINVAL, "%s: at most %d shards", what, DA_MAX_SHARDS);
+  const long long n = (long long)grid->frames * grid->height * grid->width;
+  if (a.shard_rows < 1 || a.shard_rows >= (1ll << 31) || (long long)(a.shard_count - 1) * a.shard_rows >= n ||
+      (long long)a.shard_count * a.shard_rows < n)
+    return fail(DA_EINVAL, "%s: %d shards of %lld rows do not cover %lld tokens", what, a.shard_count,
+                (long long)a.shard_rows, n);
+  for (int s = 0; s < a.shard_count; ++s) {
+    const void* ptrs[4] = {a.q_shards[s], a.k_shards[s], a.v_shards[s], a.out_shards[s]};
+    for (const void* ptr : ptrs)
+      if (!ptr || (reinterpret_cast<uintptr_t>(ptr) & 15))
+        return fail(DA_EINVAL, "%s: shard %d has a null or unaligned buffer", what, s);
+  }
+  return DA_OK;
+}
+
+// Point q/k/v/out at shard 0 when sharded (the plain pointers are unused then;
+// this keeps the null / alignment checks meaningful).
+static da_attn_args with_shard_bases(const da_attn_args& a) {
+  da_attn_args b = a;
+  if (a.layout == DA_LAYOUT_ORIGINAL && a.shard_count > 1) {
+    b.q = a.q_shards[0]; b.k = a.k_shards[0]; b.v = a.v_shards[0]; b.out = a.out_shards[0];
+  }
+  return b;
+}
+
 static int check_attn(const da_attn_args* a, const da_grid* grid) {
   if (!a || !grid_ok(grid)) return fail(DA_EINVAL, "block_sparse_fwd: bad arguments");
+  if (int rc = check_shards(*a, grid, "block_sparse_fwd")) return rc;
   if (!a->q || !a->k || !a->v || !a->out || !a->row_ptr || !a->col_idx)
     return fail(DA_EINVAL, "block_sparse_fwd: null buffer");
   if (a->heads < 1 || a->d < 1 || a->dv < 1) return fail(DA_EINVAL, "block_sparse_fwd: bad sizes");
@@ -203,7 +278,9 @@ static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, 
                                  int kblk, bool tiles_ready);
 
 int da_block_sparse_fwd(const da_attn_args* args, const da_grid* grid, void* stream) {
-  return block_sparse_fwd_impl(args, grid, stream, nullptr, 0, false);
+  if (!args) return fail(DA_EINVAL, "block_sparse_fwd: bad arguments");
+  const da_attn_args a = with_shard_bases(*args);
+  return block_sparse_fwd_impl(&a, grid, stream, nullptr, 0, false);
 }
 
 static int block_sparse_fwd_impl(const da_attn_args* args, const da_grid* grid, void* stream, const float* kpart,
@@ -300,8 +377,9 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {
   if (!pa || !grid_ok(grid)) return fail(DA_EINVAL, "sparse_attention: bad arguments");
-  const da_attn_args& a = pa->attn;
+  const da_attn_args a = with_shard_bases(pa->attn);
   if (a.layout != DA_LAYOUT_ORIGINAL) return fail(DA_EINVAL, "sparse_attention: inputs must be in original order");
+  if (int rc = check_shards(a, grid, "sparse_attention")) return rc;
   if (!pa->workspace || !pa->row_ptr || !pa->col_idx || !pa->threshold || !pa->forced || !pa->kept)
     return fail(DA_EINVAL, "sparse_attention: null buffer");
   const bool divisible = grid->height % grid->patch_h == 0 && grid->width % grid->patch_w == 0;
@@ -322,12 +400,13 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
                      (reinterpret_cast<uintptr_t>(a.v) & 15) == 0;
   // (the averaging kernel also records the pooled rows' largest norms for the fp32 selection)
   if (kblk > 0) cudaMemsetAsync(w.pnorm, 0, sizeof(unsigned long long) * 2 * a.heads, st);
+  const da::Shards shards = da::make_shards(a);
   if ((rc = cuda_status(da::launch_pool2(a.q, a.q_head_stride, a.q_row_stride, w.qp, a.k, a.k_head_stride,
                                          a.k_row_stride, w.kp, a.heads, a.d, pa->pool_mode, g, st,
                                          kblk > 0 ? w.kpart : nullptr, tiles ? a.v : nullptr, a.v_head_stride,
                                          a.v_row_stride, tiles ? da::attn_tiles(w.attn, a.heads, g, 0) : nullptr,
                                          tiles ? da::attn_tiles(w.attn, a.heads, g, 1) : nullptr,
-                                         kblk > 0 ? w.pnorm : nullptr),
+                                         kblk > 0 ? w.pnorm : nullptr, &shards),
                         "pool")))
     return rc;
   // K3: per-head selection on raw logits (the default) runs on fp32 draft

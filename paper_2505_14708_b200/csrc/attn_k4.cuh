@@ -44,6 +44,7 @@ struct Params {
   int* work;
   uint64_t pol_kv, pol_q, pol_o;
   long long* trace;  // LH_PROF output ([CTA][32]) or null
+  Shards sh;         // sequence shards of Q / out (original layout), or unsplit
 };
 
 struct Item {

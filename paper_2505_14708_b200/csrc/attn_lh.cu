@@ -218,7 +218,8 @@ DA_DEV int4 take_info(const int4* info, uint64_t* empty, int i, int lane) {
   return e;
 }
 
-__global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params p) {
+template <bool SPLIT>  // SPLIT: Q / out rows in sequence shards (Params::sh)
+__global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
   SmemAux& aux = *reinterpret_cast<SmemAux*>(smem + SMEM_END);
@@ -335,7 +336,9 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
           // no kept key region: the region's output rows are zero
           for (int e = lane; e < P * (D / 8); e += 32) {
             const long long row = token_row(p, rec.x, e / (D / 8));
-            if (row >= 0) reinterpret_cast<uint4*>(p.out + rec.w * p.oh + row * p.orow)[e % (D / 8)] = make_uint4(0, 0, 0, 0);
+            if (row >= 0)
+              reinterpret_cast<uint4*>(shard_at<SPLIT>(p.sh, SH_O, p.out, rec.w * p.oh, row, p.orow))[e % (D / 8)] =
+                  make_uint4(0, 0, 0, 0);
           }
         }
         const int slot = claimed % IR;
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
     auto issue_q = [&](const Item& itm) {
       const long long qrow = token_row(p, itm.i, r);
       if (qrow >= 0) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.q + itm.h * p.qh + qrow * p.qr) + wg * 8;
+        const uint4* src = reinterpret_cast<const uint4*>(shard_at<SPLIT>(p.sh, SH_Q, p.q, itm.h * p.qh, qrow, p.qr)) + wg * 8;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint4 w = ldg128_hint(src + k, p.pol_q);
@@ -742,7 +745,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const Params
         w[k / 2] = pack_bf16(a0 * inv, a1 * inv);
       }
       if (row >= 0) {
-        uint4* dst = reinterpret_cast<uint4*>(p.out + itm.h * p.oh + row * p.orow + wg * 64 + myhalf * 32);
+        uint4* dst = reinterpret_cast<uint4*>(shard_at<SPLIT>(p.sh, SH_O, p.out, itm.h * p.oh, row, p.orow) + wg * 64 + myhalf * 32);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           stg128_hint(dst + k, make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]), p.pol_o);
@@ -784,16 +787,17 @@ struct KvTileArgs {
   long long hs[2], rs[2];
   uint8_t* out[2];
   int layout;
+  Shards sh;  // sequence shards of K / V (original layout), or unsplit
 };
-__global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, RegionDecoder dec) {
+__global__ void __launch_bounds__(256) kv_tile_kernel(const __grid_constant__ KvTileArgs a, Geo g, RegionDecoder dec) {
 #ifdef DA_K4_TK
   __shared__ __align__(16) uint16_t vs[P * D];  // V^T (experimental transposed K4): V rows, transposed on the way out
 #endif
   const int j = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
   const RegionXY rc = dec(j);
   // z selects K (0) or V (1) without dynamic parameter indexing (no local-memory copy)
-  const uint4* src = reinterpret_cast<const uint4*>(z ? a.x[1] + h * a.hs[1] : a.x[0] + h * a.hs[0]);
-  const long long rs8 = (z ? a.rs[1] : a.rs[0]) / 8;
+  const __nv_bfloat16* xz = z ? a.x[1] : a.x[0];
+  const long long ho = h * (z ? a.hs[1] : a.hs[0]), rs = z ? a.rs[1] : a.rs[0];
   uint8_t* dst = (z ? a.out[1] : a.out[0]) + ((long long)h * g.g + j) * TILE;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -806,7 +810,9 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
       const int u = r >> 3, v = r & 7;
       row = (rc.y0 + u < g.H && rc.x0 + v < g.W) ? ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v : -1;
     }
-    const uint4 val = row >= 0 ? __ldg(src + row * rs8 + c) : make_uint4(0, 0, 0, 0);
+    const uint4 val =
+        row >= 0 ? __ldg(reinterpret_cast<const uint4*>(shard_addr(a.sh, z ? SH_V : SH_K, xz, ho, row, rs)) + c)
+                 : make_uint4(0, 0, 0, 0);
 #ifndef DA_K4_TK
     *reinterpret_cast<uint4*>(dst + kv_tile_offset_grouped(r, c >> 3, c & 7)) = val;
 #else
@@ -834,13 +840,12 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(KvTileArgs a, Geo g, Regio
 // behind the fixed softmax offset), for callers without the pooling pass.
 // grid (KBLK, heads), 256 threads: each warp reads two 256-byte rows per load.
 __global__ void __launch_bounds__(256) key_norm_kernel(const __nv_bfloat16* __restrict__ k, long long kh, long long kr,
-                                                       long long rows, float* __restrict__ kpart) {
+                                                       long long rows, float* __restrict__ kpart,
+                                                       const __grid_constant__ Shards sh) {
   __shared__ float red[8];
   const int h = blockIdx.y;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int sub = lane >> 4, c = lane & 15;
-  const uint4* base = reinterpret_cast<const uint4*>(k + h * kh);
-  const long long kr8 = kr / 8;
   const long long step = (long long)KBLK * 8 * 2;
   float mx = 0.f;
   for (long long r0 = ((long long)blockIdx.x * 8 + w) * 2 + sub; r0 < rows; r0 += 4 * step) {
@@ -848,7 +853,8 @@ __global__ void __launch_bounds__(256) key_norm_kernel(const __nv_bfloat16* __re
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const long long rr = r0 + u * step;
-      v[u] = rr < rows ? __ldg(base + rr * kr8 + c) : make_uint4(0, 0, 0, 0);
+      v[u] = rr < rows ? __ldg(reinterpret_cast<const uint4*>(shard_addr(sh, SH_K, k, h * kh, rr, kr)) + c)
+                       : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -914,6 +920,9 @@ bool tc_supported(const da_attn_args& a, const Geo& g) {
   if (a.layout == DA_LAYOUT_ORIGINAL && (g.ph != 8 || g.pw != 8)) return false;
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   if (!al16(a.q) || !al16(a.k) || !al16(a.v) || !al16(a.out)) return false;
+  if (a.layout == DA_LAYOUT_ORIGINAL && a.shard_count > 1)
+    for (int s = 0; s < a.shard_count; ++s)
+      if (!al16(a.q_shards[s]) || !al16(a.k_shards[s]) || !al16(a.v_shards[s]) || !al16(a.out_shards[s])) return false;
   if (a.q_row_stride % 8 || a.k_row_stride % 8 || a.v_row_stride % 8) return false;
   if (a.q_head_stride % 8 || a.k_head_stride % 8 || a.v_head_stride % 8) return false;
   if (a.o_row_stride % 8 || a.o_head_stride % 8) return false;
@@ -941,6 +950,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   p.geo = g;
   p.dec = make_decoder(g);
   p.per_head = make_fastdiv((uint32_t)g.g);
+  p.sh = make_shards(a);
 #ifndef LH_L2POL
 #define LH_L2POL 6  // bit 0: K/V tiles evict_last, bit 1: Q rows evict_first, bit 2: output rows evict_first (6: DRAM reads 11.0 -> 9.9 GB per HV720 launch, K4 -0.6 %, profiles/r02/l2pol)
 #endif
@@ -960,7 +970,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
     float* kp = reinterpret_cast<float*>(ws + ws_norms());
     const long long key_rows = a.layout == DA_LAYOUT_REORDERED ? g.n_pad : g.n_real;
     lhk::key_norm_kernel<<<dim3(lhk::KBLK, a.heads), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a.k),
-                                                                  a.k_head_stride, a.k_row_stride, key_rows, kp);
+                                                                  a.k_head_stride, a.k_row_stride, key_rows, kp, p.sh);
     p.kpart = kp;
     p.kblk = lhk::KBLK;
   }
@@ -984,6 +994,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
     ta.out[0] = attn_tiles(a.workspace, a.heads, g, 0);
     ta.out[1] = attn_tiles(a.workspace, a.heads, g, 1);
     ta.layout = a.layout;
+    ta.sh = p.sh;
     lhk::kv_tile_kernel<<<dim3(g.g, a.heads, 2), 256, 0, st>>>(ta, g, p.dec);
   }
   p.kt = attn_tiles(a.workspace, a.heads, g, 0);
@@ -992,13 +1003,18 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   const long long items = (long long)a.heads * g.g;
   const int grid = (int)(items < sms ? items : sms);
 #ifdef DA_K4_TK
-  if (attn_uses_tk()) {
+  if (attn_uses_tk() && p.sh.n <= 1) {  // (the experiment does not address shards)
     if ((e = launch_tk_kernel(p, grid, st)) != cudaSuccess) return e;
   } else
 #endif
   {
-    if ((e = ensure_smem_optin((const void*)lhk::sparse_attn_lh_kernel, lhk::SMEM_ALLOC)) != cudaSuccess) return e;
-    lhk::sparse_attn_lh_kernel<<<grid, lhk::THREADS, lhk::SMEM_ALLOC, st>>>(p);
+    if (p.sh.n > 1) {
+      if ((e = ensure_smem_optin((const void*)lhk::sparse_attn_lh_kernel<true>, lhk::SMEM_ALLOC)) != cudaSuccess) return e;
+      lhk::sparse_attn_lh_kernel<true><<<grid, lhk::THREADS, lhk::SMEM_ALLOC, st>>>(p);
+    } else {
+      if ((e = ensure_smem_optin((const void*)lhk::sparse_attn_lh_kernel<false>, lhk::SMEM_ALLOC)) != cudaSuccess) return e;
+      lhk::sparse_attn_lh_kernel<false><<<grid, lhk::THREADS, lhk::SMEM_ALLOC, st>>>(p);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   // rows whose fixed softmax offset underflowed: redo their regions exactly

@@ -27,6 +27,7 @@ struct PortableArgs {
   int mask_h;  // 1 = per-head masks, 0 = head 0's mask for all heads
   int kc;      // key rows per chunk (portable_key_chunk)
   Geo geo;
+  Shards sh;   // sequence shards (original layout), or unsplit
 };
 
 // row of token (region, offset) in the caller's tensor; -1 = not stored
@@ -64,7 +65,7 @@ __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) 
   for (int e = tid; e < p * d; e += nt) {
     int r = e / d, c = e - r * d;
     long long row = token_row(a, i, r);
-    Qs[e] = row >= 0 ? __bfloat162float(a.q[h * a.qh + row * a.qr + c]) : 0.f;
+    Qs[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_Q, a.q, h * a.qh + c, row, a.qr)) : 0.f;
   }
   for (int e = tid; e < p * dv; e += nt) O[e] = 0.f;
   for (int r = tid; r < p; r += nt) { M[r] = -INFINITY; L[r] = 0.f; }
@@ -77,12 +78,12 @@ __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) 
       for (int e = tid; e < nc * d; e += nt) {
         int r = e / d, c = e - r * d;
         long long row = token_row(a, j, c0 + r);
-        Ks[e] = row >= 0 ? __bfloat162float(a.k[h * a.kh + row * a.kr + c]) : 0.f;
+        Ks[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_K, a.k, h * a.kh + c, row, a.kr)) : 0.f;
       }
       for (int e = tid; e < nc * dv; e += nt) {
         int r = e / dv, c = e - r * dv;
         long long row = token_row(a, j, c0 + r);
-        Vs[e] = row >= 0 ? __bfloat162float(a.v[h * a.vh + row * a.vr + c]) : 0.f;
+        Vs[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_V, a.v, h * a.vh + c, row, a.vr)) : 0.f;
       }
       for (int r = tid; r < nc; r += nt) kval[r] = key_ok(a, j, c0 + r);
       __syncthreads();
@@ -144,18 +145,18 @@ __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) 
     if (row < 0) continue;
     float l = L[r];
     float o = l > 0.f ? O[e] / l : 0.f;
-    a.out[h * a.oh + row * a.orow + c] = __float2bfloat16_rn(o);
+    *shard_addr(a.sh, SH_O, a.out, h * a.oh + c, row, a.orow) = __float2bfloat16_rn(o);
   }
   __syncthreads();  // shared tiles are reused by the block's next region
 }
 
-__global__ void __launch_bounds__(256) portable_attn_kernel(PortableArgs a) {
+__global__ void __launch_bounds__(256) portable_attn_kernel(const __grid_constant__ PortableArgs a) {
   extern __shared__ float sm[];
   portable_region(a, blockIdx.x, blockIdx.y, sm);
 }
 
 // Regions listed in items[0 .. *count): the tcgen05 kernel's fallback rows.
-__global__ void __launch_bounds__(256) portable_list_kernel(PortableArgs a, const int* __restrict__ items,
+__global__ void __launch_bounds__(256) portable_list_kernel(const __grid_constant__ PortableArgs a, const int* __restrict__ items,
                                                             const int* __restrict__ count) {
   extern __shared__ float sm[];
   const int n = *count;
@@ -202,6 +203,7 @@ static PortableArgs portable_args(const da_attn_args& args, const Geo& geo) {
   a.mask_h = args.shared_mask ? 0 : 1;
   a.kc = portable_key_chunk(geo.p, args.d, args.dv);
   a.geo = geo;
+  a.sh = make_shards(args);
   return a;
 }
 

@@ -53,6 +53,59 @@ inline FastDiv make_fastdiv(uint32_t d) {
 }
 DA_DEV uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 
+// Token rows split over shard buffers (da_attn_args' sequence shards, possibly
+// peer GPUs' memory reached over NVLink): row r is local row r - s*rows of
+// shard s = r / rows. Kernels holding one take it as a __grid_constant__
+// parameter, so the table is indexed in the parameter bank (no local copy).
+struct Shards {
+  const char* base[4][DA_MAX_SHARDS];  // q, k, v, out
+  int n;                               // shard count; <= 1: unsplit (tables unused)
+  int rows;
+  FastDiv div;
+};
+enum { SH_Q = 0, SH_K = 1, SH_V = 2, SH_O = 3 };
+
+// Address of element (ho + row * rs) of tensor t: `plain` + that offset when
+// unsplit, else the same offset from row's shard with its local row.
+template <class T>
+DA_DEV T* shard_addr(const Shards& s, int t, T* plain, long long ho, long long row, long long rs) {
+  if (s.n <= 1) return plain + ho + row * rs;
+  const int part = (int)fdiv((uint32_t)row, s.div);
+  T* b = reinterpret_cast<T*>(const_cast<char*>(s.base[t][part]));
+  return b + ho + (row - (long long)part * s.rows) * rs;
+}
+
+// shard_addr when SPLIT, else the plain address (kernels instantiated both ways
+// keep the unsplit build's registers and code)
+template <bool SPLIT, class T>
+DA_DEV T* shard_at(const Shards& s, int t, T* plain, long long ho, long long row, long long rs) {
+  if constexpr (SPLIT) return shard_addr(s, t, plain, ho, row, rs);
+  else return plain + ho + row * rs;
+}
+
+inline Shards no_shards() {
+  Shards s = {};
+  s.n = 1;
+  s.rows = 1;
+  s.div = make_fastdiv(1);
+  return s;
+}
+
+inline Shards make_shards(const da_attn_args& a) {
+  Shards s;
+  s.n = a.layout == DA_LAYOUT_ORIGINAL && a.shard_count > 1 ? a.shard_count : 1;
+  s.rows = s.n > 1 ? (int)a.shard_rows : 1;
+  s.div = make_fastdiv((uint32_t)s.rows);
+  for (int i = 0; i < DA_MAX_SHARDS; ++i) {
+    const bool on = s.n > 1 && i < s.n;
+    s.base[SH_Q][i] = on ? static_cast<const char*>(a.q_shards[i]) : nullptr;
+    s.base[SH_K][i] = on ? static_cast<const char*>(a.k_shards[i]) : nullptr;
+    s.base[SH_V][i] = on ? static_cast<const char*>(a.v_shards[i]) : nullptr;
+    s.base[SH_O][i] = on ? static_cast<const char*>(a.out_shards[i]) : nullptr;
+  }
+  return s;
+}
+
 // Region coordinates: frame, first padded row and column of region i.
 struct RegionXY {
   int f, y0, x0;

@@ -9,6 +9,7 @@
 namespace da {
 
 struct Geo;
+struct Shards;
 
 cudaError_t launch_permute_in(const void* x, long long hs, long long rs, void* x_r, int heads, int d, const Geo& g,
                               cudaStream_t st);
@@ -24,7 +25,8 @@ cudaError_t launch_pool(const void* x, long long hs, long long rs, double* poole
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
                          long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
                          float* kpart, const void* x2 = nullptr, long long hs2 = 0, long long rs2 = 0,
-                         uint8_t* ktile = nullptr, uint8_t* vtile = nullptr, unsigned long long* pnorm = nullptr);
+                         uint8_t* ktile = nullptr, uint8_t* vtile = nullptr, unsigned long long* pnorm = nullptr,
+                         const Shards* sh = nullptr);  // sh: sequence shards of x0 / x1 / x2 (Q / K / V)
 // K / V tile buffers inside the attention workspace ([heads][g][16 KB] each),
 // in the GROUPED layout of kv_tile_offset_grouped (the K4 shared-memory image)
 uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which);

@@ -79,6 +79,7 @@ struct PoolSrc {
   double* out[2];
   uint8_t* tile[2];           // optional K / V region tiles for the attention kernel (z = 1, 2)
   unsigned long long* pnorm;  // optional [heads][2]: largest pooled row norm^2 of Q (0) and K (1), as double bits
+  Shards sh;                  // sequence shards of Q, K, V (z = 0, 1, 2), or unsplit
 };
 // element z of a 2- or 3-entry parameter array, selected without dynamic
 // indexing (which would copy the kernel parameters to local memory)
@@ -87,7 +88,7 @@ DA_DEV T pick3(const T (&a)[3], int z) { return z == 0 ? a[0] : (z == 1 ? a[1] :
 template <class T>
 DA_DEV T pick2(const T (&a)[2], int z) { return z == 0 ? a[0] : a[1]; }
 
-__global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode, Geo g) {
+__global__ void __launch_bounds__(256) pool_kernel(const __grid_constant__ PoolSrc src, int d, int mode, Geo g) {
   extern __shared__ double red[];  // [RG][d]
   const int i = blockIdx.x, h = blockIdx.y, z = blockIdx.z;
   const int d8 = d / 8;
@@ -95,7 +96,8 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode,
   const int tid = threadIdx.x;
   const int k = tid % d8, rg = tid / d8;
   const RegionCoord rc = region_coord(g, i);
-  const __nv_bfloat16* base = pick3(src.x, z) + h * pick3(src.hs, z);
+  const __nv_bfloat16* xz = pick3(src.x, z);
+  const long long ho = h * pick3(src.hs, z);
   const long long rs = pick3(src.rs, z);
   double acc[8];
   const double init = mode == 0 ? 0.0 : -INFINITY;
@@ -113,7 +115,8 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode,
       const int u = r / g.pw, v = r - u * g.pw;
       ok[i] = u < rc.vy && v < rc.vx;
       const long long row = ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
-      q[i] = ok[i] ? __ldg(reinterpret_cast<const uint4*>(base + row * rs) + k) : make_uint4(0, 0, 0, 0);
+      q[i] = ok[i] ? __ldg(reinterpret_cast<const uint4*>(shard_addr(src.sh, z, xz, ho, row, rs)) + k)
+                   : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolSrc src, int d, int mode,
     const int u = r / g.pw, v = r - u * g.pw;
     if (u >= rc.vy || v >= rc.vx) continue;
     const long long row = ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
-    uint4 q = __ldg(reinterpret_cast<const uint4*>(base + row * rs) + k);
+    uint4 q = __ldg(reinterpret_cast<const uint4*>(shard_addr(src.sh, z, xz, ho, row, rs)) + k);
     const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&q);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -282,11 +285,12 @@ cudaError_t launch_permute_out(const void* o_r, void* out, long long hs, long lo
 // the second tensor (K) the kernel also records the largest key row norm per
 // block (kpart[h][blockIdx.x]), the bound the attention kernel's fixed softmax
 // offset needs, so K is read once.
-template <int TPR>
+template <int TPR, bool SPLIT>  // SPLIT: rows in sequence shards (PoolSrc::sh)
 #ifndef DA_POOL_MINB
 #define DA_POOL_MINB 4  // 64 registers: 8 CTAs of 256 threads per SM (memory-latency bound at 2)
 #endif
-__global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src, int d, Geo g, float* __restrict__ kpart) {
+__global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(const __grid_constant__ PoolSrc src, int d, Geo g,
+                                                                   float* __restrict__ kpart) {
   constexpr int RPB = 256 / TPR;  // regions per block
   __shared__ float wmax[8];
   const int h = blockIdx.y, z = blockIdx.z;
@@ -295,8 +299,8 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
   const int k = threadIdx.x % TPR;
   const bool live = i < g.g;
   const RegionCoord rc = region_coord(g, live ? i : 0);
-  const uint4* base = reinterpret_cast<const uint4*>(pick3(src.x, z) + h * pick3(src.hs, z)) + k;
-  const long long rs8 = pick3(src.rs, z) / 8;
+  const __nv_bfloat16* xz = pick3(src.x, z);
+  const long long ho = h * pick3(src.hs, z), rs = pick3(src.rs, z);
   const bool norms = z == 1 && kpart != nullptr;
   // K / V tiles ([half][64 rows x 128 B], 128-byte swizzle, zero padding rows):
   // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
@@ -323,7 +327,8 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
       const int u = r / g.pw, v = r - u * g.pw;
       ok[t] = live && r < g.p && u < rc.vy && v < rc.vx;
       const long long row = ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v;
-      q[t] = ok[t] ? __ldg(base + row * rs8) : make_uint4(0, 0, 0, 0);
+      q[t] = ok[t] ? __ldg(reinterpret_cast<const uint4*>(shard_at<SPLIT>(src.sh, z, xz, ho, row, rs)) + k)
+                   : make_uint4(0, 0, 0, 0);
     }
     if (tdst != nullptr) {
 #ifndef DA_K4_TK
@@ -425,6 +430,18 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(PoolSrc src
   }
 }
 
+template <bool SPLIT>
+static void launch_pool_avg(int d, dim3 grid, const PoolSrc& src, const Geo& g, float* kp, cudaStream_t st) {
+  switch (d / 8) {
+    case 1: pool_avg_kernel<1, SPLIT><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+    case 2: pool_avg_kernel<2, SPLIT><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+    case 4: pool_avg_kernel<4, SPLIT><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+    case 8: pool_avg_kernel<8, SPLIT><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+    case 16: pool_avg_kernel<16, SPLIT><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+    default: pool_avg_kernel<32, SPLIT><<<grid, 256, 0, st>>>(src, d, g, kp); break;
+  }
+}
+
 int pool_norm_blocks(int d, const Geo& g) {
   const int tpr = d / 8;
   return (tpr >= 1 && tpr <= 32 && (tpr & (tpr - 1)) == 0 && d % 8 == 0) ? (g.g + 256 / tpr - 1) / (256 / tpr) : 0;
@@ -433,7 +450,8 @@ int pool_norm_blocks(int d, const Geo& g) {
 cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* out0, const void* x1, long long hs1,
                          long long rs1, double* out1, int heads, int d, int mode, const Geo& g, cudaStream_t st,
                          float* kpart, const void* x2, long long hs2, long long rs2, uint8_t* ktile,
-                         uint8_t* vtile, unsigned long long* pnorm) {
+                         uint8_t* vtile, unsigned long long* pnorm, const Shards* sh) {
+  const Shards shards = sh ? *sh : no_shards();
   if (mode == 0 && pool_norm_blocks(d, g) > 0 && rs0 % 8 == 0 && (!x1 || rs1 % 8 == 0)) {
     PoolSrc src;
     src.x[0] = static_cast<const __nv_bfloat16*>(x0);
@@ -446,16 +464,11 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
     src.tile[0] = tiles ? ktile : nullptr;
     src.tile[1] = tiles ? vtile : nullptr;
     src.pnorm = pnorm;
+    src.sh = shards;
     dim3 grid(pool_norm_blocks(d, g), heads, x1 ? (tiles ? 3 : 2) : 1);
     float* kp = x1 ? kpart : nullptr;
-    switch (d / 8) {
-      case 1: pool_avg_kernel<1><<<grid, 256, 0, st>>>(src, d, g, kp); break;
-      case 2: pool_avg_kernel<2><<<grid, 256, 0, st>>>(src, d, g, kp); break;
-      case 4: pool_avg_kernel<4><<<grid, 256, 0, st>>>(src, d, g, kp); break;
-      case 8: pool_avg_kernel<8><<<grid, 256, 0, st>>>(src, d, g, kp); break;
-      case 16: pool_avg_kernel<16><<<grid, 256, 0, st>>>(src, d, g, kp); break;
-      default: pool_avg_kernel<32><<<grid, 256, 0, st>>>(src, d, g, kp); break;
-    }
+    if (shards.n > 1) launch_pool_avg<true>(d, grid, src, g, kp, st);
+    else launch_pool_avg<false>(d, grid, src, g, kp, st);
     return cudaGetLastError();
   }
   if (kpart) return cudaErrorInvalidValue;  // norms only on the fast path
@@ -465,6 +478,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
   src.hs[0] = hs0; src.rs[0] = rs0; src.out[0] = out0;
   src.x[1] = static_cast<const __nv_bfloat16*>(x1 ? x1 : x0);
   src.hs[1] = x1 ? hs1 : hs0; src.rs[1] = x1 ? rs1 : rs0; src.out[1] = x1 ? out1 : out0;
+  src.sh = shards;
   const int d8 = d / 8;
   int rg = 256 / d8;
   if (rg < 1) rg = 1;
@@ -482,7 +496,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
 cudaError_t launch_pool(const void* x, long long hs, long long rs, double* pooled, int heads, int d, int mode,
                         const Geo& g, cudaStream_t st) {
   return launch_pool2(x, hs, rs, pooled, nullptr, 0, 0, nullptr, heads, d, mode, g, st, nullptr, nullptr, 0, 0,
-                      nullptr, nullptr);
+                      nullptr, nullptr, nullptr, nullptr);
 }
 
 cudaError_t launch_draft_scores(const double* qp, const double* kp, double* scores, int heads, int g, int d,

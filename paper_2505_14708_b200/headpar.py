@@ -22,6 +22,13 @@ the output):
   * the pipeline writes (n, heads_of_group, dv), whose per-destination row
     blocks are contiguous: it is the output all-to-all's send buffer as is.
 
+With ``transport="peer"`` there are no all-to-alls at all: every rank keeps
+its (n/P, H, d) shards in buffers the other ranks map (CUDA IPC,
+``PeerShards``), and the kernels of rank r read all ranks' rows of r's heads
+and write r's output rows into their owners' buffers over NVLink (the
+sharded C-ABI path, ``api.ShardTable``). Two stream-ordered barriers per
+call (a one-element all-reduce) order the writers and readers.
+
 ``shared_head_mask`` (sparse.py:281-297) needs the mean of every head's
 selection basis before any head can attend. The ranks fold the per-head fp64
 bases in global head order, as the reference's ``basis_sum + basis`` loop does
@@ -107,6 +114,90 @@ def _global(rank: int, group) -> int:
     return rank if group is None else dist.get_global_rank(group, rank)
 
 
+class PeerShards:
+    """This rank's sequence-shard buffers (q, k, v: (n/P, H, d); out:
+    (n/P, H, dv), bf16, one allocation) and the same buffers of every rank of
+    ``group`` mapped into this process through CUDA IPC (``da_ipc_export`` /
+    ``da_ipc_open``; peer access over NVLink between GPUs). A collective:
+    every rank constructs it with the same shape. ``close()`` (also a
+    collective) unmaps the peers' buffers."""
+
+    def __init__(self, rows: int, heads: int, d: int, dv: int, world: int, rank: int, group=None, device=None):
+        import ctypes
+
+        from ._lib import IPC_HANDLE_BYTES, check, lib
+
+        self.rows, self.heads, self.d, self.dv, self.world, self.rank, self.group = rows, heads, d, dv, world, rank, group
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.sizes = [rows * heads * d, rows * heads * d, rows * heads * dv, rows * heads * dv]
+        # one allocation, each buffer 256-byte aligned
+        self.offsets, off = [], 0
+        for n in self.sizes:
+            self.offsets.append(off)
+            off += -(-n * 2 // 256) * 256
+        self.arena = torch.empty(off, dtype=torch.uint8, device=dev)
+        views = [self.arena[o:o + n * 2].view(torch.bfloat16) for o, n in zip(self.offsets, self.sizes)]
+        self.q = views[0].view(rows, heads, d)
+        self.k = views[1].view(rows, heads, d)
+        self.v = views[2].view(rows, heads, dv)
+        self.out = views[3].view(rows, heads, dv)
+        handle = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        offset = ctypes.c_int64()
+        check(lib().da_ipc_export(self.arena.data_ptr(), handle, ctypes.byref(offset)), "ipc_export")
+        mine = (bytes(handle.raw), int(offset.value))
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        self._opened = []   # (base pointer, 0) of every mapping this process made
+        self.bases = []     # arena address of each rank, in this process
+        mapped = {}
+        for r, (h, o) in enumerate(everyone):
+            if r == rank:
+                self.bases.append(self.arena.data_ptr())
+                continue
+            if h not in mapped:
+                ptr = ctypes.c_void_p()
+                with torch.cuda.device(dev):
+                    check(lib().da_ipc_open(h, 0, ctypes.byref(ptr)), "ipc_open")
+                mapped[h] = ptr.value
+                self._opened.append(ptr.value)
+            self.bases.append(mapped[h] + o)
+        self._flag = torch.zeros(1, dtype=torch.float32, device=dev)
+
+    def table(self, h0: int, h1: int):
+        """api.ShardTable of heads [h0, h1) of every rank's shards."""
+        from .api import ShardTable
+
+        hd = self.heads
+        ptr = lambda t, h, last: tuple(b + self.offsets[t] + h * last * 2 for b in self.bases)
+        return ShardTable(ptr(0, h0, self.d), ptr(1, h0, self.d), ptr(2, h0, self.dv), ptr(3, h0, self.dv),
+                          self.rows, self.rows * self.world, h1 - h0, self.d, self.dv,
+                          (self.d, hd * self.d, self.d, hd * self.d, self.dv, hd * self.dv, self.dv, hd * self.dv))
+
+    def barrier(self):
+        """Every rank's prior device work on its current stream is complete
+        (and its writes visible) before any rank's next device work: a
+        one-element all-reduce with NCCL (stream-ordered), else a host
+        barrier after a device synchronise (gloo, tests)."""
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def close(self):
+        from ._lib import check, lib
+
+        if self.arena is None:
+            return
+        self.barrier()  # nobody reads or writes the mappings any more
+        for base in self._opened:
+            check(lib().da_ipc_close(base, 0), "ipc_close")
+        self._opened = []
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # every peer unmapped this rank's arena before it is freed
+        self.arena = None
+
+
 class HeadParallelAttention:
     """padded_sparse_attention over a sequence-sharded (n/P, H, d) input.
 
@@ -118,12 +209,34 @@ class HeadParallelAttention:
 
     def __init__(self, plan: api.PadPlan, sparsity: float, world: int, rank: int, group=None,
                  scale=None, pool_mode="average", select_on="logits", force_row_keep=True,
-                 shared_head_mask=False, head_groups=2, compute=None):
+                 shared_head_mask=False, head_groups=2, compute=None, transport="nccl"):
+        if transport not in ("nccl", "peer"):
+            raise ValueError(f"transport must be 'nccl' or 'peer', got {transport!r}")
         self.plan, self.sparsity, self.world, self.rank, self.group = plan, sparsity, world, rank, group
         self.scale, self.pool_mode, self.select_on, self.force = scale, pool_mode, select_on, force_row_keep
         self.shared = shared_head_mask
         self.groups = head_groups
         self.compute = compute
+        # the shared-head mask needs every head's basis before any selection:
+        # it keeps the all-to-all schedule (_call_shared) under either transport
+        self.transport = transport
+        self._peer = None
+
+    def peer_buffers(self, rows: int, heads: int, d: int, dv: int) -> PeerShards:
+        """The transport="peer" buffers for (rows, heads, d) shards (made on
+        first use; a collective). A caller that writes its shards straight into
+        ``.q`` / ``.k`` / ``.v`` saves the copy-in."""
+        p = self._peer
+        if p is None or (p.rows, p.heads, p.d, p.dv) != (rows, heads, d, dv):
+            if p is not None:
+                p.close()
+            self._peer = PeerShards(rows, heads, d, dv, self.world, self.rank, self.group)
+        return self._peer
+
+    def close(self):
+        if self._peer is not None:
+            self._peer.close()
+            self._peer = None
 
     # ------------------------------------------------------------ collectives
     def _pack(self, x, h0, h1):
@@ -159,6 +272,8 @@ class HeadParallelAttention:
         n = nl * self.world
         scale = self.scale if self.scale is not None else api.head_dim_scale(d)
         groups = head_groups(hl, self.groups)
+        if self.transport == "peer" and not self.shared and self.compute is None:
+            return self._call_peer(q, k, v, scale, compute_events, k4_events)
         out = torch.empty((nl, heads, dv), dtype=torch.bfloat16, device=q.device)
         if self.shared:
             return self._call_shared(q, k, v, out, groups, scale, compute_events)
@@ -184,6 +299,32 @@ class HeadParallelAttention:
             out.view(nl, self.world, hl, dv)[:, :, h0:h1, :].copy_(recv.permute(1, 0, 2, 3))
         masks = [m for m in masks if m is not None]
         return out, (api._cat_masks(masks) if masks else None)
+
+    def _call_peer(self, q, k, v, scale, compute_events=None, k4_events=None):
+        """transport="peer": shards copied into the mapped buffers (unless the
+        caller wrote them there), a barrier, ONE pipeline call over all of
+        this rank's heads reading every rank's rows in place and writing the
+        output rows into their owners' buffers, a barrier. The returned output
+        shard is a copy (the buffers are reused by the next call)."""
+        nl, heads, d = q.shape
+        dv = v.shape[2]
+        hl = heads // self.world
+        pb = self.peer_buffers(nl, heads, d, dv)
+        for src, dst in ((q, pb.q), (k, pb.k), (v, pb.v)):
+            if src.data_ptr() != dst.data_ptr():
+                dst.copy_(src)
+        pb.barrier()                                  # every rank's shards are in place
+        ev = _record(compute_events)
+        k4 = None
+        if k4_events is not None:
+            k4 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            k4_events.append(k4)
+        h0 = self.rank * hl
+        mask = api._run_sharded(pb.table(h0, h0 + hl), self.plan, self.sparsity, scale, self.pool_mode,
+                                self.select_on, self.force, False, q.device, attn_events=k4)
+        _close(ev)
+        pb.barrier()                                  # every rank's output rows have landed
+        return pb.out.clone(), mask
 
     def _compute(self, qh, kh, vh, res, scale, k4_events=None):
         if self.compute is not None:

@@ -1,0 +1,52 @@
+"""Worker of test_gpu_shards.py::test_peer_transport_two_processes_one_gpu:
+one rank of HeadParallelAttention(transport="peer") on cuda:0 (all ranks share
+the GPU; gloo carries the IPC handles and the barriers). Each rank checks its
+output shard and masks against a single-process call and writes ok<rank>."""
+
+import os
+import sys
+from pathlib import Path
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import paper_2505_14708_b200 as da  # noqa: E402
+from paper_2505_14708_b200.headpar import HeadParallelAttention  # noqa: E402
+
+
+def main(out_dir: str) -> None:
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo")
+    plan = da.pad_plan(2, 45, 80, 8, 8) if world == 2 else da.pad_plan(3, 40, 80, 8, 8)
+    heads = 2 * world
+    n = plan.num_valid
+    assert n % world == 0
+    nl = n // world
+    g = torch.Generator(device="cuda").manual_seed(5)  # identical full inputs on every rank
+    q, k, v = (torch.randn(n, heads, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    ref = da.multi_head_sparse_attention(q, k, v, plan, 0.9, qkv_layout="nhd", return_details=True)
+    rows = slice(rank * nl, (rank + 1) * nl)
+    hp = HeadParallelAttention(plan, 0.9, world, rank, transport="peer")
+    for it in range(3):  # repeated calls reuse the mapped buffers
+        out, mask = hp(q[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous())
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref.output[rows]), f"rank {rank} call {it}: output differs"
+        hl = heads // world
+        for h in range(hl):
+            assert mask.head(h).bitmap_bytes() == ref.mask.head(rank * hl + h).bitmap_bytes()
+    # a caller that writes its shards straight into the mapped buffers
+    pb = hp.peer_buffers(nl, heads, 128, 128)
+    pb.q.copy_(q[rows]); pb.k.copy_(k[rows]); pb.v.copy_(v[rows])
+    out, _ = hp(pb.q, pb.k, pb.v)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref.output[rows])
+    hp.close()
+    Path(out_dir, f"ok{rank}").write_text("ok")
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
