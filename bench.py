@@ -7,9 +7,13 @@ One step = one attention call over all heads of the configuration (pool ->
 draft scores -> global top-fraction selection -> block-sparse attention, output
 in original token order). N = 1: inputs resident in HBM (value); the same call
 through the public API with pinned-host inputs and a host copy of the output
-(e2e). N > 1: inputs arrive sequence-sharded, NCCL all-to-all reshards to
-head-sharded, each rank runs its heads, all-to-all back (strong scaling: the
-call's total work is fixed). Inputs (2.2 GB for HV720) are larger than L2, so
+(e2e). N > 1: inputs arrive sequence-sharded and each rank runs its heads
+(strong scaling: the call's total work is fixed). --transport peer (default):
+the kernels read every rank's shard rows in place over NVLink (CUDA IPC) and
+write the output rows into their owners' shards, no all-to-all; it is checked
+bit-exact against the nccl transport on the first call and falls back to it
+on any failure. --transport nccl: NCCL all-to-alls reshard to head-sharded and
+back, overlapped with the compute by head groups. Inputs (2.2 GB for HV720) are larger than L2, so
 no L2 flush is needed between steps.
 
 The line also carries dense attention at the same shape (cuDNN / flash SDPA,
@@ -209,14 +213,16 @@ def run_reference(args, cfg, name):
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(name, cfg, n, head_sharded=False):
+def _config_dict(name, cfg, n, head_sharded=False, transport="nccl"):
     f, h, w, ph, pw, heads, d, sp = cfg
     return {"workload": f"{name}: {f}x{h}x{w} tokens ({f * h * w}), {heads} heads, d={d}, "
                         f"{ph}x{pw} pool, {int(sp * 100)}% sparsity",
             "frames": f, "height": h, "width": w, "patch": [ph, pw], "heads": heads, "head_dim": d,
             "sparsity": sp,
             "parallelism": ((f"head-sharded replicas x{n} (no collective)" if head_sharded else
-                             f"head-parallel x{n} (sequence-sharded inputs, NCCL all-to-all)") if n > 1
+                             (f"head-parallel x{n} (sequence-sharded inputs read in place over NVLink, no all-to-all)"
+                              if transport == "peer" else
+                              f"head-parallel x{n} (sequence-sharded inputs, NCCL all-to-all)")) if n > 1
                             else "single GPU"),
             "l2": "inputs (3 x heads x n x d bf16) exceed the 126 MB L2; no flush needed"}
 
@@ -238,10 +244,18 @@ def run_ours(args, cfg, name):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if rank == 0:
         build()
+    # DA_BENCH_SAME_GPU=1 (a code-path check on a one-GPU box, not a measurement):
+    # every rank on cuda:0, gloo, peer transport without the nccl cross-check
+    same_gpu = os.environ.get("DA_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)  # before NCCL: its communicator binds the current device
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         dist.barrier()
     f, h, w, ph, pw, heads, d, sp = cfg
     plan = da.pad_plan(f, h, w, ph, pw)
@@ -274,6 +288,9 @@ def run_ours(args, cfg, name):
         q, k, v = (torch.randn(nl, heads, d, device=dev, generator=gen, dtype=torch.float32).to(torch.bfloat16)
                    for _ in range(3))
         hp = HeadParallelAttention(plan, sp, world, rank, head_groups=args.head_groups)
+        transport_note = None
+        if args.transport == "peer":
+            hp, q, k, v, transport_note = _peer_transport(hp, q, k, v, dev, same_gpu)
         comp_ev = [[] for _ in range(args.steps)]
         k4_ev = [[] for _ in range(args.steps)]
         step_i = [0]
@@ -362,7 +379,8 @@ def run_ours(args, cfg, name):
             "vs_baseline": None, "dtype": "bf16",
             "data": ("synthetic (torch.randn gaussian, seeded)" if args.data == "gaussian" else
                      "synthetic (smooth per-frame bilinear fields + 0.1 noise, synth.py mode, torch RNG, seeded)"),
-            "config": _config_dict(name, cfg, world, head_sharded=world > 1 and args.head_sharded),
+            "config": _config_dict(name, cfg, world, head_sharded=world > 1 and args.head_sharded,
+                                   transport=hp.transport if collective else "nccl"),
             "effective_tflops_per_gpu": eff_flops / (ms * 1e-3) / 1e12 / world,
             "kept_blocks": kept_total,
             "roofline": {"bound": "tensor", "kernel": "sparse_attn_lh_kernel (K4)", "achieved": k4_tflops,
@@ -386,7 +404,11 @@ def run_ours(args, cfg, name):
                 "ms": floor_ms, "frac": floor_ms / k4_ms, "sm_mhz": clocks.result["sm_mhz"]}
         if a2a_ms is not None:  # all-to-all time NOT hidden under compute, per call, max over ranks
             line["collective_exposed_ms"] = a2a_ms
-            line["head_groups"] = args.head_groups
+            line["transport"] = hp.transport
+            if hp.transport == "nccl":
+                line["head_groups"] = args.head_groups
+            if transport_note:
+                line["transport_note"] = transport_note
         if e2e is not None:
             line["e2e"] = e2e
         if dense_ms is not None:
@@ -398,6 +420,8 @@ def run_ours(args, cfg, name):
             line["cpu_baseline"] = cpu_base
         print(json.dumps(line), flush=True)
     if world > 1:
+        if collective:
+            hp.close()  # unmap the peers' shard buffers (peer transport) before any rank frees its own
         dist.destroy_process_group()
 
 
@@ -427,6 +451,38 @@ def _smooth_inputs(plan, heads, d, dev, gen, field_scale=0.5, noise_scale=0.1):
     return real.reshape(heads, -1, d).to(torch.bfloat16).contiguous()
 
 
+def _peer_transport(hp, q, k, v, dev, same_gpu):
+    """Switch the head-parallel call to transport="peer" with the inputs in
+    the mapped shard buffers. Unless ``same_gpu``, the first peer call is
+    compared bit for bit with the nccl transport's (the same kernels on the
+    same rows: the results are identical); any failure on any rank keeps the
+    nccl transport. Returns (hp, q, k, v, note)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_14708_b200.headpar import HeadParallelAttention
+
+    nl, heads, d = q.shape
+    peer = HeadParallelAttention(hp.plan, hp.sparsity, hp.world, hp.rank, head_groups=hp.groups, transport="peer")
+    ok, note = 1, None
+    try:
+        pb = peer.peer_buffers(nl, heads, d, v.shape[2])
+        pb.q.copy_(q); pb.k.copy_(k); pb.v.copy_(v)
+        if not same_gpu:
+            a, _ = peer(pb.q, pb.k, pb.v)
+            b, _ = hp(q, k, v)
+            torch.cuda.synchronize()
+            if not torch.equal(a, b):
+                ok, note = 0, "peer output differed from the nccl transport's"
+    except Exception as e:  # noqa: BLE001 - reported in the JSON line
+        ok, note = 0, f"peer transport failed: {type(e).__name__}: {str(e)[:200]}"
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 1:
+        return peer, pb.q, pb.k, pb.v, None
+    return hp, q, k, v, note or "another rank's peer transport failed; nccl transport used"
+
+
 def _e2e_sharded(hp, shape, dev, args, world):
     """N > 1: each rank's sequence shard starts in pinned host memory; upload,
     the head-parallel call (two NCCL all-to-alls around the pipeline) and the
@@ -437,9 +493,16 @@ def _e2e_sharded(hp, shape, dev, args, world):
     host = [torch.randn(*shape, dtype=torch.float32).to(torch.bfloat16).pin_memory() for _ in range(3)]
     out_host = torch.empty(*shape, dtype=torch.bfloat16).pin_memory()
 
+    pb = hp.peer_buffers(*shape[:3], shape[2]) if hp.transport == "peer" else None
+
     def once():
-        qd, kd, vd = (x.to(dev, non_blocking=True) for x in host)
-        o, _ = hp(qd, kd, vd)
+        if pb is not None:  # the shard lands straight in the mapped buffers
+            for x, buf in zip(host, (pb.q, pb.k, pb.v)):
+                buf.copy_(x, non_blocking=True)
+            o, _ = hp(pb.q, pb.k, pb.v)
+        else:
+            qd, kd, vd = (x.to(dev, non_blocking=True) for x in host)
+            o, _ = hp(qd, kd, vd)
         out_host.copy_(o, non_blocking=True)
 
     for _ in range(3):
@@ -540,6 +603,8 @@ def main():
                     help="synthetic input mode (synth.py): i.i.d. gaussian (primary) or smooth fields")
     ap.add_argument("--head-sharded", action="store_true",
                     help="N > 1: inputs arrive head-sharded (heads/N per rank): replicas, no collective")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: shard rows read in place over NVLink (peer) or NCCL all-to-alls (nccl)")
     ap.add_argument("--head-groups", type=int, default=3,
                     help="N > 1: head groups per rank (all-to-all / compute overlap)")
     args = ap.parse_args()

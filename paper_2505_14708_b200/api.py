@@ -542,6 +542,9 @@ def _launch_pipeline(a: DaAttnArgs, plan: PadPlan, sparsity, pool_mode, select_o
     pa.threshold, pa.forced, pa.kept = thr.data_ptr(), forced.data_ptr(), kept.data_ptr()
     pa.workspace = ws.data_ptr()
     if attn_events is not None:  # (begin, end) torch.cuda.Event pair around the K4 launch
+        for e in attn_events:
+            if not e.cuda_event:  # torch creates the CUDA event on its first record
+                e.record()
         pa.ev_attn_begin = attn_events[0].cuda_event
         pa.ev_attn_end = attn_events[1].cuda_event
     with torch.cuda.device(dev):

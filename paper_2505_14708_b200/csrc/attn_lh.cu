@@ -769,6 +769,9 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
     if (warp == 1) o[31] = clock64() - t_start;
   }
 #endif
+  // output rows stored into peer GPUs' shards: made visible system-wide before
+  // the kernel ends (the caller's cross-GPU barrier follows it)
+  if constexpr (SPLIT) __threadfence_system();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

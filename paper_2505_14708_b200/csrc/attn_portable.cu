@@ -147,6 +147,7 @@ __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) 
     float o = l > 0.f ? O[e] / l : 0.f;
     *shard_addr(a.sh, SH_O, a.out, h * a.oh + c, row, a.orow) = __float2bfloat16_rn(o);
   }
+  if (a.sh.n > 1) __threadfence_system();  // rows stored into peer GPUs' shards
   __syncthreads();  // shared tiles are reused by the block's next region
 }
 

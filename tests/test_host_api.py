@@ -177,3 +177,33 @@ def test_padded_block_sparse_attention_argument_errors():
         da.padded_block_sparse_attention(q, q, q, plan, None, qkv_layout="bhnd")
     with pytest.raises(ValueError, match="do not match"):
         da.padded_block_sparse_attention(q, q[:1], q, plan, None)
+
+
+def test_shard_table_struct_and_errors():
+    # the C-ABI shard table a sequence-sharded call passes (include/draftattn_b200.h
+    # da_attn_args.shard_*): pointers per shard, shared strides, rows per shard
+    from paper_2505_14708_b200 import _lib, api
+
+    t = api.ShardTable(q=(0x1000, 0x2000), k=(0x3000, 0x4000), v=(0x5000, 0x6000), out=(0x7000, 0x8000),
+                       rows=3600, n=7200, heads=4, d=128, dv=64,
+                       strides=(128, 3072, 128, 3072, 64, 1536, 64, 1536))
+    a = t.struct(0.125)
+    assert (a.shard_count, a.shard_rows, a.layout) == (2, 3600, _lib.LAYOUT_ORIGINAL)
+    assert list(a.q_shards)[:2] == [0x1000, 0x2000] and list(a.out_shards)[:2] == [0x7000, 0x8000]
+    assert a.q_shards[2] is None and len(a.v_shards) == _lib.MAX_SHARDS
+    assert (a.q_head_stride, a.q_row_stride, a.v_row_stride, a.o_head_stride) == (128, 3072, 1536, 64)
+    assert (a.heads, a.d, a.dv, a.scale) == (4, 128, 64, 0.125)
+    x = torch.zeros(10, 2, 8, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="shards"):
+        api._shard_table([x], [x], [x], [x])
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        api._shard_table([x, x], [x, x], [x, x], [x, x])
+
+
+def test_head_parallel_transport_argument():
+    from paper_2505_14708_b200.headpar import HeadParallelAttention
+
+    plan = da.pad_plan(2, 16, 16, 8, 8)
+    with pytest.raises(ValueError, match="transport"):
+        HeadParallelAttention(plan, 0.9, 2, 0, transport="shm")
+    assert HeadParallelAttention(plan, 0.9, 2, 0, transport="peer").transport == "peer"
