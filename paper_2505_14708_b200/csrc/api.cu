@@ -365,14 +365,14 @@ int32_t da_pipeline_launches(int32_t select_softmax, int32_t shared_head_mask) {
   // digit histograms (digit 0 fused into the GEMM on the per-head logits path)
   // and scans, candidate compaction + finish, tie counts + scan, mark, row
   // scan, collect, threshold, kept totals, packbits (bitmap requested);
-  // attention: pair plan, tcgen05 kernel, fallback list (key norms come from pooling)
+  // attention: region order, tcgen05 kernel, fallback list (key norms come from pooling)
   // (per-head logits path, average pooling: the fp32 guard-band selection — init, operand pack, GEMM,
   // 1 digit histogram + 2 scans, mark, band rescoring + finish, force, row scan, collect,
   // kept totals, packbits — followed by the gated fp64 launches, which exit
   // at once unless the fp32 path flagged a fallback)
   const int fused = (!select_softmax && !shared_head_mask) ? 1 : 0;
   const int fp64_path = 1 + (select_softmax ? 1 : 0) + (shared_head_mask ? 1 : 0) + 1 + (6 - fused) + 6 + 2 + 7 + 1;
-  return 1 + (fused ? 14 : 0) + fp64_path + 3;  // + pair plan, tcgen05 kernel, fallback list (tiles come from pooling)
+  return 1 + (fused ? 14 : 0) + fp64_path + 3;  // + region order, tcgen05 kernel, fallback list (tiles come from pooling)
 }
 
 int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* stream) {

@@ -1,8 +1,9 @@
-// K4 variant "lh" (DA_K4=lh): block-sparse FlashAttention forward with ONE
-// query region per item, two key regions per step (GEMM1 at N = 128), and the
-// two TMEM lane halves of the M = 64 tile used as an even / odd step pipeline.
+// K4, the lane-half kernel (the shipped tcgen05 path): block-sparse
+// FlashAttention forward with ONE query region per item, two key regions per
+// step (GEMM1 at N = 128), and the two TMEM lane halves of the M = 64 tile used
+// as an even / odd step pipeline.
 //
-// Same semantics as attn_pair.cu (reference sparse.py:88-166): per query
+// Semantics of the reference executor (sparse.py:88-166): per query
 // region, kept key regions in ascending order, padding keys masked, fixed
 // per-row softmax offset with the portable-kernel fallback for rows whose sum
 // underflows.
