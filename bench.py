@@ -464,23 +464,30 @@ def _peer_transport(hp, q, k, v, dev, same_gpu):
 
     nl, heads, d = q.shape
     peer = HeadParallelAttention(hp.plan, hp.sparsity, hp.world, hp.rank, head_groups=hp.groups, transport="peer")
-    ok, note = 1, None
-    try:
+    note = None
+
+    def agree(ok):  # every rank learns whether every rank succeeded (same collective sequence on all ranks)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        return int(flag.item()) == 1
+
+    ok = True
+    try:  # the mapping (one all-gather of IPC handles, then local opens)
         pb = peer.peer_buffers(nl, heads, d, v.shape[2])
         pb.q.copy_(q); pb.k.copy_(k); pb.v.copy_(v)
-        if not same_gpu:
-            a, _ = peer(pb.q, pb.k, pb.v)
-            b, _ = hp(q, k, v)
-            torch.cuda.synchronize()
-            if not torch.equal(a, b):
-                ok, note = 0, "peer output differed from the nccl transport's"
     except Exception as e:  # noqa: BLE001 - reported in the JSON line
-        ok, note = 0, f"peer transport failed: {type(e).__name__}: {str(e)[:200]}"
-    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    if int(flag.item()) == 1:
-        return peer, pb.q, pb.k, pb.v, None
-    return hp, q, k, v, note or "another rank's peer transport failed; nccl transport used"
+        ok, note = False, f"peer mapping failed: {type(e).__name__}: {str(e)[:200]}"
+    if not agree(ok):
+        return hp, q, k, v, note or "another rank's peer mapping failed; nccl transport used"
+    if not same_gpu:  # one call of each transport (both complete on every rank), compared bit for bit
+        a, _ = peer(pb.q, pb.k, pb.v)
+        b, _ = hp(q, k, v)
+        torch.cuda.synchronize()
+        ok = torch.equal(a, b)
+        if not agree(ok):
+            return hp, q, k, v, ("peer output differed from the nccl transport's" if not ok else
+                                 "another rank's peer output differed; nccl transport used")
+    return peer, pb.q, pb.k, pb.v, None
 
 
 def _e2e_sharded(hp, shape, dev, args, world):
