@@ -10,7 +10,10 @@ racecheck, synccheck, initcheck): small shapes of every device path.
   and the shared-head mask;
 * the portable executor (d = 64, 4x4 pool) and the d % 8 != 0 path;
 * the seams: reorder / restore, pool_tokens, draft_logits,
-  select_top_fraction, block_sparse_attention.
+  select_top_fraction, block_sparse_attention;
+* sequence shards (the kernels' SPLIT instantiations): the pipeline over 3
+  ragged row blocks, max pooling, the portable kernel and the cached-mask
+  executor.
 
 Each call is checked against the loose invariants the sanitizer run needs
 (finite, right shape); parity proper is tests/test_gpu_parity.py.
@@ -69,6 +72,23 @@ def main():
     m = da.select_top_fraction(s, 0.1, force_row_keep=True)
     o = da.block_sparse_attention(qr[0], kr[0], vr[0], m)
     check("block_sparse_attention", o)
+    # sequence shards: 3 row blocks (the last ragged), "nhd" views
+    def split(x, rows):
+        xt = x.transpose(0, 1)
+        return [xt[i:i + rows].contiguous() for i in range(0, xt.shape[0], rows)]
+
+    qs, ks, vs = split(q, 2500), split(k, 2500), split(v, 2500)
+    outs, mask = da.sharded_sparse_attention(qs, ks, vs, plan, 0.9, return_mask=True)
+    check("sharded pipeline", torch.cat(outs))
+    check("sharded executor (cached mask)", torch.cat(da.sharded_sparse_attention(qs, ks, vs, plan, 0.9, mask=mask)))
+    plan_m = da.pad_plan(2, 16, 24, 8, 8)
+    qm, km, vm = (rnd(plan_m.num_valid, 2, 128, seed=s_) for s_ in (7, 8, 9))
+    sp = lambda x: [x[i:i + 300].contiguous() for i in range(0, x.shape[0], 300)]
+    check("sharded max pooling", torch.cat(da.sharded_sparse_attention(sp(qm), sp(km), sp(vm), plan_m, 0.8,
+                                                                       pool_mode="max")))
+    plan_p = da.pad_plan(f2, h2, w2, 4, 4)
+    sp2 = lambda x: [t.contiguous() for t in x.transpose(0, 1).split(200)]
+    check("sharded portable", torch.cat(da.sharded_sparse_attention(sp2(q2), sp2(k2), sp2(v2), plan_p, 0.5)))
 
 
 if __name__ == "__main__":
