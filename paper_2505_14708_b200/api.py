@@ -225,6 +225,15 @@ class RegionMask:
                           self.col_idx[h:h + 1], self.thresholds[h:h + 1], self.forced[h:h + 1],
                           self.kept_counts[h:h + 1], single=True)
 
+    def head_range(self, h0: int, h1: int) -> "RegionMask":
+        """Masks h0 .. h1 - 1 of a stacked mask (views, no copies); a shared
+        (single) mask is returned as is."""
+        if self.single or self.heads == 1:
+            return self
+        return RegionMask(self.g, self.keep_ratio, None if self.packed is None else self.packed[h0:h1],
+                          self.row_ptr[h0:h1], self.col_idx[h0:h1], self.thresholds[h0:h1], self.forced[h0:h1],
+                          self.kept_counts[h0:h1], single=h1 - h0 == 1)
+
     @classmethod
     def from_kept(cls, kept, keep_ratio: float, threshold, forced_row_keeps=0, device=None) -> "RegionMask":
         """A GPU mask (executor lists + packed bitmap) from a boolean (g, g) or
@@ -724,6 +733,7 @@ class ShardTable:
         a.heads, a.d, a.dv, a.layout = self.heads, self.d, self.dv, _lib.LAYOUT_ORIGINAL
         a.scale = float(scale)
         a.shard_count, a.shard_rows = len(self.q), self.rows
+        a.q, a.k, a.v, a.out = self.q[0], self.k[0], self.v[0], self.out[0]  # (one shard: a plain tensor)
         for i in range(len(self.q)):
             a.q_shards[i], a.k_shards[i] = self.q[i], self.k[i]
             a.v_shards[i], a.out_shards[i] = self.v[i], self.out[i]

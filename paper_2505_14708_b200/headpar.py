@@ -257,9 +257,12 @@ class HeadParallelAttention:
         return bufs, works
 
     # ------------------------------------------------------------ call
-    def __call__(self, q, k, v, compute_events=None, k4_events=None):
+    def __call__(self, q, k, v, compute_events=None, k4_events=None, mask=None):
         """q, k, v: this rank's (n/P, H, d) sequence shards. Returns the
-        (n/P, H, dv) output shard and this rank's mask(s). ``compute_events``
+        (n/P, H, dv) output shard and this rank's mask(s). ``mask``: a mask
+        this rank returned before (its H/P heads, or one shared mask) to run
+        the executor alone (mask caching across denoising steps: no pooling or
+        selection). ``compute_events``
         (timing): a list that receives one (begin, end) CUDA event pair per
         compute phase on the current stream; the collectives run on NCCL's
         stream, so call time minus compute time is the exposed communication.
@@ -272,10 +275,12 @@ class HeadParallelAttention:
         n = nl * self.world
         scale = self.scale if self.scale is not None else api.head_dim_scale(d)
         groups = head_groups(hl, self.groups)
-        if self.transport == "peer" and not self.shared and self.compute is None:
-            return self._call_peer(q, k, v, scale, compute_events, k4_events)
+        if mask is not None and mask.heads not in (1, hl):
+            raise ValueError(f"mask of {mask.heads} heads does not fit this rank's {hl} heads")
+        if self.transport == "peer" and (not self.shared or mask is not None) and self.compute is None:
+            return self._call_peer(q, k, v, scale, compute_events, k4_events, mask)
         out = torch.empty((nl, heads, dv), dtype=torch.bfloat16, device=q.device)
-        if self.shared:
+        if self.shared and mask is None:
             return self._call_shared(q, k, v, out, groups, scale, compute_events)
 
         inflight = {0: self._issue_inputs(q, k, v, *groups[0])}
@@ -289,18 +294,25 @@ class HeadParallelAttention:
             hg = h1 - h0
             res = torch.empty((n, hg, dv), dtype=torch.bfloat16, device=q.device)
             ev = _record(compute_events)
-            masks.append(self._compute(qh.view(n, hg, d), kh.view(n, hg, d), vh.view(n, hg, dv), res, scale,
-                                       k4_events))
+            if mask is not None:  # cached mask: the executor alone
+                api._attend(qh.view(n, hg, d), kh.view(n, hg, d), vh.view(n, hg, dv), self.plan,
+                            mask.head_range(h0, h1), scale, qkv_layout="nhd", out_dev=res)
+                masks.append(mask.head_range(h0, h1) if mask.heads > 1 else None)
+            else:
+                masks.append(self._compute(qh.view(n, hg, d), kh.view(n, hg, d), vh.view(n, hg, dv), res, scale,
+                                           k4_events))
             _close(ev)
             recv = torch.empty((self.world, nl, hg, dv), dtype=torch.bfloat16, device=q.device)
             outs.append((h0, h1, recv, self._a2a(recv, res.view(self.world, nl, hg, dv))))
         for h0, h1, recv, work in outs:
             work.wait()
             out.view(nl, self.world, hl, dv)[:, :, h0:h1, :].copy_(recv.permute(1, 0, 2, 3))
+        if mask is not None:
+            return out, mask
         masks = [m for m in masks if m is not None]
         return out, (api._cat_masks(masks) if masks else None)
 
-    def _call_peer(self, q, k, v, scale, compute_events=None, k4_events=None):
+    def _call_peer(self, q, k, v, scale, compute_events=None, k4_events=None, mask=None):
         """transport="peer": shards copied into the mapped buffers (unless the
         caller wrote them there), a barrier, ONE pipeline call over all of
         this rank's heads reading every rank's rows in place and writing the
@@ -316,12 +328,12 @@ class HeadParallelAttention:
         pb.barrier()                                  # every rank's shards are in place
         ev = _record(compute_events)
         k4 = None
-        if k4_events is not None:
+        if k4_events is not None and mask is None:
             k4 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             k4_events.append(k4)
         h0 = self.rank * hl
         mask = api._run_sharded(pb.table(h0, h0 + hl), self.plan, self.sparsity, scale, self.pool_mode,
-                                self.select_on, self.force, False, q.device, attn_events=k4)
+                                self.select_on, self.force, False, q.device, attn_events=k4, mask=mask)
         _close(ev)
         pb.barrier()                                  # every rank's output rows have landed
         return pb.out.clone(), mask

@@ -43,7 +43,26 @@ def main(out_dir: str) -> None:
     out, _ = hp(pb.q, pb.k, pb.v)
     torch.cuda.synchronize()
     assert torch.equal(out, ref.output[rows])
+    # cached mask: the executor alone on the next step's inputs
+    q2 = (q.float() * 0.5).to(torch.bfloat16)
+    ref_exec = da.padded_block_sparse_attention(q2, k, v, plan, ref.mask, qkv_layout="nhd")
+    out, m2 = hp(q2[rows].contiguous(), k[rows].contiguous(), v[rows].contiguous(), mask=mask)
+    torch.cuda.synchronize()
+    assert m2 is mask and torch.equal(out, ref_exec[rows]), f"rank {rank}: cached-mask output differs"
     hp.close()
+    # the DiT call, sequence parallel: draft step, cached step, refresh
+    from paper_2505_14708_b200.dit import DraftAttention
+
+    f, hh, ww = plan.frames, plan.height, plan.width
+    att = DraftAttention(f, hh, ww, sparsity=0.9, mask_refresh_every=2, world=world, rank=rank, transport="peer")
+    qb, kb, vb = (x[rows].unsqueeze(0).contiguous() for x in (q, k, v))
+    o0 = att(qb, kb, vb, step=0)
+    assert torch.equal(o0[0], ref.output[rows]) and att.mode(1) == "cached"
+    o1 = att(q2[rows].unsqueeze(0).contiguous(), kb, vb, step=1)
+    assert torch.equal(o1[0], ref_exec[rows])
+    o2 = att(qb, kb, vb, step=2)
+    assert torch.equal(o2[0], ref.output[rows])
+    att.close()
     Path(out_dir, f"ok{rank}").write_text("ok")
     dist.destroy_process_group()
 

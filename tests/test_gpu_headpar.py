@@ -72,3 +72,33 @@ def test_head_parallel_shared_mask_equals_single_call(nccl):
         assert mask.bitmap_bytes() == ref.mask.bitmap_bytes()
         assert mask.kept_count == ref.mask.kept_count and mask.threshold == ref.mask.threshold
         assert (out.float() - ref.output.float()).abs().max().item() <= 4e-3
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_head_parallel_cached_mask_runs_the_executor(nccl, transport):
+    # mask caching across denoising steps: a returned mask fed back runs the
+    # executor alone (padded_block_sparse_attention with that mask)
+    import paper_2505_14708_b200 as da
+    from paper_2505_14708_b200.headpar import HeadParallelAttention
+
+    plan, q, k, v = _inputs(heads=4, seed=6)
+    hp = HeadParallelAttention(plan, 0.9, 1, 0, head_groups=2, transport=transport)
+    out, mask = hp(q, k, v)
+    ref = da.multi_head_sparse_attention(q, k, v, plan, 0.9, qkv_layout="nhd")
+    assert torch.equal(out, ref)
+    q2 = (q.float() * 0.5).to(torch.bfloat16)  # the next step's inputs, same mask
+    out2, mask2 = hp(q2, k, v, mask=mask)
+    assert mask2 is mask
+    assert torch.equal(out2, da.padded_block_sparse_attention(q2, k, v, plan, mask, qkv_layout="nhd"))
+    hp.close()
+
+
+def test_dit_world1_parallel_api_matches(nccl):
+    # DraftAttention's sequence-parallel branch at world 1 would be the plain
+    # call; world > 1 runs in tests/_peer_worker.py (two processes, one GPU)
+    from paper_2505_14708_b200.dit import DraftAttention
+
+    att = DraftAttention(3, 45, 80, sparsity=0.9, mask_refresh_every=2)
+    plan, q, k, v = _inputs(heads=2, seed=8)
+    o = att(q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0), step=0)
+    assert o.shape == (1, plan.num_valid, 2, 128) and att.mode(1) == "cached"
