@@ -383,7 +383,12 @@ def run_ours(args, cfg, name):
             cpu_base = {"value": cms, "unit": "ms/call", "cores": threads, "kind": kind, "sample": sample,
                         "extrapolated": True}
     if rank == 0:
-        launches = _lib.lib().da_pipeline_launches(0, 0) * args.steps
+        calls_per_step = 1  # pipeline calls per step: one per head group on the nccl transport
+        if collective and hp.transport == "nccl":
+            from paper_2505_14708_b200.headpar import head_groups as _hg
+
+            calls_per_step = len(_hg(hl, args.head_groups))
+        launches = _lib.lib().da_pipeline_launches(0, 0) * calls_per_step * args.steps
         line = {
             "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
