@@ -562,7 +562,8 @@ def test_selection_fast_path_decides_the_mask(kind, expect_fallback):
     assert dbg["selection_fallback"] == expect_fallback
 
 
-@pytest.mark.parametrize("dims", [(2, 16, 48, 4, 16, 128, 2, 12), (3, 24, 40, 8, 8, 64, 2, 13)])
+@pytest.mark.parametrize("dims", [(2, 16, 48, 4, 16, 128, 2, 12), (3, 24, 40, 8, 8, 64, 2, 13),
+                                  (2, 16, 48, 8, 16, 128, 2, 14), (2, 20, 40, 8, 16, 128, 2, 15)])
 def test_pipeline_other_pools_and_head_dims(dims):
     # 64-token regions that are not 8x8 (4x16), and d = 64 with 8x8 pools:
     # shapes the tcgen05 kernels do not take (the portable executor runs)
@@ -631,7 +632,7 @@ def test_mask_density_stats_vs_oracle():
         assert res.mask_stats[h] == got
 
 
-@pytest.mark.parametrize("d,dv,p", [(128, 64, 64), (64, 128, 16), (128, 32, 64)])
+@pytest.mark.parametrize("d,dv,p", [(128, 64, 64), (64, 128, 16), (128, 32, 64), (128, 128, 128)])
 def test_block_sparse_seam_dv_differs_from_d(d, dv, p):
     # test_sparse.py:193-202: value width differs from the key width
     g = 24

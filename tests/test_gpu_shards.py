@@ -46,6 +46,7 @@ CASES = [
     ((3, 45, 80, 8, 8), 4, 128, 3600, 0.85, "average", "logits", True, 1.0),     # shared head mask
     ((2, 16, 24, 8, 8), 2, 128, 300, 0.8, "max", "logits", False, 1.0),          # max pooling
     ((2, 12, 20, 4, 4), 3, 64, 170, 0.7, "average", "logits", False, 1.0),       # portable kernel (p = 16, d = 64)
+    ((2, 16, 48, 8, 16), 2, 128, 600, 0.8, "average", "logits", False, 1.0),    # portable, 8x16 pool (key chunks)
     ((2, 45, 80, 8, 8), 2, 128, 2500, 0.9, "average", "logits", False, 40.0),    # K4 fallback rows (portable list)
 ]
 
