@@ -45,6 +45,11 @@ struct Params {
   uint64_t pol_kv, pol_q, pol_o;
   long long* trace;  // LH_PROF output ([CTA][32]) or null
   Shards sh;         // sequence shards of Q / out (original layout), or unsplit
+  // 1: 128-token regions run as their two 64-token column halves (geo is the
+  // half-region geometry, attn_geo): item i_v = 2 i + half of region i takes
+  // region i's mask list, each kept key region j as ONE step of the two halves
+  // 2 j and 2 j + 1 (row_ptr / col_idx / cap stay the 128-token mask's)
+  int split;
 };
 
 struct Item {
@@ -62,9 +67,10 @@ DA_DEV int4 item_record(const Params& p, long long it, long long items) {
   const int g = p.geo.g;
   const int h = (int)fdiv((uint32_t)it, p.per_head);
   const int i = (int)(it - (long long)h * g);
-  const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (g + 1);
-  const int b = rp[i];
-  return make_int4(i, b, rp[i + 1] - b, h);
+  const int gm = g >> p.split;  // regions of the mask
+  const int* rp = p.row_ptr + (long long)(h * p.mask_h) * (gm + 1);
+  const int b = rp[i >> p.split];
+  return make_int4(i, b, rp[(i >> p.split) + 1] - b, h);
 }
 
 DA_DEV bool item_from_record(const Params& p, const int4 r, Item& o) {
@@ -72,7 +78,7 @@ DA_DEV bool item_from_record(const Params& p, const int4 r, Item& o) {
   o.h = r.w;
   o.i = r.x;
   o.list = p.col_idx + (long long)(r.w * p.mask_h) * p.cap + r.y;
-  o.n = r.z;
+  o.n = r.z << p.split;  // key regions of the item (split: two halves per mask entry)
   return true;
 }
 

@@ -156,8 +156,9 @@ static_assert(SMEM_ALLOC <= 227 * 1024, "shared memory budget");
 // puts the heaviest items first (the order within a count does not matter:
 // every region's output is computed independently). One block per head:
 // count histogram, block-wide exclusive scan, atomic placement.
+// split: every mask region is two items (its halves 2 i, 2 i + 1, Params::split).
 __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restrict__ row_ptr, int g, int mask_h,
-                                                            int4* __restrict__ meta) {
+                                                            int split, int4* __restrict__ meta) {
   extern __shared__ int bins[];  // [g + 1], key = g - count
   __shared__ int wsum[32];
   const int h = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restric
   const int nb = g + 1;
   for (int i = t; i < nb; i += blockDim.x) bins[i] = 0;
   __syncthreads();
-  for (int i = t; i < g; i += blockDim.x) atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1);
+  for (int i = t; i < g; i += blockDim.x) atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1 << split);
   __syncthreads();
   const int per = (nb + blockDim.x - 1) / blockDim.x;
   const int k0 = min(nb, t * per), k1 = min(nb, k0 + per);
@@ -198,9 +199,11 @@ __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restric
   }
   __syncthreads();
   for (int i = t; i < g; i += blockDim.x) {
-    const int pos = atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1);
+    const int pos = atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1 << split);
     const int b = rp[i];
-    meta[(long long)h * g + pos] = make_int4(i, b, rp[i + 1] - b, h);  // the item record (attn_k4.cuh)
+    int4* m = meta + ((long long)h * g << split) + pos;
+    for (int s = 0; s <= split; ++s)  // the item records (attn_k4.cuh)
+      m[s] = make_int4((i << split) + s, b, rp[i + 1] - b, h);
   }
 }
 
@@ -353,10 +356,11 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
       } else {
         if (!item_from_record(p, next_item(), itm)) break;
       }
-      const bool staged = is_k && itm.n <= LISTCAP;
+      const int nlist = itm.n >> p.split;  // mask entries of the item
+      const bool staged = is_k && nlist <= LISTCAP;
       if (staged) {
         __syncwarp();
-        for (int e = lane; e < itm.n; e += 32) aux.list[e] = __ldg(itm.list + e);
+        for (int e = lane; e < nlist; e += 32) aux.list[e] = __ldg(itm.list + e);
         __syncwarp();
       }
       if (lane == 0) {
@@ -366,8 +370,14 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
           int4 e;
           const int ii = kq % INFO;
           if (is_k) {
-            const int j0 = staged ? aux.list[2 * t] : __ldg(itm.list + 2 * t);
-            const int j1 = 2 * t + 1 < itm.n ? (staged ? aux.list[2 * t + 1] : __ldg(itm.list + 2 * t + 1)) : -1;
+            int j0, j1;
+            if (p.split) {  // both halves of mask entry t
+              j0 = 2 * (staged ? aux.list[t] : __ldg(itm.list + t));
+              j1 = j0 + 1;
+            } else {
+              j0 = staged ? aux.list[2 * t] : __ldg(itm.list + 2 * t);
+              j1 = 2 * t + 1 < itm.n ? (staged ? aux.list[2 * t + 1] : __ldg(itm.list + 2 * t + 1)) : -1;
+            }
             int fl = 1;
             if (bitmap ? (aux.ragged[j0 >> 5] >> (j0 & 31)) & 1 : key_mask(p, j0) != ~0ull) fl |= 4;
             if (j1 >= 0) {
@@ -755,7 +765,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
         const unsigned bal = __ballot_sync(0xffffffffu, bad && row >= 0 && lane < 16);
         if (bal != 0u && lane == 0) {
           const int slot = atomicAdd(p.fb_count, 1);
-          p.fb_items[slot] = itm.h * p.geo.g + itm.i;
+          p.fb_items[slot] = itm.h * (p.geo.g >> p.split) + (itm.i >> p.split);  // (split: the whole region)
         }
       }
       ++qi;
@@ -811,7 +821,7 @@ __global__ void __launch_bounds__(256) kv_tile_kernel(const __grid_constant__ Kv
     if (a.layout == DA_LAYOUT_REORDERED) {
       row = (long long)j * P + r;
     } else {
-      const int u = r >> 3, v = r & 7;
+      const int u = r / g.pw, v = r - u * g.pw;
       row = (rc.y0 + u < g.H && rc.x0 + v < g.W) ? ((long long)rc.f * g.H + rc.y0 + u) * g.W + rc.x0 + v : -1;
     }
     const uint4 val =
@@ -902,11 +912,30 @@ static size_t ws_items(int heads) { return ws_norms() + align256(sizeof(float) *
 static size_t ws_order(int heads, const Geo& g) { return ws_items(heads) + align256(sizeof(int) * 4 * (size_t)heads * g.g); }
 static size_t ws_tiles(int heads, const Geo& g) { return ws_order(heads, g) + align256(sizeof(int4) * (size_t)heads * g.g); }
 
-uint8_t* attn_tiles(void* ws, int heads, const Geo& g, int which) {
+// The geometry K4 runs on: 64-token regions as they are; 128-token regions
+// with an even pool width as their two column halves (Params::split), so the
+// paper's 8x16 pools run as 8x8 half-regions on the same kernel.
+bool attn_split(const Geo& g) { return g.p == 128 && g.pw % 2 == 0; }
+
+Geo attn_geo(const Geo& g) {
+  if (!attn_split(g)) return g;
+  Geo v = g;
+  v.pw = g.pw / 2;
+  v.Pw = 2 * g.Pw;  // halves of padding-only columns stay (all keys invalid, no output rows)
+  v.p = 64;
+  v.g = 2 * g.g;
+  return v;
+}
+
+uint8_t* attn_tiles(void* ws, int heads, const Geo& g0, int which) {
+  const Geo g = attn_geo(g0);
   return static_cast<uint8_t*>(ws) + ws_tiles(heads, g) + (size_t)which * heads * g.g * lhk::TILE;
 }
 
-size_t attn_workspace_size(int heads, const Geo& g) { return ws_tiles(heads, g) + 2 * (size_t)heads * g.g * lhk::TILE; }
+size_t attn_workspace_size(int heads, const Geo& g0) {
+  const Geo g = attn_geo(g0);
+  return ws_tiles(heads, g) + 2 * (size_t)heads * g.g * lhk::TILE;
+}
 
 // The lane-half kernel is the shipped K4; DA_K4_TK builds the transposed
 // TMEM-fed kernel instead (A/B experiments, tools/probes/k4_variants.py)
@@ -919,9 +948,8 @@ bool attn_uses_tk() {
 }
 
 bool tc_supported(const da_attn_args& a, const Geo& g) {
-  if (a.d != 128 || a.dv != 128 || g.p != 64) return false;
+  if (a.d != 128 || a.dv != 128 || (g.p != 64 && !attn_split(g))) return false;
   if (!(a.scale > 0.0)) return false;  // the fixed softmax offset bounds scale * |q| |k| from above
-  if (a.layout == DA_LAYOUT_ORIGINAL && (g.ph != 8 || g.pw != 8)) return false;
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   if (!al16(a.q) || !al16(a.k) || !al16(a.v) || !al16(a.out)) return false;
   if (a.layout == DA_LAYOUT_ORIGINAL && a.shard_count > 1)
@@ -933,9 +961,11 @@ bool tc_supported(const da_attn_args& a, const Geo& g) {
   return (long long)a.heads * g.g < (1ll << 31);
 }
 
-cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st, const float* kpart, int kblk,
+cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& gm, cudaStream_t st, const float* kpart, int kblk,
                            bool tiles_ready) {
+  const Geo g = attn_geo(gm);  // gm: the mask's geometry; g: K4's (half-regions when split)
   lhk::Params p;
+  p.split = attn_split(gm) ? 1 : 0;
   p.trace = g_trace;
   p.q = static_cast<const __nv_bfloat16*>(a.q);
   p.qh = a.q_head_stride;
@@ -980,9 +1010,9 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   }
   cudaError_t e;
   {
-    const size_t smem = sizeof(int) * ((size_t)g.g + 1);
+    const size_t smem = sizeof(int) * ((size_t)gm.g + 1);
     if (smem <= 200 * 1024 && ensure_smem_optin((const void*)lhk::region_order_kernel, (int)smem) == cudaSuccess) {
-      lhk::region_order_kernel<<<a.heads, 1024, smem, st>>>(a.row_ptr, g.g, a.shared_mask ? 0 : 1, meta);
+      lhk::region_order_kernel<<<a.heads, 1024, smem, st>>>(a.row_ptr, gm.g, a.shared_mask ? 0 : 1, p.split, meta);
       p.meta = meta;
     } else {
       cudaGetLastError();
@@ -1007,7 +1037,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
   const long long items = (long long)a.heads * g.g;
   const int grid = (int)(items < sms ? items : sms);
 #ifdef DA_K4_TK
-  if (attn_uses_tk() && p.sh.n <= 1) {  // (the experiment does not address shards)
+  if (attn_uses_tk() && p.sh.n <= 1 && !p.split) {  // (the experiment addresses neither shards nor halves)
     if ((e = launch_tk_kernel(p, grid, st)) != cudaSuccess) return e;
   } else
 #endif
@@ -1022,7 +1052,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& g, cudaStream_t st,
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   // rows whose fixed softmax offset underflowed: redo their regions exactly
-  return launch_portable_list(a, g, st, p.fb_items, p.fb_count, 2 * sms);
+  return launch_portable_list(a, gm, st, p.fb_items, p.fb_count, 2 * sms);
 }
 
 }  // namespace da

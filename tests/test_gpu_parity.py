@@ -379,12 +379,35 @@ def test_block_sparse_key_valid_and_dropped_rows():
     _close(out[0], ref)
 
 
-def test_tcgen05_matches_portable_kernel():
-    q, k, v, scores, _ = _seam_case(48, 64, 128, 3, 0.2, 17)
+@pytest.mark.parametrize("p,key_valid", [(64, False), (128, False), (128, True)])
+def test_tcgen05_matches_portable_kernel(p, key_valid):
+    # p = 128: the tcgen05 kernel runs the regions as their two 64-token halves
+    q, k, v, scores, kv = _seam_case(48, p, 128, 3, 0.2, 17 + p, key_valid=key_valid)
     mask = da.select_top_fraction(torch.from_numpy(scores).cuda(), 0.2, True)
-    a = da.block_sparse_attention(q, k, v, mask).float()
-    b = da.block_sparse_attention(q, k, v, mask, force_portable=True).float()
+    kv_t = None if kv is None else torch.from_numpy(kv).cuda()
+    a = da.block_sparse_attention(q, k, v, mask, key_valid=kv_t).float()
+    b = da.block_sparse_attention(q, k, v, mask, key_valid=kv_t, force_portable=True).float()
     assert (a - b).abs().max().item() <= 4e-3
+
+
+@pytest.mark.parametrize("dims", [(2, 16, 48, 8, 16), (3, 45, 80, 8, 16), (2, 20, 72, 8, 16), (2, 24, 40, 4, 16),
+                                  (2, 21, 40, 16, 4)])
+def test_pipeline_tcgen05_matches_portable_other_pools(dims):
+    # the paper's 8x16 pools (half-regions on tcgen05) and other 64-token pool
+    # shapes, padded grids included: same masks, outputs within the bf16 tolerance
+    from paper_2505_14708_b200 import api
+
+    plan = da.pad_plan(*dims)
+    g = torch.Generator(device="cuda").manual_seed(sum(dims))
+    q, k, v = (torch.randn(3, plan.num_valid, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    scale = da.head_dim_scale(128)
+    a, ma, _ = api._pipeline(q, k, v, plan, 0.85, scale, "average", "logits", True, False, "hnd")
+    b, mb, _ = api._pipeline(q, k, v, plan, 0.85, scale, "average", "logits", True, False, "hnd", force_portable=True)
+    for h in range(3):
+        assert ma.head(h).bitmap_bytes() == mb.head(h).bitmap_bytes()
+    # the stated output tolerance: one bf16 rounding apart is 7.8e-3 at |o| >= 1
+    assert (a.float() - b.float()).abs().max().item() <= 1e-2
+    assert torch.nn.functional.cosine_similarity(a.float().flatten(), b.float().flatten(), dim=0).item() >= 0.9999
 
 
 def test_extreme_logits_stay_finite():
