@@ -106,6 +106,7 @@ DA_DEV unsigned long long key_mask(const Params& p, int j) {
   const RegionXY rc = p.dec(j);
   const int vy = min(p.geo.ph, p.geo.H - rc.y0), vx = min(p.geo.pw, p.geo.W - rc.x0);
   if (vy == p.geo.ph && vx == p.geo.pw) return ~0ull;
+  if (vy <= 0 || vx <= 0) return 0ull;  // a half of a 128-token region can lie wholly in the padding
   const unsigned long long rowm = (1ull << vx) - 1ull;
   unsigned long long m = 0;
   for (int u = 0; u < vy; ++u) m |= rowm << (u * p.geo.pw);
