@@ -73,17 +73,25 @@ def _profile_traffic(config_name):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    The sampler process starts before the warm-up (``start()``) so it is
+    already emitting samples when the timed region opens; ``begin()`` /
+    ``end()`` mark the region in wall time and only samples stamped inside it
+    count (if the region is shorter than the 100 ms cadence, the first sample
+    after it opened stands in, flagged ``nearest``)."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.result = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -93,34 +101,48 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def __exit__(self, *exc):
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+        time.sleep(0.25)  # let the sample after the region arrive
+        self._collect()
+
+    def _collect(self):
+        import datetime
+
         self.result = None
         if self.proc is None:
-            return False
+            return
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except Exception:  # noqa: BLE001
             self.proc.kill()
             out = ""
-        sms, maxes, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        samples = []
         for line in out.strip().splitlines():
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) != 6:
+            if len(parts) != 7:
                 continue
             try:
-                sms.append(float(parts[0]))
-                maxes.append(float(parts[1]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                samples.append((ts, float(parts[1]), float(parts[2]),
+                                {n for n, v in zip(names, parts[3:]) if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for name, val in zip(names, parts[2:]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        if sms:
-            self.result = {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(maxes),
-                           "reasons": sorted(reasons), "samples": len(sms)}
-        return False
+        inside = [x for x in samples if self.t0 is not None and self.t0 <= x[0] <= self.t1]
+        nearest = False
+        if not inside:
+            after = [x for x in samples if self.t0 is not None and x[0] >= self.t0]
+            inside, nearest = after[:1], True
+        if inside:
+            self.result = {"sm_mhz": statistics.median(x[1] for x in inside), "sm_max_mhz": max(x[2] for x in inside),
+                           "reasons": sorted(set().union(*(x[3] for x in inside))), "samples": len(inside)}
+            if nearest:
+                self.result["nearest"] = True
 
 
 # --------------------------------------------------------------------------
@@ -304,6 +326,7 @@ def run_ours(args, cfg, name):
             step_i[0] += 1
             return hp(q, k, v, compute_events=comp_ev[s_], k4_events=k4_ev[s_])
 
+    clocks = ClockSampler(local).start()  # running (and sampling) before the timed region opens
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -318,17 +341,18 @@ def run_ours(args, cfg, name):
     # step boundaries: per-call times for the median (median of >= 20 calls)
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
     kept_total = None
-    with ClockSampler(local) as clocks:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        start.record()
-        for s in range(args.steps):
-            res = step(ev[s])
-            if s < args.steps - 1:
-                marks[s].record()
-        end.record()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.begin()
+    start.record()
+    for s in range(args.steps):
+        res = step(ev[s])
+        if s < args.steps - 1:
+            marks[s].record()
+    end.record()
+    torch.cuda.synchronize()
+    clocks.end()
     elapsed = start.elapsed_time(end)
     bounds = [start] + marks + [end]
     per_call = [bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps)]
@@ -394,7 +418,8 @@ def run_ours(args, cfg, name):
         line = {
             "metric": METRIC, "value": ms, "unit": "ms/call", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-            "ms_median": ms_median, "vs_baseline": None, "dtype": "bf16",
+            "ms_median": ms_median, "ms_calls": [round(x, 3) for x in per_call],
+            "vs_baseline": None, "dtype": "bf16",
             "data": ("synthetic (torch.randn gaussian, seeded)" if args.data == "gaussian" else
                      "synthetic (smooth per-frame bilinear fields + 0.1 noise, synth.py mode, torch RNG, seeded)"),
             "config": _config_dict(name, cfg, world, head_sharded=world > 1 and args.head_sharded,

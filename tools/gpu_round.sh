@@ -16,7 +16,9 @@ for s in $STAGES; do
     ref) timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_ref.log ;;
     sweep)
       for sp in 0.5 0.75 0.95; do timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu --sparsity $sp > gpurun_out/bench_hv720_$sp.log 2>&1; echo "sweep $sp rc=$?"; done
-      timeout 900 python bench.py --config wan720 --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_wan720.log 2>&1; echo "wan720 rc=$?" ;;
+      timeout 900 python bench.py --config wan720 --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_wan720.log 2>&1; echo "wan720 rc=$?"
+      timeout 900 python bench.py --config hv720_8x16 --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_hv720_8x16.log 2>&1; echo "8x16 rc=$?"
+      timeout 900 python bench.py --data smooth --steps 5 --warmup 3 --no-cpu --no-dense > gpurun_out/bench_hv720_smooth.log 2>&1; echo "smooth rc=$?" ;;
     seams) timeout 300 python tools/probes/seam_k1k5.py > gpurun_out/seams.log 2>&1; echo "seams rc=$?"; cat gpurun_out/seams.log | tail -1
       timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:permute -c 4 --csv --log-file gpurun_out/seams_ncu.csv python tools/probes/seam_k1k5.py --reps 1 > /dev/null 2>&1; echo "seams ncu rc=$?" ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-dense > gpurun_out/launches.log 2>&1; echo "launches rc=$?" ;;
