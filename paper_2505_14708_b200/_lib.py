@@ -16,6 +16,7 @@ LIB_NAME = "libdraftattn_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 DA_OK, DA_EINVAL, DA_ECUDA = 0, 1, 2
+ABI_VERSION = 101  # da_version() of the library these struct layouts match
 LAYOUT_REORDERED, LAYOUT_ORIGINAL = 0, 1
 MAX_SHARDS = 8
 IPC_HANDLE_BYTES = 64
@@ -103,6 +104,9 @@ def lib() -> ctypes.CDLL:
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
+        if handle.da_version() != ABI_VERSION:  # a stale build would misread the argument structs
+            raise RuntimeError(f"{path} has ABI version {handle.da_version()}, this package needs {ABI_VERSION}: "
+                               "rebuild it with `python -m paper_2505_14708_b200.build`")
         _LIB = handle
     return _LIB
 
