@@ -390,6 +390,28 @@ def test_tcgen05_matches_portable_kernel(p, key_valid):
     assert (a - b).abs().max().item() <= 4e-3
 
 
+@pytest.mark.parametrize("shared,select_on,qmul", [(True, "logits", 1.0), (False, "softmax", 1.0), (True, "softmax", 1.0),
+                                                   (False, "logits", 40.0)])
+def test_8x16_pools_shared_softmax_and_fallback_rows_vs_oracle(shared, select_on, qmul):
+    # 8x16 pools on the tcgen05 half-regions with the other selection options,
+    # and with large logits (rows whose fixed offset underflows are recomputed
+    # region-wise by the portable kernel at the 128-token geometry)
+    dims = (2, 20, 40, 8, 16)
+    plan = da.pad_plan(*dims)
+    rng = np.random.default_rng(int(qmul) + (2 if shared else 0) + (1 if select_on == "softmax" else 0))
+    q, k, v = (torch.from_numpy(rng.standard_normal((2, plan.num_valid, 128))).float().cuda() for _ in range(3))
+    q, k, v = (q * qmul).to(torch.bfloat16), k.to(torch.bfloat16), v.to(torch.bfloat16)
+    q64, k64, v64 = (x.double().cpu().numpy() for x in (q, k, v))
+    res = da.multi_head_sparse_attention(q, k, v, plan, 0.8, shared_head_mask=shared, select_on=select_on,
+                                         return_details=True)
+    ref = O.multi_head_sparse_attention(q64, k64, v64, *dims, 0.8, shared_head_mask=shared, select_on=select_on)
+    out = res.output.float().cpu().numpy()
+    for hh in range(2):
+        _close(out[hh], ref[hh], max_abs=1e-2 * max(1.0, float(np.abs(ref[hh]).max())))
+    assert torch.equal(da.multi_head_sparse_attention(q, k, v, plan, 0.8, shared_head_mask=shared,
+                                                      select_on=select_on), res.output)  # deterministic
+
+
 @pytest.mark.parametrize("dims", [(2, 16, 48, 8, 16), (3, 45, 80, 8, 16), (2, 20, 72, 8, 16), (2, 12, 20, 8, 16),
                                   (2, 13, 37, 8, 16), (2, 24, 40, 4, 16), (2, 21, 40, 16, 4)])
 def test_pipeline_tcgen05_matches_portable_other_pools(dims):

@@ -48,6 +48,8 @@ CASES = [
     ((2, 12, 20, 4, 4), 3, 64, 170, 0.7, "average", "logits", False, 1.0),       # portable kernel (p = 16, d = 64)
     ((2, 16, 48, 8, 16), 2, 128, 600, 0.8, "average", "logits", False, 1.0),    # portable, 8x16 pool (key chunks)
     ((2, 45, 80, 8, 8), 2, 128, 2500, 0.9, "average", "logits", False, 40.0),    # K4 fallback rows (portable list)
+    ((2, 20, 40, 8, 16), 2, 128, 500, 0.8, "average", "logits", False, 40.0),    # the same with 8x16 half-regions
+    ((2, 20, 40, 8, 16), 3, 128, 700, 0.8, "average", "softmax", True, 1.0),     # 8x16, shared mask, softmax basis
 ]
 
 
