@@ -913,3 +913,33 @@ def test_repeated_calls_bit_identical():
     ref_s = da.multi_head_sparse_attention(qs, ks, vs, small, 0.75)
     for _ in range(40):
         assert torch.equal(da.multi_head_sparse_attention(qs, ks, vs, small, 0.75), ref_s)
+
+
+@pytest.mark.gpu
+def test_pipeline_is_cuda_graph_capturable():
+    # no host synchronisation or allocation inside the C ABI: one call can be
+    # captured into a CUDA graph and replayed (a DiT loop with static buffers)
+    from paper_2505_14708_b200 import api
+
+    plan = da.pad_plan(3, 45, 80, 8, 8)
+    g = torch.Generator(device="cuda").manual_seed(12)
+    q, k, v = (torch.randn(4, plan.num_valid, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    run = lambda: api._pipeline(q, k, v, plan, 0.9, da.head_dim_scale(128), "average", "logits", True, False, "hnd",
+                                want_bitmap=False)[0]
+    ref = run().clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        out = run()
+    q.mul_(0.5)  # new contents of the static input buffer
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, run())
+    q.mul_(2.0)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
