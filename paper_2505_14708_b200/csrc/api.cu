@@ -396,8 +396,8 @@ int da_sparse_attention(const da_pipeline_args* pa, const da_grid* grid, void* s
   // (average pooling also records K's row-norm maxima for the attention kernel)
   // (and, on the tcgen05 shape, writes K and V as the attention kernel's region tiles)
   const int kblk = pa->pool_mode == 0 ? da::pool_norm_blocks(a.d, g) : 0;
-  // (64-token regions, or 128-token ones with an even pool width: K4's half-region tiles)
-  const bool tiles = kblk > 0 && a.d == 128 && a.dv == 128 && (g.p == 64 || (g.p == 128 && g.pw % 2 == 0)) &&
+  // (64-token regions, or 64 x 2^s-token ones as K4's column-part tiles)
+  const bool tiles = kblk > 0 && a.d == 128 && a.dv == 128 && da::region_parts_shift(g) >= 0 &&
                      a.v_row_stride % 8 == 0 && (reinterpret_cast<uintptr_t>(a.v) & 15) == 0 &&
                      da::tc_supported(a, g) && !a.force_portable;
   // (the averaging kernel also records the pooled rows' largest norms for the fp32 selection)

@@ -45,10 +45,11 @@ struct Params {
   uint64_t pol_kv, pol_q, pol_o;
   long long* trace;  // LH_PROF output ([CTA][32]) or null
   Shards sh;         // sequence shards of Q / out (original layout), or unsplit
-  // 1: 128-token regions run as their two 64-token column halves (geo is the
-  // half-region geometry, attn_geo): item i_v = 2 i + half of region i takes
-  // region i's mask list, each kept key region j as ONE step of the two halves
-  // 2 j and 2 j + 1 (row_ptr / col_idx / cap stay the 128-token mask's)
+  // s > 0: 64 x 2^s-token regions run as their 2^s column parts of 64 tokens
+  // (geo is the part geometry, attn_geo): item i_v = 2^s i + part of region i
+  // takes region i's mask list, each kept key region j as 2^(s-1) steps over
+  // the parts 2^s j .. 2^s j + 2^s - 1, two per step (row_ptr / col_idx / cap
+  // stay the mask's). s = 1: the paper's 8x16 pools as two 8x8 halves.
   int split;
 };
 

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(1024) region_order_kernel(const int* __restric
     const int pos = atomicAdd(&bins[g - min(g, rp[i + 1] - rp[i])], 1 << split);
     const int b = rp[i];
     int4* m = meta + ((long long)h * g << split) + pos;
-    for (int s = 0; s <= split; ++s)  // the item records (attn_k4.cuh)
+    for (int s = 0; s < (1 << split); ++s)  // the item records (attn_k4.cuh)
       m[s] = make_int4((i << split) + s, b, rp[i + 1] - b, h);
   }
 }
@@ -371,8 +371,9 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
           const int ii = kq % INFO;
           if (is_k) {
             int j0, j1;
-            if (p.split) {  // both halves of mask entry t
-              j0 = 2 * (staged ? aux.list[t] : __ldg(itm.list + t));
+            if (p.split) {  // parts 2 sub and 2 sub + 1 of mask entry t >> (split - 1)
+              const int e_ = t >> (p.split - 1), sub = t & ((1 << (p.split - 1)) - 1);
+              j0 = ((staged ? aux.list[e_] : __ldg(itm.list + e_)) << p.split) + 2 * sub;
               j1 = j0 + 1;
             } else {
               j0 = staged ? aux.list[2 * t] : __ldg(itm.list + 2 * t);
@@ -912,18 +913,17 @@ static size_t ws_items(int heads) { return ws_norms() + align256(sizeof(float) *
 static size_t ws_order(int heads, const Geo& g) { return ws_items(heads) + align256(sizeof(int) * 4 * (size_t)heads * g.g); }
 static size_t ws_tiles(int heads, const Geo& g) { return ws_order(heads, g) + align256(sizeof(int4) * (size_t)heads * g.g); }
 
-// The geometry K4 runs on: 64-token regions as they are; 128-token regions
-// with an even pool width as their two column halves (Params::split), so the
-// paper's 8x16 pools run as 8x8 half-regions on the same kernel.
-bool attn_split(const Geo& g) { return g.p == 128 && g.pw % 2 == 0; }
-
+// The geometry K4 runs on: 64-token regions as they are; 64 x 2^s-token
+// regions as their 2^s column parts (Params::split = s), so the paper's 8x16
+// pools run as 8x8 half-regions on the same kernel.
 Geo attn_geo(const Geo& g) {
-  if (!attn_split(g)) return g;
+  const int s = region_parts_shift(g);
+  if (s <= 0) return g;
   Geo v = g;
-  v.pw = g.pw / 2;
-  v.Pw = 2 * g.Pw;  // halves of padding-only columns stay (all keys invalid, no output rows)
+  v.pw = g.pw >> s;
+  v.Pw = g.Pw << s;  // parts of padding-only columns stay (all keys invalid, no output rows)
   v.p = 64;
-  v.g = 2 * g.g;
+  v.g = g.g << s;
   return v;
 }
 
@@ -948,7 +948,7 @@ bool attn_uses_tk() {
 }
 
 bool tc_supported(const da_attn_args& a, const Geo& g) {
-  if (a.d != 128 || a.dv != 128 || (g.p != 64 && !attn_split(g))) return false;
+  if (a.d != 128 || a.dv != 128 || region_parts_shift(g) < 0) return false;
   if (!(a.scale > 0.0)) return false;  // the fixed softmax offset bounds scale * |q| |k| from above
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   if (!al16(a.q) || !al16(a.k) || !al16(a.v) || !al16(a.out)) return false;
@@ -965,7 +965,7 @@ cudaError_t launch_tc_attn(const da_attn_args& a, const Geo& gm, cudaStream_t st
                            bool tiles_ready) {
   const Geo g = attn_geo(gm);  // gm: the mask's geometry; g: K4's (half-regions when split)
   lhk::Params p;
-  p.split = attn_split(gm) ? 1 : 0;
+  p.split = region_parts_shift(gm) > 0 ? region_parts_shift(gm) : 0;
   p.trace = g_trace;
   p.q = static_cast<const __nv_bfloat16*>(a.q);
   p.qh = a.q_head_stride;

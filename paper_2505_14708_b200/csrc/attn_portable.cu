@@ -4,9 +4,10 @@
 // (sparse.py:88-166): per query region, kept key regions in ascending order,
 // streaming softmax over valid keys, fully dropped rows -> 0.
 //
-// grid: (g, heads); block 256. Shared memory: the Q tile and the output
-// accumulator (fp32, p rows), per-row m / l, and one key chunk: K and V rows
-// (fp32) and the p x kc score tile.
+// grid: (g, heads); block 256. Shared memory: a chunk of qc query rows (Q and
+// the output accumulator, fp32), per-row m / l, and one key chunk: K and V
+// rows (fp32) and the qc x kc score tile. Large regions run as several query
+// chunks (each streams the region's keys again).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,7 +26,8 @@ struct PortableArgs {
   long long cap;
   const uint8_t* key_valid;
   int mask_h;  // 1 = per-head masks, 0 = head 0's mask for all heads
-  int kc;      // key rows per chunk (portable_key_chunk)
+  int kc;      // key rows per chunk (portable_chunks)
+  int qc;      // query rows per chunk
   Geo geo;
   Shards sh;   // sequence shards (original layout), or unsplit
 };
@@ -45,16 +47,16 @@ DA_DEV bool key_ok(const PortableArgs& a, int region, int r) {
 // Each kept key region is consumed in chunks of kc key rows so that large
 // regions (8x16 pools: p = 128) fit in shared memory with d = 128.
 __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) {
-  const int p = a.geo.p, d = a.d, dv = a.dv, kc = a.kc;
-  float* Qs = sm;                 // p*d
-  float* O = Qs + p * d;          // p*dv
-  float* M = O + p * dv;          // p
-  float* L = M + p;               // p
-  float* alpha = L + p;           // p
-  float* Ks = alpha + p;          // kc*d
+  const int p = a.geo.p, d = a.d, dv = a.dv, kc = a.kc, qc = a.qc;
+  float* Qs = sm;                 // qc*d
+  float* O = Qs + qc * d;         // qc*dv
+  float* M = O + qc * dv;         // qc
+  float* L = M + qc;              // qc
+  float* alpha = L + qc;          // qc
+  float* Ks = alpha + qc;         // kc*d
   float* Vs = Ks + kc * d;        // kc*dv
-  float* S = Vs + kc * dv;        // p*kc
-  int* kval = reinterpret_cast<int*>(S + p * kc);  // kc
+  float* S = Vs + kc * dv;        // qc*kc
+  int* kval = reinterpret_cast<int*>(S + qc * kc);  // kc
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int g = a.geo.g;
@@ -62,93 +64,96 @@ __device__ void portable_region(const PortableArgs& a, int i, int h, float* sm) 
   const int beg = rp[i], end = rp[i + 1];
   const int* cols = a.col_idx + (long long)(h * a.mask_h) * a.cap;
 
-  for (int e = tid; e < p * d; e += nt) {
-    int r = e / d, c = e - r * d;
-    long long row = token_row(a, i, r);
-    Qs[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_Q, a.q, h * a.qh + c, row, a.qr)) : 0.f;
-  }
-  for (int e = tid; e < p * dv; e += nt) O[e] = 0.f;
-  for (int r = tid; r < p; r += nt) { M[r] = -INFINITY; L[r] = 0.f; }
-  __syncthreads();
+  for (int q0 = 0; q0 < p; q0 += qc) {
+    const int nq = min(qc, p - q0);
+    for (int e = tid; e < nq * d; e += nt) {
+      int r = e / d, c = e - r * d;
+      long long row = token_row(a, i, q0 + r);
+      Qs[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_Q, a.q, h * a.qh + c, row, a.qr)) : 0.f;
+    }
+    for (int e = tid; e < nq * dv; e += nt) O[e] = 0.f;
+    for (int r = tid; r < nq; r += nt) { M[r] = -INFINITY; L[r] = 0.f; }
+    __syncthreads();
 
-  for (int t = beg; t < end; ++t) {
-    const int j = cols[t];
-    for (int c0 = 0; c0 < p; c0 += kc) {
-      const int nc = min(kc, p - c0);
-      for (int e = tid; e < nc * d; e += nt) {
-        int r = e / d, c = e - r * d;
-        long long row = token_row(a, j, c0 + r);
-        Ks[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_K, a.k, h * a.kh + c, row, a.kr)) : 0.f;
-      }
-      for (int e = tid; e < nc * dv; e += nt) {
-        int r = e / dv, c = e - r * dv;
-        long long row = token_row(a, j, c0 + r);
-        Vs[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_V, a.v, h * a.vh + c, row, a.vr)) : 0.f;
-      }
-      for (int r = tid; r < nc; r += nt) kval[r] = key_ok(a, j, c0 + r);
-      __syncthreads();
-      for (int e = tid; e < p * nc; e += nt) {
-        int r = e / nc, c = e - r * nc;
-        float s = -INFINITY;
-        if (kval[c]) {
-          float acc = 0.f;
-          for (int kk = 0; kk < d; ++kk) acc = fmaf(Qs[r * d + kk], Ks[c * d + kk], acc);
-          s = acc * a.scale;
+    for (int t = beg; t < end; ++t) {
+      const int j = cols[t];
+      for (int c0 = 0; c0 < p; c0 += kc) {
+        const int nc = min(kc, p - c0);
+        for (int e = tid; e < nc * d; e += nt) {
+          int r = e / d, c = e - r * d;
+          long long row = token_row(a, j, c0 + r);
+          Ks[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_K, a.k, h * a.kh + c, row, a.kr)) : 0.f;
         }
-        S[r * kc + c] = s;
-      }
-      __syncthreads();
-      // per-row online softmax update, one warp per row
-      const int lane = tid % 32, w = tid / 32, nw = nt / 32;
-      for (int r = w; r < p; r += nw) {
-        float mx = -INFINITY;
-        for (int c = lane; c < nc; c += 32) mx = fmaxf(mx, S[r * kc + c]);
+        for (int e = tid; e < nc * dv; e += nt) {
+          int r = e / dv, c = e - r * dv;
+          long long row = token_row(a, j, c0 + r);
+          Vs[e] = row >= 0 ? __bfloat162float(*shard_addr(a.sh, SH_V, a.v, h * a.vh + c, row, a.vr)) : 0.f;
+        }
+        for (int r = tid; r < nc; r += nt) kval[r] = key_ok(a, j, c0 + r);
+        __syncthreads();
+        for (int e = tid; e < nq * nc; e += nt) {
+          int r = e / nc, c = e - r * nc;
+          float s = -INFINITY;
+          if (kval[c]) {
+            float acc = 0.f;
+            for (int kk = 0; kk < d; ++kk) acc = fmaf(Qs[r * d + kk], Ks[c * d + kk], acc);
+            s = acc * a.scale;
+          }
+          S[r * kc + c] = s;
+        }
+        __syncthreads();
+        // per-row online softmax update, one warp per row
+        const int lane = tid % 32, w = tid / 32, nw = nt / 32;
+        for (int r = w; r < nq; r += nw) {
+          float mx = -INFINITY;
+          for (int c = lane; c < nc; c += 32) mx = fmaxf(mx, S[r * kc + c]);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        float mold = M[r];
-        float mnew = fmaxf(mold, mx);
-        float sum = 0.f;
-        if (mnew == -INFINITY) {  // chunk entirely invalid for this row: skip
-          for (int c = lane; c < nc; c += 32) S[r * kc + c] = 0.f;
-        } else {
-          for (int c = lane; c < nc; c += 32) {
-            float s = S[r * kc + c];
-            float pr = s == -INFINITY ? 0.f : expf(s - mnew);
-            S[r * kc + c] = pr;
-            sum += pr;
+          for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          float mold = M[r];
+          float mnew = fmaxf(mold, mx);
+          float sum = 0.f;
+          if (mnew == -INFINITY) {  // chunk entirely invalid for this row: skip
+            for (int c = lane; c < nc; c += 32) S[r * kc + c] = 0.f;
+          } else {
+            for (int c = lane; c < nc; c += 32) {
+              float s = S[r * kc + c];
+              float pr = s == -INFINITY ? 0.f : expf(s - mnew);
+              S[r * kc + c] = pr;
+              sum += pr;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          __syncwarp();  // every lane has read M[r] before lane 0 rewrites it
+          if (lane == 0) {
+            float al = (mold == -INFINITY) ? 0.f : expf(mold - mnew);
+            if (mnew == -INFINITY) al = 1.f;
+            alpha[r] = al;
+            L[r] = L[r] * al + sum;
+            M[r] = mnew;
           }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        __syncwarp();  // every lane has read M[r] before lane 0 rewrites it
-        if (lane == 0) {
-          float al = (mold == -INFINITY) ? 0.f : expf(mold - mnew);
-          if (mnew == -INFINITY) al = 1.f;
-          alpha[r] = al;
-          L[r] = L[r] * al + sum;
-          M[r] = mnew;
+        __syncthreads();
+        for (int e = tid; e < nq * dv; e += nt) {
+          int r = e / dv, c = e - r * dv;
+          float acc = O[e] * alpha[r];
+          for (int kk = 0; kk < nc; ++kk) acc = fmaf(S[r * kc + kk], Vs[kk * dv + c], acc);
+          O[e] = acc;
         }
+        __syncthreads();
       }
-      __syncthreads();
-      for (int e = tid; e < p * dv; e += nt) {
-        int r = e / dv, c = e - r * dv;
-        float acc = O[e] * alpha[r];
-        for (int kk = 0; kk < nc; ++kk) acc = fmaf(S[r * kc + kk], Vs[kk * dv + c], acc);
-        O[e] = acc;
-      }
-      __syncthreads();
     }
-  }
-  for (int e = tid; e < p * dv; e += nt) {
-    int r = e / dv, c = e - r * dv;
-    long long row = token_row(a, i, r);
-    if (row < 0) continue;
-    float l = L[r];
-    float o = l > 0.f ? O[e] / l : 0.f;
-    *shard_addr(a.sh, SH_O, a.out, h * a.oh + c, row, a.orow) = __float2bfloat16_rn(o);
+    for (int e = tid; e < nq * dv; e += nt) {
+      int r = e / dv, c = e - r * dv;
+      long long row = token_row(a, i, q0 + r);
+      if (row < 0) continue;
+      float l = L[r];
+      float o = l > 0.f ? O[e] / l : 0.f;
+      *shard_addr(a.sh, SH_O, a.out, h * a.oh + c, row, a.orow) = __float2bfloat16_rn(o);
+    }
+    __syncthreads();  // shared tiles are reused by the next query chunk / region
   }
   if (a.sh.n > 1) __threadfence_system();  // rows stored into peer GPUs' shards
-  __syncthreads();  // shared tiles are reused by the block's next region
 }
 
 __global__ void __launch_bounds__(256) portable_attn_kernel(const __grid_constant__ PortableArgs a) {
@@ -167,24 +172,43 @@ __global__ void __launch_bounds__(256) portable_list_kernel(const __grid_constan
   }
 }
 
-static size_t portable_smem_for(int p, int d, int dv, int kc) {
-  return sizeof(float) * ((size_t)p * d + (size_t)p * dv + 3 * (size_t)p + (size_t)kc * (d + dv + p)) +
+static size_t portable_smem_for(int qc, int d, int dv, int kc) {
+  return sizeof(float) * ((size_t)qc * d + (size_t)qc * dv + 3 * (size_t)qc + (size_t)kc * (d + dv + qc)) +
          sizeof(int) * kc;
 }
 
-// Largest key chunk (the whole region, else a power of two) whose tiles fit
-// in the 227 KB of shared memory a CTA may opt into; 0 if none does.
-static int portable_key_chunk(int p, int d, int dv) {
+// Query and key chunks whose tiles fit in the 227 KB of shared memory a CTA
+// may opt into: the whole region if possible, else the most query rows (each
+// query chunk re-streams the keys) with the largest key chunk; {0, 0} if none.
+struct Chunks {
+  int qc, kc;
+};
+static Chunks portable_chunks(int p, int d, int dv) {
   constexpr size_t kMax = 227 * 1024;
-  if (portable_smem_for(p, d, dv, p) <= kMax) return p;
-  for (int kc = 256; kc >= 1; kc >>= 1)
-    if (kc < p && portable_smem_for(p, d, dv, kc) <= kMax) return kc;
-  return 0;
+  auto fit = [&](int qc, Chunks& out) {
+    if (portable_smem_for(qc, d, dv, p) <= kMax) {
+      out = {qc, p};
+      return true;
+    }
+    for (int kc = 256; kc >= 1; kc >>= 1)
+      if (kc < p && portable_smem_for(qc, d, dv, kc) <= kMax) {
+        out = {qc, kc};
+        return true;
+      }
+    return false;
+  };
+  Chunks c = {0, 0};
+  if (fit(p, c)) return c;
+  int q = 1;
+  while (2 * q < p) q *= 2;  // the largest power of two below p
+  for (; q >= 1; q >>= 1)
+    if (fit(q, c)) return c;
+  return c;
 }
 
 size_t portable_smem_bytes(int p, int d, int dv) {
-  const int kc = portable_key_chunk(p, d, dv);
-  return portable_smem_for(p, d, dv, kc ? kc : 1);
+  const Chunks c = portable_chunks(p, d, dv);
+  return c.qc ? portable_smem_for(c.qc, d, dv, c.kc) : ~size_t(0);
 }
 
 static PortableArgs portable_args(const da_attn_args& args, const Geo& geo) {
@@ -202,7 +226,9 @@ static PortableArgs portable_args(const da_attn_args& args, const Geo& geo) {
   a.row_ptr = args.row_ptr; a.col_idx = args.col_idx; a.cap = args.mask_cap;
   a.key_valid = args.key_valid;
   a.mask_h = args.shared_mask ? 0 : 1;
-  a.kc = portable_key_chunk(geo.p, args.d, args.dv);
+  const Chunks ch = portable_chunks(geo.p, args.d, args.dv);
+  a.kc = ch.kc;
+  a.qc = ch.qc;
   a.geo = geo;
   a.sh = make_shards(args);
   return a;

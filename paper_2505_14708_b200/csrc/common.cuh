@@ -38,6 +38,15 @@ inline Geo make_geo(const da_grid& gr) {
   return g;
 }
 
+// 64-token regions run on the tcgen05 kernel as they are (0); 64 x 2^s-token
+// regions whose pool width 2^s divides run as 2^s column parts of 64 tokens
+// (s = 1..3: e.g. the paper's 8x16 pools as two 8x8 halves); -1: neither.
+__host__ __device__ inline int region_parts_shift(const Geo& g) {
+  for (int s = 0; s <= 3; ++s)
+    if (g.p == (64 << s) && g.pw % (1 << s) == 0) return s;
+  return -1;
+}
+
 // Division by a runtime constant with a precomputed multiplier
 // (q = (umulhi(n, mul) + n) >> shift; exact for n < 2^31).
 struct FastDiv {

@@ -305,9 +305,9 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(const __gri
   // K / V tiles ([half][64 rows x 128 B], 128-byte swizzle, zero padding rows):
   // byte-for-byte the shared-memory image the attention MMAs read (d = 128, p = 64)
   uint8_t* const tz = z >= 1 ? pick2(src.tile, z - 1) : nullptr;
-  // 128-token regions (tiles only with an even pool width): the two column
-  // halves' tiles, 2 i and 2 i + 1 (the attention kernel's split mode)
-  const int split = g.p == 128 ? 1 : 0;
+  // 64 x 2^s-token regions: the tiles of their 2^s column parts, 2^s i + part
+  // (the attention kernel's split mode; region_parts_shift)
+  const int split = max(0, region_parts_shift(g));
   uint8_t* tdst = (tz != nullptr && live) ? tz + ((long long)h * g.g + i) * (16384 << split) : nullptr;
 #ifdef DA_K4_TK
   uint4 vprev[4];  // V^T tiles (the experimental transposed K4's layout): the previous 4-row batch
@@ -341,9 +341,9 @@ __global__ void __launch_bounds__(256, DA_POOL_MINB) pool_avg_kernel(const __gri
         if (r >= g.p) continue;
         int rt = r, half = 0;
         if (split) {
-          const int hw = g.pw >> 1, u = r / g.pw, v = r - u * g.pw;
-          half = v >= hw;
-          rt = u * hw + v - half * hw;
+          const int pw = g.pw >> split, u = r / g.pw, v = r - u * g.pw;
+          half = v / pw;  // the column part
+          rt = u * pw + v - half * pw;
         }
         *reinterpret_cast<uint4*>(tdst + half * 16384 + kv_tile_offset_grouped(rt, k >> 3, k & 7)) = q[t];
       }
@@ -468,8 +468,7 @@ cudaError_t launch_pool2(const void* x0, long long hs0, long long rs0, double* o
     src.hs[0] = hs0; src.rs[0] = rs0; src.out[0] = out0;
     src.x[1] = static_cast<const __nv_bfloat16*>(x1 ? x1 : x0);
     src.hs[1] = x1 ? hs1 : hs0; src.rs[1] = x1 ? rs1 : rs0; src.out[1] = x1 ? out1 : out0;
-    const bool tiles = x1 && x2 && ktile && vtile && d == 128 && (g.p == 64 || (g.p == 128 && g.pw % 2 == 0)) &&
-                       rs2 % 8 == 0;
+    const bool tiles = x1 && x2 && ktile && vtile && d == 128 && region_parts_shift(g) >= 0 && rs2 % 8 == 0;
     src.x[2] = static_cast<const __nv_bfloat16*>(tiles ? x2 : x0);
     src.hs[2] = tiles ? hs2 : hs0; src.rs[2] = tiles ? rs2 : rs0;
     src.tile[0] = tiles ? ktile : nullptr;

@@ -354,7 +354,8 @@ def _seam_case(g, p, d, heads, density, seed, key_valid=False):
 
 
 @pytest.mark.parametrize("g,p,d,force_portable", [(40, 64, 128, False), (40, 64, 128, True), (30, 16, 64, False),
-                                                   (20, 128, 64, False), (25, 64, 128, False)])
+                                                   (20, 128, 64, False), (25, 64, 128, False), (12, 256, 128, False),
+                                                   (12, 256, 128, True), (8, 512, 128, False)])
 def test_block_sparse_seam_vs_oracle(g, p, d, force_portable):
     q, k, v, scores, _ = _seam_case(g, p, d, 2, 0.3, g + p + d)
     mask = da.select_top_fraction(torch.from_numpy(scores).cuda(), 0.3, True)
@@ -413,7 +414,10 @@ def test_8x16_pools_shared_softmax_and_fallback_rows_vs_oracle(shared, select_on
 
 
 @pytest.mark.parametrize("dims", [(2, 16, 48, 8, 16), (3, 45, 80, 8, 16), (2, 20, 72, 8, 16), (2, 12, 20, 8, 16),
-                                  (2, 13, 37, 8, 16), (2, 24, 40, 4, 16), (2, 21, 40, 16, 4)])
+                                  (2, 13, 37, 8, 16), (2, 24, 40, 4, 16), (2, 21, 40, 16, 4),
+                                  # 256- and 512-token regions: four / eight column parts on tcgen05; the
+                                  # portable kernel runs them in query chunks
+                                  (2, 32, 48, 16, 16), (2, 16, 64, 8, 32), (2, 20, 72, 16, 32), (2, 16, 48, 16, 8)])
 def test_pipeline_tcgen05_matches_portable_other_pools(dims):
     # the paper's 8x16 pools (half-regions on tcgen05) and other 64-token pool
     # shapes, padded grids included: same masks, outputs within the bf16 tolerance
