@@ -117,9 +117,9 @@ int da_select(const double* scores, int32_t heads, int32_t g, int64_t m, int32_t
  * layout 1 (ORIGINAL): q/k/v/out hold real tokens only, in original order,
  *   with the given strides; permutation and padding happen inside the kernel
  *   (padding.py:139-157 fused). key_valid must be NULL.
- * d == dv == 128 with p == 64 (any pool shape), or p == 128 with an even
- * pool width (e.g. the paper's 8x16, run as two 64-token column halves), take
- * the tcgen05/TMEM lane-half kernel (da_sparse_attention feeds it the K/V
+ * d == dv == 128 with p == 64 (any pool shape), or p == 64 x 2^s (s <= 3)
+ * with a pool width divisible by 2^s (e.g. the paper's 8x16, run as two
+ * 64-token column halves), take the tcgen05/TMEM lane-half kernel (da_sparse_attention feeds it the K/V
  * region tiles its pooling pass writes; da_block_sparse_fwd writes them first);
  * any other shape takes the portable CUDA-core kernel (same semantics). */
 #define DA_LAYOUT_REORDERED 0
