@@ -135,32 +135,53 @@ class PeerShards:
         for n in self.sizes:
             self.offsets.append(off)
             off += -(-n * 2 // 256) * 256
-        self.arena = torch.empty(off, dtype=torch.uint8, device=dev)
+        # a local failure (allocation, export) must not skip the collective
+        # below, or the other ranks would wait in it: it is raised after it
+        failure, mine = None, None
+        try:
+            self.arena = torch.empty(off, dtype=torch.uint8, device=dev)
+            handle = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+            offset = ctypes.c_int64()
+            check(lib().da_ipc_export(self.arena.data_ptr(), handle, ctypes.byref(offset)), "ipc_export")
+            mine = (bytes(handle.raw), int(offset.value))
+        except Exception as e:  # noqa: BLE001
+            failure = e
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        if failure is not None:
+            raise failure
+        if any(x is None for x in everyone):
+            raise RuntimeError("a peer rank could not allocate or export its shard buffers")
         views = [self.arena[o:o + n * 2].view(torch.bfloat16) for o, n in zip(self.offsets, self.sizes)]
         self.q = views[0].view(rows, heads, d)
         self.k = views[1].view(rows, heads, d)
         self.v = views[2].view(rows, heads, dv)
         self.out = views[3].view(rows, heads, dv)
-        handle = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
-        offset = ctypes.c_int64()
-        check(lib().da_ipc_export(self.arena.data_ptr(), handle, ctypes.byref(offset)), "ipc_export")
-        mine = (bytes(handle.raw), int(offset.value))
-        everyone = [None] * world
-        dist.all_gather_object(everyone, mine, group=group)
         self._opened = []   # (base pointer, 0) of every mapping this process made
         self.bases = []     # arena address of each rank, in this process
         mapped = {}
-        for r, (h, o) in enumerate(everyone):
-            if r == rank:
-                self.bases.append(self.arena.data_ptr())
-                continue
-            if h not in mapped:
-                ptr = ctypes.c_void_p()
-                with torch.cuda.device(dev):
-                    check(lib().da_ipc_open(h, 0, ctypes.byref(ptr)), "ipc_open")
-                mapped[h] = ptr.value
-                self._opened.append(ptr.value)
-            self.bases.append(mapped[h] + o)
+        try:
+            for r, (h, o) in enumerate(everyone):
+                if r == rank:
+                    self.bases.append(self.arena.data_ptr())
+                    continue
+                if h not in mapped:
+                    ptr = ctypes.c_void_p()
+                    with torch.cuda.device(dev):
+                        check(lib().da_ipc_open(h, 0, ctypes.byref(ptr)), "ipc_open")
+                    mapped[h] = ptr.value
+                    self._opened.append(ptr.value)
+                self.bases.append(mapped[h] + o)
+        except Exception as e:  # noqa: BLE001
+            failure = e
+        # every rank learns whether every rank mapped every peer, and all raise together
+        oks = [None] * world
+        dist.all_gather_object(oks, failure is None, group=group)
+        if not all(oks):
+            for base in self._opened:
+                lib().da_ipc_close(base, 0)
+            self._opened = []
+            raise failure if failure is not None else RuntimeError("a peer rank could not map the shard buffers")
         self._flag = torch.zeros(1, dtype=torch.float32, device=dev)
 
     def table(self, h0: int, h1: int):
