@@ -1,5 +1,6 @@
-"""CUDA-graph capture of the pipeline call (HV720 / 90 %): eager vs replay,
-CUDA events, and the outputs compared."""
+"""CUDA-graph capture of the pipeline call (HV720 / 90 %, all tokens, H heads:
+24 = one GPU, 3 = one rank's share at P = 8): eager vs replay, CUDA events,
+K4's share, and the outputs compared.  python tools/probes/graph_probe.py [H]"""
 import statistics
 import sys
 from pathlib import Path
@@ -12,7 +13,8 @@ from paper_2505_14708_b200 import api  # noqa: E402
 
 plan = da.pad_plan(33, 45, 80, 8, 8)
 g = torch.Generator(device="cuda").manual_seed(0)
-q, k, v = (torch.randn(24, plan.num_valid, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+H = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+q, k, v = (torch.randn(H, plan.num_valid, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
 scale = da.head_dim_scale(128)
 run = lambda: api._pipeline(q, k, v, plan, 0.9, scale, "average", "logits", True, False, "hnd", want_bitmap=False)
 for _ in range(3):
@@ -43,7 +45,14 @@ def timeit(fn, n=20):
 
 
 for rep in range(2):
-    print("eager ms", round(timeit(run), 3), "graph ms", round(timeit(graph.replay), 3), flush=True)
+    print(f"H={H} eager ms", round(timeit(run), 3), "graph ms", round(timeit(graph.replay), 3), flush=True)
+k4 = []
+for _ in range(10):
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    api._pipeline(q, k, v, plan, 0.9, scale, "average", "logits", True, False, "hnd", want_bitmap=False, attn_events=ev)
+    torch.cuda.synchronize()
+    k4.append(ev[0].elapsed_time(ev[1]))
+print(f"H={H} K4 (region order + kernel + fallback list) ms", round(statistics.median(k4), 3))
 graph.replay()
 torch.cuda.synchronize()
 print("graph output == eager:", torch.equal(out_g, ref))
