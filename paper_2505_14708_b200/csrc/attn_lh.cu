@@ -106,6 +106,28 @@ constexpr int SMEM_V = SMEM_K + KSL * SLOT;
 constexpr int SMEM_END = SMEM_V + VSL * SLOT;
 
 constexpr uint32_t TMEM_COLS = 512;
+// wait flavours: 1 = test_wait spin (lowest wake-up latency, but a spinning
+// warp takes issue slots from the warps sharing its scheduler), 0 = try_wait
+// with a suspend hint (the warp sleeps until the phase completes)
+#ifndef LH_SM_SPIN
+#define LH_SM_SPIN 1  // the softmax warps' waits (S full, step info, P free)
+#endif
+#ifndef LH_G_SPIN
+#define LH_G_SPIN 1  // the GEMM issuers' waits
+#endif
+#if LH_SM_SPIN
+#define LH_SMWAIT mbar_wait_spin
+#else
+#define LH_SMWAIT mbar_wait
+#endif
+#if LH_G_SPIN
+#define LH_GWAIT mbar_wait_spin
+#else
+#define LH_GWAIT mbar_wait
+#endif
+#ifndef LH_POLY8
+#define LH_POLY8 0  // bit k % 8 (k even): exponential pair k on the FMA pipe (degree-3 polynomial) instead of MUFU; 0x40 (one pair in four) measured 1.9 % slower than none (profiles/r02/k4_variants_final.log)
+#endif
 #ifndef LH_S2
 #define LH_S2 0  // 1: two S buffers per lane half (O single-buffered) instead of one (O double-buffered); measured equal
 #endif
@@ -421,7 +443,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
       if (!item_from_record(p, next_item(), itm)) break;
       { LH_T0(); mbar_wait(&B.q_full, qi & 1); LH_ACC(1); }
       for (;;) {
-        { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(2); }
+        { LH_T0(); LH_GWAIT(&B.info_full[iidx], iph); LH_ACC(2); }
         const int4 e = take_info(aux.info, &B.info_empty[iidx], iidx, lane);
         const int last = e.w & 1;
         const int h = gs & 1;
@@ -430,11 +452,11 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
         const int sb = (gs >> 1) % NSB;
         if (gs >= 2 * NSB) {
           LH_T0();
-          mbar_wait_spin(&B.s_free[h][sb], (uint32_t)(((gs / (2 * NSB)) - 1) & 1));
+          LH_GWAIT(&B.s_free[h][sb], (uint32_t)(((gs / (2 * NSB)) - 1) & 1));
           LH_ACC(3);
         }
         const int s = gs % KSL;
-        { LH_T0(); mbar_wait_spin(&B.k_full[s], (uint32_t)((gs / KSL) & 1)); LH_ACC(4); }
+        { LH_T0(); LH_GWAIT(&B.k_full[s], (uint32_t)((gs / KSL) & 1)); LH_ACC(4); }
         tc_fence_after();
         if (elect_one_sync()) {
           const uint32_t lo = h ? LANE_H : 0u;
@@ -468,13 +490,13 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
       const int ob = qi % NOB;
       int t = 0;
       for (;;) {
-        { LH_T0(); mbar_wait_spin(&B.info_full[iidx], iph); LH_ACC(5); }
+        { LH_T0(); LH_GWAIT(&B.info_full[iidx], iph); LH_ACC(5); }
         const int4 e = take_info(aux.info, &B.info_empty[iidx], iidx, lane);
         const int last = e.w & 1;
         const int h = gs & 1;
         const int s = gs % VSL;
-        { LH_T0(); mbar_wait_spin(&B.v_full[s], (uint32_t)((gs / VSL) & 1)); LH_ACC(6); }
-        { LH_T0(); mbar_wait_spin(&B.p_full[h], (uint32_t)((gs >> 1) & 1)); LH_ACC(7); }
+        { LH_T0(); LH_GWAIT(&B.v_full[s], (uint32_t)((gs / VSL) & 1)); LH_ACC(6); }
+        { LH_T0(); LH_GWAIT(&B.p_full[h], (uint32_t)((gs >> 1) & 1)); LH_ACC(7); }
         if (t == 0 && qi >= NOB) {
           LH_T0();
           mbar_wait(&B.o_empty[ob], (uint32_t)(((qi / NOB) - 1) & 1));
@@ -633,10 +655,10 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
         }
 #endif
         const int ii = gs & (INFO - 1);
-        { LH_T0(); mbar_wait_spin(&B.info_full[ii], (uint32_t)((gs / INFO) & 1)); LH_ACC(9); }
+        { LH_T0(); LH_SMWAIT(&B.info_full[ii], (uint32_t)((gs / INFO) & 1)); LH_ACC(9); }
         const int4 e = take_info(aux.info, &B.info_empty[ii], ii, lane);
         const int sb = (gs >> 1) % NSB;
-        { LH_T0(); mbar_wait_spin(&B.s_full[wg][sb], (uint32_t)((gs / (2 * NSB)) & 1)); LH_ACC(10); }
+        { LH_T0(); LH_SMWAIT(&B.s_full[wg][sb], (uint32_t)((gs / (2 * NSB)) & 1)); LH_ACC(10); }
         tc_fence_after();
         const bool kp = ((e.z >> c) & 1) && !(LH_FAKELOAD & 4);
         if (!(LH_FAKELOAD & 4)) {
@@ -686,7 +708,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
 #pragma unroll
           for (int k = 0; k < 64; k += 2) {
             const float2 ev = ffma2(make_float2(x[k], x[k + 1]), sc, nm);
-            const float2 pe = (k % 8 == 6) ? exp2_poly2(ev) : make_float2(fast_exp2(ev.x), fast_exp2(ev.y));
+            const float2 pe = ((LH_POLY8 >> (k % 8)) & 1) ? exp2_poly2(ev) : make_float2(fast_exp2(ev.x), fast_exp2(ev.y));
             acc = fadd2(acc, pe);
             pk[k / 2] = kp ? pack_bf16(pe.x, pe.y) : 0u;
           }
@@ -694,7 +716,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_attn_lh_kernel(const __grid
         }
         // this half's P buffer: GEMM2 of step gs - 2 has read it
         if (gs >= 2) {
-          { LH_T0(); mbar_wait_spin(&B.p_free[wg], (uint32_t)(((gs >> 1) - 1) & 1)); LH_ACC(11); }
+          { LH_T0(); LH_SMWAIT(&B.p_free[wg], (uint32_t)(((gs >> 1) - 1) & 1)); LH_ACC(11); }
           tc_fence_after();
         }
         tmem_st16x2_16(th + COL_P, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
