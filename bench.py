@@ -92,11 +92,20 @@ class ClockSampler:
         self.t0 = self.t1 = None
 
     def start(self):
+        """Start sampling and wait (up to 5 s) for the first sample, so that
+        nvidia-smi's own start-up (which can stall the GPU's host thread for
+        milliseconds) is over before any timed work."""
+        import select
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            ready, _, _ = select.select([self.proc.stdout], [], [], 5.0)
+            if ready:
+                self.proc.stdout.readline()
+            time.sleep(0.3)  # a few more samples: past the start-up
         except Exception:  # noqa: BLE001
             self.proc = None
         return self
@@ -327,8 +336,12 @@ def run_ours(args, cfg, name):
             return hp(q, k, v, compute_events=comp_ev[s_], k4_events=k4_ev[s_])
 
     clocks = ClockSampler(local).start()  # running (and sampling) before the timed region opens
+    res = None
     for _ in range(args.warmup):
-        step()
+        # keep each result alive until the next step returns, as the timed
+        # loop does, so the caching allocator has already grown to that
+        # footprint (a cudaMalloc inside the timed steps would stall one call)
+        res = step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
