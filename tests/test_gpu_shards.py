@@ -104,7 +104,7 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_peer_transport_two_processes_one_gpu(world, tmp_path):
     # world processes on the one GPU, gloo for the host-side exchange: every
     # rank maps the others' shard buffers through CUDA IPC and the kernels read
