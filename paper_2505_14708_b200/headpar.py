@@ -123,6 +123,7 @@ class PeerShards:
     collective) unmaps the peers' buffers."""
 
     def __init__(self, rows: int, heads: int, d: int, dv: int, world: int, rank: int, group=None, device=None):
+        import contextlib
         import ctypes
 
         from ._lib import IPC_HANDLE_BYTES, check, lib
@@ -167,7 +168,7 @@ class PeerShards:
                     continue
                 if h not in mapped:
                     ptr = ctypes.c_void_p()
-                    with torch.cuda.device(dev):
+                    with (torch.cuda.device(dev) if dev.type == "cuda" else contextlib.nullcontext()):
                         check(lib().da_ipc_open(h, 0, ctypes.byref(ptr)), "ipc_open")
                     mapped[h] = ptr.value
                     self._opened.append(ptr.value)

@@ -133,3 +133,67 @@ def test_head_groups_split():
         for G in range(1, 6):
             gs = head_groups(hl, G)
             assert gs[0][0] == 0 and gs[-1][1] == hl and all(a[1] == b[0] for a, b in zip(gs, gs[1:]))
+
+
+class _FakeLib:
+    """Stands in for the C library in the PeerShards set-up: export / open
+    succeed or fail per rank (no GPU needed for the agreement logic)."""
+
+    def __init__(self, fail_export, fail_open):
+        self.fail_export, self.fail_open, self.closed = fail_export, fail_open, []
+
+    def da_ipc_export(self, ptr, handle, offset):
+        if self.fail_export:
+            return 2
+        handle.raw = bytes([dist.get_rank() + 1]) * 64
+        return 0
+
+    def da_ipc_open(self, handle, offset, out):
+        if self.fail_open:
+            return 2
+        out._obj.value = 4096 * (1 + handle[0] if isinstance(handle, bytes) else 1)
+        return 0
+
+    def da_ipc_close(self, ptr, offset):
+        self.closed.append(ptr)
+        return 0
+
+    def da_last_error(self):
+        return b"simulated failure"
+
+
+def _peer_setup_worker(rank, world, port, fail_export_rank, fail_open_rank, results):
+    # one rank's export or mapping fails: every rank must raise, none may be
+    # left waiting in a collective (the next collective below would hang)
+    _init(rank, world, port)
+    try:
+        from paper_2505_14708_b200 import _lib
+        from paper_2505_14708_b200.headpar import PeerShards
+
+        fake = _FakeLib(rank == fail_export_rank, rank == fail_open_rank)
+        _lib.lib = lambda: fake
+        raised = False
+        try:
+            PeerShards(4, 2, 8, 8, world, rank, device="cpu")
+        except (RuntimeError, ValueError):
+            raised = True
+        flag = torch.tensor([1])
+        dist.all_reduce(flag)  # every rank reaches the next collective
+        results[rank] = (raised, int(flag.item()), len(fake.closed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_export_rank,fail_open_rank", [(1, -1), (-1, 1), (-1, -1)])
+def test_peer_shard_setup_failures_are_collective(fail_export_rank, fail_open_rank):
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_peer_setup_worker, args=(world, _free_port(), fail_export_rank, fail_open_rank, results),
+             nprocs=world, join=True)
+    res = dict(results)
+    expect_raise = fail_export_rank >= 0 or fail_open_rank >= 0
+    assert all(res[r][0] == expect_raise for r in range(world)), res
+    assert all(res[r][1] == world for r in range(world))
+    if fail_open_rank >= 0:  # the rank whose mapping succeeded unmapped it again
+        assert res[1 - fail_open_rank][2] == 1
