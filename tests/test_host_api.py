@@ -207,3 +207,19 @@ def test_head_parallel_transport_argument():
     with pytest.raises(ValueError, match="transport"):
         HeadParallelAttention(plan, 0.9, 2, 0, transport="shm")
     assert HeadParallelAttention(plan, 0.9, 2, 0, transport="peer").transport == "peer"
+
+
+def test_documented_entry_points_exist():
+    # the README's entry-point table and INTEGRATION.md name these
+    import paper_2505_14708_b200.dit as dit
+    import paper_2505_14708_b200.headpar as headpar
+
+    for name in ("padded_sparse_attention", "draft_sparse_attention", "multi_head_sparse_attention",
+                 "padded_block_sparse_attention", "block_sparse_attention", "select_top_fraction", "draft_logits",
+                 "draft_attention_map", "pool_regions", "pool_tokens", "reorder_tokens", "restore_tokens",
+                 "RegionMask", "mask_to_json_dict", "mask_from_json_dict", "mask_to_bitmap", "kept_from_bitmap",
+                 "mask_density_stats", "flops_count", "sharded_sparse_attention", "pad_plan", "PadPlan",
+                 "LatentLayout", "PipelineResult", "FlopsReport", "top_fraction_count", "head_dim_scale"):
+        assert callable(getattr(da, name)), name
+    assert callable(headpar.HeadParallelAttention) and callable(headpar.PeerShards)
+    assert callable(dit.DraftAttention)
