@@ -118,3 +118,21 @@ def test_peer_transport_two_processes_one_gpu(world, tmp_path):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for rank in range(world):
         assert (tmp_path / f"ok{rank}").read_text() == "ok"
+
+
+def test_bench_multi_rank_code_path_one_gpu():
+    # bench.py's N > 1 path (peer transport, max-over-ranks timing, e2e through
+    # the mapped buffers) with two ranks sharing the GPU: a code-path check of
+    # the driver's scaling command, not a measurement
+    import json
+
+    env = dict(os.environ, DA_BENCH_SAME_GPU="1", PYTHONPATH=str(ROOT))
+    port = str(_free_port())
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", "2",
+           "--config", "tiny", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-dense"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["transport"] == "peer" and line["value"] > 0
+    assert line["e2e"]["value"] > 0 and "collective_exposed_ms" in line
